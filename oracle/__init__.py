@@ -1,0 +1,197 @@
+"""CPU oracle for the batched 3DGS hot path — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and --impl reference)
+may import this package.  The product path (paper_2604_25459_b200) never imports it and
+shares no code with it (no kernels, headers, helpers, constants or pre/post-processing).
+
+Layout:
+  gsb_oracle.c  plain C, fp64 (+ the exact fp32 depth chain, reading R11), pthreads:
+                per-pixel brute force over all Gaussians in (z_f32 bits, id) order.
+  mini.py       independent NumPy re-implementation (fp64) for small frames (pin 11).
+  binning.py    integer-path oracle: fp32 tile rects (R9) and per-tile (zbits, id) lists (R10).
+
+Each function cites the passage it follows; DESIGN.md §2 lists every reading (R1-R28).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "gsb_oracle.c")
+
+NF = 17
+F_U, F_V, F_SXX, F_SXY, F_SYY, F_A, F_B, F_C, F_R, F_G, F_BL, F_O, F_KAPPA, F_Z32, F_Z64, F_XC, F_YC = range(NF)
+
+# parity tolerances (BASELINE.json north_star) and mask margins (reading R28)
+TOL_RGB = 2e-3
+TOL_DEPTH_REL = 1e-3
+TOL_DEPTH_ABS = 1e-6
+DELTA_ALPHA = 1e-3
+DELTA_T = 1e-3
+
+
+def build_oracle(force: bool = False) -> str:
+    """Compile liboracle.so: plain C, -O2, no fast-math, no FMA contraction (R11)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+               "-pthread", "-o", _SO, _SRC, "-lm"]
+        subprocess.check_call(cmd)
+    return _SO
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build_oracle()
+        L = ctypes.CDLL(_SO)
+        P = ctypes.c_void_p
+        L.gsbo_project.restype = ctypes.c_int
+        L.gsbo_project.argtypes = [P, P, P, P, P, ctypes.c_int, ctypes.c_int, P, ctypes.c_int64, P,
+                                   ctypes.c_int, P, P, ctypes.c_int, ctypes.c_int, ctypes.c_float,
+                                   ctypes.c_float, P, P, P]
+        L.gsbo_composite.restype = ctypes.c_int
+        L.gsbo_composite.argtypes = [P, P, ctypes.c_int64, P, P, ctypes.c_int64, P, ctypes.c_int,
+                                     ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                     P, P, P, P, P, P, P, ctypes.c_int]
+        L.gsbo_depth_key.restype = ctypes.c_float
+        L.gsbo_depth_key.argtypes = [P, P, P]
+        L.gsbo_fmaf.restype = ctypes.c_float
+        L.gsbo_fmaf.argtypes = [ctypes.c_float, ctypes.c_float, ctypes.c_float]
+        L.gsbo_sh_basis.restype = None
+        L.gsbo_sh_basis.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double, P]
+        _lib = L
+    return _lib
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+@dataclass
+class RenderParams:
+    width: int
+    height: int
+    near: float = 0.01      # R4
+    far: float = 1000.0
+    bg: tuple = (0.0, 0.0, 0.0)   # R15
+    sh_degree: Optional[int] = None
+
+
+def project(scene, pose_env: np.ndarray, intr: np.ndarray, w2c: np.ndarray, prm: RenderParams):
+    """Steps 1-5 (pose, depth key, cull, EWA projection, SH colour) for one frame.
+    Returns (proj [N,NF] f64, zbits [N] u32, valid [N] bool)."""
+    L = lib()
+    N = scene.n
+    D = scene.sh_degree if prm.sh_degree is None else prm.sh_degree
+    out = np.zeros((N, NF), np.float64)
+    zb = np.zeros(N, np.uint32)
+    valid = np.zeros(N, np.uint8)
+    keep = [_c(scene.means, np.float32), _c(scene.scales, np.float32), _c(scene.quats, np.float32),
+            _c(scene.opacities, np.float32), _c(scene.sh, np.float32), _c(scene.body_id, np.int32),
+            _c(pose_env, np.float32).reshape(-1), _c(intr, np.float32).reshape(-1),
+            _c(w2c, np.float32).reshape(-1)]
+    rc = L.gsbo_project(_p(keep[0]), _p(keep[1]), _p(keep[2]), _p(keep[3]), _p(keep[4]),
+                        scene.sh_degree, D, _p(keep[5]), N, _p(keep[6]), scene.n_bodies,
+                        _p(keep[7]), _p(keep[8]), prm.width, prm.height, prm.near, prm.far,
+                        _p(out), _p(zb), _p(valid))
+    if rc != 0:
+        raise ValueError("oracle: body index out of range")
+    return out, zb, valid.astype(bool)
+
+
+def depth_order(zbits: np.ndarray, valid: np.ndarray) -> np.ndarray:
+    """Step 6 / reading R10: valid ids sorted by (bits(z_f32) as u32, id) ascending."""
+    ids = np.nonzero(valid)[0].astype(np.uint32)
+    return ids[np.lexsort((ids, zbits[ids]))].astype(np.uint32)
+
+
+@dataclass
+class FrameResult:
+    rgb: np.ndarray        # [npix,3] (or [H,W,3] for full frames)
+    depth: np.ndarray
+    alpha: np.ndarray
+    term_id: np.ndarray    # id of the Gaussian at which the pixel terminated, -1 if none
+    n_eval_all: np.ndarray  # entries visited in the all-Gaussian order (diagnostic)
+    masked: np.ndarray     # reading R28 threshold-margin mask
+    budget_rgb: np.ndarray
+    budget_depth: np.ndarray
+    proj: np.ndarray
+    zbits: np.ndarray
+    valid: np.ndarray
+    order: np.ndarray
+
+
+def composite(proj, order, px, py, prm: RenderParams, mode: str = "box", nthreads: Optional[int] = None,
+              delta_alpha: float = DELTA_ALPHA, delta_T: float = DELTA_T, valid=None):
+    """Step 7-9 for the listed pixel coordinates (see gsb_oracle.c)."""
+    L = lib()
+    px = _c(px, np.int32).reshape(-1)
+    py = _c(py, np.int32).reshape(-1)
+    npix = px.size
+    order = _c(order, np.uint32)
+    bg = _c(prm.bg, np.float32)
+    if order.size:
+        cmax = float(max(proj[order][:, F_R:F_BL + 1].max(), np.abs(bg).max()))
+        zmax = float(proj[order][:, F_Z32].max())
+    else:
+        cmax, zmax = float(np.abs(bg).max()), 0.0
+    rgb = np.zeros((npix, 3)); dep = np.zeros(npix); alp = np.zeros(npix)
+    term = np.zeros(npix, np.int64); nev = np.zeros(npix, np.int64)
+    brgb = np.zeros(npix); bdep = np.zeros(npix)
+    if nthreads is None:
+        nthreads = os.cpu_count() or 1
+    proj = _c(proj, np.float64)
+    L.gsbo_composite(_p(proj), _p(order), order.size, _p(px), _p(py), npix, _p(bg),
+                     1 if mode == "box" else 0, delta_alpha, delta_T, cmax, zmax,
+                     _p(rgb), _p(dep), _p(alp), _p(term), _p(nev), _p(brgb), _p(bdep), int(nthreads))
+    masked = (brgb > 0.5 * TOL_RGB) | (bdep > 0.5 * (TOL_DEPTH_REL * dep + TOL_DEPTH_ABS))
+    return rgb, dep, alp, term, nev, masked, brgb, bdep
+
+
+def render_frame(scene, pose_env, intr, w2c, prm: RenderParams, pixels=None, mode: str = "box",
+                 nthreads: Optional[int] = None, **kw) -> FrameResult:
+    """One frame end to end.  pixels: None (full frame) or (px, py) int arrays."""
+    proj, zb, valid = project(scene, pose_env, intr, w2c, prm)
+    order = depth_order(zb, valid)
+    full = pixels is None
+    if full:
+        py, px = np.meshgrid(np.arange(prm.height), np.arange(prm.width), indexing="ij")
+        px, py = px.reshape(-1), py.reshape(-1)
+    else:
+        px, py = pixels
+    rgb, dep, alp, term, nev, masked, brgb, bdep = composite(proj, order, px, py, prm, mode, nthreads, **kw)
+    if full:
+        H, W = prm.height, prm.width
+        rgb, dep, alp = rgb.reshape(H, W, 3), dep.reshape(H, W), alp.reshape(H, W)
+        term, nev, masked = term.reshape(H, W), nev.reshape(H, W), masked.reshape(H, W)
+        brgb, bdep = brgb.reshape(H, W), bdep.reshape(H, W)
+    return FrameResult(rgb, dep, alp, term, nev, masked, brgb, bdep, proj, zb, valid, order)
+
+
+def depth_key(w2c, pose_or_none, mu) -> np.float32:
+    """R11 exact fp32 depth key of a single mean (C implementation)."""
+    L = lib()
+    w = _c(w2c, np.float32).reshape(-1)
+    m = _c(mu, np.float32).reshape(-1)
+    p = None if pose_or_none is None else _c(pose_or_none, np.float32).reshape(-1)
+    return np.float32(L.gsbo_depth_key(_p(w), _p(p), _p(m)))
+
+
+def sh_basis(deg: int, x: float, y: float, z: float) -> np.ndarray:
+    Y = np.zeros(16)
+    lib().gsbo_sh_basis(deg, x, y, z, _p(Y))
+    return Y[: (deg + 1) ** 2]

@@ -1,0 +1,394 @@
+/*
+ * gsb_oracle.c — plain, slow, obviously-correct CPU ORACLE for the batched 3DGS hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code with
+ * the CUDA path (paper_2604_25459_b200/csrc) and includes none of its headers.
+ *
+ * What it computes (DESIGN.md §2 "the definition"):
+ *   for one frame (env e, camera c), per pixel, brute force over ALL Gaussians of the
+ *   scene in (fp32 depth bits, id) order — there is no tile concept here.
+ *
+ *   step 1  pose:        PAPER.md App. B.2 Eqs., Alg. 1 l.12-14
+ *                        mu_w = R(q_k) mu_i + t_k ; Sigma_w = R(q_k) Sigma_local R(q_k)^T
+ *                        (reading R23: q_world = q_k (x) q_local => Sigma rotates with q_k)
+ *   step 2  depth key:   exact fp32 chain, reading R11
+ *   step 3  cull:        near < z <= far and o >= 1/255  (readings R4, R5)
+ *   step 4  projection:  EWA splatting [3DGS-conv, cited by the paper at P:212],
+ *                        readings R2, R3, R6, R7 — all in fp64
+ *   step 5  colour:      real SH, degree <= 3, body-frame view direction (R18, R19)
+ *   step 6  order:       (bits(z_f32), id) ascending (R10) — done by the caller (numpy lexsort)
+ *   step 7  composite:   front-to-back alpha blending, alpha = min(0.99, o e^power),
+ *                        skip alpha < 1/255, stop before blending when T(1-alpha) < 1e-4
+ *                        (north_star; readings R12-R16), outputs RGB + T*bg, depth = sum w z,
+ *                        alpha = 1 - T ("RGB images and depth maps")
+ *   step 8  margin:      flip-effect budgets for the threshold mask (reading R28)
+ *   step 9  optional box acceleration (R8): skip i when the pixel centre is outside
+ *                        [u +- r_x] x [v +- r_y]; provably identical to brute force.
+ *
+ * Precision: fp64 everywhere except the depth key (fp32 chain, R11).  Build with
+ * -O2 -ffp-contract=off (no FMA contraction, no fast-math).
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define GSBO_NF 17
+enum {
+  F_U = 0, F_V, F_SXX, F_SXY, F_SYY, F_A, F_B, F_C, F_R, F_G, F_BL, F_O, F_KAPPA,
+  F_Z32, F_Z64, F_XC, F_YC
+};
+
+int gsbo_num_fields(void) { return GSBO_NF; }
+
+/* ---------------------------------------------------------------------------------
+ * Reading R11: the exact fp32 depth chain.  Every operation is a separately rounded
+ * IEEE binary32 op (float arithmetic on x86-64 SSE, -ffp-contract=off) or fmaf()
+ * (correctly rounded fused multiply-add from libm).
+ * ------------------------------------------------------------------------------- */
+static void r11_rot_f32(const float q[4], float R[3][3]) {
+  float qw = q[0], qx = q[1], qy = q[2], qz = q[3];
+  float xx = qx * qx, yy = qy * qy, zz = qz * qz;
+  float xy = qx * qy, xz = qx * qz, yz = qy * qz;
+  float wx = qw * qx, wy = qw * qy, wz = qw * qz;
+  float s;
+  s = yy + zz; R[0][0] = 1.0f - 2.0f * s;
+  s = xy - wz; R[0][1] = 2.0f * s;
+  s = xz + wy; R[0][2] = 2.0f * s;
+  s = xy + wz; R[1][0] = 2.0f * s;
+  s = xx + zz; R[1][1] = 1.0f - 2.0f * s;
+  s = yz - wx; R[1][2] = 2.0f * s;
+  s = xz - wy; R[2][0] = 2.0f * s;
+  s = yz + wx; R[2][1] = 2.0f * s;
+  s = xx + yy; R[2][2] = 1.0f - 2.0f * s;
+}
+
+/* depth row of the camera<-local transform: M2c, m2 (R11) */
+static void r11_depth_row(const float* w2c /*3x4*/, const float* pose /*7 or NULL*/,
+                          float M2[3], float* m2) {
+  const float W20 = w2c[8], W21 = w2c[9], W22 = w2c[10], t2 = w2c[11];
+  if (!pose) {
+    M2[0] = W20; M2[1] = W21; M2[2] = W22; *m2 = t2;
+    return;
+  }
+  float R[3][3];
+  r11_rot_f32(pose + 3, R);
+  for (int c = 0; c < 3; ++c) {
+    float p = W22 * R[2][c];
+    M2[c] = fmaf(W20, R[0][c], fmaf(W21, R[1][c], p));
+  }
+  *m2 = fmaf(W20, pose[0], fmaf(W21, pose[1], fmaf(W22, pose[2], t2)));
+}
+
+static float r11_depth(const float M2[3], float m2, const float mu[3]) {
+  return fmaf(M2[0], mu[0], fmaf(M2[1], mu[1], fmaf(M2[2], mu[2], m2)));
+}
+
+/* fp32 depth key of one Gaussian — exported so tests can pin the chain on its own */
+float gsbo_depth_key(const float* w2c, const float* pose_or_null, const float* mu) {
+  float M2[3], m2;
+  r11_depth_row(w2c, pose_or_null, M2, &m2);
+  return r11_depth(M2, m2, mu);
+}
+
+/* ---------------------------------------------------------------------------------
+ * fp64 helpers
+ * ------------------------------------------------------------------------------- */
+/* rotation matrix of a quaternion (w,x,y,z) used AS GIVEN (reading R22: per-frame
+   quaternions are assumed unit; template quaternions are normalised by the caller) */
+static void rot_from_quat(const double q[4], double R[3][3]) {
+  double w = q[0], x = q[1], y = q[2], z = q[3];
+  R[0][0] = 1 - 2 * (y * y + z * z); R[0][1] = 2 * (x * y - w * z); R[0][2] = 2 * (x * z + w * y);
+  R[1][0] = 2 * (x * y + w * z); R[1][1] = 1 - 2 * (x * x + z * z); R[1][2] = 2 * (y * z - w * x);
+  R[2][0] = 2 * (x * z - w * y); R[2][1] = 2 * (y * z + w * x); R[2][2] = 1 - 2 * (x * x + y * y);
+}
+
+static void matmul3(const double A[3][3], const double B[3][3], double C[3][3]) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      double s = 0;
+      for (int k = 0; k < 3; ++k) s += A[i][k] * B[k][j];
+      C[i][j] = s;
+    }
+}
+
+static void transpose3(const double A[3][3], double T[3][3]) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) T[i][j] = A[j][i];
+}
+
+/* reading R18: 3DGS real SH basis constants and sign pattern */
+static const double SH_C0 = 0.28209479177387814;
+static const double SH_C1 = 0.4886025119029199;
+static const double SH_C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                                -1.0925484305920792, 0.5462742152960396};
+static const double SH_C3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
+                                0.3731763325901154, -0.4570457994644658, 1.445305721320277,
+                                -0.5900435899266435};
+
+/* SH basis values Y_j(dir), j < (deg+1)^2, exactly as multiplied in R18 */
+void gsbo_sh_basis(int deg, double x, double y, double z, double* Y) {
+  Y[0] = SH_C0;
+  if (deg < 1) return;
+  Y[1] = -SH_C1 * y; Y[2] = SH_C1 * z; Y[3] = -SH_C1 * x;
+  if (deg < 2) return;
+  double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+  Y[4] = SH_C2[0] * xy;
+  Y[5] = SH_C2[1] * yz;
+  Y[6] = SH_C2[2] * (2 * zz - xx - yy);
+  Y[7] = SH_C2[3] * xz;
+  Y[8] = SH_C2[4] * (xx - yy);
+  if (deg < 3) return;
+  Y[9] = SH_C3[0] * y * (3 * xx - yy);
+  Y[10] = SH_C3[1] * xy * z;
+  Y[11] = SH_C3[2] * y * (4 * zz - xx - yy);
+  Y[12] = SH_C3[3] * z * (2 * zz - 3 * xx - 3 * yy);
+  Y[13] = SH_C3[4] * x * (4 * zz - xx - yy);
+  Y[14] = SH_C3[5] * z * (xx - yy);
+  Y[15] = SH_C3[6] * x * (xx - 3 * yy);
+}
+
+/* ---------------------------------------------------------------------------------
+ * Steps 1-5 for every Gaussian of one frame.
+ *   means/scales/quats/opac/sh/body_id: the scene template (fp32, as given to the ABI)
+ *   pose: [n_bodies][7] (tx,ty,tz,qw,qx,qy,qz) world<-body of THIS env (reading R22)
+ *   intr: fx,fy,cx,cy (px); w2c: 3x4 row-major [R|t], OpenCV axes (reading R2)
+ *   out: [n][GSBO_NF] doubles; zbits: [n]; valid: [n] (cull result)
+ * Returns 0, or -1 on a body index out of range (SPEC S:652 UnknownBody).
+ * ------------------------------------------------------------------------------- */
+int gsbo_project(const float* means, const float* scales, const float* quats, const float* opac,
+                 const float* sh, int sh_degree_scene, int sh_degree, const int32_t* body_id,
+                 int64_t n, const float* pose, int n_bodies, const float* intr, const float* w2c,
+                 int width, int height, float near_plane, float far_plane, double* out,
+                 uint32_t* zbits, uint8_t* valid) {
+  const int ncoef_scene = (sh_degree_scene + 1) * (sh_degree_scene + 1);
+  const double fx = intr[0], fy = intr[1], cx = intr[2], cy = intr[3];
+  double Wc[3][3], tc[3];
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) Wc[r][c] = w2c[r * 4 + c];
+    tc[r] = w2c[r * 4 + 3];
+  }
+  /* camera centre in world: c_w = -W^T t */
+  double cw[3];
+  for (int c = 0; c < 3; ++c) cw[c] = -(Wc[0][c] * tc[0] + Wc[1][c] * tc[1] + Wc[2][c] * tc[2]);
+  const double limx = 1.3 * (double)width / (2.0 * fx);   /* reading R6 */
+  const double limy = 1.3 * (double)height / (2.0 * fy);
+
+  for (int64_t i = 0; i < n; ++i) {
+    double* o = out + i * GSBO_NF;
+    memset(o, 0, sizeof(double) * GSBO_NF);
+    const int k = body_id[i];
+    if (k < -1 || k >= n_bodies) return -1;
+    /* step 1: RLGK pose of body k */
+    double Rk[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}}, tk[3] = {0, 0, 0};
+    const float* pk = NULL;
+    if (k >= 0) {
+      pk = pose + (int64_t)k * 7;
+      double qk[4] = {pk[3], pk[4], pk[5], pk[6]};
+      rot_from_quat(qk, Rk);
+      tk[0] = pk[0]; tk[1] = pk[1]; tk[2] = pk[2];
+    }
+    const double mu[3] = {means[3 * i], means[3 * i + 1], means[3 * i + 2]};
+    double muw[3];
+    for (int r = 0; r < 3; ++r) muw[r] = Rk[r][0] * mu[0] + Rk[r][1] * mu[1] + Rk[r][2] * mu[2] + tk[r];
+    /* Sigma_local = R(q_i) diag(s^2) R(q_i)^T with q_i normalised (reading R24) */
+    double qi[4] = {quats[4 * i], quats[4 * i + 1], quats[4 * i + 2], quats[4 * i + 3]};
+    double qn = sqrt(qi[0] * qi[0] + qi[1] * qi[1] + qi[2] * qi[2] + qi[3] * qi[3]);
+    for (int c = 0; c < 4; ++c) qi[c] /= qn;
+    double Ri[3][3], RiT[3][3], S2[3][3] = {{0}}, T1[3][3], Sl[3][3];
+    rot_from_quat(qi, Ri);
+    for (int c = 0; c < 3; ++c) S2[c][c] = (double)scales[3 * i + c] * (double)scales[3 * i + c];
+    matmul3(Ri, S2, T1);
+    transpose3(Ri, RiT);
+    matmul3(T1, RiT, Sl);
+    double RkT[3][3], Sw[3][3];
+    matmul3(Rk, Sl, T1);
+    transpose3(Rk, RkT);
+    matmul3(T1, RkT, Sw);
+
+    /* step 2: exact fp32 depth key (R11) */
+    float M2[3], m2;
+    r11_depth_row(w2c, pk, M2, &m2);
+    const float z32 = r11_depth(M2, m2, means + 3 * i);
+    uint32_t zb;
+    memcpy(&zb, &z32, 4);
+    zbits[i] = zb;
+    o[F_Z32] = z32;
+    o[F_O] = opac[i];
+
+    /* step 3: cull (R4, R5) */
+    const int keep = (z32 > near_plane) && (z32 <= far_plane) && ((double)opac[i] >= 1.0 / 255.0);
+    valid[i] = (uint8_t)keep;
+
+    /* step 4: EWA projection, fp64 (R2, R3, R6, R7) */
+    double xc[3];
+    for (int r = 0; r < 3; ++r) xc[r] = Wc[r][0] * muw[0] + Wc[r][1] * muw[1] + Wc[r][2] * muw[2] + tc[r];
+    const double z = xc[2];
+    o[F_Z64] = z; o[F_XC] = xc[0]; o[F_YC] = xc[1];
+    o[F_U] = fx * xc[0] / z + cx;
+    o[F_V] = fy * xc[1] / z + cy;
+    double txz = xc[0] / z, tyz = xc[1] / z;
+    if (txz < -limx) txz = -limx;
+    if (txz > limx) txz = limx;
+    if (tyz < -limy) tyz = -limy;
+    if (tyz > limy) tyz = limy;
+    const double tx = z * txz, ty = z * tyz;
+    const double J[2][3] = {{fx / z, 0.0, -fx * tx / (z * z)}, {0.0, fy / z, -fy * ty / (z * z)}};
+    double WcT[3][3], Sc[3][3];
+    matmul3(Wc, Sw, T1);
+    transpose3(Wc, WcT);
+    matmul3(T1, WcT, Sc);
+    double S2d[2][2];
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        double s = 0;
+        for (int p = 0; p < 3; ++p)
+          for (int q = 0; q < 3; ++q) s += J[a][p] * Sc[p][q] * J[b][q];
+        S2d[a][b] = s;
+      }
+    S2d[0][0] += 0.3;
+    S2d[1][1] += 0.3;
+    const double det = S2d[0][0] * S2d[1][1] - S2d[0][1] * S2d[1][0];
+    o[F_SXX] = S2d[0][0]; o[F_SXY] = S2d[0][1]; o[F_SYY] = S2d[1][1];
+    o[F_A] = S2d[1][1] / det;
+    o[F_B] = -S2d[0][1] / det;
+    o[F_C] = S2d[0][0] / det;
+    o[F_KAPPA] = 2.0 * log(255.0 * (double)opac[i]);
+
+    /* step 5: colour, body-frame view direction (R18, R19) */
+    double cb[3];
+    for (int c = 0; c < 3; ++c) {
+      /* c_body = R(q_k)^T (c_world - t_k) */
+      cb[c] = Rk[0][c] * (cw[0] - tk[0]) + Rk[1][c] * (cw[1] - tk[1]) + Rk[2][c] * (cw[2] - tk[2]);
+    }
+    double d[3] = {mu[0] - cb[0], mu[1] - cb[1], mu[2] - cb[2]};
+    double dn = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    d[0] /= dn; d[1] /= dn; d[2] /= dn;
+    double Y[16];
+    gsbo_sh_basis(sh_degree, d[0], d[1], d[2], Y);
+    const int ncoef = (sh_degree + 1) * (sh_degree + 1);
+    for (int ch = 0; ch < 3; ++ch) {
+      double s = 0;
+      for (int j = 0; j < ncoef; ++j) s += Y[j] * (double)sh[(i * ncoef_scene + j) * 3 + ch];
+      s += 0.5;
+      o[F_R + ch] = s > 0 ? s : 0.0;
+    }
+  }
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------------
+ * Step 7 (+8, +9): composite a list of pixels over the depth-ordered Gaussians.
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+  const double* proj;
+  const uint32_t* order;
+  int64_t n_order;
+  const int32_t* px;
+  const int32_t* py;
+  int64_t p0, p1;
+  double bg[3];
+  int mode; /* 0 = pure brute force, 1 = box accelerated (R8) */
+  double delta_alpha, delta_T, cmax, zmax;
+  double* out_rgb;
+  double* out_depth;
+  double* out_alpha;
+  int64_t* out_term_id;
+  int64_t* out_n_eval;
+  double* out_budget_rgb;
+  double* out_budget_depth;
+} comp_job;
+
+static void composite_pixel(const comp_job* jb, int64_t p) {
+  const double pxc = (double)jb->px[p] + 0.5, pyc = (double)jb->py[p] + 0.5; /* R3 */
+  double T = 1.0, C[3] = {0, 0, 0}, D = 0.0;
+  double brgb = 0.0, bdep = 0.0;
+  int64_t term = -1, n_eval = 0;
+  const double thr = 1.0 / 255.0;
+  for (int64_t j = 0; j < jb->n_order; ++j) {
+    const uint32_t i = jb->order[j];
+    const double* g = jb->proj + (int64_t)i * GSBO_NF;
+    if (jb->mode == 1) { /* R8: exact bounding box of {alpha >= 1/255} */
+      const double rx = sqrt(g[F_KAPPA] * g[F_SXX]), ry = sqrt(g[F_KAPPA] * g[F_SYY]);
+      if (pxc < g[F_U] - rx || pxc > g[F_U] + rx || pyc < g[F_V] - ry || pyc > g[F_V] + ry) continue;
+    }
+    n_eval++;
+    const double dx = g[F_U] - pxc, dy = g[F_V] - pyc;
+    const double power = -0.5 * (g[F_A] * dx * dx + g[F_C] * dy * dy) - g[F_B] * dx * dy; /* R12 */
+    if (power > 0.0) continue;
+    const double araw = g[F_O] * exp(power);
+    /* R28: skip-threshold flip budget (effect of blending vs skipping this entry) */
+    if (fabs(araw - thr) <= jb->delta_alpha * thr) {
+      brgb += T * thr * (1.0 + jb->delta_alpha) * jb->cmax;
+      bdep += T * thr * (1.0 + jb->delta_alpha) * jb->zmax;
+    }
+    const double alpha = araw < 0.99 ? araw : 0.99;
+    if (alpha < thr) continue;
+    const double tT = T * (1.0 - alpha); /* R13 */
+    /* R28: termination flip budget (stop vs continue at this entry) */
+    if (fabs(tT - 1e-4) <= jb->delta_T * 1e-4) {
+      brgb += T * 2.0 * jb->cmax;
+      bdep += T * jb->zmax;
+    }
+    if (tT < 1e-4) {
+      term = (int64_t)i;
+      break;
+    }
+    const double w = alpha * T; /* R14 */
+    C[0] += w * g[F_R];
+    C[1] += w * g[F_G];
+    C[2] += w * g[F_BL];
+    D += w * g[F_Z32];
+    T = tT;
+  }
+  for (int c = 0; c < 3; ++c) jb->out_rgb[p * 3 + c] = C[c] + T * jb->bg[c];
+  jb->out_depth[p] = D;          /* R16 */
+  jb->out_alpha[p] = 1.0 - T;
+  jb->out_term_id[p] = term;
+  jb->out_n_eval[p] = n_eval;
+  jb->out_budget_rgb[p] = brgb;
+  jb->out_budget_depth[p] = bdep;
+}
+
+static void* composite_worker(void* arg) {
+  const comp_job* jb = (const comp_job*)arg;
+  for (int64_t p = jb->p0; p < jb->p1; ++p) composite_pixel(jb, p);
+  return NULL;
+}
+
+int gsbo_composite(const double* proj, const uint32_t* order, int64_t n_order, const int32_t* px,
+                   const int32_t* py, int64_t npix, const float* bg, int mode, double delta_alpha,
+                   double delta_T, double cmax, double zmax, double* out_rgb, double* out_depth,
+                   double* out_alpha, int64_t* out_term_id, int64_t* out_n_eval,
+                   double* out_budget_rgb, double* out_budget_depth, int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  if ((int64_t)nthreads > npix) nthreads = npix > 0 ? (int)npix : 1;
+  comp_job jobs[256];
+  pthread_t th[256];
+  for (int t = 0; t < nthreads; ++t) {
+    comp_job* jb = &jobs[t];
+    jb->proj = proj; jb->order = order; jb->n_order = n_order;
+    jb->px = px; jb->py = py;
+    jb->p0 = npix * t / nthreads;
+    jb->p1 = npix * (t + 1) / nthreads;
+    for (int c = 0; c < 3; ++c) jb->bg[c] = bg[c];
+    jb->mode = mode;
+    jb->delta_alpha = delta_alpha; jb->delta_T = delta_T; jb->cmax = cmax; jb->zmax = zmax;
+    jb->out_rgb = out_rgb; jb->out_depth = out_depth; jb->out_alpha = out_alpha;
+    jb->out_term_id = out_term_id; jb->out_n_eval = out_n_eval;
+    jb->out_budget_rgb = out_budget_rgb; jb->out_budget_depth = out_budget_depth;
+  }
+  if (nthreads == 1) {
+    composite_worker(&jobs[0]);
+    return 0;
+  }
+  for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, composite_worker, &jobs[t]);
+  for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+  return 0;
+}
+
+/* correctly rounded binary32 fma — exported to pin the numpy emulation */
+float gsbo_fmaf(float a, float b, float c) { return fmaf(a, b, c); }
