@@ -1,0 +1,186 @@
+/*
+ * gsb.h — C ABI of libgsb, a B200-native (sm_100a) batched 3D Gaussian Splatting renderer:
+ * the data-parallel hot path of GS-Playground (arXiv 2604.25459).
+ *
+ * The operation (PAPER.md, cited by line "P:n"; readings R1-R28 in DESIGN.md §2):
+ *   * one Gaussian TEMPLATE is uploaded once (App. B.2; Alg. 1 l.2-7);
+ *   * every step, batch body states S_t in R^{B x N_bodies x 7} arrive (Alg. 1 l.9,
+ *     P:726); each Gaussian i attached to body k moves rigidly (RLGK, Eqs.):
+ *         p_world = R(q_k) p_local + t_k ,   q_world = q_k (x) q_local;
+ *   * each env's cameras (per-env intrinsics/extrinsics, domain-randomised) render
+ *     RGB images and depth maps with the 3DGS rasteriser the paper builds on
+ *     ("BatchSplat" P:139): EWA projection + SH colour, 16x16 tile binning,
+ *     a (tile, depth, id) sort, and front-to-back alpha compositing with alpha clamped at
+ *     0.99, alpha < 1/255 skipped, termination when T(1-alpha) < 1e-4 (north_star).
+ *
+ * Conventions (DESIGN.md readings):
+ *   R2  pinhole, (fx, fy, cx, cy) in pixels; world_to_cam = [R | t] row-major 3x4, OpenCV
+ *       axes (x right, y down, z forward); depth = camera z of the mean.
+ *   R3  pixel (px, py) has centre (px + 0.5, py + 0.5).
+ *   R17 outputs fp32, planar: rgb [B][C][3][H][W]; depth/alpha/n_eval [B][C][H][W].
+ *   R21 body indices are 0-based, -1 = static world Gaussian.
+ *   R22 pose vector = (tx, ty, tz, qw, qx, qy, qz), world <- body, scalar-first Hamilton
+ *       quaternion used as given (unit assumed).
+ *   R24 template parameters are ACTIVATED values: linear scales > 0, opacity in (0, 1];
+ *       template quaternions are normalised by gsb_create_scene.
+ *
+ * Errors: every entry point returns gsb_status (0 = OK).  Arguments are validated on the
+ * host before anything is enqueued; on failure nothing is enqueued and gsb_last_error()
+ * returns a thread-local message.  CUDA launch errors return GSB_ERR_CUDA; device faults
+ * surface at the caller's next synchronisation.  Non-finite poses/cameras are not errors:
+ * the affected Gaussians fail the cull tests deterministically.
+ *
+ * Threading: one scene is used by one host thread and one stream at a time.
+ * Determinism: for fixed inputs the outputs are bit-identical across runs, chunk sizes,
+ * batch sizes and env slicing (every env-camera frame is computed independently).
+ */
+#ifndef GSB_H_
+#define GSB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gsb_scene_t* gsb_scene; /* opaque, bound to one CUDA device */
+typedef struct CUstream_st* gsb_stream; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  GSB_OK = 0,
+  GSB_ERR_INVALID_ARGUMENT = 1,
+  GSB_ERR_SHAPE_MISMATCH = 2, /* cf. SPEC S:661 ShapeMismatch */
+  GSB_ERR_UNKNOWN_BODY = 3,   /* cf. SPEC S:652 UnknownBody: body_id outside [-1, n_bodies) */
+  GSB_ERR_OUT_OF_MEMORY = 4,
+  GSB_ERR_CAPACITY = 5,       /* N >= 2^32, render larger than the reservation, or one
+                                 frame's tile keys exceed the key workspace */
+  GSB_ERR_CUDA = 6,
+  GSB_ERR_DEVICE = 7          /* device is not sm_100 (B200) */
+} gsb_status;
+
+/* render flags */
+#define GSB_FLAG_STATS 1u   /* count V (visible pairs), K (tile keys), P (pixel-Gaussian
+                               evaluations) for gsb_get_stats */
+#define GSB_FLAG_TIMING 2u  /* record CUDA events around every kernel class on the render
+                               stream for gsb_get_timings */
+
+/* reserve flags */
+#define GSB_RESERVE_HOST_IO 1u /* also reserve device staging for gsb_render_host */
+
+typedef struct {
+  int32_t width, height;   /* image size in pixels, 1..4096 each */
+  float near_plane;        /* keep near < z <= far (reading R4); default 0.01 */
+  float far_plane;         /* default 1000 */
+  float background[3];     /* RGB added with weight T (R15); contributes 0 to depth */
+  int32_t sh_degree;       /* SH degree used, 0..scene degree; -1 = the scene's degree */
+  uint32_t flags;          /* GSB_FLAG_* */
+} gsb_render_params;
+
+/* Create a scene template on CUDA device `device` (all pointers HOST, read during the call):
+ *   means     [N,3] metres — body-local if body_id >= 0, world if body_id == -1
+ *   scales    [N,3] linear sigma > 0 (metres)
+ *   quats     [N,4] (w,x,y,z), any non-zero norm (normalised here)
+ *   opacities [N]   in (0,1]; Gaussians with o < 1/255 are never visible (reading R5)
+ *   sh        [N,(D+1)^2,3] coefficient-major (coefficient j, channel c at [(i*(D+1)^2+j)*3+c])
+ *   sh_degree D in 0..3
+ *   body_id   [N] int32 in [-1, n_bodies)
+ * N may be 0 (renders the background).  Ownership: the scene owns device copies.
+ * Errors: INVALID_ARGUMENT (null pointer, bad degree, non-positive scale, opacity outside
+ * (0,1], zero quaternion, non-finite value), UNKNOWN_BODY, CAPACITY (N >= 2^32),
+ * DEVICE, OUT_OF_MEMORY, CUDA. */
+gsb_status gsb_create_scene(const float* means, const float* scales, const float* quats,
+                            const float* opacities, const float* sh, int32_t sh_degree,
+                            const int32_t* body_id, int64_t n_gaussians, int32_t n_bodies,
+                            int32_t device, gsb_scene* out);
+
+/* Size the device workspace for renders of up to max_envs envs x n_cams cameras at
+ * width x height (allocations happen here, never in gsb_render).  chunk_frames = number of
+ * env-camera frames processed per pipeline chunk (0 = automatic).  key_capacity = tile keys
+ * held per chunk (0 = automatic); a chunk whose keys exceed it is split by frames, a single
+ * frame exceeding it fails with GSB_ERR_CAPACITY.  flags: GSB_RESERVE_HOST_IO. */
+gsb_status gsb_reserve(gsb_scene scene, int32_t max_envs, int32_t n_cams, int32_t width,
+                       int32_t height, int32_t chunk_frames, int64_t key_capacity,
+                       uint32_t flags);
+
+/* Render every env-camera frame f = e*C + c (ALL pointers DEVICE, on the scene's device):
+ *   body_poses   [B, n_bodies, 7] fp32 (R22); may be NULL iff n_bodies == 0
+ *   intrinsics   [B, C, 4] fp32 (fx, fy, cx, cy) pixels
+ *   world_to_cam [B, C, 3, 4] fp32 row-major [R | t], OpenCV axes
+ *   out_rgb      [B, C, 3, H, W] fp32  C + T * background            (required)
+ *   out_depth    [B, C, H, W] fp32     sum_i w_i z_i  (R16)          (nullable)
+ *   out_alpha    [B, C, H, W] fp32     1 - T                         (nullable)
+ *   out_n_eval   [B, C, H, W] int32    tile-list entries evaluated up to and including the
+ *                                      termination entry (list length if none)  (nullable)
+ * Work is enqueued on `stream`; the host may block until the last chunk's projection has
+ * finished (per-chunk key-count readback that sizes the binning).
+ * Outputs are fully overwritten.  Caller keeps every buffer alive until `stream` completes.
+ * Errors: INVALID_ARGUMENT, SHAPE_MISMATCH (B*C or W,H beyond the reservation, C != the
+ * reserved camera count is allowed if B*C fits), CAPACITY, CUDA. */
+gsb_status gsb_render(gsb_scene scene, const float* body_poses, int32_t n_envs, int32_t n_cams,
+                      const float* intrinsics, const float* world_to_cam,
+                      const gsb_render_params* params, float* out_rgb, float* out_depth,
+                      float* out_alpha, int32_t* out_n_eval, gsb_stream stream);
+
+/* Same operation with HOST buffers (inputs read, outputs written; pinned memory recommended):
+ * uploads the inputs, renders, and downloads rgb (+depth/alpha/n_eval when non-NULL), with
+ * the downloads of one chunk overlapping the rendering of the next.  Synchronous: returns
+ * when the outputs are in host memory.  Requires gsb_reserve(..., GSB_RESERVE_HOST_IO). */
+gsb_status gsb_render_host(gsb_scene scene, const float* body_poses, int32_t n_envs,
+                           int32_t n_cams, const float* intrinsics, const float* world_to_cam,
+                           const gsb_render_params* params, float* out_rgb, float* out_depth,
+                           float* out_alpha, int32_t* out_n_eval, gsb_stream stream);
+
+/* Counters of the last render made with GSB_FLAG_STATS (synchronises with it). */
+gsb_status gsb_get_stats(gsb_scene scene, int64_t* visible_V, int64_t* keys_K, int64_t* pairs_P);
+
+/* Per-kernel-class device time of the last render made with GSB_FLAG_TIMING, in ms
+ * (synchronises with it), and the number of kernels libgsb launched in that render. */
+typedef struct {
+  double setup_ms;     /* K0: per-(frame, body) RLGK transforms */
+  double project_ms;   /* K1: fused pose + projection + 2D covariance + SH, tile histogram */
+  double scan_ms;      /* K2a: per-frame tile offsets */
+  double emit_ms;      /* K2b: key emission */
+  double sort_ms;      /* K3: segmented radix sort */
+  double composite_ms; /* K4: per-tile compositing */
+  int64_t launches;    /* kernels launched by libgsb in the last render */
+  int64_t composite_launches;
+  int64_t chunks;
+} gsb_timings;
+gsb_status gsb_get_timings(gsb_scene scene, gsb_timings* out);
+
+gsb_status gsb_destroy_scene(gsb_scene scene);
+
+/* Thread-local message for the last non-OK status (never NULL). */
+const char* gsb_last_error(void);
+
+/* Library version string, e.g. "gsb 0.1 sm_100a". */
+const char* gsb_version(void);
+
+/* ------------------------------------------------------------------ test-only entry points */
+
+/* K1 projection only, dense per (frame, Gaussian) (DEVICE pointers, same inputs as gsb_render):
+ *   out_rec   [F, N, 12] fp32: u, v, conic a, b, c, opacity, r, g, b, z, Sigma2D_xx, Sigma2D_yy
+ *   out_zbits [F, N] uint32  bits of the fp32 depth key (reading R11)
+ *   out_valid [F, N] uint8   near < z <= far and o >= 1/255 (R4, R5)
+ * Requires the same reservation as gsb_render for B*C frames. */
+gsb_status gsb_debug_project(gsb_scene scene, const float* body_poses, int32_t n_envs,
+                             int32_t n_cams, const float* intrinsics, const float* world_to_cam,
+                             const gsb_render_params* params, float* out_rec, uint32_t* out_zbits,
+                             uint8_t* out_valid, gsb_stream stream);
+
+/* K2 + K3 on externally supplied projections (the ORACLE's values rounded to fp32), all
+ * [F, N] DEVICE arrays: u, v, Sigma2D_xx, Sigma2D_yy, kappa = 2 ln(255 o), zbits, valid.
+ * Computes tile rects by reading R9, bins, sorts every (frame, tile) list by (zbits, id)
+ * (reading R10) and writes out_tile_offsets [F, T_t + 1] (DEVICE, int64, absolute positions
+ * in out_ids) and out_ids [cap] (DEVICE uint32).  *out_K (HOST) receives the total.
+ * Allocates its own scratch (test-only).  CAPACITY if the total exceeds cap. */
+gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, const float* syy,
+                              const float* kappa, const uint32_t* zbits, const uint8_t* valid,
+                              int32_t n_frames, int64_t n_gaussians, int32_t width, int32_t height,
+                              int64_t* out_tile_offsets, uint32_t* out_ids, int64_t cap,
+                              int64_t* out_K, gsb_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSB_H_ */

@@ -1,0 +1,234 @@
+"""paper_2604_25459_b200 — thin Python binding of libgsb (include/gsb.h).
+
+Argument marshalling only: every step of the render runs in libgsb's sm_100a kernels.
+PyTorch supplies device memory and streams (tensor.data_ptr(), current_stream().cuda_stream).
+There is no CPU fallback: importing works everywhere, but any call needs libgsb.so built
+for sm_100a and a B200; a missing library raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgsb.so")
+
+GSB_FLAG_STATS = 1
+GSB_FLAG_TIMING = 2
+GSB_RESERVE_HOST_IO = 1
+
+STATUS = {0: "GSB_OK", 1: "GSB_ERR_INVALID_ARGUMENT", 2: "GSB_ERR_SHAPE_MISMATCH",
+          3: "GSB_ERR_UNKNOWN_BODY", 4: "GSB_ERR_OUT_OF_MEMORY", 5: "GSB_ERR_CAPACITY",
+          6: "GSB_ERR_CUDA", 7: "GSB_ERR_DEVICE"}
+
+# every symbol include/gsb.h declares
+EXPORTS = ["gsb_create_scene", "gsb_reserve", "gsb_render", "gsb_render_host", "gsb_get_stats",
+           "gsb_get_timings", "gsb_destroy_scene", "gsb_last_error", "gsb_version",
+           "gsb_debug_project", "gsb_debug_bin_sort"]
+
+
+class GsbError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class gsb_render_params(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32), ("near_plane", ctypes.c_float),
+                ("far_plane", ctypes.c_float), ("background", ctypes.c_float * 3),
+                ("sh_degree", ctypes.c_int32), ("flags", ctypes.c_uint32)]
+
+
+class gsb_timings(ctypes.Structure):
+    _fields_ = [("setup_ms", ctypes.c_double), ("project_ms", ctypes.c_double), ("scan_ms", ctypes.c_double),
+                ("emit_ms", ctypes.c_double), ("sort_ms", ctypes.c_double), ("composite_ms", ctypes.c_double),
+                ("launches", ctypes.c_int64), ("composite_launches", ctypes.c_int64), ("chunks", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libgsb.so (built by paper_2604_25459_b200/build.py).  Fails loudly if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libgsb.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, U32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32
+    L.gsb_create_scene.argtypes = [P, P, P, P, P, I32, P, I64, I32, I32, ctypes.POINTER(P)]
+    L.gsb_reserve.argtypes = [P, I32, I32, I32, I32, I32, I64, U32]
+    rp = ctypes.POINTER(gsb_render_params)
+    L.gsb_render.argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P, P]
+    L.gsb_render_host.argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P, P]
+    L.gsb_get_stats.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]
+    L.gsb_get_timings.argtypes = [P, ctypes.POINTER(gsb_timings)]
+    L.gsb_destroy_scene.argtypes = [P]
+    L.gsb_last_error.restype = ctypes.c_char_p
+    L.gsb_version.restype = ctypes.c_char_p
+    L.gsb_debug_project.argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P]
+    L.gsb_debug_bin_sort.argtypes = [P, P, P, P, P, P, P, I32, I64, I32, I32, P, P, I64,
+                                     ctypes.POINTER(I64), P]
+    for name in EXPORTS:
+        if name not in ("gsb_last_error", "gsb_version"):
+            getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        raise GsbError(status, lib().gsb_last_error().decode())
+
+
+def _ptr(t) -> Optional[int]:
+    """Device pointer of a CUDA tensor (or None)."""
+    if t is None:
+        return None
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return t.data_ptr()
+
+
+def _hptr(a) -> Optional[int]:
+    """Host pointer of a numpy array or a CPU tensor."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags.c_contiguous:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data
+    if a.is_cuda or not a.is_contiguous():
+        raise ValueError("expected a contiguous host tensor")
+    return a.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+@dataclass
+class RenderParams:
+    width: int
+    height: int
+    near: float = 0.01
+    far: float = 1000.0
+    background: Sequence[float] = (0.0, 0.0, 0.0)
+    sh_degree: int = -1
+    stats: bool = False
+    timing: bool = False
+
+    def to_c(self) -> gsb_render_params:
+        p = gsb_render_params()
+        p.width, p.height, p.near_plane, p.far_plane = self.width, self.height, self.near, self.far
+        for k in range(3):
+            p.background[k] = float(self.background[k])
+        p.sh_degree = self.sh_degree
+        p.flags = (GSB_FLAG_STATS if self.stats else 0) | (GSB_FLAG_TIMING if self.timing else 0)
+        return p
+
+
+class Scene:
+    """A scene template on one device (gsb_create_scene) with its reserved workspace."""
+
+    def __init__(self, means, scales, quats, opacities, sh, sh_degree: int, body_id, n_bodies: int,
+                 device: int = 0):
+        L = lib()
+        self._keep = [np.ascontiguousarray(means, np.float32), np.ascontiguousarray(scales, np.float32),
+                      np.ascontiguousarray(quats, np.float32), np.ascontiguousarray(opacities, np.float32),
+                      np.ascontiguousarray(sh, np.float32), np.ascontiguousarray(body_id, np.int32)]
+        m, s, q, o, c, b = self._keep
+        self.n = int(m.shape[0])
+        self.n_bodies = int(n_bodies)
+        self.sh_degree = int(sh_degree)
+        self.device = device
+        h = ctypes.c_void_p()
+        _check(L.gsb_create_scene(m.ctypes.data, s.ctypes.data, q.ctypes.data, o.ctypes.data, c.ctypes.data,
+                                  int(sh_degree), b.ctypes.data, self.n, self.n_bodies, int(device),
+                                  ctypes.byref(h)))
+        self._h = h
+        self._keep = None
+
+    @classmethod
+    def from_synth(cls, scene, device: int = 0) -> "Scene":
+        return cls(scene.means, scene.scales, scene.quats, scene.opacities, scene.sh, scene.sh_degree,
+                   scene.body_id, scene.n_bodies, device)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().gsb_destroy_scene(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reserve(self, max_envs: int, n_cams: int, width: int, height: int, chunk_frames: int = 0,
+                key_capacity: int = 0, host_io: bool = False):
+        _check(lib().gsb_reserve(self._h, max_envs, n_cams, width, height, chunk_frames, key_capacity,
+                                 GSB_RESERVE_HOST_IO if host_io else 0))
+
+    def render(self, poses, intrinsics, world_to_cam, params: RenderParams, out_rgb, out_depth=None,
+               out_alpha=None, out_n_eval=None, stream=None):
+        """gsb_render on CUDA tensors: poses [B,nb,7], intrinsics [B,C,4], world_to_cam [B,C,3,4],
+        out_rgb [B,C,3,H,W] (float32), out_depth/out_alpha [B,C,H,W] float32, out_n_eval int32."""
+        B, C = int(intrinsics.shape[0]), int(intrinsics.shape[1])
+        p = params.to_c()
+        _check(lib().gsb_render(self._h, _ptr(poses) if self.n_bodies else None, B, C, _ptr(intrinsics),
+                                _ptr(world_to_cam), ctypes.byref(p), _ptr(out_rgb), _ptr(out_depth),
+                                _ptr(out_alpha), _ptr(out_n_eval), _stream(stream)))
+
+    def render_host(self, poses, intrinsics, world_to_cam, params: RenderParams, out_rgb, out_depth=None,
+                    out_alpha=None, out_n_eval=None, stream=None):
+        """gsb_render_host on host (pinned) buffers; synchronous."""
+        B, C = int(intrinsics.shape[0]), int(intrinsics.shape[1])
+        p = params.to_c()
+        _check(lib().gsb_render_host(self._h, _hptr(poses) if self.n_bodies else None, B, C,
+                                     _hptr(intrinsics), _hptr(world_to_cam), ctypes.byref(p), _hptr(out_rgb),
+                                     _hptr(out_depth), _hptr(out_alpha), _hptr(out_n_eval), _stream(stream)))
+
+    def stats(self):
+        V, K, P = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().gsb_get_stats(self._h, ctypes.byref(V), ctypes.byref(K), ctypes.byref(P)))
+        return {"V": V.value, "K": K.value, "P": P.value}
+
+    def timings(self):
+        t = gsb_timings()
+        _check(lib().gsb_get_timings(self._h, ctypes.byref(t)))
+        return {k: getattr(t, k) for k, _ in gsb_timings._fields_}
+
+    def debug_project(self, poses, intrinsics, world_to_cam, params: RenderParams, out_rec, out_zbits,
+                      out_valid, stream=None):
+        B, C = int(intrinsics.shape[0]), int(intrinsics.shape[1])
+        p = params.to_c()
+        _check(lib().gsb_debug_project(self._h, _ptr(poses) if self.n_bodies else None, B, C, _ptr(intrinsics),
+                                       _ptr(world_to_cam), ctypes.byref(p), _ptr(out_rec), _ptr(out_zbits),
+                                       _ptr(out_valid), _stream(stream)))
+
+
+def debug_bin_sort(u, v, sxx, syy, kappa, zbits, valid, width: int, height: int, cap: int, stream=None):
+    """gsb_debug_bin_sort on CUDA tensors [F,N]; returns (offsets [F,T+1] int64, ids[:K] uint32 as int64)."""
+    import torch
+    F, N = int(u.shape[0]), int(u.shape[1])
+    T = ((width + 15) // 16) * ((height + 15) // 16)
+    dev = u.device
+    offs = torch.empty((F, T + 1), dtype=torch.int64, device=dev)
+    ids = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    K = ctypes.c_int64()
+    _check(lib().gsb_debug_bin_sort(_ptr(u), _ptr(v), _ptr(sxx), _ptr(syy), _ptr(kappa), _ptr(zbits), _ptr(valid),
+                                    F, N, width, height, _ptr(offs), _ptr(ids), cap, ctypes.byref(K), _stream(stream)))
+    return offs, ids[:K.value]
+
+
+def version() -> str:
+    return lib().gsb_version().decode()

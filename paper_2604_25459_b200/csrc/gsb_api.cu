@@ -1,0 +1,697 @@
+// gsb_api.cu — libgsb host runtime: the C ABI of include/gsb.h.
+//
+// Owns the scene template (K5: one read-only copy shared by every env), the reserved
+// workspace, and the chunked render pipeline:
+//
+//   K0 setup (all frames) ;  for each chunk c of E frames (double-buffered slot c&1):
+//     K1 project(c) -> records + tile histogram ; K2a scan(c) ; D2H frame key counts (event)
+//     [host waits for chunk c-1's counts — the GPU is busy with chunk c meanwhile]
+//     K2b emit(c-1) ; K3 sort(c-1) ; K4 composite(c-1)   (split by frames if keys > capacity)
+//
+// No allocation happens in gsb_render; all buffers are sized by gsb_reserve.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gsb.h"
+#include "gsb_common.cuh"
+#include "gsb_kernels.cuh"
+
+using namespace gsb;
+
+namespace {
+
+thread_local std::string g_err = "no error";
+
+gsb_status fail(gsb_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(e_ == cudaErrorMemoryAllocation ? GSB_ERR_OUT_OF_MEMORY : GSB_ERR_CUDA, \
+                  "%s failed: %s", #expr, cudaGetErrorString(e_));                      \
+  } while (0)
+
+#define LAUNCH_CHECK()                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess) return fail(GSB_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e_)); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) return cudaSuccess;
+  return cudaMalloc((void**)p, count * sizeof(T));
+}
+
+enum KClass { KC_SETUP = 0, KC_PROJECT, KC_SCAN, KC_EMIT, KC_SORT, KC_COMPOSITE, KC_N };
+
+}  // namespace
+
+struct gsb_scene_t {
+  int device = 0;
+  int64_t n = 0;
+  int n_bodies = 0;
+  int sh_degree = 0;
+  int sh_planes = 1;
+  // template (K5)
+  float4 *d_mean = nullptr, *d_L0 = nullptr, *d_L1 = nullptr, *d_L2 = nullptr, *d_sh = nullptr;
+  // reservation
+  bool reserved = false;
+  int max_frames = 0, res_w = 0, res_h = 0, chunk = 0;
+  int tiles_x = 0, tiles_y = 0, n_tiles = 0;
+  int64_t hist_stride = 0;
+  int64_t cap = 0;
+  float4* table = nullptr;
+  FrameCam* cams = nullptr;
+  float4* rec[2] = {nullptr, nullptr};
+  int* vcount[2] = {nullptr, nullptr};
+  int* hist[2] = {nullptr, nullptr};
+  uint32_t* off[2] = {nullptr, nullptr};
+  uint64_t* frame_base[2] = {nullptr, nullptr};
+  uint64_t* h_fb[2] = {nullptr, nullptr};   // pinned
+  int* h_vc[2] = {nullptr, nullptr};        // pinned
+  cudaEvent_t ev_counts[2] = {nullptr, nullptr};
+  uint64_t *keys = nullptr, *keys_alt = nullptr;
+  uint32_t* sorted = nullptr;
+  unsigned long long* d_pairs = nullptr;
+  // host-io staging
+  bool host_io = false;
+  int max_envs = 0, res_cams = 0;
+  float *st_poses = nullptr, *st_intr = nullptr, *st_w2c = nullptr;
+  float *st_rgb = nullptr, *st_depth = nullptr, *st_alpha = nullptr;
+  int32_t* st_neval = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copy = nullptr;
+  // last-render bookkeeping
+  cudaStream_t last_stream = nullptr;
+  bool stats_valid = false;
+  int64_t stat_V = 0, stat_K = 0;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<std::pair<int, size_t>> ev_marks;  // (class, index of begin event)
+  bool timing_valid = false;
+  int64_t launches = 0, comp_launches = 0, chunks = 0;
+  // host-io: where to download outputs of each pass
+  float *dl_rgb = nullptr, *dl_depth = nullptr, *dl_alpha = nullptr;
+  int32_t* dl_neval = nullptr;
+
+  void free_workspace() {
+    cudaFree(table); cudaFree(cams);
+    for (int s = 0; s < 2; ++s) {
+      cudaFree(rec[s]); cudaFree(vcount[s]); cudaFree(hist[s]); cudaFree(off[s]);
+      cudaFree(frame_base[s]);
+      if (h_fb[s]) cudaFreeHost(h_fb[s]);
+      if (h_vc[s]) cudaFreeHost(h_vc[s]);
+      if (ev_counts[s]) cudaEventDestroy(ev_counts[s]);
+      rec[s] = nullptr; vcount[s] = nullptr; hist[s] = nullptr; off[s] = nullptr;
+      frame_base[s] = nullptr; h_fb[s] = nullptr; h_vc[s] = nullptr; ev_counts[s] = nullptr;
+    }
+    cudaFree(keys); cudaFree(keys_alt); cudaFree(sorted); cudaFree(d_pairs);
+    cudaFree(st_poses); cudaFree(st_intr); cudaFree(st_w2c);
+    cudaFree(st_rgb); cudaFree(st_depth); cudaFree(st_alpha); cudaFree(st_neval);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (ev_copy) cudaEventDestroy(ev_copy);
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    ev_pool.clear();
+    table = nullptr; cams = nullptr; keys = keys_alt = nullptr; sorted = nullptr; d_pairs = nullptr;
+    st_poses = st_intr = st_w2c = st_rgb = st_depth = st_alpha = nullptr; st_neval = nullptr;
+    copy_stream = nullptr; ev_copy = nullptr;
+    reserved = false;
+  }
+};
+
+namespace {
+
+bool finite_all(const float* p, int64_t n) {
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(p[i])) return false;
+  return true;
+}
+
+gsb_status check_device(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    return fail(GSB_ERR_DEVICE, "no CUDA device visible");
+  if (device < 0 || device >= count) return fail(GSB_ERR_INVALID_ARGUMENT, "device %d out of range", device);
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(GSB_ERR_DEVICE, "device %d is sm_%d%d, libgsb needs sm_100", device, prop.major, prop.minor);
+  return GSB_OK;
+}
+
+// timing helpers
+struct Timer {
+  gsb_scene_t* s;
+  cudaStream_t st;
+  bool on;
+  size_t begin_idx = 0;
+  int cls = 0;
+  void begin(int c) {
+    if (!on) return;
+    if (s->ev_used + 2 > s->ev_pool.size()) { on = false; return; }
+    cls = c;
+    begin_idx = s->ev_used;
+    cudaEventRecord(s->ev_pool[s->ev_used++], st);
+  }
+  void end() {
+    if (!on) return;
+    cudaEventRecord(s->ev_pool[s->ev_used++], st);
+    s->ev_marks.push_back({cls, begin_idx});
+  }
+};
+
+gsb_status validate_render(gsb_scene s, const float* poses, int n_envs, int n_cams, const float* intr,
+                           const float* w2c, const gsb_render_params* p, const float* out_rgb) {
+  if (!s) return fail(GSB_ERR_INVALID_ARGUMENT, "scene is NULL");
+  if (!s->reserved) return fail(GSB_ERR_INVALID_ARGUMENT, "gsb_reserve was not called");
+  if (!p) return fail(GSB_ERR_INVALID_ARGUMENT, "params is NULL");
+  if (n_envs < 0 || n_cams < 1) return fail(GSB_ERR_INVALID_ARGUMENT, "n_envs=%d n_cams=%d", n_envs, n_cams);
+  const int64_t F = (int64_t)n_envs * n_cams;
+  if (F > s->max_frames)
+    return fail(GSB_ERR_SHAPE_MISMATCH, "%lld frames exceed the reservation (%d)", (long long)F, s->max_frames);
+  if (p->width < 1 || p->height < 1 || p->width > s->res_w || p->height > s->res_h)
+    return fail(GSB_ERR_SHAPE_MISMATCH, "image %dx%d outside the reservation %dx%d", p->width, p->height, s->res_w, s->res_h);
+  if (!(p->near_plane > 0.f) || !(p->far_plane > p->near_plane))
+    return fail(GSB_ERR_INVALID_ARGUMENT, "need 0 < near < far");
+  if (p->sh_degree > s->sh_degree || p->sh_degree < -1)
+    return fail(GSB_ERR_INVALID_ARGUMENT, "sh_degree %d not in [-1, %d]", p->sh_degree, s->sh_degree);
+  if (F > 0) {
+    if (!intr || !w2c || !out_rgb) return fail(GSB_ERR_INVALID_ARGUMENT, "NULL intrinsics/world_to_cam/out_rgb");
+    if (s->n_bodies > 0 && !poses) return fail(GSB_ERR_INVALID_ARGUMENT, "body_poses is NULL but the scene has bodies");
+  }
+  return GSB_OK;
+}
+
+struct Pipeline {
+  gsb_scene_t* s;
+  cudaStream_t st;
+  const gsb_render_params* p;
+  int F, W, H, tiles_x, n_tiles, D;
+  Timer tm;
+  float* out_rgb;
+  float* out_depth;
+  float* out_alpha;
+  int32_t* out_neval;
+
+  gsb_status project_chunk(int c, int f0, int nf) {
+    const int sl = c & 1;
+    CUDA_TRY(cudaMemsetAsync(s->vcount[sl], 0, sizeof(int) * nf, st));
+    CUDA_TRY(cudaMemsetAsync(s->hist[sl], 0, sizeof(int) * s->hist_stride * nf, st));
+    K1Args a{};
+    a.g_mean = s->d_mean; a.g_L0 = s->d_L0; a.g_L1 = s->d_L1; a.g_L2 = s->d_L2; a.g_sh = s->d_sh;
+    a.n = s->n; a.table = s->table; a.cams = s->cams; a.nb1 = s->n_bodies + 1;
+    a.f0 = f0; a.n_frames = nf; a.width = W; a.height = H; a.tiles_x = tiles_x;
+    a.near_plane = p->near_plane; a.far_plane = p->far_plane;
+    a.rec = s->rec[sl]; a.vcount = s->vcount[sl]; a.hist = s->hist[sl]; a.hist_stride = s->hist_stride;
+    tm.begin(KC_PROJECT);
+    launch_k1(a, D, st);
+    if (s->n > 0) s->launches++;
+    LAUNCH_CHECK();
+    tm.end();
+    tm.begin(KC_SCAN);
+    launch_k2_scan(s->hist[sl], s->off[sl], s->hist_stride, nf, n_tiles, s->frame_base[sl], st);
+    s->launches += 2;
+    LAUNCH_CHECK();
+    tm.end();
+    CUDA_TRY(cudaMemcpyAsync(s->h_fb[sl], s->frame_base[sl], sizeof(uint64_t) * (nf + 1), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(s->h_vc[sl], s->vcount[sl], sizeof(int) * nf, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(s->ev_counts[sl], st));
+    return GSB_OK;
+  }
+
+  gsb_status pass(int sl, int f0, int fs, int fe, uint64_t key_base) {
+    ChunkArgs a{};
+    a.rec = s->rec[sl]; a.n = s->n; a.vcount = s->vcount[sl]; a.hist = s->hist[sl];
+    a.hist_stride = s->hist_stride; a.off = s->off[sl]; a.frame_base = s->frame_base[sl];
+    a.n_tiles = n_tiles; a.tiles_x = tiles_x; a.fs = fs; a.fe = fe; a.key_base = key_base;
+    a.keys = s->keys; a.keys_alt = s->keys_alt; a.sorted = s->sorted;
+    tm.begin(KC_EMIT);
+    launch_k2_emit(a, st);
+    if (s->n > 0) s->launches++;
+    LAUNCH_CHECK();
+    tm.end();
+    tm.begin(KC_SORT);
+    launch_k3_sort(a, st);
+    s->launches++;
+    LAUNCH_CHECK();
+    tm.end();
+    CompositeArgs c{};
+    c.rec = s->rec[sl]; c.n = s->n; c.off = s->off[sl]; c.frame_base = s->frame_base[sl];
+    c.hist_stride = s->hist_stride; c.sorted = s->sorted; c.key_base = key_base;
+    c.fs = fs; c.fe = fe; c.f0 = f0; c.width = W; c.height = H; c.tiles_x = tiles_x; c.n_tiles = n_tiles;
+    c.bg0 = p->background[0]; c.bg1 = p->background[1]; c.bg2 = p->background[2];
+    c.out_rgb = out_rgb; c.out_depth = out_depth; c.out_alpha = out_alpha; c.out_n_eval = out_neval;
+    c.stat_pairs = (p->flags & GSB_FLAG_STATS) ? s->d_pairs : nullptr;
+    tm.begin(KC_COMPOSITE);
+    launch_k4_composite(c, st);
+    s->launches++;
+    s->comp_launches++;
+    LAUNCH_CHECK();
+    tm.end();
+    if (s->dl_rgb) {  // host-io: download this pass's frames on the copy stream
+      CUDA_TRY(cudaEventRecord(s->ev_copy, st));
+      CUDA_TRY(cudaStreamWaitEvent(s->copy_stream, s->ev_copy, 0));
+      const size_t plane = (size_t)W * H;
+      const size_t a0 = (size_t)(f0 + fs), cnt = (size_t)(fe - fs);
+      CUDA_TRY(cudaMemcpyAsync(s->dl_rgb + a0 * 3 * plane, out_rgb + a0 * 3 * plane, cnt * 3 * plane * 4,
+                               cudaMemcpyDeviceToHost, s->copy_stream));
+      if (s->dl_depth)
+        CUDA_TRY(cudaMemcpyAsync(s->dl_depth + a0 * plane, out_depth + a0 * plane, cnt * plane * 4,
+                                 cudaMemcpyDeviceToHost, s->copy_stream));
+      if (s->dl_alpha)
+        CUDA_TRY(cudaMemcpyAsync(s->dl_alpha + a0 * plane, out_alpha + a0 * plane, cnt * plane * 4,
+                                 cudaMemcpyDeviceToHost, s->copy_stream));
+      if (s->dl_neval)
+        CUDA_TRY(cudaMemcpyAsync(s->dl_neval + a0 * plane, out_neval + a0 * plane, cnt * plane * 4,
+                                 cudaMemcpyDeviceToHost, s->copy_stream));
+    }
+    return GSB_OK;
+  }
+
+  gsb_status finish_chunk(int c, int f0, int nf) {
+    const int sl = c & 1;
+    CUDA_TRY(cudaEventSynchronize(s->ev_counts[sl]));
+    const uint64_t* fb = s->h_fb[sl];
+    for (int i = 0; i < nf; ++i) s->stat_V += s->h_vc[sl][i];
+    s->stat_K += (int64_t)fb[nf];
+    s->chunks++;
+    if (fb[nf] <= (uint64_t)s->cap) return pass(sl, f0, 0, nf, 0);
+    // split the chunk's frames into passes that fit the key workspace
+    int fs = 0;
+    while (fs < nf) {
+      int fe = fs;
+      while (fe < nf && fb[fe + 1] - fb[fs] <= (uint64_t)s->cap) ++fe;
+      if (fe == fs)
+        return fail(GSB_ERR_CAPACITY, "frame %d needs %llu tile keys > key capacity %lld", f0 + fs,
+                    (unsigned long long)(fb[fs + 1] - fb[fs]), (long long)s->cap);
+      gsb_status r = pass(sl, f0, fs, fe, fb[fs]);
+      if (r != GSB_OK) return r;
+      fs = fe;
+    }
+    return GSB_OK;
+  }
+
+  gsb_status run(const float* poses, const float* intr, const float* w2c, int n_cams) {
+    tm.begin(KC_SETUP);
+    launch_k0(poses, intr, w2c, F, n_cams, s->n_bodies, W, H, s->table, s->cams, st);
+    s->launches++;
+    LAUNCH_CHECK();
+    tm.end();
+    const int E = s->chunk;
+    const int nchunks = (F + E - 1) / E;
+    for (int c = 0; c < nchunks; ++c) {
+      const int f0 = c * E, nf = std::min(E, F - f0);
+      gsb_status r = project_chunk(c, f0, nf);
+      if (r != GSB_OK) return r;
+      if (c > 0) {
+        r = finish_chunk(c - 1, (c - 1) * E, E);
+        if (r != GSB_OK) return r;
+      }
+    }
+    if (nchunks > 0) {
+      const int c = nchunks - 1;
+      return finish_chunk(c, c * E, F - c * E);
+    }
+    return GSB_OK;
+  }
+};
+
+gsb_status render_impl(gsb_scene s, const float* poses, int n_envs, int n_cams, const float* intr,
+                       const float* w2c, const gsb_render_params* p, float* out_rgb, float* out_depth,
+                       float* out_alpha, int32_t* out_neval, cudaStream_t st) {
+  const int F = n_envs * n_cams;
+  s->last_stream = st;
+  s->stat_V = s->stat_K = 0;
+  s->launches = s->comp_launches = s->chunks = 0;
+  s->ev_used = 0;
+  s->ev_marks.clear();
+  const bool timing = (p->flags & GSB_FLAG_TIMING) != 0;
+  if (timing && s->ev_pool.empty()) {
+    s->ev_pool.resize(8192);
+    for (auto& e : s->ev_pool) CUDA_TRY(cudaEventCreate(&e));
+  }
+  if (p->flags & GSB_FLAG_STATS) CUDA_TRY(cudaMemsetAsync(s->d_pairs, 0, sizeof(unsigned long long), st));
+  Pipeline pl{};
+  pl.s = s; pl.st = st; pl.p = p; pl.F = F; pl.W = p->width; pl.H = p->height;
+  pl.tiles_x = (p->width + kTile - 1) / kTile;
+  pl.n_tiles = pl.tiles_x * ((p->height + kTile - 1) / kTile);
+  pl.D = p->sh_degree < 0 ? s->sh_degree : p->sh_degree;
+  pl.tm = Timer{s, st, timing};
+  pl.out_rgb = out_rgb; pl.out_depth = out_depth; pl.out_alpha = out_alpha; pl.out_neval = out_neval;
+  gsb_status r = pl.run(poses, intr, w2c, n_cams);
+  s->stats_valid = (r == GSB_OK) && (p->flags & GSB_FLAG_STATS);
+  s->timing_valid = (r == GSB_OK) && timing;
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gsb_last_error(void) { return g_err.c_str(); }
+
+const char* gsb_version(void) { return "gsb 0.1 sm_100a"; }
+
+gsb_status gsb_create_scene(const float* means, const float* scales, const float* quats,
+                            const float* opacities, const float* sh, int32_t sh_degree,
+                            const int32_t* body_id, int64_t n, int32_t n_bodies, int32_t device,
+                            gsb_scene* out) {
+  if (!out) return fail(GSB_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (n < 0) return fail(GSB_ERR_INVALID_ARGUMENT, "n_gaussians < 0");
+  if (n >= (int64_t)1 << 31) return fail(GSB_ERR_CAPACITY, "n_gaussians >= 2^31");
+  if (sh_degree < 0 || sh_degree > 3) return fail(GSB_ERR_INVALID_ARGUMENT, "sh_degree %d not in 0..3", sh_degree);
+  if (n_bodies < 0) return fail(GSB_ERR_INVALID_ARGUMENT, "n_bodies < 0");
+  if (n > 0 && (!means || !scales || !quats || !opacities || !sh || !body_id))
+    return fail(GSB_ERR_INVALID_ARGUMENT, "NULL template pointer");
+  const int nc = (sh_degree + 1) * (sh_degree + 1);
+  if (!finite_all(means, 3 * n) || !finite_all(scales, 3 * n) || !finite_all(quats, 4 * n) ||
+      !finite_all(opacities, n) || !finite_all(sh, 3 * nc * n))
+    return fail(GSB_ERR_INVALID_ARGUMENT, "non-finite template value");
+  gsb_status st = check_device(device);
+  if (st != GSB_OK) return st;
+  const int np = (3 * nc + 3) / 4;
+  std::vector<float4> hm(n), h0(n), h1(n), h2(n), hs((size_t)np * n);
+  for (int64_t i = 0; i < n; ++i) {
+    const int b = body_id[i];
+    if (b < -1 || b >= n_bodies) return fail(GSB_ERR_UNKNOWN_BODY, "body_id[%lld] = %d not in [-1, %d)", (long long)i, b, n_bodies);
+    const double o = opacities[i];
+    if (!(o > 0.0 && o <= 1.0)) return fail(GSB_ERR_INVALID_ARGUMENT, "opacity[%lld] = %g not in (0,1]", (long long)i, o);
+    double q[4] = {quats[4 * i], quats[4 * i + 1], quats[4 * i + 2], quats[4 * i + 3]};
+    const double qn = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    if (!(qn > 0)) return fail(GSB_ERR_INVALID_ARGUMENT, "quaternion %lld has zero norm", (long long)i);
+    for (double& c : q) c /= qn;
+    const double w = q[0], x = q[1], y = q[2], z = q[3];
+    const double R[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
+                            {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
+                            {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)}};
+    double s3[3];
+    for (int c = 0; c < 3; ++c) {
+      s3[c] = scales[3 * i + c];
+      if (!(s3[c] > 0)) return fail(GSB_ERR_INVALID_ARGUMENT, "scale[%lld] not > 0", (long long)i);
+    }
+    float L[9];
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) L[r * 3 + c] = (float)(R[r][c] * s3[c]);
+    int bb = b;
+    float bf;
+    std::memcpy(&bf, &bb, 4);
+    hm[i] = make_float4(means[3 * i], means[3 * i + 1], means[3 * i + 2], bf);
+    h0[i] = make_float4(L[0], L[1], L[2], L[3]);
+    h1[i] = make_float4(L[4], L[5], L[6], L[7]);
+    h2[i] = make_float4(L[8], opacities[i], (float)(2.0 * std::log(255.0 * o)), (float)std::log2(o));
+    for (int pl = 0; pl < np; ++pl) {
+      float v4[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int k = 0; k < 4; ++k) {
+        const int fidx = 4 * pl + k;
+        if (fidx < 3 * nc) v4[k] = sh[(size_t)i * 3 * nc + fidx];
+      }
+      hs[(size_t)pl * n + i] = make_float4(v4[0], v4[1], v4[2], v4[3]);
+    }
+  }
+  DeviceGuard g(device);
+  gsb_scene_t* s = new gsb_scene_t();
+  s->device = device; s->n = n; s->n_bodies = n_bodies; s->sh_degree = sh_degree; s->sh_planes = np;
+  auto up = [&](float4** d, const std::vector<float4>& h) -> cudaError_t {
+    cudaError_t e = dalloc(d, h.size());
+    if (e != cudaSuccess) return e;
+    if (h.empty()) return cudaSuccess;
+    return cudaMemcpy(*d, h.data(), h.size() * sizeof(float4), cudaMemcpyHostToDevice);
+  };
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = up(&s->d_mean, hm);
+  if (e == cudaSuccess) e = up(&s->d_L0, h0);
+  if (e == cudaSuccess) e = up(&s->d_L1, h1);
+  if (e == cudaSuccess) e = up(&s->d_L2, h2);
+  if (e == cudaSuccess) e = up(&s->d_sh, hs);
+  if (e != cudaSuccess) {
+    gsb_destroy_scene(s);
+    return fail(e == cudaErrorMemoryAllocation ? GSB_ERR_OUT_OF_MEMORY : GSB_ERR_CUDA, "upload: %s", cudaGetErrorString(e));
+  }
+  *out = s;
+  return GSB_OK;
+}
+
+gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t width, int32_t height,
+                       int32_t chunk_frames, int64_t key_capacity, uint32_t flags) {
+  if (!s) return fail(GSB_ERR_INVALID_ARGUMENT, "scene is NULL");
+  if (max_envs < 1 || n_cams < 1) return fail(GSB_ERR_INVALID_ARGUMENT, "max_envs/n_cams < 1");
+  if (width < 1 || height < 1 || width > kMaxDim || height > kMaxDim)
+    return fail(GSB_ERR_INVALID_ARGUMENT, "image %dx%d outside 1..%d", width, height, kMaxDim);
+  if (chunk_frames < 0 || key_capacity < 0) return fail(GSB_ERR_INVALID_ARGUMENT, "negative chunk/capacity");
+  const int64_t F = (int64_t)max_envs * n_cams;
+  if (F > (1 << 30)) return fail(GSB_ERR_CAPACITY, "too many frames");
+  DeviceGuard g(s->device);
+  cudaDeviceSynchronize();
+  s->free_workspace();
+  s->max_frames = (int)F; s->res_w = width; s->res_h = height;
+  s->max_envs = max_envs; s->res_cams = n_cams;
+  s->tiles_x = (width + kTile - 1) / kTile;
+  s->tiles_y = (height + kTile - 1) / kTile;
+  s->n_tiles = s->tiles_x * s->tiles_y;
+  s->hist_stride = ((int64_t)s->n_tiles + 1 + 31) / 32 * 32;
+  const int E = chunk_frames > 0 ? std::min<int64_t>(chunk_frames, F) : (int)std::min<int64_t>(64, F);
+  s->chunk = E;
+  int64_t cap = key_capacity;
+  if (cap == 0) cap = std::max<int64_t>((int64_t)1 << 22, std::min<int64_t>(3 * (int64_t)E * std::max<int64_t>(s->n, 1), ((int64_t)1 << 32) - 1));
+  s->cap = cap;
+  const int nb1 = s->n_bodies + 1;
+  CUDA_TRY(dalloc(&s->table, (size_t)F * nb1 * 4));
+  CUDA_TRY(dalloc(&s->cams, (size_t)F));
+  for (int sl = 0; sl < 2; ++sl) {
+    CUDA_TRY(dalloc(&s->rec[sl], (size_t)E * std::max<int64_t>(s->n, 1) * 3));
+    CUDA_TRY(dalloc(&s->vcount[sl], (size_t)E));
+    CUDA_TRY(dalloc(&s->hist[sl], (size_t)E * s->hist_stride));
+    CUDA_TRY(dalloc(&s->off[sl], (size_t)E * s->hist_stride));
+    CUDA_TRY(dalloc(&s->frame_base[sl], (size_t)E + 1));
+    CUDA_TRY(cudaMallocHost((void**)&s->h_fb[sl], sizeof(uint64_t) * (E + 1)));
+    CUDA_TRY(cudaMallocHost((void**)&s->h_vc[sl], sizeof(int) * E));
+    CUDA_TRY(cudaEventCreateWithFlags(&s->ev_counts[sl], cudaEventDisableTiming));
+  }
+  CUDA_TRY(dalloc(&s->keys, (size_t)cap));
+  CUDA_TRY(dalloc(&s->keys_alt, (size_t)cap));
+  CUDA_TRY(dalloc(&s->sorted, (size_t)cap));
+  CUDA_TRY(dalloc(&s->d_pairs, 1));
+  s->host_io = (flags & GSB_RESERVE_HOST_IO) != 0;
+  if (s->host_io) {
+    const size_t plane = (size_t)width * height;
+    CUDA_TRY(dalloc(&s->st_poses, (size_t)max_envs * std::max(s->n_bodies, 1) * 7));
+    CUDA_TRY(dalloc(&s->st_intr, (size_t)F * 4));
+    CUDA_TRY(dalloc(&s->st_w2c, (size_t)F * 12));
+    CUDA_TRY(dalloc(&s->st_rgb, (size_t)F * 3 * plane));
+    CUDA_TRY(dalloc(&s->st_depth, (size_t)F * plane));
+    CUDA_TRY(dalloc(&s->st_alpha, (size_t)F * plane));
+    CUDA_TRY(dalloc(&s->st_neval, (size_t)F * plane));
+    CUDA_TRY(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&s->ev_copy, cudaEventDisableTiming));
+  }
+  s->reserved = true;
+  return GSB_OK;
+}
+
+gsb_status gsb_render(gsb_scene s, const float* poses, int32_t n_envs, int32_t n_cams, const float* intr,
+                      const float* w2c, const gsb_render_params* p, float* out_rgb, float* out_depth,
+                      float* out_alpha, int32_t* out_neval, gsb_stream stream) {
+  gsb_status r = validate_render(s, poses, n_envs, n_cams, intr, w2c, p, out_rgb);
+  if (r != GSB_OK) return r;
+  DeviceGuard g(s->device);
+  s->dl_rgb = nullptr; s->dl_depth = nullptr; s->dl_alpha = nullptr; s->dl_neval = nullptr;
+  return render_impl(s, poses, n_envs, n_cams, intr, w2c, p, out_rgb, out_depth, out_alpha, out_neval,
+                     (cudaStream_t)stream);
+}
+
+gsb_status gsb_render_host(gsb_scene s, const float* poses, int32_t n_envs, int32_t n_cams,
+                           const float* intr, const float* w2c, const gsb_render_params* p,
+                           float* out_rgb, float* out_depth, float* out_alpha, int32_t* out_neval,
+                           gsb_stream stream) {
+  gsb_status r = validate_render(s, poses, n_envs, n_cams, intr, w2c, p, out_rgb);
+  if (r != GSB_OK) return r;
+  if (!s->host_io) return fail(GSB_ERR_INVALID_ARGUMENT, "reserve with GSB_RESERVE_HOST_IO for gsb_render_host");
+  if (n_envs > s->max_envs) return fail(GSB_ERR_SHAPE_MISMATCH, "n_envs beyond the host-io reservation");
+  DeviceGuard g(s->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t F = (size_t)n_envs * n_cams;
+  if (s->n_bodies > 0 && n_envs > 0)
+    CUDA_TRY(cudaMemcpyAsync(s->st_poses, poses, sizeof(float) * (size_t)n_envs * s->n_bodies * 7, cudaMemcpyHostToDevice, st));
+  if (F > 0) {
+    CUDA_TRY(cudaMemcpyAsync(s->st_intr, intr, sizeof(float) * F * 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(s->st_w2c, w2c, sizeof(float) * F * 12, cudaMemcpyHostToDevice, st));
+  }
+  s->dl_rgb = out_rgb; s->dl_depth = out_depth; s->dl_alpha = out_alpha; s->dl_neval = out_neval;
+  r = render_impl(s, s->st_poses, n_envs, n_cams, s->st_intr, s->st_w2c, p, s->st_rgb,
+                  out_depth ? s->st_depth : nullptr, out_alpha ? s->st_alpha : nullptr,
+                  out_neval ? s->st_neval : nullptr, st);
+  s->dl_rgb = nullptr; s->dl_depth = nullptr; s->dl_alpha = nullptr; s->dl_neval = nullptr;
+  if (r != GSB_OK) return r;
+  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaStreamSynchronize(s->copy_stream));
+  return GSB_OK;
+}
+
+gsb_status gsb_get_stats(gsb_scene s, int64_t* V, int64_t* K, int64_t* P) {
+  if (!s) return fail(GSB_ERR_INVALID_ARGUMENT, "scene is NULL");
+  if (!s->stats_valid) return fail(GSB_ERR_INVALID_ARGUMENT, "last render had no GSB_FLAG_STATS");
+  DeviceGuard g(s->device);
+  CUDA_TRY(cudaStreamSynchronize(s->last_stream));
+  unsigned long long pairs = 0;
+  CUDA_TRY(cudaMemcpy(&pairs, s->d_pairs, sizeof(pairs), cudaMemcpyDeviceToHost));
+  if (V) *V = s->stat_V;
+  if (K) *K = s->stat_K;
+  if (P) *P = (int64_t)pairs;
+  return GSB_OK;
+}
+
+gsb_status gsb_get_timings(gsb_scene s, gsb_timings* out) {
+  if (!s || !out) return fail(GSB_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!s->timing_valid) return fail(GSB_ERR_INVALID_ARGUMENT, "last render had no GSB_FLAG_TIMING");
+  DeviceGuard g(s->device);
+  CUDA_TRY(cudaStreamSynchronize(s->last_stream));
+  double ms[KC_N] = {0};
+  for (auto& m : s->ev_marks) {
+    float t = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&t, s->ev_pool[m.second], s->ev_pool[m.second + 1]));
+    ms[m.first] += t;
+  }
+  out->setup_ms = ms[KC_SETUP]; out->project_ms = ms[KC_PROJECT]; out->scan_ms = ms[KC_SCAN];
+  out->emit_ms = ms[KC_EMIT]; out->sort_ms = ms[KC_SORT]; out->composite_ms = ms[KC_COMPOSITE];
+  out->launches = s->launches; out->composite_launches = s->comp_launches; out->chunks = s->chunks;
+  return GSB_OK;
+}
+
+gsb_status gsb_destroy_scene(gsb_scene s) {
+  if (!s) return GSB_OK;
+  DeviceGuard g(s->device);
+  cudaDeviceSynchronize();
+  s->free_workspace();
+  cudaFree(s->d_mean); cudaFree(s->d_L0); cudaFree(s->d_L1); cudaFree(s->d_L2); cudaFree(s->d_sh);
+  delete s;
+  return GSB_OK;
+}
+
+gsb_status gsb_debug_project(gsb_scene s, const float* poses, int32_t n_envs, int32_t n_cams,
+                             const float* intr, const float* w2c, const gsb_render_params* p,
+                             float* out_rec, uint32_t* out_zbits, uint8_t* out_valid, gsb_stream stream) {
+  gsb_status r = validate_render(s, poses, n_envs, n_cams, intr, w2c, p, out_rec);
+  if (r != GSB_OK) return r;
+  if (!out_zbits || !out_valid) return fail(GSB_ERR_INVALID_ARGUMENT, "NULL debug output");
+  DeviceGuard g(s->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int F = n_envs * n_cams;
+  launch_k0(poses, intr, w2c, F, n_cams, s->n_bodies, p->width, p->height, s->table, s->cams, st);
+  LAUNCH_CHECK();
+  K1Args a{};
+  a.g_mean = s->d_mean; a.g_L0 = s->d_L0; a.g_L1 = s->d_L1; a.g_L2 = s->d_L2; a.g_sh = s->d_sh;
+  a.n = s->n; a.table = s->table; a.cams = s->cams; a.nb1 = s->n_bodies + 1;
+  a.f0 = 0; a.n_frames = F; a.width = p->width; a.height = p->height;
+  a.tiles_x = (p->width + kTile - 1) / kTile;
+  a.near_plane = p->near_plane; a.far_plane = p->far_plane;
+  a.rec = nullptr;
+  a.dbg_rec = out_rec; a.dbg_zbits = out_zbits; a.dbg_valid = out_valid;
+  launch_k1(a, p->sh_degree < 0 ? s->sh_degree : p->sh_degree, st);
+  LAUNCH_CHECK();
+  return GSB_OK;
+}
+
+gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, const float* syy,
+                              const float* kappa, const uint32_t* zbits, const uint8_t* valid,
+                              int32_t F, int64_t n, int32_t width, int32_t height,
+                              int64_t* out_offsets, uint32_t* out_ids, int64_t cap, int64_t* out_K,
+                              gsb_stream stream) {
+  if (F < 1 || n < 0 || width < 1 || height < 1 || width > kMaxDim || height > kMaxDim || cap < 0 || !out_K ||
+      !out_offsets || (n > 0 && (!u || !v || !sxx || !syy || !kappa || !zbits || !valid)))
+    return fail(GSB_ERR_INVALID_ARGUMENT, "bad debug_bin_sort arguments");
+  if (n >= (int64_t)1 << 31) return fail(GSB_ERR_CAPACITY, "n >= 2^31");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int tiles_x = (width + kTile - 1) / kTile;
+  const int n_tiles = tiles_x * ((height + kTile - 1) / kTile);
+  const int64_t stride = ((int64_t)n_tiles + 1 + 31) / 32 * 32;
+  float4* rec = nullptr; int* vcount = nullptr; int* hist = nullptr; uint32_t* off = nullptr;
+  uint64_t* fbase = nullptr; uint64_t* keys = nullptr; uint64_t* keys_alt = nullptr; uint32_t* sorted = nullptr;
+  gsb_status result = GSB_OK;
+  auto cleanup = [&]() {
+    cudaFree(rec); cudaFree(vcount); cudaFree(hist); cudaFree(off); cudaFree(fbase);
+    cudaFree(keys); cudaFree(keys_alt); cudaFree(sorted);
+  };
+#define DBG_TRY(expr)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (expr);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      cleanup();                                                                   \
+      return fail(GSB_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_));          \
+    }                                                                              \
+  } while (0)
+  DBG_TRY(dalloc(&rec, (size_t)F * std::max<int64_t>(n, 1) * 3));
+  DBG_TRY(dalloc(&vcount, (size_t)F));
+  DBG_TRY(dalloc(&hist, (size_t)F * stride));
+  DBG_TRY(dalloc(&off, (size_t)F * stride));
+  DBG_TRY(dalloc(&fbase, (size_t)F + 1));
+  DBG_TRY(cudaMemsetAsync(vcount, 0, sizeof(int) * F, st));
+  DBG_TRY(cudaMemsetAsync(hist, 0, sizeof(int) * F * stride, st));
+  launch_k1_external(u, v, sxx, syy, kappa, zbits, valid, n, 0, F, width, height, tiles_x, rec, vcount,
+                     hist, stride, st);
+  launch_k2_scan(hist, off, stride, F, n_tiles, fbase, st);
+  DBG_TRY(cudaGetLastError());
+  std::vector<uint64_t> hfb(F + 1);
+  DBG_TRY(cudaMemcpyAsync(hfb.data(), fbase, sizeof(uint64_t) * (F + 1), cudaMemcpyDeviceToHost, st));
+  DBG_TRY(cudaStreamSynchronize(st));
+  const uint64_t K = hfb[F];
+  *out_K = (int64_t)K;
+  if (K > (uint64_t)cap) {
+    cleanup();
+    return fail(GSB_ERR_CAPACITY, "K = %llu exceeds cap %lld", (unsigned long long)K, (long long)cap);
+  }
+  DBG_TRY(dalloc(&keys, std::max<uint64_t>(K, 1)));
+  DBG_TRY(dalloc(&keys_alt, std::max<uint64_t>(K, 1)));
+  DBG_TRY(dalloc(&sorted, std::max<uint64_t>(K, 1)));
+  ChunkArgs a{};
+  a.rec = rec; a.n = n; a.vcount = vcount; a.hist = hist; a.hist_stride = stride; a.off = off;
+  a.frame_base = fbase; a.n_tiles = n_tiles; a.tiles_x = tiles_x; a.fs = 0; a.fe = F; a.key_base = 0;
+  a.keys = keys; a.keys_alt = keys_alt; a.sorted = sorted;
+  launch_k2_emit(a, st);
+  launch_k3_sort(a, st);
+  if (K > 0) launch_slots_to_ids(a, out_ids, K, st);
+  DBG_TRY(cudaGetLastError());
+  std::vector<uint32_t> hoff((size_t)F * stride);
+  DBG_TRY(cudaMemcpyAsync(hoff.data(), off, sizeof(uint32_t) * hoff.size(), cudaMemcpyDeviceToHost, st));
+  DBG_TRY(cudaStreamSynchronize(st));
+  std::vector<int64_t> ho((size_t)F * (n_tiles + 1));
+  for (int f = 0; f < F; ++f)
+    for (int t = 0; t <= n_tiles; ++t) ho[(size_t)f * (n_tiles + 1) + t] = (int64_t)hfb[f] + hoff[(size_t)f * stride + t];
+  DBG_TRY(cudaMemcpyAsync(out_offsets, ho.data(), sizeof(int64_t) * ho.size(), cudaMemcpyHostToDevice, st));
+  DBG_TRY(cudaStreamSynchronize(st));
+  cleanup();
+  return result;
+#undef DBG_TRY
+}
+
+}  // extern "C"

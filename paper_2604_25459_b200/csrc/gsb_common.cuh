@@ -1,0 +1,103 @@
+// gsb_common.cuh — device-side data layout and exact-arithmetic helpers of libgsb.
+//
+// Shared by the kernels K0-K4 only (NOT by the CPU oracle, which is written independently).
+// Data layout in HBM:
+//   template (K5, read-only, shared by every env):  SoA float4 planes of N entries
+//     g_mean[N]  = (x, y, z, body as int bits; -2 = never visible (o < 1/255))
+//     g_L0[N]    = (L00, L01, L02, L10)   L = R(q_i) diag(s_i): Sigma_local = L L^T
+//     g_L1[N]    = (L11, L12, L20, L21)
+//     g_L2[N]    = (L22, opacity, kappa = 2 ln(255 o), log2 o)
+//     g_sh[P][N] = SH coefficients, P = ceil(3 (D+1)^2 / 4) float4 planes, coefficient-major
+//   per frame-body table (K0 -> K1): 4 float4 = M row 0 | m0, row 1 | m1, row 2 | m2, c_body
+//   compact projected record (K1 -> K2/K3/K4), 48 B:
+//     R0 = (u, v, p', q')          whitening factor of Sigma2D^-1 scaled by sqrt(log2(e)/2)
+//     R1 = (r', log2 o, z, id)     z = fp32 depth key (R11), id as int bits
+//     R2 = (r, g, b, rect)         rect = tx0 | tx1 << 8 | ty0 << 16 | ty1 << 24
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gsb {
+
+constexpr int kTile = 16;             // reading R9: tiles fixed at 16x16 pixels
+constexpr int kMaxDim = 4096;         // width, height <= 4096 -> tile coords fit in 8 bits
+constexpr float kAlphaMax = 0.99f;    // north_star: alpha clamped at 0.99
+constexpr float kTermT = 1e-4f;       // reading R13
+// log2(1/255): alpha >= 1/255  <=>  log2(o) - Q/2 * log2(e) >= log2(1/255)
+constexpr float kLog2AlphaMin = -7.99435343685885793f;
+constexpr int kBodyNever = -2;
+
+struct FrameCam {
+  float fx, fy, cx, cy;
+  float limx, limy;  // reading R6: 1.3 * W / (2 fx), 1.3 * H / (2 fy)
+  float pad0, pad1;
+};
+
+// ---------------------------------------------------------------- reading R11 (exact chain)
+// Each op is a separately rounded IEEE binary32 op; fmas are explicit.
+__device__ __forceinline__ void r11_rot(float qw, float qx, float qy, float qz, float R[3][3]) {
+  const float xx = __fmul_rn(qx, qx), yy = __fmul_rn(qy, qy), zz = __fmul_rn(qz, qz);
+  const float xy = __fmul_rn(qx, qy), xz = __fmul_rn(qx, qz), yz = __fmul_rn(qy, qz);
+  const float wx = __fmul_rn(qw, qx), wy = __fmul_rn(qw, qy), wz = __fmul_rn(qw, qz);
+  R[0][0] = __fsub_rn(1.0f, __fmul_rn(2.0f, __fadd_rn(yy, zz)));
+  R[0][1] = __fmul_rn(2.0f, __fsub_rn(xy, wz));
+  R[0][2] = __fmul_rn(2.0f, __fadd_rn(xz, wy));
+  R[1][0] = __fmul_rn(2.0f, __fadd_rn(xy, wz));
+  R[1][1] = __fsub_rn(1.0f, __fmul_rn(2.0f, __fadd_rn(xx, zz)));
+  R[1][2] = __fmul_rn(2.0f, __fsub_rn(yz, wx));
+  R[2][0] = __fmul_rn(2.0f, __fsub_rn(xz, wy));
+  R[2][1] = __fmul_rn(2.0f, __fadd_rn(yz, wx));
+  R[2][2] = __fsub_rn(1.0f, __fmul_rn(2.0f, __fadd_rn(xx, yy)));
+}
+
+__device__ __forceinline__ float r11_depth(float4 row2, float mx, float my, float mz) {
+  return __fmaf_rn(row2.x, mx, __fmaf_rn(row2.y, my, __fmaf_rn(row2.z, mz, row2.w)));
+}
+
+// ---------------------------------------------------------------- reading R9 (tile rect)
+// Returns false when culled.  Tile rect written as [tx0, tx1] x [ty0, ty1].
+__device__ __forceinline__ bool r9_rect(float u, float v, float sxx, float syy, float kappa,
+                                        int width, int height, int& tx0, int& tx1, int& ty0,
+                                        int& ty1) {
+  const float rx = __fsqrt_rn(__fmul_rn(kappa, sxx));
+  const float ry = __fsqrt_rn(__fmul_rn(kappa, syy));
+  const float xl = __fsub_rn(__fsub_rn(u, rx), 0.5f);
+  const float xh = __fsub_rn(__fadd_rn(u, rx), 0.5f);
+  const float yl = __fsub_rn(__fsub_rn(v, ry), 0.5f);
+  const float yh = __fsub_rn(__fadd_rn(v, ry), 0.5f);
+  if (!(isfinite(xl) && isfinite(xh) && isfinite(yl) && isfinite(yh))) return false;
+  const float pxl = fmaxf(ceilf(xl), 0.0f);
+  const float pxh = fminf(floorf(xh), (float)(width - 1));
+  const float pyl = fmaxf(ceilf(yl), 0.0f);
+  const float pyh = fminf(floorf(yh), (float)(height - 1));
+  if (!(pxl <= pxh) || !(pyl <= pyh)) return false;
+  tx0 = ((int)pxl) >> 4;
+  tx1 = ((int)pxh) >> 4;
+  ty0 = ((int)pyl) >> 4;
+  ty1 = ((int)pyh) >> 4;
+  return true;
+}
+
+__device__ __forceinline__ uint32_t pack_rect(int tx0, int tx1, int ty0, int ty1) {
+  return (uint32_t)tx0 | ((uint32_t)tx1 << 8) | ((uint32_t)ty0 << 16) | ((uint32_t)ty1 << 24);
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Warp-aggregated compaction: returns the slot of this lane (valid only if `take`).
+__device__ __forceinline__ int warp_compact_slot(bool take, int* counter) {
+  const unsigned mask = __ballot_sync(0xffffffffu, take);
+  if (mask == 0) return -1;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(mask) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(counter, __popc(mask));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return base + __popc(mask & lanemask_lt());
+}
+
+}  // namespace gsb

@@ -1,0 +1,91 @@
+// gsb_kernels.cuh — launch interface between the host runtime (gsb_api.cu) and K0-K4.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "gsb_common.cuh"
+
+namespace gsb {
+
+struct K1Args {
+  // template (K5: shared read-only buffer, one copy for every env)
+  const float4* g_mean;
+  const float4* g_L0;
+  const float4* g_L1;
+  const float4* g_L2;
+  const float4* g_sh;
+  int64_t n;
+  // per-frame transforms (K0)
+  const float4* table;
+  const FrameCam* cams;
+  int nb1;
+  // chunk
+  int f0;          // first frame of the chunk
+  int n_frames;    // E
+  int width, height, tiles_x;
+  float near_plane, far_plane;
+  // outputs
+  float4* rec;     // [E][N][3] compact records (slots), nullptr for debug-only launches
+  int* vcount;     // [E]
+  int* hist;       // [E][hist_stride]
+  int64_t hist_stride;
+  // debug (dense) outputs, nullptr unless gsb_debug_project
+  float* dbg_rec;
+  uint32_t* dbg_zbits;
+  uint8_t* dbg_valid;
+};
+
+struct ChunkArgs {
+  const float4* rec;      // [E][N][3]
+  int64_t n;              // record stride per frame (= N)
+  const int* vcount;      // [E]
+  int* hist;              // [E][hist_stride]  (counts; reused as emission cursors)
+  int64_t hist_stride;
+  uint32_t* off;          // [E][hist_stride] exclusive tile offsets within the frame, [T] = K_f
+  uint64_t* frame_base;   // [E+1] exclusive prefix of K_f over the chunk's frames
+  int n_tiles, tiles_x;
+  int fs, fe;             // frame range [fs, fe) of this pass (relative to the chunk)
+  uint64_t key_base;      // frame_base[fs]: keys of this pass start at key index 0
+  uint64_t* keys;         // [cap]   (zbits << 32) | slot
+  uint64_t* keys_alt;     // [cap]   scratch for oversize segments
+  uint32_t* sorted;       // [cap]   sorted slots
+};
+
+struct CompositeArgs {
+  const float4* rec;
+  int64_t n;
+  const uint32_t* off;
+  const uint64_t* frame_base;
+  int64_t hist_stride;
+  const uint32_t* sorted;
+  uint64_t key_base;
+  int fs, fe;             // relative frames of this pass
+  int f0;                 // absolute frame index of chunk frame 0
+  int width, height, tiles_x, n_tiles;
+  float bg0, bg1, bg2;
+  float* out_rgb;         // [F][3][H][W]
+  float* out_depth;       // [F][H][W] or nullptr
+  float* out_alpha;
+  int32_t* out_n_eval;
+  unsigned long long* stat_pairs;  // nullptr unless STATS
+};
+
+void launch_k0(const float* poses, const float* intr, const float* w2c, int n_frames, int n_cams,
+               int n_bodies, int width, int height, float4* table, FrameCam* cams,
+               cudaStream_t s);
+void launch_k1(const K1Args& a, int sh_degree, cudaStream_t s);
+
+// K1 variant for gsb_debug_bin_sort: records from externally supplied fp32 projections
+void launch_k1_external(const float* u, const float* v, const float* sxx, const float* syy,
+                        const float* kappa, const uint32_t* zbits, const uint8_t* valid,
+                        int64_t n, int f0, int n_frames, int width, int height, int tiles_x,
+                        float4* rec, int* vcount, int* hist, int64_t hist_stride, cudaStream_t s);
+
+void launch_k2_scan(int* hist, uint32_t* off, int64_t hist_stride, int n_frames, int n_tiles,
+                    uint64_t* frame_base, cudaStream_t s);
+void launch_k2_emit(const ChunkArgs& a, cudaStream_t s);
+void launch_k3_sort(const ChunkArgs& a, cudaStream_t s);
+void launch_k4_composite(const CompositeArgs& a, cudaStream_t s);
+void launch_slots_to_ids(const ChunkArgs& a, uint32_t* ids, uint64_t count, cudaStream_t s);
+
+}  // namespace gsb

@@ -1,0 +1,257 @@
+// k1_project.cu — K0 (per-(frame, body) RLGK transforms) and K1 (fused pose transform,
+// EWA projection, 2D covariance, SH colour, compaction and tile histogram).
+//
+// PAPER.md App. B.2: RLGK moves every Gaussian of body k by that env's pose,
+//   p_world = R(q_k) p_local + t_k, q_world = q_k (x) q_local  (Eqs.).
+// Alg. 1 materialises P_world, Q_world for all B x M Gaussians (l.12-15); here the
+// transform is folded into the camera transform per (frame, body) — K0 computes
+//   M = W_f R(q_k),  m = W_f t_k + t_f,  c_body = R(q_k)^T (c_f - t_k)
+// once per (frame, body), and K1 applies x_c = M mu_local + m per (frame, Gaussian), so the
+// B x M world state is never written (reading R20).  Sigma_world = R(q_k) Sigma_local R(q_k)^T
+// (reading R23) enters as the factor M L with Sigma_local = L L^T.
+//
+// K1 is Gaussian-major: one thread owns one template Gaussian (its parameters stay in
+// registers) and loops over the E frames of a chunk, so the shared read-only template (K5)
+// is read from HBM once per chunk, not once per frame.
+#include "gsb_common.cuh"
+#include "gsb_kernels.cuh"
+
+namespace gsb {
+
+// ------------------------------------------------------------------------------ K0
+__global__ void k0_setup(const float* __restrict__ poses, const float* __restrict__ intr,
+                         const float* __restrict__ w2c, int n_frames, int n_cams, int n_bodies,
+                         int width, int height, float4* __restrict__ table,
+                         FrameCam* __restrict__ cams) {
+  const int nb1 = n_bodies + 1;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_frames * nb1) return;
+  const int f = idx / nb1;
+  const int k = idx % nb1 - 1;
+  const int e = f / n_cams;
+  const float* W = w2c + (size_t)f * 12;
+  float R[3][3] = {{1.f, 0.f, 0.f}, {0.f, 1.f, 0.f}, {0.f, 0.f, 1.f}};
+  float t[3] = {0.f, 0.f, 0.f};
+  if (k >= 0) {
+    const float* p = poses + ((size_t)e * n_bodies + k) * 7;
+    r11_rot(p[3], p[4], p[5], p[6], R);
+    t[0] = p[0]; t[1] = p[1]; t[2] = p[2];
+  }
+  float M[3][3], m[3];
+  for (int r = 0; r < 2; ++r) {
+    for (int c = 0; c < 3; ++c)
+      M[r][c] = fmaf(W[r * 4 + 0], R[0][c], fmaf(W[r * 4 + 1], R[1][c], W[r * 4 + 2] * R[2][c]));
+    m[r] = fmaf(W[r * 4 + 0], t[0], fmaf(W[r * 4 + 1], t[1], fmaf(W[r * 4 + 2], t[2], W[r * 4 + 3])));
+  }
+  // depth row: exact chain, reading R11
+  if (k < 0) {
+    M[2][0] = W[8]; M[2][1] = W[9]; M[2][2] = W[10]; m[2] = W[11];
+  } else {
+    for (int c = 0; c < 3; ++c)
+      M[2][c] = __fmaf_rn(W[8], R[0][c], __fmaf_rn(W[9], R[1][c], __fmul_rn(W[10], R[2][c])));
+    m[2] = __fmaf_rn(W[8], t[0], __fmaf_rn(W[9], t[1], __fmaf_rn(W[10], t[2], W[11])));
+  }
+  // camera centre c_w = -W^T t_f, then into the body frame (reading R19)
+  float cw[3], cb[3];
+  for (int c = 0; c < 3; ++c) cw[c] = -(W[c] * W[3] + W[4 + c] * W[7] + W[8 + c] * W[11]);
+  for (int c = 0; c < 3; ++c)
+    cb[c] = R[0][c] * (cw[0] - t[0]) + R[1][c] * (cw[1] - t[1]) + R[2][c] * (cw[2] - t[2]);
+  float4* o = table + (size_t)idx * 4;
+  o[0] = make_float4(M[0][0], M[0][1], M[0][2], m[0]);
+  o[1] = make_float4(M[1][0], M[1][1], M[1][2], m[1]);
+  o[2] = make_float4(M[2][0], M[2][1], M[2][2], m[2]);
+  o[3] = make_float4(cb[0], cb[1], cb[2], 0.f);
+  if (k < 0) {
+    const float* K = intr + (size_t)f * 4;
+    FrameCam fc;
+    fc.fx = K[0]; fc.fy = K[1]; fc.cx = K[2]; fc.cy = K[3];
+    fc.limx = 1.3f * (float)width / (2.0f * K[0]);
+    fc.limy = 1.3f * (float)height / (2.0f * K[1]);
+    fc.pad0 = fc.pad1 = 0.f;
+    cams[f] = fc;
+  }
+}
+
+// ------------------------------------------------------------------------------ SH (R18)
+template <int D>
+__device__ __forceinline__ float3 sh_colour(const float4* __restrict__ g_sh, int64_t n, int64_t i,
+                                            float x, float y, float z) {
+  constexpr int NC = (D + 1) * (D + 1);
+  constexpr int NP = (3 * NC + 3) / 4;
+  float c[NP * 4];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const float4 q = __ldg(g_sh + (size_t)p * n + i);
+    c[4 * p + 0] = q.x; c[4 * p + 1] = q.y; c[4 * p + 2] = q.z; c[4 * p + 3] = q.w;
+  }
+  const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
+  float r = C0 * c[0], g = C0 * c[1], b = C0 * c[2];
+  if (D >= 1) {
+    const float y1 = -C1 * y, y2 = C1 * z, y3 = -C1 * x;
+    r += y1 * c[3] + y2 * c[6] + y3 * c[9];
+    g += y1 * c[4] + y2 * c[7] + y3 * c[10];
+    b += y1 * c[5] + y2 * c[8] + y3 * c[11];
+  }
+  if (D >= 2) {
+    const float xx = x * x, yy = y * y, zz = z * z;
+    const float Y[5] = {1.0925484305920792f * x * y, -1.0925484305920792f * y * z,
+                        0.31539156525252005f * (2.f * zz - xx - yy), -1.0925484305920792f * x * z,
+                        0.5462742152960396f * (xx - yy)};
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      r += Y[j] * c[3 * (4 + j) + 0];
+      g += Y[j] * c[3 * (4 + j) + 1];
+      b += Y[j] * c[3 * (4 + j) + 2];
+    }
+    if (D >= 3) {
+      const float Y3[7] = {-0.5900435899266435f * y * (3.f * xx - yy),
+                           2.890611442640554f * x * y * z,
+                           -0.4570457994644658f * y * (4.f * zz - xx - yy),
+                           0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy),
+                           -0.4570457994644658f * x * (4.f * zz - xx - yy),
+                           1.445305721320277f * z * (xx - yy),
+                           -0.5900435899266435f * x * (xx - 3.f * yy)};
+#pragma unroll
+      for (int j = 0; j < 7; ++j) {
+        r += Y3[j] * c[3 * (9 + j) + 0];
+        g += Y3[j] * c[3 * (9 + j) + 1];
+        b += Y3[j] * c[3 * (9 + j) + 2];
+      }
+    }
+  }
+  return make_float3(fmaxf(r + 0.5f, 0.f), fmaxf(g + 0.5f, 0.f), fmaxf(b + 0.5f, 0.f));
+}
+
+// accurate 2x2 determinant a*d - b*c (Kahan): error ~1.5 ulp of the result
+__device__ __forceinline__ float det2(float a, float b, float c, float d) {
+  const float w = b * c;
+  const float e = fmaf(-b, c, w);
+  const float f = fmaf(a, d, -w);
+  return f + e;
+}
+
+// ------------------------------------------------------------------------------ K1
+template <int D>
+__global__ void __launch_bounds__(128) k1_project(K1Args a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool in = i < a.n;
+  float4 mean = make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+  float4 l0 = make_float4(0.f, 0.f, 0.f, 0.f), l1 = l0, l2 = l0;
+  if (in) {
+    mean = __ldg(a.g_mean + i);
+    l0 = __ldg(a.g_L0 + i);
+    l1 = __ldg(a.g_L1 + i);
+    l2 = __ldg(a.g_L2 + i);
+  }
+  const int body = __float_as_int(mean.w);
+  const float L[3][3] = {{l0.x, l0.y, l0.z}, {l0.w, l1.x, l1.y}, {l1.z, l1.w, l2.x}};
+  const float opac = l2.y, kappa = l2.z, log2o = l2.w;
+  // reading R5: o < 1/255 is never visible (binary32 compare == the exact compare)
+  const bool o_ok = in && (opac >= 1.0f / 255.0f);
+  const bool debug = a.dbg_rec != nullptr;
+  const float wscale = 0.84932180028801904f;  // sqrt(log2(e) / 2)
+
+  for (int fl = 0; fl < a.n_frames; ++fl) {
+    const int f = a.f0 + fl;
+    const float4* tb = a.table + ((size_t)f * a.nb1 + (body + 1)) * 4;
+    const float4 r2 = __ldg(tb + 2);
+    const float z = r11_depth(r2, mean.x, mean.y, mean.z);   // exact fp32 key (R11)
+    const bool keep = o_ok && (z > a.near_plane) && (z <= a.far_plane);
+    bool vis = false;
+    float u = 0.f, v = 0.f, pw = 0.f, qw = 0.f, rw = 0.f;
+    float3 rgb = make_float3(0.f, 0.f, 0.f);
+    int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;
+    if (keep || (debug && in)) {
+      const float4 r0 = __ldg(tb + 0), r1 = __ldg(tb + 1);
+      const FrameCam cam = a.cams[f];
+      const float x = fmaf(r0.x, mean.x, fmaf(r0.y, mean.y, fmaf(r0.z, mean.z, r0.w)));
+      const float y = fmaf(r1.x, mean.x, fmaf(r1.y, mean.y, fmaf(r1.z, mean.z, r1.w)));
+      const float iz = 1.0f / z;
+      const float xz = x * iz, yz = y * iz;
+      u = fmaf(cam.fx, xz, cam.cx);
+      v = fmaf(cam.fy, yz, cam.cy);
+      // EWA Jacobian with the 1.3 frustum clamp (reading R6), applied to M: rows of J M
+      const float txz = fminf(fmaxf(xz, -cam.limx), cam.limx);
+      const float tyz = fminf(fmaxf(yz, -cam.limy), cam.limy);
+      const float jx = cam.fx * iz, jy = cam.fy * iz;
+      const float m0[3] = {jx * fmaf(-txz, r2.x, r0.x), jx * fmaf(-txz, r2.y, r0.y), jx * fmaf(-txz, r2.z, r0.z)};
+      const float m1[3] = {jy * fmaf(-tyz, r2.x, r1.x), jy * fmaf(-tyz, r2.y, r1.y), jy * fmaf(-tyz, r2.z, r1.z)};
+      // A = (J M) L (2x3); Sigma2D = A A^T + 0.3 I (reading R7)
+      float A0[3], A1[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        A0[c] = fmaf(m0[0], L[0][c], fmaf(m0[1], L[1][c], m0[2] * L[2][c]));
+        A1[c] = fmaf(m1[0], L[0][c], fmaf(m1[1], L[1][c], m1[2] * L[2][c]));
+      }
+      const float sxx0 = fmaf(A0[0], A0[0], fmaf(A0[1], A0[1], A0[2] * A0[2]));
+      const float syy0 = fmaf(A1[0], A1[0], fmaf(A1[1], A1[1], A1[2] * A1[2]));
+      const float sxy = fmaf(A0[0], A1[0], fmaf(A0[1], A1[1], A0[2] * A1[2]));
+      const float sxx = sxx0 + 0.3f, syy = syy0 + 0.3f;
+      // det(A A^T) by Cauchy-Binet (sum of squared 2x2 minors) + 0.3 tr + 0.09: no cancellation
+      const float n01 = det2(A0[0], A0[1], A1[0], A1[1]);
+      const float n02 = det2(A0[0], A0[2], A1[0], A1[2]);
+      const float n12 = det2(A0[1], A0[2], A1[1], A1[2]);
+      const float det = fmaf(n01, n01, fmaf(n02, n02, fmaf(n12, n12, fmaf(0.3f, sxx0 + syy0, 0.09f))));
+      // whitening (Cholesky) factor of Sigma2D^-1:  Q = (p dx)^2 + (q dx + r dy)^2
+      const float il11 = 1.0f / sqrtf(sxx);
+      const float r_ = 1.0f / sqrtf(det / sxx);
+      const float q_ = -sxy * il11 * il11 * r_;
+      pw = wscale * il11;
+      qw = wscale * q_;
+      rw = wscale * r_;
+      const bool rect_ok = r9_rect(u, v, sxx, syy, kappa, a.width, a.height, tx0, tx1, ty0, ty1);
+      vis = keep && rect_ok;
+      if (vis || debug) {
+        // view direction in the body frame (reading R19)
+        const float4 cb = __ldg(tb + 3);
+        const float dx = mean.x - cb.x, dy = mean.y - cb.y, dz = mean.z - cb.z;
+        const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
+        rgb = sh_colour<D>(a.g_sh, a.n, in ? i : 0, dx * inv, dy * inv, dz * inv);
+      }
+      if (debug && in) {
+        const size_t o = (size_t)f * a.n + i;
+        float* d = a.dbg_rec + o * 12;
+        const float idet = 1.0f / det;
+        d[0] = u; d[1] = v; d[2] = syy * idet; d[3] = -sxy * idet; d[4] = sxx * idet;
+        d[5] = opac; d[6] = rgb.x; d[7] = rgb.y; d[8] = rgb.z; d[9] = z; d[10] = sxx; d[11] = syy;
+      }
+    }
+    if (debug && in) {
+      a.dbg_zbits[(size_t)f * a.n + i] = __float_as_uint(z);
+      a.dbg_valid[(size_t)f * a.n + i] = (uint8_t)keep;
+    }
+    if (a.rec == nullptr) continue;  // debug-only launch
+    const int slot = warp_compact_slot(vis, a.vcount + fl);
+    if (vis) {
+      float4* r = a.rec + ((size_t)fl * a.n + slot) * 3;
+      r[0] = make_float4(u, v, pw, qw);
+      r[1] = make_float4(rw, log2o, z, __int_as_float((int)i));
+      r[2] = make_float4(rgb.x, rgb.y, rgb.z, __uint_as_float(pack_rect(tx0, tx1, ty0, ty1)));
+      int* h = a.hist + (size_t)fl * a.hist_stride;
+      for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(h + ty * a.tiles_x + tx, 1);
+    }
+  }
+}
+
+void launch_k0(const float* poses, const float* intr, const float* w2c, int n_frames, int n_cams,
+               int n_bodies, int width, int height, float4* table, FrameCam* cams,
+               cudaStream_t s) {
+  const int total = n_frames * (n_bodies + 1);
+  if (total == 0) return;
+  k0_setup<<<(total + 127) / 128, 128, 0, s>>>(poses, intr, w2c, n_frames, n_cams, n_bodies, width,
+                                                height, table, cams);
+}
+
+void launch_k1(const K1Args& a, int sh_degree, cudaStream_t s) {
+  if (a.n == 0) return;
+  const unsigned grid = (unsigned)((a.n + 127) / 128);
+  switch (sh_degree) {
+    case 0: k1_project<0><<<grid, 128, 0, s>>>(a); break;
+    case 1: k1_project<1><<<grid, 128, 0, s>>>(a); break;
+    case 2: k1_project<2><<<grid, 128, 0, s>>>(a); break;
+    default: k1_project<3><<<grid, 128, 0, s>>>(a); break;
+  }
+}
+
+}  // namespace gsb

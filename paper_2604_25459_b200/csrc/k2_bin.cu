@@ -1,0 +1,166 @@
+// k2_bin.cu — K2: tile-intersection offsets (per-frame exclusive scan of the tile histogram
+// built by K1) and emission of one 64-bit key per (visible Gaussian, overlapped tile).
+//
+// 3DGS tile binning [3DGS-conv, cited P:212]; keys are unique (reading R10):
+//   key = bits(z_f32) << 32 | slot        (slot -> record -> Gaussian id)
+// and land directly in their (frame, tile) bucket, so K3 only sorts within a bucket.
+// The tile coordinate is implied by the bucket; the frame by the chunk's frame_base.
+#include "gsb_common.cuh"
+#include "gsb_kernels.cuh"
+
+namespace gsb {
+
+constexpr int kScanThreads = 1024;
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+// per-frame exclusive scan of hist[f][0..T) -> off[f][0..T]; hist is zeroed (becomes the
+// emission cursor).  One block per frame.
+__global__ void __launch_bounds__(kScanThreads) k2_scan_tiles(int* __restrict__ hist,
+                                                              uint32_t* __restrict__ off,
+                                                              int64_t stride, int n_tiles) {
+  __shared__ uint32_t wsum[kScanThreads / 32];
+  __shared__ uint32_t carry_s;
+  const int f = blockIdx.x;
+  int* h = hist + (size_t)f * stride;
+  uint32_t* o = off + (size_t)f * stride;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) carry_s = 0;
+  __syncthreads();
+  for (int base = 0; base < n_tiles; base += kScanThreads) {
+    const int t = base + tid;
+    const uint32_t x = t < n_tiles ? (uint32_t)h[t] : 0u;
+    const uint32_t inc = warp_incl_scan(x);
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t w = lane < kScanThreads / 32 ? wsum[lane] : 0u;
+      const uint32_t wi = warp_incl_scan(w);
+      if (lane < kScanThreads / 32) wsum[lane] = wi - w;
+    }
+    __syncthreads();
+    const uint32_t carry = carry_s;
+    if (t < n_tiles) {
+      o[t] = carry + wsum[warp] + inc - x;
+      h[t] = 0;
+    }
+    __syncthreads();
+    if (tid == kScanThreads - 1) carry_s = carry + wsum[warp] + inc;
+    __syncthreads();
+  }
+  if (tid == 0) o[n_tiles] = carry_s;
+}
+
+// frame_base[0..E] = exclusive prefix of K_f = off[f][T] (single block)
+__global__ void k2_scan_frames(const uint32_t* __restrict__ off, int64_t stride, int n_tiles,
+                               int n_frames, uint64_t* __restrict__ frame_base) {
+  if (threadIdx.x != 0) return;
+  uint64_t acc = 0;
+  for (int f = 0; f < n_frames; ++f) {
+    frame_base[f] = acc;
+    acc += off[(size_t)f * stride + n_tiles];
+  }
+  frame_base[n_frames] = acc;
+}
+
+void launch_k2_scan(int* hist, uint32_t* off, int64_t hist_stride, int n_frames, int n_tiles,
+                    uint64_t* frame_base, cudaStream_t s) {
+  k2_scan_tiles<<<n_frames, kScanThreads, 0, s>>>(hist, off, hist_stride, n_tiles);
+  k2_scan_frames<<<1, 32, 0, s>>>(off, hist_stride, n_tiles, n_frames, frame_base);
+}
+
+// ------------------------------------------------------------------------------ emission
+__global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
+  const int fl = a.fs + blockIdx.y;
+  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= a.vcount[fl]) return;
+  const float4* r = a.rec + ((size_t)fl * a.n + slot) * 3;
+  const float z = __ldg(&r[1].z);
+  const uint32_t rect = __float_as_uint(__ldg(&r[2].w));
+  const int tx0 = rect & 0xff, tx1 = (rect >> 8) & 0xff, ty0 = (rect >> 16) & 0xff, ty1 = rect >> 24;
+  const uint64_t key = ((uint64_t)__float_as_uint(z) << 32) | (uint64_t)slot;
+  int* cur = a.hist + (size_t)fl * a.hist_stride;
+  const uint32_t* off = a.off + (size_t)fl * a.hist_stride;
+  const uint64_t fb = a.frame_base[fl] - a.key_base;
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) {
+      const int t = ty * a.tiles_x + tx;
+      const uint32_t pos = (uint32_t)atomicAdd(cur + t, 1);
+      a.keys[fb + off[t] + pos] = key;
+    }
+}
+
+void launch_k2_emit(const ChunkArgs& a, cudaStream_t s) {
+  const int nf = a.fe - a.fs;
+  if (nf <= 0 || a.n == 0) return;
+  dim3 grid((unsigned)((a.n + 255) / 256), (unsigned)nf);
+  k2_emit<<<grid, 256, 0, s>>>(a);
+}
+
+// ------------------------------------------------- records from external fp32 projections
+__global__ void __launch_bounds__(128) k1_external(const float* __restrict__ u, const float* __restrict__ v,
+                                                   const float* __restrict__ sxx, const float* __restrict__ syy,
+                                                   const float* __restrict__ kappa,
+                                                   const uint32_t* __restrict__ zbits,
+                                                   const uint8_t* __restrict__ valid, int64_t n, int f0,
+                                                   int n_frames, int width, int height, int tiles_x,
+                                                   float4* __restrict__ rec, int* __restrict__ vcount,
+                                                   int* __restrict__ hist, int64_t hist_stride) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool in = i < n;
+  for (int fl = 0; fl < n_frames; ++fl) {
+    const size_t o = (size_t)(f0 + fl) * n + (in ? i : 0);
+    int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;
+    bool vis = false;
+    if (in && valid[o])
+      vis = r9_rect(u[o], v[o], sxx[o], syy[o], kappa[o], width, height, tx0, tx1, ty0, ty1);
+    const int slot = warp_compact_slot(vis, vcount + fl);
+    if (vis) {
+      float4* r = rec + ((size_t)fl * n + slot) * 3;
+      r[0] = make_float4(u[o], v[o], 0.f, 0.f);
+      r[1] = make_float4(0.f, 0.f, __uint_as_float(zbits[o]), __int_as_float((int)i));
+      r[2] = make_float4(0.f, 0.f, 0.f, __uint_as_float(pack_rect(tx0, tx1, ty0, ty1)));
+      int* h = hist + (size_t)fl * hist_stride;
+      for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(h + ty * tiles_x + tx, 1);
+    }
+  }
+}
+
+void launch_k1_external(const float* u, const float* v, const float* sxx, const float* syy,
+                        const float* kappa, const uint32_t* zbits, const uint8_t* valid,
+                        int64_t n, int f0, int n_frames, int width, int height, int tiles_x,
+                        float4* rec, int* vcount, int* hist, int64_t hist_stride, cudaStream_t s) {
+  if (n == 0) return;
+  k1_external<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(u, v, sxx, syy, kappa, zbits, valid, n, f0,
+                                                          n_frames, width, height, tiles_x, rec,
+                                                          vcount, hist, hist_stride);
+}
+
+// sorted slots -> Gaussian ids (debug_bin_sort output)
+__global__ void k_slots_to_ids(ChunkArgs a, uint32_t* __restrict__ ids) {
+  const int fl = a.fs + blockIdx.y;
+  const uint64_t b = a.frame_base[fl] - a.key_base, e = a.frame_base[fl + 1] - a.key_base;
+  for (uint64_t k = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < e;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t slot = a.sorted[k];
+    ids[k] = (uint32_t)__float_as_int(a.rec[((size_t)fl * a.n + slot) * 3 + 1].w);
+  }
+}
+
+void launch_slots_to_ids(const ChunkArgs& a, uint32_t* ids, uint64_t count, cudaStream_t s) {
+  (void)count;
+  const int nf = a.fe - a.fs;
+  if (nf <= 0) return;
+  k_slots_to_ids<<<dim3(64, (unsigned)nf), 256, 0, s>>>(a, ids);
+}
+
+}  // namespace gsb

@@ -1,0 +1,77 @@
+"""C-ABI library: builds, loads without a GPU, exports every symbol include/gsb.h declares,
+and validates arguments on the host (no compute calls)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2604_25459_b200 as gsb
+from paper_2604_25459_b200 import build as gsb_build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "gsb.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gsb_[a-z_]+)\s*\(", src)))
+
+
+def test_library_builds_and_exports_header_symbols():
+    gsb_build.build()
+    L = gsb.lib()
+    declared = header_functions()
+    assert len(declared) >= 11
+    assert sorted(declared) == sorted(gsb.EXPORTS)
+    for name in declared:
+        assert hasattr(L, name), name
+    assert gsb.version().startswith("gsb")
+
+
+def test_sm100a_only_cubin():
+    """The library carries sm_100a SASS (no other arch, no PTX JIT fallback)."""
+    import subprocess
+    gsb_build.build()
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", gsb.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(8\d|9\d)", out)
+
+
+def test_host_side_validation_without_gpu():
+    L = gsb.lib()
+    n = 4
+    m = np.zeros((n, 3), np.float32)
+    s = np.ones((n, 3), np.float32)
+    q = np.tile(np.float32([1, 0, 0, 0]), (n, 1))
+    o = np.full(n, 0.5, np.float32)
+    sh = np.zeros((n, 1, 3), np.float32)
+    b = np.full(n, -1, np.int32)
+    h = ctypes.c_void_p()
+    p = lambda a: a.ctypes.data
+    # NULL out
+    assert L.gsb_create_scene(p(m), p(s), p(q), p(o), p(sh), 0, p(b), n, 0, 0, None) == 1
+    # bad SH degree
+    assert L.gsb_create_scene(p(m), p(s), p(q), p(o), p(sh), 5, p(b), n, 0, 0, ctypes.byref(h)) == 1
+    # non-finite value
+    m2 = m.copy()
+    m2[0, 0] = np.nan
+    assert L.gsb_create_scene(p(m2), p(s), p(q), p(o), p(sh), 0, p(b), n, 0, 0, ctypes.byref(h)) == 1
+    assert b"non-finite" in L.gsb_last_error()
+    # valid arguments, but no sm_100 device in this container
+    import torch
+    if not torch.cuda.is_available():
+        assert L.gsb_create_scene(p(m), p(s), p(q), p(o), p(sh), 0, p(b), n, 0, 0, ctypes.byref(h)) == 7
+    # NULL scene everywhere
+    assert L.gsb_reserve(None, 1, 1, 64, 48, 0, 0, 0) == 1
+    prm = gsb.RenderParams(64, 48).to_c()
+    assert L.gsb_render(None, None, 1, 1, None, None, ctypes.byref(prm), None, None, None, None, None) == 1
+    assert L.gsb_destroy_scene(None) == 0
+    assert L.gsb_debug_bin_sort(None, None, None, None, None, None, None, 0, 0, 8, 8, None, None, 0, None, None) == 1
+
+
+def test_render_params_layout_matches_header():
+    assert ctypes.sizeof(gsb.gsb_render_params) == 4 * 9
+    assert ctypes.sizeof(gsb.gsb_timings) == 8 * 9

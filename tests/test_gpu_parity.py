@@ -1,0 +1,285 @@
+"""GPU parity: libgsb (through its C ABI) against the CPU oracle, element by element.
+
+Bars (BASELINE.json north_star):
+  * integer outputs bit-exact: depth-key bits and cull flags for every (frame, Gaussian);
+    per-(frame, tile) offsets and id lists given the oracle's fp32 projected values;
+  * floats: max |dRGB| <= 2e-3, |d depth| <= 1e-3 depth + 1e-6, |d alpha| <= 2e-3 on pixels
+    outside the reading-R28 threshold-margin mask; n_eval exact there;
+  * K1 records: u, v within 1e-3 px; conic, Sigma2D, rgb within 1e-5 relative.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2604_25459_b200 as gsb
+import synth
+from oracle import binning
+from tests import gpu_util as gu
+from tests.helpers import identity_cam, scene_from
+
+pytestmark = pytest.mark.gpu
+
+MASK_CAP = 0.02  # masked-pixel fraction allowed per frame (reported; R28)
+
+
+def _oracle_frame(scene, batch, e, c, cfg_w, cfg_h, bg=(0, 0, 0), pixels=None, sh_degree=None):
+    prm = oracle.RenderParams(cfg_w, cfg_h, bg=bg, sh_degree=sh_degree)
+    return oracle.render_frame(scene, batch.poses[e], batch.intrinsics[e, c], batch.w2c[e, c], prm, pixels=pixels)
+
+
+# --------------------------------------------------------------------------- K1 records
+@pytest.mark.parametrize("name", ["C1", "T1", "T4", "T5"])
+def test_k1_projection_matches_oracle(name):
+    cfg = synth.CONFIGS[name]
+    sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
+    g = gsb.Scene.from_synth(sc)
+    g.reserve(cfg.n_envs, cfg.n_cams, cfg.width, cfg.height)
+    rec, zb, valid = gu.gpu_project(g, b, cfg.width, cfg.height)
+    prm = oracle.RenderParams(cfg.width, cfg.height)
+    for e in range(cfg.n_envs):
+        for c in range(cfg.n_cams):
+            f = e * cfg.n_cams + c
+            proj, ozb, ovalid = oracle.project(sc, b.poses[e], b.intrinsics[e, c], b.w2c[e, c], prm)
+            assert np.array_equal(zb[f], ozb), "depth-key bits (R11) must be bit-exact"
+            assert np.array_equal(valid[f], ovalid)
+            v = ovalid
+            r = rec[f][v]
+            p = proj[v]
+            assert np.abs(r[:, 0] - p[:, oracle.F_U]).max() <= 1e-3
+            assert np.abs(r[:, 1] - p[:, oracle.F_V]).max() <= 1e-3
+            cn = np.abs(p[:, oracle.F_A]) + np.abs(p[:, oracle.F_C])
+            for k, fk in ((2, oracle.F_A), (3, oracle.F_B), (4, oracle.F_C)):
+                assert (np.abs(r[:, k] - p[:, fk]) / cn).max() <= 1e-5, k
+            for k, fk in ((10, oracle.F_SXX), (11, oracle.F_SYY)):
+                assert (np.abs(r[:, k] - p[:, fk]) / np.abs(p[:, fk])).max() <= 1e-5, k
+            rgb_ref = p[:, oracle.F_R:oracle.F_BL + 1]
+            assert (np.abs(r[:, 6:9] - rgb_ref) / np.maximum(np.abs(rgb_ref), 1.0)).max() <= 1e-5
+            assert np.array_equal(r[:, 9].view(np.uint32), ozb[v])
+
+
+# --------------------------------------------------------------------------- K2 + K3 bit-exact
+def _oracle_fp32_projections(sc, b, cfg):
+    F, N = cfg.n_frames, sc.n
+    arr = {k: np.zeros((F, N), np.float32) for k in ("u", "v", "sxx", "syy", "kappa")}
+    zb = np.zeros((F, N), np.uint32)
+    va = np.zeros((F, N), np.uint8)
+    prm = oracle.RenderParams(cfg.width, cfg.height)
+    for e in range(cfg.n_envs):
+        for c in range(cfg.n_cams):
+            f = e * cfg.n_cams + c
+            proj, z, v = oracle.project(sc, b.poses[e], b.intrinsics[e, c], b.w2c[e, c], prm)
+            arr["u"][f], arr["v"][f] = proj[:, oracle.F_U], proj[:, oracle.F_V]
+            arr["sxx"][f], arr["syy"][f] = proj[:, oracle.F_SXX], proj[:, oracle.F_SYY]
+            arr["kappa"][f] = proj[:, oracle.F_KAPPA]
+            zb[f], va[f] = z, v
+    return arr, zb, va
+
+
+@pytest.mark.parametrize("name", ["C1", "T1", "T2", "T4"])
+def test_bin_sort_bit_exact_against_binning_oracle(name):
+    cfg = synth.CONFIGS[name]
+    sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
+    arr, zb, va = _oracle_fp32_projections(sc, b, cfg)
+    offs_ref, ids_ref = binning.bin_frames(arr["u"], arr["v"], arr["sxx"], arr["syy"], arr["kappa"], zb, va,
+                                           cfg.width, cfg.height)
+    d = {k: gu.to_dev(v) for k, v in arr.items()}
+    offs, ids = gsb.debug_bin_sort(d["u"], d["v"], d["sxx"], d["syy"], d["kappa"],
+                                   gu.to_dev(zb.view(np.int32)), gu.to_dev(va), cfg.width, cfg.height,
+                                   cap=int(ids_ref.size) + 16)
+    assert np.array_equal(offs.cpu().numpy(), offs_ref)
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), ids_ref)
+
+
+def test_bin_sort_oversize_segment_global_path_and_depth_ties():
+    """A tile list longer than the shared-memory sort capacity (4096) goes through the HBM
+    ping-pong path; many exactly equal depths exercise the id tie-break."""
+    rng = np.random.default_rng(3)
+    F, N, W, H = 2, 9000, 32, 32
+    u = rng.uniform(2, 14, (F, N)).astype(np.float32)
+    v = rng.uniform(2, 14, (F, N)).astype(np.float32)
+    sxx = rng.uniform(0.5, 3, (F, N)).astype(np.float32)
+    syy = rng.uniform(0.5, 3, (F, N)).astype(np.float32)
+    kap = rng.uniform(0.5, 8, (F, N)).astype(np.float32)
+    z = rng.choice(np.float32([1.0, 1.5, 2.0, 2.25]), (F, N)).astype(np.float32)
+    z[:, ::3] = rng.uniform(0.5, 5, (F, (N + 2) // 3)).astype(np.float32)
+    zb = z.view(np.uint32)
+    va = (rng.random((F, N)) < 0.95).astype(np.uint8)
+    offs_ref, ids_ref = binning.bin_frames(u, v, sxx, syy, kap, zb, va, W, H)
+    assert np.diff(offs_ref[0]).max() > 4096
+    offs, ids = gsb.debug_bin_sort(gu.to_dev(u), gu.to_dev(v), gu.to_dev(sxx), gu.to_dev(syy), gu.to_dev(kap),
+                                   gu.to_dev(zb.view(np.int32)), gu.to_dev(va), W, H, cap=int(ids_ref.size))
+    assert np.array_equal(offs.cpu().numpy(), offs_ref)
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), ids_ref)
+
+
+# --------------------------------------------------------------------------- full render
+@pytest.mark.parametrize("name", ["C1", "T1", "T2", "T3", "T4", "T5"])
+def test_render_full_frames_match_oracle(name):
+    cfg = synth.CONFIGS[name]
+    sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
+    bg = (0.1, 0.2, 0.3) if name in ("T3", "T5") else (0.0, 0.0, 0.0)
+    gout = gu.gpu_render(sc, b, cfg.width, cfg.height, bg=bg)
+    rec, zb, va = gu.gpu_project(gout["scene"], b, cfg.width, cfg.height)
+    kap = gu.kappa_f32(sc)
+    for e in range(cfg.n_envs):
+        for c in range(cfg.n_cams):
+            f = e * cfg.n_cams + c
+            ref = _oracle_frame(sc, b, e, c, cfg.width, cfg.height, bg=bg)
+            r = gu.compare_frame(gout, e, c, ref, cfg.width, cfg.height, gpu_rec=rec[f], gpu_zb=zb[f],
+                                 gpu_valid=va[f], kap=kap)
+            print(name, e, c, r)
+            assert r["rgb_fail"] == 0 and r["dep_fail"] == 0 and r["alp_fail"] == 0, r
+            assert r["n_eval_fail"] == 0, r
+            assert r["masked_frac"] <= MASK_CAP, r
+            assert np.isfinite(gout["rgb"][e, c]).all()
+
+
+def test_render_oversize_tile_list_matches_oracle():
+    """> 4096 Gaussians overlapping one tile: the sort's global path inside a full render."""
+    rng = np.random.default_rng(7)
+    n = 6000
+    means = np.stack([rng.uniform(-0.05, 0.05, n), rng.uniform(-0.05, 0.05, n), rng.uniform(2, 3, n)], 1)
+    sc = scene_from(means, rng.uniform(0.002, 0.01, (n, 3)), opac=rng.uniform(0.01, 0.3, n),
+                    colours=rng.uniform(0, 1, (n, 3)))
+    K, Wc = identity_cam(fx=100, fy=100, cx=16, cy=16)
+    b = synth.Batch(np.zeros((1, 0, 7), np.float32), K[None, None], Wc[None, None])
+    gout = gu.gpu_render(sc, b, 32, 32)
+    rec, zb, va = gu.gpu_project(gout["scene"], b, 32, 32)
+    ref = oracle.render_frame(sc, b.poses[0], K, Wc, oracle.RenderParams(32, 32))
+    r = gu.compare_frame(gout, 0, 0, ref, 32, 32, gpu_rec=rec[0], gpu_zb=zb[0], gpu_valid=va[0],
+                         kap=gu.kappa_f32(sc))
+    print(r)
+    assert gout["n_eval"].max() > 0
+    assert r["rgb_fail"] == 0 and r["dep_fail"] == 0 and r["n_eval_fail"] == 0, r
+
+
+@pytest.mark.slow
+def test_render_c3_full_size_sampled_pixels():
+    """BASELINE configs[2] at full size, in the bench's launch configuration (1024 envs, one call):
+    sampled pixels of frames {0, B/2, B-1} against the oracle."""
+    cfg = synth.CONFIGS["C3"]
+    sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
+    gout = gu.gpu_render(sc, b, cfg.width, cfg.height, stats=True)
+    kap = gu.kappa_f32(sc)
+    rng = np.random.default_rng(33)
+    for e in (0, cfg.n_envs // 2, cfg.n_envs - 1):
+        px = rng.integers(0, cfg.width, 384)
+        py = rng.integers(0, cfg.height, 384)
+        ref = _oracle_frame(sc, b, e, 0, cfg.width, cfg.height, pixels=(px, py))
+        sub = synth.Batch(b.poses[e:e + 1], b.intrinsics[e:e + 1], b.w2c[e:e + 1])
+        rec, zb, va = gu.gpu_project(gout["scene"], sub, cfg.width, cfg.height)
+        r = gu.compare_frame(gout, e, 0, ref, cfg.width, cfg.height, pix=(px, py), gpu_rec=rec[0], gpu_zb=zb[0],
+                             gpu_valid=va[0], kap=kap)
+        print("C3", e, r)
+        assert r["rgb_fail"] == 0 and r["dep_fail"] == 0 and r["alp_fail"] == 0, r
+        assert r["n_eval_fail"] == 0, r
+        assert r["masked_frac"] <= MASK_CAP, r
+    st = gout["stats"]
+    assert st["V"] > 0 and st["K"] >= st["V"] and st["P"] > 0
+    assert st["P"] == int(gout["n_eval"].astype(np.int64).sum())
+
+
+# --------------------------------------------------------------------------- invariants
+def test_batch_slicing_and_chunking_bit_identical():
+    """Per-env frames are bit-identical whether rendered in one call, as env slices (the
+    multi-GPU sharding), with other chunk sizes, or with a key capacity that forces split
+    passes."""
+    cfg = synth.CONFIGS["T2"]
+    sc = synth.make_scene(cfg)
+    b = synth.make_batch(cfg, np.arange(6))
+    full = gu.gpu_render(sc, b, cfg.width, cfg.height)
+    for lo, hi in ((0, 2), (2, 5), (5, 6)):
+        sub = synth.make_batch(cfg, np.arange(lo, hi))
+        part = gu.gpu_render(sc, sub, cfg.width, cfg.height)
+        for k in ("rgb", "depth", "alpha", "n_eval"):
+            assert np.array_equal(full[k][lo:hi], part[k]), k
+    ch = gu.gpu_render(sc, b, cfg.width, cfg.height, chunk_frames=4)
+    st = gu.gpu_render(sc, b, cfg.width, cfg.height, stats=True)
+    small_cap = int(st["stats"]["K"] // 6 + 1)
+    sp = gu.gpu_render(sc, b, cfg.width, cfg.height, chunk_frames=6, key_capacity=small_cap)
+    for k in ("rgb", "depth", "alpha", "n_eval"):
+        assert np.array_equal(full[k], ch[k]), k
+        assert np.array_equal(full[k], sp[k]), k
+
+
+def test_outputs_deterministic_and_invariants():
+    cfg = synth.CONFIGS["T1"]
+    sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
+    a = gu.gpu_render(sc, b, cfg.width, cfg.height, stats=True)
+    c = gu.gpu_render(sc, b, cfg.width, cfg.height, stats=True)
+    for k in ("rgb", "depth", "alpha", "n_eval"):
+        assert np.array_equal(a[k], c[k])
+    assert np.all((a["alpha"] >= 0) & (a["alpha"] <= 1))
+    assert np.all(a["rgb"] >= 0) and np.all(a["depth"] >= 0)
+    assert a["stats"] == c["stats"]
+    assert a["stats"]["P"] == int(a["n_eval"].astype(np.int64).sum())
+    # constant colour scene with bg = colour renders that colour everywhere (partition of unity)
+    cst = synth.Scene(sc.means, sc.scales, sc.quats, sc.opacities, np.zeros_like(sc.sh), sc.sh_degree,
+                      sc.body_id, sc.n_bodies)
+    cst.sh[:, 0, :] = (np.float32([0.3, 0.6, 0.1]) - 0.5) / 0.28209479177387814
+    o = gu.gpu_render(cst, b, cfg.width, cfg.height, bg=(0.3, 0.6, 0.1))
+    assert np.abs(o["rgb"] - np.float32([0.3, 0.6, 0.1])[None, None, :, None, None]).max() < 1e-5
+
+
+def test_edge_cases_empty_culled_tiny_and_lower_sh():
+    cfg = synth.CONFIGS["T5"]
+    sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
+    # empty scene: background everywhere
+    empty = synth.Scene(sc.means[:0], sc.scales[:0], sc.quats[:0], sc.opacities[:0], sc.sh[:0], sc.sh_degree,
+                        sc.body_id[:0], sc.n_bodies)
+    o = gu.gpu_render(empty, b, cfg.width, cfg.height, bg=(0.25, 0.5, 0.75))
+    assert np.all(o["rgb"][:, :, 0] == np.float32(0.25)) and np.all(o["alpha"] == 0) and np.all(o["n_eval"] == 0)
+    # everything behind the far plane: all culled
+    o = gu.gpu_render(sc, b, cfg.width, cfg.height, far=0.02)
+    assert np.all(o["rgb"] == 0) and np.all(o["n_eval"] == 0)
+    # 1x1 and ragged 17x9 images against the oracle
+    for (W, H) in ((1, 1), (17, 9)):
+        bb = synth.Batch(b.poses[:1], b.intrinsics[:1].copy(), b.w2c[:1])
+        bb.intrinsics[..., 2] = W / 2
+        bb.intrinsics[..., 3] = H / 2
+        bb.intrinsics[..., :2] *= W / cfg.width
+        o = gu.gpu_render(sc, bb, W, H)
+        ref = oracle.render_frame(sc, bb.poses[0], bb.intrinsics[0, 0], bb.w2c[0, 0], oracle.RenderParams(W, H))
+        r = gu.compare_frame(o, 0, 0, ref, W, H)
+        assert r["rgb_fail"] == 0 and r["dep_fail"] == 0, r
+    # lower SH degree than the scene's
+    o = gu.gpu_render(sc, b, cfg.width, cfg.height, sh_degree=1)
+    ref = _oracle_frame(sc, b, 0, 0, cfg.width, cfg.height, sh_degree=1)
+    r = gu.compare_frame(o, 0, 0, ref, cfg.width, cfg.height)
+    assert r["rgb_fail"] == 0, r
+
+
+def test_host_path_matches_device_path():
+    cfg = synth.CONFIGS["T1"]
+    sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
+    dev = gu.gpu_render(sc, b, cfg.width, cfg.height)
+    g = gsb.Scene.from_synth(sc)
+    g.reserve(cfg.n_envs, cfg.n_cams, cfg.width, cfg.height, host_io=True)
+    B, C = cfg.n_envs, cfg.n_cams
+    rgb = torch.empty((B, C, 3, cfg.height, cfg.width), pin_memory=True)
+    dep = torch.empty((B, C, cfg.height, cfg.width), pin_memory=True)
+    g.render_host(torch.from_numpy(b.poses), torch.from_numpy(b.intrinsics), torch.from_numpy(b.w2c),
+                  gsb.RenderParams(cfg.width, cfg.height), rgb, dep)
+    assert np.array_equal(rgb.numpy(), dev["rgb"])
+    assert np.array_equal(dep.numpy(), dev["depth"])
+
+
+def test_invalid_arguments_rejected_before_enqueue():
+    cfg = synth.CONFIGS["T3"]
+    sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
+    g = gsb.Scene.from_synth(sc)
+    g.reserve(2, 1, cfg.width, cfg.height)
+    out = torch.zeros((4, 1, 3, cfg.height, cfg.width), device="cuda")
+    with pytest.raises(gsb.GsbError) as ei:  # more frames than reserved
+        g.render(gu.to_dev(np.zeros((4, 0, 7), np.float32)), gu.to_dev(np.repeat(b.intrinsics, 1, 0)[:1].repeat(4, 0)),
+                 gu.to_dev(b.w2c[:1].repeat(4, 0)), gsb.RenderParams(cfg.width, cfg.height), out)
+    assert ei.value.status == 2
+    with pytest.raises(gsb.GsbError) as ei:
+        g.render(None, gu.to_dev(b.intrinsics), gu.to_dev(b.w2c), gsb.RenderParams(cfg.width, cfg.height, near=0), out)
+    assert ei.value.status == 1
+    bad = synth.Scene(sc.means, sc.scales, sc.quats, sc.opacities, sc.sh, sc.sh_degree, sc.body_id.copy(), 0)
+    bad.body_id[0] = 3
+    with pytest.raises(gsb.GsbError) as ei:
+        gsb.Scene.from_synth(bad)
+    assert ei.value.status == 3
