@@ -33,8 +33,9 @@ F_U, F_V, F_SXX, F_SXY, F_SYY, F_A, F_B, F_C, F_R, F_G, F_BL, F_O, F_KAPPA, F_Z3
 TOL_RGB = 2e-3
 TOL_DEPTH_REL = 1e-3
 TOL_DEPTH_ABS = 1e-6
-DELTA_ALPHA = 1e-3
-DELTA_T = 1e-3
+DELTA_ALPHA = 1e-4
+DELTA_T = 1e-4
+DELTA_T_INT = 2e-3   # n_eval (an integer decided by the termination test) — reading R28
 
 
 def build_oracle(force: bool = False) -> str:
@@ -62,7 +63,7 @@ def lib():
         L.gsbo_composite.restype = ctypes.c_int
         L.gsbo_composite.argtypes = [P, P, ctypes.c_int64, P, P, ctypes.c_int64, P, ctypes.c_int,
                                      ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
-                                     P, P, P, P, P, P, P, ctypes.c_int]
+                                     P, P, P, P, P, P, P, P, ctypes.c_double, ctypes.c_int]
         L.gsbo_depth_key.restype = ctypes.c_float
         L.gsbo_depth_key.argtypes = [P, P, P]
         L.gsbo_fmaf.restype = ctypes.c_float
@@ -133,6 +134,7 @@ class FrameResult:
     zbits: np.ndarray
     valid: np.ndarray
     order: np.ndarray
+    term_near: np.ndarray  # a termination test within DELTA_T_INT of 1e-4 (n_eval not compared)
 
 
 def composite(proj, order, px, py, prm: RenderParams, mode: str = "box", nthreads: Optional[int] = None,
@@ -152,14 +154,16 @@ def composite(proj, order, px, py, prm: RenderParams, mode: str = "box", nthread
     rgb = np.zeros((npix, 3)); dep = np.zeros(npix); alp = np.zeros(npix)
     term = np.zeros(npix, np.int64); nev = np.zeros(npix, np.int64)
     brgb = np.zeros(npix); bdep = np.zeros(npix)
+    tnear = np.zeros(npix, np.uint8)
     if nthreads is None:
         nthreads = os.cpu_count() or 1
     proj = _c(proj, np.float64)
     L.gsbo_composite(_p(proj), _p(order), order.size, _p(px), _p(py), npix, _p(bg),
                      1 if mode == "box" else 0, delta_alpha, delta_T, cmax, zmax,
-                     _p(rgb), _p(dep), _p(alp), _p(term), _p(nev), _p(brgb), _p(bdep), int(nthreads))
+                     _p(rgb), _p(dep), _p(alp), _p(term), _p(nev), _p(brgb), _p(bdep), _p(tnear),
+                     DELTA_T_INT, int(nthreads))
     masked = (brgb > 0.5 * TOL_RGB) | (bdep > 0.5 * (TOL_DEPTH_REL * dep + TOL_DEPTH_ABS))
-    return rgb, dep, alp, term, nev, masked, brgb, bdep
+    return rgb, dep, alp, term, nev, masked, brgb, bdep, tnear.astype(bool)
 
 
 def render_frame(scene, pose_env, intr, w2c, prm: RenderParams, pixels=None, mode: str = "box",
@@ -173,13 +177,13 @@ def render_frame(scene, pose_env, intr, w2c, prm: RenderParams, pixels=None, mod
         px, py = px.reshape(-1), py.reshape(-1)
     else:
         px, py = pixels
-    rgb, dep, alp, term, nev, masked, brgb, bdep = composite(proj, order, px, py, prm, mode, nthreads, **kw)
+    rgb, dep, alp, term, nev, masked, brgb, bdep, tnear = composite(proj, order, px, py, prm, mode, nthreads, **kw)
     if full:
         H, W = prm.height, prm.width
         rgb, dep, alp = rgb.reshape(H, W, 3), dep.reshape(H, W), alp.reshape(H, W)
-        term, nev, masked = term.reshape(H, W), nev.reshape(H, W), masked.reshape(H, W)
+        term, nev, masked, tnear = term.reshape(H, W), nev.reshape(H, W), masked.reshape(H, W), tnear.reshape(H, W)
         brgb, bdep = brgb.reshape(H, W), bdep.reshape(H, W)
-    return FrameResult(rgb, dep, alp, term, nev, masked, brgb, bdep, proj, zb, valid, order)
+    return FrameResult(rgb, dep, alp, term, nev, masked, brgb, bdep, proj, zb, valid, order, tnear)
 
 
 def depth_key(w2c, pose_or_none, mu) -> np.float32:

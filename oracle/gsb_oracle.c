@@ -299,6 +299,8 @@ typedef struct {
   int64_t* out_n_eval;
   double* out_budget_rgb;
   double* out_budget_depth;
+  uint8_t* out_term_near;
+  double delta_T_int;
 } comp_job;
 
 static void composite_pixel(const comp_job* jb, int64_t p) {
@@ -306,6 +308,7 @@ static void composite_pixel(const comp_job* jb, int64_t p) {
   double T = 1.0, C[3] = {0, 0, 0}, D = 0.0;
   double brgb = 0.0, bdep = 0.0;
   int64_t term = -1, n_eval = 0;
+  uint8_t term_near = 0;
   const double thr = 1.0 / 255.0;
   for (int64_t j = 0; j < jb->n_order; ++j) {
     const uint32_t i = jb->order[j];
@@ -332,6 +335,8 @@ static void composite_pixel(const comp_job* jb, int64_t p) {
       brgb += T * 2.0 * jb->cmax;
       bdep += T * jb->zmax;
     }
+    /* R28: the integer n_eval is decided by this test; flag it when within fp32 reach */
+    if (fabs(tT - 1e-4) <= jb->delta_T_int * 1e-4) term_near = 1;
     if (tT < 1e-4) {
       term = (int64_t)i;
       break;
@@ -350,6 +355,7 @@ static void composite_pixel(const comp_job* jb, int64_t p) {
   jb->out_n_eval[p] = n_eval;
   jb->out_budget_rgb[p] = brgb;
   jb->out_budget_depth[p] = bdep;
+  jb->out_term_near[p] = term_near;
 }
 
 static void* composite_worker(void* arg) {
@@ -362,7 +368,8 @@ int gsbo_composite(const double* proj, const uint32_t* order, int64_t n_order, c
                    const int32_t* py, int64_t npix, const float* bg, int mode, double delta_alpha,
                    double delta_T, double cmax, double zmax, double* out_rgb, double* out_depth,
                    double* out_alpha, int64_t* out_term_id, int64_t* out_n_eval,
-                   double* out_budget_rgb, double* out_budget_depth, int nthreads) {
+                   double* out_budget_rgb, double* out_budget_depth, uint8_t* out_term_near,
+                   double delta_T_int, int nthreads) {
   if (nthreads < 1) nthreads = 1;
   if (nthreads > 256) nthreads = 256;
   if ((int64_t)nthreads > npix) nthreads = npix > 0 ? (int)npix : 1;
@@ -380,6 +387,7 @@ int gsbo_composite(const double* proj, const uint32_t* order, int64_t n_order, c
     jb->out_rgb = out_rgb; jb->out_depth = out_depth; jb->out_alpha = out_alpha;
     jb->out_term_id = out_term_id; jb->out_n_eval = out_n_eval;
     jb->out_budget_rgb = out_budget_rgb; jb->out_budget_depth = out_budget_depth;
+    jb->out_term_near = out_term_near; jb->delta_T_int = delta_T_int;
   }
   if (nthreads == 1) {
     composite_worker(&jobs[0]);

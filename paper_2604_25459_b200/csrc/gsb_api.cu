@@ -85,6 +85,7 @@ struct gsb_scene_t {
   int sh_planes = 1;
   // template (K5)
   float4 *d_mean = nullptr, *d_L0 = nullptr, *d_L1 = nullptr, *d_L2 = nullptr, *d_sh = nullptr;
+  int2* d_ids = nullptr;  // internal (Morton) index -> (creation index = id of reading R10, body)
   // reservation
   bool reserved = false;
   int max_frames = 0, res_w = 0, res_h = 0, chunk = 0;
@@ -95,6 +96,8 @@ struct gsb_scene_t {
   FrameCam* cams = nullptr;
   float4* rec[2] = {nullptr, nullptr};
   int* vcount[2] = {nullptr, nullptr};
+  uint32_t* vis_bits[2] = {nullptr, nullptr};
+  int64_t vis_words = 0;
   int* hist[2] = {nullptr, nullptr};
   uint32_t* off[2] = {nullptr, nullptr};
   uint64_t* frame_base[2] = {nullptr, nullptr};
@@ -128,7 +131,8 @@ struct gsb_scene_t {
   void free_workspace() {
     cudaFree(table); cudaFree(cams);
     for (int s = 0; s < 2; ++s) {
-      cudaFree(rec[s]); cudaFree(vcount[s]); cudaFree(hist[s]); cudaFree(off[s]);
+      cudaFree(rec[s]); cudaFree(vcount[s]); cudaFree(hist[s]); cudaFree(off[s]); cudaFree(vis_bits[s]);
+      vis_bits[s] = nullptr;
       cudaFree(frame_base[s]);
       if (h_fb[s]) cudaFreeHost(h_fb[s]);
       if (h_vc[s]) cudaFreeHost(h_vc[s]);
@@ -229,10 +233,12 @@ struct Pipeline {
     CUDA_TRY(cudaMemsetAsync(s->hist[sl], 0, sizeof(int) * s->hist_stride * nf, st));
     K1Args a{};
     a.g_mean = s->d_mean; a.g_L0 = s->d_L0; a.g_L1 = s->d_L1; a.g_L2 = s->d_L2; a.g_sh = s->d_sh;
+    a.g_ids = s->d_ids;
     a.n = s->n; a.table = s->table; a.cams = s->cams; a.nb1 = s->n_bodies + 1;
     a.f0 = f0; a.n_frames = nf; a.width = W; a.height = H; a.tiles_x = tiles_x;
     a.near_plane = p->near_plane; a.far_plane = p->far_plane;
     a.rec = s->rec[sl]; a.vcount = s->vcount[sl]; a.hist = s->hist[sl]; a.hist_stride = s->hist_stride;
+    a.vis_bits = s->vis_bits[sl]; a.vis_words = s->vis_words;
     tm.begin(KC_PROJECT);
     launch_k1(a, D, st);
     if (s->n > 0) s->launches++;
@@ -243,31 +249,34 @@ struct Pipeline {
     s->launches += 2;
     LAUNCH_CHECK();
     tm.end();
-    CUDA_TRY(cudaMemcpyAsync(s->h_fb[sl], s->frame_base[sl], sizeof(uint64_t) * (nf + 1), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(s->h_fb[sl], s->frame_base[sl], sizeof(uint64_t) * (nf + 2), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(s->h_vc[sl], s->vcount[sl], sizeof(int) * nf, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaEventRecord(s->ev_counts[sl], st));
     return GSB_OK;
   }
 
-  gsb_status pass(int sl, int f0, int fs, int fe, uint64_t key_base) {
+  gsb_status pass(int sl, int f0, int fs, int fe, uint64_t key_base, uint64_t max_seg) {
     ChunkArgs a{};
-    a.rec = s->rec[sl]; a.n = s->n; a.vcount = s->vcount[sl]; a.hist = s->hist[sl];
+    a.rec = s->rec[sl]; a.n = s->n; a.vis_bits = s->vis_bits[sl]; a.vis_words = s->vis_words; a.hist = s->hist[sl];
     a.hist_stride = s->hist_stride; a.off = s->off[sl]; a.frame_base = s->frame_base[sl];
     a.n_tiles = n_tiles; a.tiles_x = tiles_x; a.fs = fs; a.fe = fe; a.key_base = key_base;
     a.keys = s->keys; a.keys_alt = s->keys_alt; a.sorted = s->sorted;
+    a.min_n = kFusedSortCap + 1;
     tm.begin(KC_EMIT);
     launch_k2_emit(a, st);
     if (s->n > 0) s->launches++;
     LAUNCH_CHECK();
     tm.end();
-    tm.begin(KC_SORT);
-    launch_k3_sort(a, st);
-    s->launches++;
-    LAUNCH_CHECK();
-    tm.end();
+    if (max_seg > (uint64_t)kFusedSortCap) {  // only lists too long for K4's fused sort
+      tm.begin(KC_SORT);
+      launch_k3_sort(a, st);
+      s->launches++;
+      LAUNCH_CHECK();
+      tm.end();
+    }
     CompositeArgs c{};
     c.rec = s->rec[sl]; c.n = s->n; c.off = s->off[sl]; c.frame_base = s->frame_base[sl];
-    c.hist_stride = s->hist_stride; c.sorted = s->sorted; c.key_base = key_base;
+    c.hist_stride = s->hist_stride; c.sorted = s->sorted; c.keys = s->keys; c.key_base = key_base;
     c.fs = fs; c.fe = fe; c.f0 = f0; c.width = W; c.height = H; c.tiles_x = tiles_x; c.n_tiles = n_tiles;
     c.bg0 = p->background[0]; c.bg1 = p->background[1]; c.bg2 = p->background[2];
     c.out_rgb = out_rgb; c.out_depth = out_depth; c.out_alpha = out_alpha; c.out_n_eval = out_neval;
@@ -305,7 +314,8 @@ struct Pipeline {
     for (int i = 0; i < nf; ++i) s->stat_V += s->h_vc[sl][i];
     s->stat_K += (int64_t)fb[nf];
     s->chunks++;
-    if (fb[nf] <= (uint64_t)s->cap) return pass(sl, f0, 0, nf, 0);
+    const uint64_t max_seg = fb[nf + 1];
+    if (fb[nf] <= (uint64_t)s->cap) return pass(sl, f0, 0, nf, 0, max_seg);
     // split the chunk's frames into passes that fit the key workspace
     int fs = 0;
     while (fs < nf) {
@@ -314,7 +324,7 @@ struct Pipeline {
       if (fe == fs)
         return fail(GSB_ERR_CAPACITY, "frame %d needs %llu tile keys > key capacity %lld", f0 + fs,
                     (unsigned long long)(fb[fs + 1] - fb[fs]), (long long)s->cap);
-      gsb_status r = pass(sl, f0, fs, fe, fb[fs]);
+      gsb_status r = pass(sl, f0, fs, fe, fb[fs], max_seg);
       if (r != GSB_OK) return r;
       fs = fe;
     }
@@ -401,10 +411,52 @@ gsb_status gsb_create_scene(const float* means, const float* scales, const float
   gsb_status st = check_device(device);
   if (st != GSB_OK) return st;
   const int np = (3 * nc + 3) / 4;
-  std::vector<float4> hm(n), h0(n), h1(n), h2(n), hs((size_t)np * n);
   for (int64_t i = 0; i < n; ++i) {
     const int b = body_id[i];
     if (b < -1 || b >= n_bodies) return fail(GSB_ERR_UNKNOWN_BODY, "body_id[%lld] = %d not in [-1, %d)", (long long)i, b, n_bodies);
+  }
+  // Internal order (K5 layout): grouped by body, then Morton (Z-order) of the template position,
+  // so a warp's 32 Gaussians are spatial neighbours: uniform visibility per warp and few
+  // distinct tiles per warp (aggregated atomics).  Results are independent of this order:
+  // ordering and tie-breaks use (z, creation index) only (reading R10).
+  std::vector<int64_t> perm(n);
+  {
+    std::vector<double> lo(3 * (n_bodies + 1), 1e300), hi(3 * (n_bodies + 1), -1e300);
+    for (int64_t i = 0; i < n; ++i)
+      for (int c = 0; c < 3; ++c) {
+        const int g = body_id[i] + 1;
+        lo[3 * g + c] = std::min(lo[3 * g + c], (double)means[3 * i + c]);
+        hi[3 * g + c] = std::max(hi[3 * g + c], (double)means[3 * i + c]);
+      }
+    auto spread = [](uint64_t x) {
+      x &= 0x1fffff;
+      x = (x | x << 32) & 0x1f00000000ffffull;
+      x = (x | x << 16) & 0x1f0000ff0000ffull;
+      x = (x | x << 8) & 0x100f00f00f00f00full;
+      x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+      x = (x | x << 2) & 0x1249249249249249ull;
+      return x;
+    };
+    std::vector<std::pair<std::pair<int, uint64_t>, int64_t>> key(n);
+    for (int64_t i = 0; i < n; ++i) {
+      const int g = body_id[i] + 1;
+      uint64_t code = 0;
+      for (int c = 0; c < 3; ++c) {
+        const double ext = hi[3 * g + c] - lo[3 * g + c];
+        const double t = ext > 0 ? ((double)means[3 * i + c] - lo[3 * g + c]) / ext : 0.0;
+        code |= spread((uint64_t)std::min(2097151.0, std::max(0.0, t * 2097151.0))) << c;
+      }
+      key[i] = {{body_id[i], code}, i};
+    }
+    std::sort(key.begin(), key.end());
+    for (int64_t j = 0; j < n; ++j) perm[j] = key[j].second;
+  }
+  std::vector<float4> hm(n), h0(n), h1(n), h2(n), hs((size_t)np * n);
+  std::vector<int2> hids(n);
+  for (int64_t j = 0; j < n; ++j) {
+    const int64_t i = perm[j];
+    const int b = body_id[i];
+    hids[j] = make_int2((int)i, b);
     const double o = opacities[i];
     if (!(o > 0.0 && o <= 1.0)) return fail(GSB_ERR_INVALID_ARGUMENT, "opacity[%lld] = %g not in (0,1]", (long long)i, o);
     double q[4] = {quats[4 * i], quats[4 * i + 1], quats[4 * i + 2], quats[4 * i + 3]};
@@ -423,20 +475,18 @@ gsb_status gsb_create_scene(const float* means, const float* scales, const float
     float L[9];
     for (int r = 0; r < 3; ++r)
       for (int c = 0; c < 3; ++c) L[r * 3 + c] = (float)(R[r][c] * s3[c]);
-    int bb = b;
-    float bf;
-    std::memcpy(&bf, &bb, 4);
-    hm[i] = make_float4(means[3 * i], means[3 * i + 1], means[3 * i + 2], bf);
-    h0[i] = make_float4(L[0], L[1], L[2], L[3]);
-    h1[i] = make_float4(L[4], L[5], L[6], L[7]);
-    h2[i] = make_float4(L[8], opacities[i], (float)(2.0 * std::log(255.0 * o)), (float)std::log2(o));
+    const double smax = std::max(s3[0], std::max(s3[1], s3[2]));
+    hm[j] = make_float4(means[3 * i], means[3 * i + 1], means[3 * i + 2], (float)(smax * smax * (1.0 + 1e-6)));
+    h0[j] = make_float4(L[0], L[1], L[2], L[3]);
+    h1[j] = make_float4(L[4], L[5], L[6], L[7]);
+    h2[j] = make_float4(L[8], opacities[i], (float)(2.0 * std::log(255.0 * o)), (float)std::log2(o));
     for (int pl = 0; pl < np; ++pl) {
       float v4[4] = {0.f, 0.f, 0.f, 0.f};
       for (int k = 0; k < 4; ++k) {
         const int fidx = 4 * pl + k;
         if (fidx < 3 * nc) v4[k] = sh[(size_t)i * 3 * nc + fidx];
       }
-      hs[(size_t)pl * n + i] = make_float4(v4[0], v4[1], v4[2], v4[3]);
+      hs[(size_t)pl * n + j] = make_float4(v4[0], v4[1], v4[2], v4[3]);
     }
   }
   DeviceGuard g(device);
@@ -454,6 +504,8 @@ gsb_status gsb_create_scene(const float* means, const float* scales, const float
   if (e == cudaSuccess) e = up(&s->d_L1, h1);
   if (e == cudaSuccess) e = up(&s->d_L2, h2);
   if (e == cudaSuccess) e = up(&s->d_sh, hs);
+  if (e == cudaSuccess) e = dalloc(&s->d_ids, (size_t)n);
+  if (e == cudaSuccess && n > 0) e = cudaMemcpy(s->d_ids, hids.data(), sizeof(int2) * n, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     gsb_destroy_scene(s);
     return fail(e == cudaErrorMemoryAllocation ? GSB_ERR_OUT_OF_MEMORY : GSB_ERR_CUDA, "upload: %s", cudaGetErrorString(e));
@@ -479,22 +531,24 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
   s->tiles_x = (width + kTile - 1) / kTile;
   s->tiles_y = (height + kTile - 1) / kTile;
   s->n_tiles = s->tiles_x * s->tiles_y;
-  s->hist_stride = ((int64_t)s->n_tiles + 1 + 31) / 32 * 32;
+  s->hist_stride = ((int64_t)s->n_tiles + 2 + 31) / 32 * 32;
   const int E = chunk_frames > 0 ? std::min<int64_t>(chunk_frames, F) : (int)std::min<int64_t>(64, F);
   s->chunk = E;
   int64_t cap = key_capacity;
   if (cap == 0) cap = std::max<int64_t>((int64_t)1 << 22, std::min<int64_t>(3 * (int64_t)E * std::max<int64_t>(s->n, 1), ((int64_t)1 << 32) - 1));
   s->cap = cap;
+  s->vis_words = (s->n + 31) / 32;
   const int nb1 = s->n_bodies + 1;
   CUDA_TRY(dalloc(&s->table, (size_t)F * nb1 * 4));
   CUDA_TRY(dalloc(&s->cams, (size_t)F));
   for (int sl = 0; sl < 2; ++sl) {
     CUDA_TRY(dalloc(&s->rec[sl], (size_t)E * std::max<int64_t>(s->n, 1) * 3));
     CUDA_TRY(dalloc(&s->vcount[sl], (size_t)E));
+    CUDA_TRY(dalloc(&s->vis_bits[sl], (size_t)E * std::max<int64_t>(s->vis_words, 1)));
     CUDA_TRY(dalloc(&s->hist[sl], (size_t)E * s->hist_stride));
     CUDA_TRY(dalloc(&s->off[sl], (size_t)E * s->hist_stride));
-    CUDA_TRY(dalloc(&s->frame_base[sl], (size_t)E + 1));
-    CUDA_TRY(cudaMallocHost((void**)&s->h_fb[sl], sizeof(uint64_t) * (E + 1)));
+    CUDA_TRY(dalloc(&s->frame_base[sl], (size_t)E + 2));
+    CUDA_TRY(cudaMallocHost((void**)&s->h_fb[sl], sizeof(uint64_t) * (E + 2)));
     CUDA_TRY(cudaMallocHost((void**)&s->h_vc[sl], sizeof(int) * E));
     CUDA_TRY(cudaEventCreateWithFlags(&s->ev_counts[sl], cudaEventDisableTiming));
   }
@@ -594,6 +648,7 @@ gsb_status gsb_destroy_scene(gsb_scene s) {
   cudaDeviceSynchronize();
   s->free_workspace();
   cudaFree(s->d_mean); cudaFree(s->d_L0); cudaFree(s->d_L1); cudaFree(s->d_L2); cudaFree(s->d_sh);
+  cudaFree(s->d_ids);
   delete s;
   return GSB_OK;
 }
@@ -611,6 +666,7 @@ gsb_status gsb_debug_project(gsb_scene s, const float* poses, int32_t n_envs, in
   LAUNCH_CHECK();
   K1Args a{};
   a.g_mean = s->d_mean; a.g_L0 = s->d_L0; a.g_L1 = s->d_L1; a.g_L2 = s->d_L2; a.g_sh = s->d_sh;
+    a.g_ids = s->d_ids;
   a.n = s->n; a.table = s->table; a.cams = s->cams; a.nb1 = s->n_bodies + 1;
   a.f0 = 0; a.n_frames = F; a.width = p->width; a.height = p->height;
   a.tiles_x = (p->width + kTile - 1) / kTile;
@@ -634,12 +690,14 @@ gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, 
   cudaStream_t st = (cudaStream_t)stream;
   const int tiles_x = (width + kTile - 1) / kTile;
   const int n_tiles = tiles_x * ((height + kTile - 1) / kTile);
-  const int64_t stride = ((int64_t)n_tiles + 1 + 31) / 32 * 32;
+  const int64_t stride = ((int64_t)n_tiles + 2 + 31) / 32 * 32;
   float4* rec = nullptr; int* vcount = nullptr; int* hist = nullptr; uint32_t* off = nullptr;
+  uint32_t* vbits = nullptr;
+  const int64_t vwords = (n + 31) / 32;
   uint64_t* fbase = nullptr; uint64_t* keys = nullptr; uint64_t* keys_alt = nullptr; uint32_t* sorted = nullptr;
   gsb_status result = GSB_OK;
   auto cleanup = [&]() {
-    cudaFree(rec); cudaFree(vcount); cudaFree(hist); cudaFree(off); cudaFree(fbase);
+    cudaFree(rec); cudaFree(vcount); cudaFree(hist); cudaFree(off); cudaFree(fbase); cudaFree(vbits);
     cudaFree(keys); cudaFree(keys_alt); cudaFree(sorted);
   };
 #define DBG_TRY(expr)                                                              \
@@ -652,17 +710,18 @@ gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, 
   } while (0)
   DBG_TRY(dalloc(&rec, (size_t)F * std::max<int64_t>(n, 1) * 3));
   DBG_TRY(dalloc(&vcount, (size_t)F));
+  DBG_TRY(dalloc(&vbits, (size_t)F * std::max<int64_t>(vwords, 1)));
   DBG_TRY(dalloc(&hist, (size_t)F * stride));
   DBG_TRY(dalloc(&off, (size_t)F * stride));
-  DBG_TRY(dalloc(&fbase, (size_t)F + 1));
+  DBG_TRY(dalloc(&fbase, (size_t)F + 2));
   DBG_TRY(cudaMemsetAsync(vcount, 0, sizeof(int) * F, st));
   DBG_TRY(cudaMemsetAsync(hist, 0, sizeof(int) * F * stride, st));
-  launch_k1_external(u, v, sxx, syy, kappa, zbits, valid, n, 0, F, width, height, tiles_x, rec, vcount,
-                     hist, stride, st);
+  launch_k1_external(u, v, sxx, syy, kappa, zbits, valid, n, 0, F, width, height, tiles_x, rec, vbits, vwords,
+                     vcount, hist, stride, st);
   launch_k2_scan(hist, off, stride, F, n_tiles, fbase, st);
   DBG_TRY(cudaGetLastError());
-  std::vector<uint64_t> hfb(F + 1);
-  DBG_TRY(cudaMemcpyAsync(hfb.data(), fbase, sizeof(uint64_t) * (F + 1), cudaMemcpyDeviceToHost, st));
+  std::vector<uint64_t> hfb(F + 2);
+  DBG_TRY(cudaMemcpyAsync(hfb.data(), fbase, sizeof(uint64_t) * (F + 2), cudaMemcpyDeviceToHost, st));
   DBG_TRY(cudaStreamSynchronize(st));
   const uint64_t K = hfb[F];
   *out_K = (int64_t)K;
@@ -674,8 +733,9 @@ gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, 
   DBG_TRY(dalloc(&keys_alt, std::max<uint64_t>(K, 1)));
   DBG_TRY(dalloc(&sorted, std::max<uint64_t>(K, 1)));
   ChunkArgs a{};
-  a.rec = rec; a.n = n; a.vcount = vcount; a.hist = hist; a.hist_stride = stride; a.off = off;
+  a.rec = rec; a.n = n; a.vis_bits = vbits; a.vis_words = vwords; a.hist = hist; a.hist_stride = stride; a.off = off;
   a.frame_base = fbase; a.n_tiles = n_tiles; a.tiles_x = tiles_x; a.fs = 0; a.fe = F; a.key_base = 0;
+  a.min_n = 0;  // K3 sorts every list here
   a.keys = keys; a.keys_alt = keys_alt; a.sorted = sorted;
   launch_k2_emit(a, st);
   launch_k3_sort(a, st);

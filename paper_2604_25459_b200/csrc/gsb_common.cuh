@@ -3,7 +3,9 @@
 // Shared by the kernels K0-K4 only (NOT by the CPU oracle, which is written independently).
 // Data layout in HBM:
 //   template (K5, read-only, shared by every env):  SoA float4 planes of N entries
-//     g_mean[N]  = (x, y, z, body as int bits; -2 = never visible (o < 1/255))
+//     (internal order: by body, then Morton order of the template position)
+//     g_mean[N]  = (x, y, z, max_c s_c^2)
+//     g_ids[N]   = (creation index = the id of reading R10, body; -1 = static)
 //     g_L0[N]    = (L00, L01, L02, L10)   L = R(q_i) diag(s_i): Sigma_local = L L^T
 //     g_L1[N]    = (L11, L12, L20, L21)
 //     g_L2[N]    = (L22, opacity, kappa = 2 ln(255 o), log2 o)
@@ -25,7 +27,6 @@ constexpr float kAlphaMax = 0.99f;    // north_star: alpha clamped at 0.99
 constexpr float kTermT = 1e-4f;       // reading R13
 // log2(1/255): alpha >= 1/255  <=>  log2(o) - Q/2 * log2(e) >= log2(1/255)
 constexpr float kLog2AlphaMin = -7.99435343685885793f;
-constexpr int kBodyNever = -2;
 
 struct FrameCam {
   float fx, fy, cx, cy;
@@ -98,6 +99,37 @@ __device__ __forceinline__ int warp_compact_slot(bool take, int* counter) {
   if (lane == leader) base = atomicAdd(counter, __popc(mask));
   base = __shfl_sync(0xffffffffu, base, leader);
   return base + __popc(mask & lanemask_lt());
+}
+
+// Add 1 to counter[t] for every tile t of this lane's rect (when `has`), aggregated over the
+// warp: lanes whose r-th tile coincides share one atomic (__match_any_sync).  Rects with more
+// than kBigRect tiles are walked by the whole warp cooperatively afterwards.  All 32 lanes of
+// the warp must call this.
+constexpr int kBigRect = 8;
+
+__device__ __forceinline__ void warp_tile_count(bool has, uint32_t rect, int tiles_x, int* counter) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int tx0 = rect & 0xff, tx1 = (rect >> 8) & 0xff, ty0 = (rect >> 16) & 0xff, ty1 = rect >> 24;
+  const int w = tx1 - tx0 + 1;
+  const int nt = has ? w * (ty1 - ty0 + 1) : 0;
+  const bool big = nt > kBigRect;
+  const int rounds = __reduce_max_sync(FULL, big ? 0 : nt);
+  for (int r = 0; r < rounds; ++r) {
+    const bool act = !big && r < nt;
+    const int t = act ? (ty0 + r / w) * tiles_x + tx0 + r % w : -1 - lane;
+    const unsigned peers = __match_any_sync(FULL, t);
+    if (act && lane == __ffs(peers) - 1) atomicAdd(counter + t, __popc(peers));
+  }
+  unsigned bm = __ballot_sync(FULL, big);
+  while (bm) {
+    const int j = __ffs(bm) - 1;
+    bm &= bm - 1;
+    const uint32_t rj = __shfl_sync(FULL, rect, j);
+    const int jx0 = rj & 0xff, jx1 = (rj >> 8) & 0xff, jy0 = (rj >> 16) & 0xff, jy1 = rj >> 24;
+    const int jw = jx1 - jx0 + 1, jn = jw * (jy1 - jy0 + 1);
+    for (int k = lane; k < jn; k += 32) atomicAdd(counter + (jy0 + k / jw) * tiles_x + jx0 + k % jw, 1);
+  }
 }
 
 }  // namespace gsb

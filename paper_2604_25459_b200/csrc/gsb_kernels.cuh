@@ -7,6 +7,8 @@
 
 namespace gsb {
 
+constexpr int kFusedSortCap = 1920;  // tile lists up to this length are sorted inside K4 (6 CTAs/SM)
+
 struct K1Args {
   // template (K5: shared read-only buffer, one copy for every env)
   const float4* g_mean;
@@ -14,6 +16,7 @@ struct K1Args {
   const float4* g_L1;
   const float4* g_L2;
   const float4* g_sh;
+  const int2* g_ids;   // (creation index = id, body) per internal index
   int64_t n;
   // per-frame transforms (K0)
   const float4* table;
@@ -25,8 +28,10 @@ struct K1Args {
   int width, height, tiles_x;
   float near_plane, far_plane;
   // outputs
-  float4* rec;     // [E][N][3] compact records (slots), nullptr for debug-only launches
-  int* vcount;     // [E]
+  float4* rec;     // [E][N][3] records at the internal index, nullptr for debug-only launches
+  uint32_t* vis_bits;  // [E][vis_words] visibility ballot of each warp (32 internal indices)
+  int64_t vis_words;   // ceil(N / 32)
+  int* vcount;     // [E] visible pairs (statistics)
   int* hist;       // [E][hist_stride]
   int64_t hist_stride;
   // debug (dense) outputs, nullptr unless gsb_debug_project
@@ -38,7 +43,8 @@ struct K1Args {
 struct ChunkArgs {
   const float4* rec;      // [E][N][3]
   int64_t n;              // record stride per frame (= N)
-  const int* vcount;      // [E]
+  const uint32_t* vis_bits;  // [E][vis_words]
+  int64_t vis_words;
   int* hist;              // [E][hist_stride]  (counts; reused as emission cursors)
   int64_t hist_stride;
   uint32_t* off;          // [E][hist_stride] exclusive tile offsets within the frame, [T] = K_f
@@ -46,6 +52,7 @@ struct ChunkArgs {
   int n_tiles, tiles_x;
   int fs, fe;             // frame range [fs, fe) of this pass (relative to the chunk)
   uint64_t key_base;      // frame_base[fs]: keys of this pass start at key index 0
+  int min_n;              // K3 sorts only segments with n >= min_n (smaller ones: inside K4)
   uint64_t* keys;         // [cap]   (zbits << 32) | slot
   uint64_t* keys_alt;     // [cap]   scratch for oversize segments
   uint32_t* sorted;       // [cap]   sorted slots
@@ -57,7 +64,8 @@ struct CompositeArgs {
   const uint32_t* off;
   const uint64_t* frame_base;
   int64_t hist_stride;
-  const uint32_t* sorted;
+  const uint32_t* sorted;   // sorted slots of segments longer than kFusedSortCap (K3)
+  const uint64_t* keys;     // unsorted keys: segments up to kFusedSortCap are sorted in K4
   uint64_t key_base;
   int fs, fe;             // relative frames of this pass
   int f0;                 // absolute frame index of chunk frame 0
@@ -79,8 +87,11 @@ void launch_k1(const K1Args& a, int sh_degree, cudaStream_t s);
 void launch_k1_external(const float* u, const float* v, const float* sxx, const float* syy,
                         const float* kappa, const uint32_t* zbits, const uint8_t* valid,
                         int64_t n, int f0, int n_frames, int width, int height, int tiles_x,
-                        float4* rec, int* vcount, int* hist, int64_t hist_stride, cudaStream_t s);
+                        float4* rec, uint32_t* vis_bits, int64_t vis_words, int* vcount, int* hist,
+                        int64_t hist_stride, cudaStream_t s);
 
+// off[f][T] = K_f, off[f][T+1] = longest tile list of frame f; frame_base[E] = total keys,
+// frame_base[E+1] = longest tile list of the chunk
 void launch_k2_scan(int* hist, uint32_t* off, int64_t hist_stride, int n_frames, int n_tiles,
                     uint64_t* frame_base, cudaStream_t s);
 void launch_k2_emit(const ChunkArgs& a, cudaStream_t s);

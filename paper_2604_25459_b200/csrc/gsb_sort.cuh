@@ -1,0 +1,155 @@
+// gsb_sort.cuh — block-wide segment sort used by K3 (long tile lists, in HBM) and by K4
+// (tile lists up to kFusedSortCap, in shared memory).
+//
+// north_star (3): hand-written segmented radix sort, deterministic tie-break on Gaussian id;
+// reading R10: a tile list is ordered by (bits(z_f32), id).  LSD radix (8-bit digits) over the
+// top 16 varying depth bits; every pass is a stable counting scatter ranked per warp with
+// __match_any_sync; runs equal on those bits are finished by (zbits, id) (ids read from the
+// records), so the result is unique whatever order the keys arrived in.
+#pragma once
+#include "gsb_common.cuh"
+
+namespace gsb {
+
+// Block sort over NT threads (NT = 128 in K4, 256 in K3); 8-bit digits, 256 bins.
+template <int NT>
+struct SortShared {
+  static constexpr int kWarps = NT / 32;
+  uint32_t whist[kWarps][256];
+  uint32_t base[256];
+  uint32_t wred[kWarps];
+};
+
+__device__ __forceinline__ uint32_t hi32(uint64_t k) { return (uint32_t)(k >> 32); }
+
+// exclusive scan over the block of one value per bin (256 bins, NT threads)
+template <int NT>
+__device__ __forceinline__ void bins_excl_scan(SortShared<NT>& sm) {
+  constexpr int PER = 256 / NT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t v[PER], sum = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) { v[k] = sm.base[tid * PER + k]; sum += v[k]; }
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) sm.wred[warp] = inc;
+  __syncthreads();
+  uint32_t run = inc - sum;
+#pragma unroll
+  for (int w = 0; w < SortShared<NT>::kWarps; ++w) run += (w < warp) ? sm.wred[w] : 0u;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) { sm.base[tid * PER + k] = run; run += v[k]; }
+  __syncthreads();
+}
+
+// one stable counting pass on digit (hi32(key) >> shift) & 0xff: src -> dst
+template <int NT, typename Ptr>
+__device__ __forceinline__ void radix_pass(const Ptr src, Ptr dst, int n, int shift, SortShared<NT>& sm) {
+  constexpr int kWarps = SortShared<NT>::kWarps;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // digit histogram
+  for (int b = tid; b < 256; b += NT) sm.base[b] = 0;
+  __syncthreads();
+  for (int e = tid; e < n; e += NT) atomicAdd(&sm.base[(hi32(src[e]) >> shift) & 0xffu], 1u);
+  __syncthreads();
+  bins_excl_scan(sm);
+  // chunked stable scatter
+  for (int c = 0; c < n; c += NT) {
+    const int e = c + tid;
+    const bool valid = e < n;
+    const uint64_t key = valid ? src[e] : 0ull;
+    const uint32_t d = valid ? ((hi32(key) >> shift) & 0xffu) : 256u + lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t rank = __popc(peers & lanemask_lt());
+    for (int b = tid; b < 256; b += NT)
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) sm.whist[w][b] = 0;
+    __syncthreads();
+    if (valid && rank == 0) sm.whist[warp][d] = __popc(peers);
+    __syncthreads();
+    for (int b = tid; b < 256; b += NT) {
+      uint32_t run = sm.base[b];
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const uint32_t t = sm.whist[w][b];
+        sm.whist[w][b] = run;
+        run += t;
+      }
+      sm.base[b] = run;
+    }
+    __syncthreads();
+    if (valid) dst[sm.whist[warp][d] + rank] = key;
+    __syncthreads();
+  }
+}
+
+// Sort keys[0..n) into (bits(z), id) order.  Two stable 8-bit LSD passes order the keys by
+// the 16 highest bits of z that vary over the segment (bits above them are constant); runs
+// that agree on those bits (rare: it takes two depths within 2^-16 of the segment's depth
+// range) are then insertion-sorted by the full (zbits, id).  The id of a key is read from
+// its record (key low 32 bits = record slot).  Returns true if the result ended in `b`.
+template <int NT, typename Ptr>
+__device__ __forceinline__ bool segment_sort(Ptr a, Ptr b, int n, const float4* __restrict__ rec,
+                                             SortShared<NT>& sm) {
+  constexpr int kWarps = SortShared<NT>::kWarps;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // which depth bits vary over the segment?
+  const uint32_t first = hi32(a[0]);
+  uint32_t orx = 0;
+  for (int e = tid; e < n; e += NT) orx |= hi32(a[e]) ^ first;
+  orx = __reduce_or_sync(0xffffffffu, orx);
+  if (lane == 0) sm.wred[warp] = orx;
+  __syncthreads();
+  orx = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) orx |= sm.wred[w];
+  __syncthreads();
+  const int hb = orx ? 31 - __clz(orx) : -1;       // highest varying bit
+  const int lo = hb >= 16 ? hb - 15 : 0;           // sort bits [lo, lo + 16)
+  bool in_b = false;
+  if (hb >= 0) {
+    if (((orx >> lo) & 0xffu) != 0) {
+      radix_pass(a, b, n, lo, sm);
+      in_b = true;
+    }
+    if (((orx >> (lo + 8)) & 0xffu) != 0) {
+      if (in_b) radix_pass(b, a, n, lo + 8, sm);
+      else radix_pass(a, b, n, lo + 8, sm);
+      in_b = !in_b;
+    }
+  }
+  Ptr r = in_b ? b : a;
+  // runs equal on the sorted bits: finish them by (zbits, id) (reading R10 tie-break on id)
+  int dup = 0;
+  for (int e = tid + 1; e < n; e += NT) dup |= (hi32(r[e]) >> lo) == (hi32(r[e - 1]) >> lo);
+  if (__syncthreads_or(dup)) {
+    for (int e = tid; e < n; e += NT) {
+      const uint32_t h = hi32(r[e]) >> lo;
+      const bool start = (e == 0 || (hi32(r[e - 1]) >> lo) != h) && (e + 1 < n && (hi32(r[e + 1]) >> lo) == h);
+      if (!start) continue;
+      int end = e + 1;
+      while (end < n && (hi32(r[end]) >> lo) == h) ++end;
+      for (int x = e + 1; x < end; ++x) {  // insertion sort of the run by (zbits, id)
+        const uint64_t kx = r[x];
+        const uint64_t fx = ((uint64_t)hi32(kx) << 32) | (uint32_t)__float_as_int(rec[(size_t)(uint32_t)kx * 3 + 1].w);
+        int y = x - 1;
+        while (y >= e) {
+          const uint64_t ky = r[y];
+          const uint64_t fy = ((uint64_t)hi32(ky) << 32) | (uint32_t)__float_as_int(rec[(size_t)(uint32_t)ky * 3 + 1].w);
+          if (fy <= fx) break;
+          r[y + 1] = ky;
+          --y;
+        }
+        r[y + 1] = kx;
+      }
+    }
+    __syncthreads();
+  }
+  return in_b;
+}
+
+}  // namespace gsb

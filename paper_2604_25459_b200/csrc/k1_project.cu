@@ -132,24 +132,29 @@ __device__ __forceinline__ float det2(float a, float b, float c, float d) {
 
 // ------------------------------------------------------------------------------ K1
 template <int D>
-__global__ void __launch_bounds__(128) k1_project(K1Args a) {
+__global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool in = i < a.n;
-  float4 mean = make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+  float4 mean = make_float4(0.f, 0.f, 0.f, 0.f);
   float4 l0 = make_float4(0.f, 0.f, 0.f, 0.f), l1 = l0, l2 = l0;
+  int2 ids = make_int2(0, -1);
   if (in) {
     mean = __ldg(a.g_mean + i);
     l0 = __ldg(a.g_L0 + i);
     l1 = __ldg(a.g_L1 + i);
     l2 = __ldg(a.g_L2 + i);
+    ids = __ldg(a.g_ids + i);
   }
-  const int body = __float_as_int(mean.w);
+  const int id = ids.x;     // creation index (reading R10 tie-break)
+  const int body = ids.y;   // -1 = static
+  const float smax2 = mean.w;  // largest squared scale: bounds the 2D extent (screen cull)
   const float L[3][3] = {{l0.x, l0.y, l0.z}, {l0.w, l1.x, l1.y}, {l1.z, l1.w, l2.x}};
   const float opac = l2.y, kappa = l2.z, log2o = l2.w;
   // reading R5: o < 1/255 is never visible (binary32 compare == the exact compare)
   const bool o_ok = in && (opac >= 1.0f / 255.0f);
   const bool debug = a.dbg_rec != nullptr;
   const float wscale = 0.84932180028801904f;  // sqrt(log2(e) / 2)
+  const float fw = (float)a.width, fh = (float)a.height;
 
   for (int fl = 0; fl < a.n_frames; ++fl) {
     const int f = a.f0 + fl;
@@ -166,71 +171,84 @@ __global__ void __launch_bounds__(128) k1_project(K1Args a) {
       const FrameCam cam = a.cams[f];
       const float x = fmaf(r0.x, mean.x, fmaf(r0.y, mean.y, fmaf(r0.z, mean.z, r0.w)));
       const float y = fmaf(r1.x, mean.x, fmaf(r1.y, mean.y, fmaf(r1.z, mean.z, r1.w)));
-      const float iz = 1.0f / z;
+      const float iz = __frcp_rn(z);
       const float xz = x * iz, yz = y * iz;
       u = fmaf(cam.fx, xz, cam.cx);
       v = fmaf(cam.fy, yz, cam.cy);
-      // EWA Jacobian with the 1.3 frustum clamp (reading R6), applied to M: rows of J M
-      const float txz = fminf(fmaxf(xz, -cam.limx), cam.limx);
-      const float tyz = fminf(fmaxf(yz, -cam.limy), cam.limy);
       const float jx = cam.fx * iz, jy = cam.fy * iz;
-      const float m0[3] = {jx * fmaf(-txz, r2.x, r0.x), jx * fmaf(-txz, r2.y, r0.y), jx * fmaf(-txz, r2.z, r0.z)};
-      const float m1[3] = {jy * fmaf(-tyz, r2.x, r1.x), jy * fmaf(-tyz, r2.y, r1.y), jy * fmaf(-tyz, r2.z, r1.z)};
-      // A = (J M) L (2x3); Sigma2D = A A^T + 0.3 I (reading R7)
-      float A0[3], A1[3];
+      // Conservative screen cull: Sigma2D_xx <= jx^2 (1 + limx^2) smax^2 + 0.3 (rows of M are
+      // orthonormal, |t/z| <= lim after the clamp), so the exact R9 extents are inside
+      // bx, by; a Gaussian whose bound box misses the image has an empty R9 rect as well.
+      const float bx = 1.02f * sqrtf(kappa * fmaf(jx * jx * (1.f + cam.limx * cam.limx), smax2, 0.3f)) + 1.f;
+      const float by = 1.02f * sqrtf(kappa * fmaf(jy * jy * (1.f + cam.limy * cam.limy), smax2, 0.3f)) + 1.f;
+      const bool offscreen = (u + bx < 0.f) || (u - bx > fw) || (v + by < 0.f) || (v - by > fh);
+      if (!offscreen || debug) {
+        // EWA Jacobian with the 1.3 frustum clamp (reading R6), applied to M: rows of J M
+        const float txz = fminf(fmaxf(xz, -cam.limx), cam.limx);
+        const float tyz = fminf(fmaxf(yz, -cam.limy), cam.limy);
+        const float m0[3] = {jx * fmaf(-txz, r2.x, r0.x), jx * fmaf(-txz, r2.y, r0.y), jx * fmaf(-txz, r2.z, r0.z)};
+        const float m1[3] = {jy * fmaf(-tyz, r2.x, r1.x), jy * fmaf(-tyz, r2.y, r1.y), jy * fmaf(-tyz, r2.z, r1.z)};
+        // A = (J M) L (2x3); Sigma2D = A A^T + 0.3 I (reading R7)
+        float A0[3], A1[3];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        A0[c] = fmaf(m0[0], L[0][c], fmaf(m0[1], L[1][c], m0[2] * L[2][c]));
-        A1[c] = fmaf(m1[0], L[0][c], fmaf(m1[1], L[1][c], m1[2] * L[2][c]));
-      }
-      const float sxx0 = fmaf(A0[0], A0[0], fmaf(A0[1], A0[1], A0[2] * A0[2]));
-      const float syy0 = fmaf(A1[0], A1[0], fmaf(A1[1], A1[1], A1[2] * A1[2]));
-      const float sxy = fmaf(A0[0], A1[0], fmaf(A0[1], A1[1], A0[2] * A1[2]));
-      const float sxx = sxx0 + 0.3f, syy = syy0 + 0.3f;
-      // det(A A^T) by Cauchy-Binet (sum of squared 2x2 minors) + 0.3 tr + 0.09: no cancellation
-      const float n01 = det2(A0[0], A0[1], A1[0], A1[1]);
-      const float n02 = det2(A0[0], A0[2], A1[0], A1[2]);
-      const float n12 = det2(A0[1], A0[2], A1[1], A1[2]);
-      const float det = fmaf(n01, n01, fmaf(n02, n02, fmaf(n12, n12, fmaf(0.3f, sxx0 + syy0, 0.09f))));
-      // whitening (Cholesky) factor of Sigma2D^-1:  Q = (p dx)^2 + (q dx + r dy)^2
-      const float il11 = 1.0f / sqrtf(sxx);
-      const float r_ = 1.0f / sqrtf(det / sxx);
-      const float q_ = -sxy * il11 * il11 * r_;
-      pw = wscale * il11;
-      qw = wscale * q_;
-      rw = wscale * r_;
-      const bool rect_ok = r9_rect(u, v, sxx, syy, kappa, a.width, a.height, tx0, tx1, ty0, ty1);
-      vis = keep && rect_ok;
-      if (vis || debug) {
-        // view direction in the body frame (reading R19)
-        const float4 cb = __ldg(tb + 3);
-        const float dx = mean.x - cb.x, dy = mean.y - cb.y, dz = mean.z - cb.z;
-        const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
-        rgb = sh_colour<D>(a.g_sh, a.n, in ? i : 0, dx * inv, dy * inv, dz * inv);
-      }
-      if (debug && in) {
-        const size_t o = (size_t)f * a.n + i;
-        float* d = a.dbg_rec + o * 12;
-        const float idet = 1.0f / det;
-        d[0] = u; d[1] = v; d[2] = syy * idet; d[3] = -sxy * idet; d[4] = sxx * idet;
-        d[5] = opac; d[6] = rgb.x; d[7] = rgb.y; d[8] = rgb.z; d[9] = z; d[10] = sxx; d[11] = syy;
+        for (int c = 0; c < 3; ++c) {
+          A0[c] = fmaf(m0[0], L[0][c], fmaf(m0[1], L[1][c], m0[2] * L[2][c]));
+          A1[c] = fmaf(m1[0], L[0][c], fmaf(m1[1], L[1][c], m1[2] * L[2][c]));
+        }
+        const float sxx0 = fmaf(A0[0], A0[0], fmaf(A0[1], A0[1], A0[2] * A0[2]));
+        const float syy0 = fmaf(A1[0], A1[0], fmaf(A1[1], A1[1], A1[2] * A1[2]));
+        const float sxy = fmaf(A0[0], A1[0], fmaf(A0[1], A1[1], A0[2] * A1[2]));
+        const float sxx = sxx0 + 0.3f, syy = syy0 + 0.3f;
+        // det(A A^T) by Cauchy-Binet (sum of squared 2x2 minors) + 0.3 tr + 0.09: no cancellation
+        const float n01 = det2(A0[0], A0[1], A1[0], A1[1]);
+        const float n02 = det2(A0[0], A0[2], A1[0], A1[2]);
+        const float n12 = det2(A0[1], A0[2], A1[1], A1[2]);
+        const float det = fmaf(n01, n01, fmaf(n02, n02, fmaf(n12, n12, fmaf(0.3f, sxx0 + syy0, 0.09f))));
+        // whitening (Cholesky) factor of Sigma2D^-1:  Q = (p dx)^2 + (q dx + r dy)^2
+        const float il11 = rsqrtf(sxx);
+        const float r_ = rsqrtf(__fdividef(det, sxx));
+        const float q_ = -sxy * il11 * il11 * r_;
+        pw = wscale * il11;
+        qw = wscale * q_;
+        rw = wscale * r_;
+        const bool rect_ok = r9_rect(u, v, sxx, syy, kappa, a.width, a.height, tx0, tx1, ty0, ty1);
+        vis = keep && rect_ok;
+        if (vis || debug) {
+          // view direction in the body frame (reading R19)
+          const float4 cb = __ldg(tb + 3);
+          const float dx = mean.x - cb.x, dy = mean.y - cb.y, dz = mean.z - cb.z;
+          const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
+          rgb = sh_colour<D>(a.g_sh, a.n, in ? i : 0, dx * inv, dy * inv, dz * inv);
+        }
+        if (debug && in) {
+          const size_t o = (size_t)f * a.n + id;
+          float* d = a.dbg_rec + o * 12;
+          const float idet = 1.0f / det;
+          d[0] = u; d[1] = v; d[2] = syy * idet; d[3] = -sxy * idet; d[4] = sxx * idet;
+          d[5] = opac; d[6] = rgb.x; d[7] = rgb.y; d[8] = rgb.z; d[9] = z; d[10] = sxx; d[11] = syy;
+          if (offscreen && rect_ok) d[11] = __int_as_float(0x7fc0dead);  // bound violated: flag loudly
+        }
       }
     }
     if (debug && in) {
-      a.dbg_zbits[(size_t)f * a.n + i] = __float_as_uint(z);
-      a.dbg_valid[(size_t)f * a.n + i] = (uint8_t)keep;
+      a.dbg_zbits[(size_t)f * a.n + id] = __float_as_uint(z);
+      a.dbg_valid[(size_t)f * a.n + id] = (uint8_t)keep;
     }
     if (a.rec == nullptr) continue;  // debug-only launch
-    const int slot = warp_compact_slot(vis, a.vcount + fl);
-    if (vis) {
-      float4* r = a.rec + ((size_t)fl * a.n + slot) * 3;
-      r[0] = make_float4(u, v, pw, qw);
-      r[1] = make_float4(rw, log2o, z, __int_as_float((int)i));
-      r[2] = make_float4(rgb.x, rgb.y, rgb.z, __uint_as_float(pack_rect(tx0, tx1, ty0, ty1)));
-      int* h = a.hist + (size_t)fl * a.hist_stride;
-      for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(h + ty * a.tiles_x + tx, 1);
+    // record slot = internal index: no compaction atomics; one visibility word per warp
+    const unsigned bal = __ballot_sync(0xffffffffu, vis);
+    if ((threadIdx.x & 31) == 0 && i < a.n) {
+      a.vis_bits[(size_t)fl * a.vis_words + (i >> 5)] = bal;
+      if (bal) atomicAdd(a.vcount + fl, __popc(bal));  // V counter (no return value: RED)
     }
+    const uint32_t rect = pack_rect(tx0, tx1, ty0, ty1);
+    if (vis) {
+      float4* r = a.rec + ((size_t)fl * a.n + i) * 3;
+      r[0] = make_float4(u, v, pw, qw);
+      r[1] = make_float4(rw, log2o, z, __int_as_float(id));
+      r[2] = make_float4(rgb.x, rgb.y, rgb.z, __uint_as_float(rect));
+    }
+    warp_tile_count(vis, rect, a.tiles_x, a.hist + (size_t)fl * a.hist_stride);
   }
 }
 

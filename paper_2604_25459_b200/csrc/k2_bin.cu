@@ -28,16 +28,18 @@ __global__ void __launch_bounds__(kScanThreads) k2_scan_tiles(int* __restrict__ 
                                                               uint32_t* __restrict__ off,
                                                               int64_t stride, int n_tiles) {
   __shared__ uint32_t wsum[kScanThreads / 32];
-  __shared__ uint32_t carry_s;
+  __shared__ uint32_t carry_s, max_s;
   const int f = blockIdx.x;
   int* h = hist + (size_t)f * stride;
   uint32_t* o = off + (size_t)f * stride;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) carry_s = 0;
+  if (tid == 0) carry_s = 0, max_s = 0;
   __syncthreads();
+  uint32_t mx = 0;
   for (int base = 0; base < n_tiles; base += kScanThreads) {
     const int t = base + tid;
     const uint32_t x = t < n_tiles ? (uint32_t)h[t] : 0u;
+    mx = max(mx, x);
     const uint32_t inc = warp_incl_scan(x);
     if (lane == 31) wsum[warp] = inc;
     __syncthreads();
@@ -56,19 +58,27 @@ __global__ void __launch_bounds__(kScanThreads) k2_scan_tiles(int* __restrict__ 
     if (tid == kScanThreads - 1) carry_s = carry + wsum[warp] + inc;
     __syncthreads();
   }
-  if (tid == 0) o[n_tiles] = carry_s;
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0) atomicMax(&max_s, mx);
+  __syncthreads();
+  if (tid == 0) {
+    o[n_tiles] = carry_s;
+    o[n_tiles + 1] = max_s;
+  }
 }
 
 // frame_base[0..E] = exclusive prefix of K_f = off[f][T] (single block)
 __global__ void k2_scan_frames(const uint32_t* __restrict__ off, int64_t stride, int n_tiles,
                                int n_frames, uint64_t* __restrict__ frame_base) {
   if (threadIdx.x != 0) return;
-  uint64_t acc = 0;
+  uint64_t acc = 0, mx = 0;
   for (int f = 0; f < n_frames; ++f) {
     frame_base[f] = acc;
     acc += off[(size_t)f * stride + n_tiles];
+    mx = max(mx, (uint64_t)off[(size_t)f * stride + n_tiles + 1]);
   }
   frame_base[n_frames] = acc;
+  frame_base[n_frames + 1] = mx;
 }
 
 void launch_k2_scan(int* hist, uint32_t* off, int64_t hist_stride, int n_frames, int n_tiles,
@@ -78,24 +88,57 @@ void launch_k2_scan(int* hist, uint32_t* off, int64_t hist_stride, int n_frames,
 }
 
 // ------------------------------------------------------------------------------ emission
+// One thread per (frame, internal index); warps with no visible Gaussian (ballot word 0) exit
+// at once.  Keys of a warp's Gaussians that land in the same tile share one cursor atomic (the
+// template is Morton-ordered, so a warp's Gaussians overlap the same tiles); rects with more
+// than kBigRect tiles are emitted by the whole warp cooperatively.
 __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
+  const unsigned FULL = 0xffffffffu;
   const int fl = a.fs + blockIdx.y;
-  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (slot >= a.vcount[fl]) return;
-  const float4* r = a.rec + ((size_t)fl * a.n + slot) * 3;
-  const float z = __ldg(&r[1].z);
-  const uint32_t rect = __float_as_uint(__ldg(&r[2].w));
-  const int tx0 = rect & 0xff, tx1 = (rect >> 8) & 0xff, ty0 = (rect >> 16) & 0xff, ty1 = rect >> 24;
-  const uint64_t key = ((uint64_t)__float_as_uint(z) << 32) | (uint64_t)slot;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) >= a.n) return;  // whole warp past N
+  const unsigned word = a.vis_bits[(size_t)fl * a.vis_words + (i >> 5)];
+  if (word == 0) return;  // warp-uniform
+  const int lane = threadIdx.x & 31;
+  const bool has = (word >> lane) & 1u;
+  uint32_t rect = 0, zb = 0;
+  if (has) {
+    const float4* r = a.rec + ((size_t)fl * a.n + i) * 3;
+    zb = __float_as_uint(__ldg(&r[1].z));
+    rect = __float_as_uint(__ldg(&r[2].w));
+  }
+  const uint64_t key = ((uint64_t)zb << 32) | (uint64_t)i;
   int* cur = a.hist + (size_t)fl * a.hist_stride;
   const uint32_t* off = a.off + (size_t)fl * a.hist_stride;
-  const uint64_t fb = a.frame_base[fl] - a.key_base;
-  for (int ty = ty0; ty <= ty1; ++ty)
-    for (int tx = tx0; tx <= tx1; ++tx) {
-      const int t = ty * a.tiles_x + tx;
-      const uint32_t pos = (uint32_t)atomicAdd(cur + t, 1);
-      a.keys[fb + off[t] + pos] = key;
+  uint64_t* keys = a.keys + (a.frame_base[fl] - a.key_base);
+  const int tx0 = rect & 0xff, tx1 = (rect >> 8) & 0xff, ty0 = (rect >> 16) & 0xff, ty1 = rect >> 24;
+  const int w = tx1 - tx0 + 1;
+  const int nt = has ? w * (ty1 - ty0 + 1) : 0;
+  const bool big = nt > kBigRect;
+  const int rounds = __reduce_max_sync(FULL, big ? 0 : nt);
+  for (int r = 0; r < rounds; ++r) {
+    const bool act = !big && r < nt;
+    const int t = act ? (ty0 + r / w) * a.tiles_x + tx0 + r % w : -1 - lane;
+    const unsigned peers = __match_any_sync(FULL, t);
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (act && lane == leader) base = atomicAdd(cur + t, __popc(peers));
+    base = __shfl_sync(FULL, base, leader);
+    if (act) keys[off[t] + base + __popc(peers & lanemask_lt())] = key;
+  }
+  unsigned bm = __ballot_sync(FULL, big);
+  while (bm) {
+    const int j = __ffs(bm) - 1;
+    bm &= bm - 1;
+    const uint32_t rj = __shfl_sync(FULL, rect, j);
+    const uint64_t kj = __shfl_sync(FULL, key, j);
+    const int jx0 = rj & 0xff, jx1 = (rj >> 8) & 0xff, jy0 = (rj >> 16) & 0xff, jy1 = rj >> 24;
+    const int jw = jx1 - jx0 + 1, jn = jw * (jy1 - jy0 + 1);
+    for (int k = lane; k < jn; k += 32) {
+      const int t = (jy0 + k / jw) * a.tiles_x + jx0 + k % jw;
+      keys[off[t] + atomicAdd(cur + t, 1)] = kj;
     }
+  }
 }
 
 void launch_k2_emit(const ChunkArgs& a, cudaStream_t s) {
@@ -112,7 +155,8 @@ __global__ void __launch_bounds__(128) k1_external(const float* __restrict__ u, 
                                                    const uint32_t* __restrict__ zbits,
                                                    const uint8_t* __restrict__ valid, int64_t n, int f0,
                                                    int n_frames, int width, int height, int tiles_x,
-                                                   float4* __restrict__ rec, int* __restrict__ vcount,
+                                                   float4* __restrict__ rec, uint32_t* __restrict__ vis_bits,
+                                                   int64_t vis_words, int* __restrict__ vcount,
                                                    int* __restrict__ hist, int64_t hist_stride) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool in = i < n;
@@ -122,27 +166,31 @@ __global__ void __launch_bounds__(128) k1_external(const float* __restrict__ u, 
     bool vis = false;
     if (in && valid[o])
       vis = r9_rect(u[o], v[o], sxx[o], syy[o], kappa[o], width, height, tx0, tx1, ty0, ty1);
-    const int slot = warp_compact_slot(vis, vcount + fl);
+    const unsigned bal = __ballot_sync(0xffffffffu, vis);
+    if ((threadIdx.x & 31) == 0 && i < n) {
+      vis_bits[(size_t)fl * vis_words + (i >> 5)] = bal;
+      if (bal) atomicAdd(vcount + fl, __popc(bal));
+    }
+    const uint32_t rect = pack_rect(tx0, tx1, ty0, ty1);
     if (vis) {
-      float4* r = rec + ((size_t)fl * n + slot) * 3;
+      float4* r = rec + ((size_t)fl * n + i) * 3;
       r[0] = make_float4(u[o], v[o], 0.f, 0.f);
       r[1] = make_float4(0.f, 0.f, __uint_as_float(zbits[o]), __int_as_float((int)i));
-      r[2] = make_float4(0.f, 0.f, 0.f, __uint_as_float(pack_rect(tx0, tx1, ty0, ty1)));
-      int* h = hist + (size_t)fl * hist_stride;
-      for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(h + ty * tiles_x + tx, 1);
+      r[2] = make_float4(0.f, 0.f, 0.f, __uint_as_float(rect));
     }
+    warp_tile_count(vis, rect, tiles_x, hist + (size_t)fl * hist_stride);
   }
 }
 
 void launch_k1_external(const float* u, const float* v, const float* sxx, const float* syy,
                         const float* kappa, const uint32_t* zbits, const uint8_t* valid,
                         int64_t n, int f0, int n_frames, int width, int height, int tiles_x,
-                        float4* rec, int* vcount, int* hist, int64_t hist_stride, cudaStream_t s) {
+                        float4* rec, uint32_t* vis_bits, int64_t vis_words, int* vcount, int* hist,
+                        int64_t hist_stride, cudaStream_t s) {
   if (n == 0) return;
   k1_external<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(u, v, sxx, syy, kappa, zbits, valid, n, f0,
-                                                          n_frames, width, height, tiles_x, rec,
-                                                          vcount, hist, hist_stride);
+                                                          n_frames, width, height, tiles_x, rec, vis_bits,
+                                                          vis_words, vcount, hist, hist_stride);
 }
 
 // sorted slots -> Gaussian ids (debug_bin_sort output)

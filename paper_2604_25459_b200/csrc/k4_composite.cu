@@ -1,4 +1,4 @@
-// k4_composite.cu — K4: per-tile front-to-back alpha compositing.
+// k4_composite.cu — K4: per-tile depth sort + front-to-back alpha compositing.
 //
 // north_star / readings R12-R16 (3DGS formulation, cited P:212; outputs per P:225):
 //   for each pixel, over its tile's list in (depth, id) order:
@@ -11,15 +11,37 @@
 // so "alpha < 1/255" is the test arg < log2(1/255), decided before any exp2; the exp2 is
 // the MUFU ex2.approx (reading R27).
 //
-// One CTA per (frame, 16x16 tile), one pixel per thread; records are staged through shared
-// memory 256 at a time; the CTA stops as soon as every pixel has terminated
-// (__syncthreads_count vote on the per-thread done flags).
+// One CTA per (frame, 16x16 tile), 128 threads, two vertically adjacent pixels per thread
+// (the dx terms of the quadratic form and the shared-memory loads serve both).  The tile's keys (unsorted, as K2
+// emitted them) are loaded into shared memory and sorted there by the segmented radix sort
+// of gsb_sort.cuh (lists longer than kFusedSortCap were sorted by K3 into HBM instead) — so
+// sorting, which is barrier-bound, overlaps with the ALU-bound compositing of the other CTAs
+// resident on the SM.  Records are then staged through shared memory 256 at a time and the
+// CTA stops as soon as every pixel has terminated (__syncthreads_count vote).
 #include "gsb_common.cuh"
 #include "gsb_kernels.cuh"
+#include "gsb_sort.cuh"
 
 namespace gsb {
 
-constexpr int kCompThreads = 256;
+constexpr int kCompThreads = 128;          // 2 pixels per thread: a 16x16 tile per CTA
+constexpr int kBatch = 256;                // records staged per shared-memory round
+static_assert(kBatch == 2 * kCompThreads, "each thread stages two records per round");
+
+// Shared memory: the sort's two key buffers are dead once the tile list is ordered, so the
+// sorted slots (u32) and the record staging area reuse them (6 CTAs = 24 warps per SM).
+struct K4Shared {
+  SortShared<kCompThreads> sort;
+  union {
+    uint64_t keys[2][kFusedSortCap];
+    struct {
+      uint32_t slots[kFusedSortCap];
+      float4 s0[kBatch], s1[kBatch], s2[kBatch];
+    } c;
+  } u;
+  unsigned long long red[kCompThreads / 32];
+};
+static_assert(sizeof(uint32_t) * kFusedSortCap + 3 * 16 * kBatch <= 2 * 8 * kFusedSortCap, "union layout");
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -27,84 +49,144 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-__global__ void __launch_bounds__(kCompThreads) k4_composite(CompositeArgs a) {
-  __shared__ float4 s0[kCompThreads], s1[kCompThreads], s2[kCompThreads];
-  __shared__ unsigned long long red[kCompThreads / 32];
+// Front-to-back blend of one list entry into one pixel (readings R12-R14), predicated on
+// `use` (alpha >= 1/255 for a live pixel).  A pixel that terminates gets its centre moved to
+// kFar: every later quadratic form is then huge and every later entry fails the alpha test
+// without any per-pixel "done" test in the hot loop.
+constexpr float kFar = 1e20f;
+
+__device__ __forceinline__ void blend(bool use, float arg, const float4& r1, const float4& r2, float& T,
+                                      float& cr, float& cg, float& cb, float& dep, float& pyc, int& n_eval,
+                                      int idx) {
+  const float alpha = fminf(kAlphaMax, ex2_approx(arg));
+  const float w = alpha * T;
+  const float tT = T - w;                       // T (1 - alpha)
+  const bool term = use && tT < kTermT;         // stop before blending (R13)
+  const bool add = use && !term;
+  const float wa = add ? w : 0.f;
+  cr = fmaf(wa, r2.x, cr);
+  cg = fmaf(wa, r2.y, cg);
+  cb = fmaf(wa, r2.z, cb);
+  dep = fmaf(wa, r1.z, dep);
+  T = add ? tT : T;
+  if (term) {
+    n_eval = idx + 1;
+    pyc = kFar;
+  }
+}
+
+__global__ void __launch_bounds__(kCompThreads, 6) k4_composite(CompositeArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K4Shared& sm = *reinterpret_cast<K4Shared*>(smem_raw);
   const int fl = a.fs + blockIdx.x / a.n_tiles;
   const int t = blockIdx.x % a.n_tiles;
   const int tx = t % a.tiles_x, ty = t / a.tiles_x;
   const int tid = threadIdx.x;
-  const int px = tx * kTile + (tid & 15), py = ty * kTile + (tid >> 4);
-  const bool inside = px < a.width && py < a.height;
+  // thread -> pixels (px, py0) and (px, py0 + 1): a warp covers 16 x 4 pixels
+  const int px = tx * kTile + (tid & 15);
+  const int py0 = ty * kTile + 2 * (tid >> 4);
+  const bool in_x = px < a.width;
+  const bool in0 = in_x && py0 < a.height, in1 = in_x && py0 + 1 < a.height;
   const uint32_t* off = a.off + (size_t)fl * a.hist_stride;
   const uint64_t start = a.frame_base[fl] - a.key_base + off[t];
   const int len = (int)(off[t + 1] - off[t]);
   const float4* rec = a.rec + (size_t)fl * a.n * 3;
-  const float pxc = (float)px + 0.5f, pyc = (float)py + 0.5f;
+  const float pxc = (float)px + 0.5f;
 
-  float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f, dep = 0.f;
-  bool done = !inside;
-  int n_eval = len;
-  for (int b = 0; b < len; b += kCompThreads) {
-    const int k = b + tid;
-    if (k < len) {
-      const uint32_t slot = a.sorted[start + k];
-      const float4* r = rec + (size_t)slot * 3;
-      s0[tid] = __ldg(r);
-      s1[tid] = __ldg(r + 1);
-      s2[tid] = __ldg(r + 2);
+  // depth order of this tile's list (reading R10): sorted here, or by K3 if too long
+  const bool fused = len <= kFusedSortCap;
+  if (fused && len > 0) {
+    for (int e = tid; e < len; e += kCompThreads) sm.u.keys[0][e] = a.keys[start + e];
+    __syncthreads();
+    const bool in_b = len > 1 && segment_sort(sm.u.keys[0], sm.u.keys[1], len, rec, sm.sort);
+    uint32_t sl[kFusedSortCap / kCompThreads];
+#pragma unroll
+    for (int k = 0; k < kFusedSortCap / kCompThreads; ++k) {
+      const int e = tid + k * kCompThreads;
+      if (e < len) sl[k] = (uint32_t)sm.u.keys[in_b ? 1 : 0][e];
     }
     __syncthreads();
-    if (!done) {
-      const int cnt = min(kCompThreads, len - b);
-      for (int j = 0; j < cnt; ++j) {
-        const float4 r0 = s0[j];
-        const float4 r1 = s1[j];
-        const float dx = r0.x - pxc, dy = r0.y - pyc;
-        const float t1 = r0.z * dx;
-        const float t2 = fmaf(r0.w, dx, r1.x * dy);
-        const float arg = fmaf(-t1, t1, fmaf(-t2, t2, r1.y));
-        if (arg < kLog2AlphaMin) continue;  // alpha < 1/255: skipped
-        const float alpha = fminf(kAlphaMax, ex2_approx(arg));
-        const float tT = T * (1.f - alpha);
-        if (tT < kTermT) {
-          done = true;
-          n_eval = b + j + 1;
-          break;
-        }
-        const float w = alpha * T;
-        const float4 r2 = s2[j];
-        cr = fmaf(w, r2.x, cr);
-        cg = fmaf(w, r2.y, cg);
-        cb = fmaf(w, r2.z, cb);
-        dep = fmaf(w, r1.z, dep);
-        T = tT;
-      }
+#pragma unroll
+    for (int k = 0; k < kFusedSortCap / kCompThreads; ++k) {
+      const int e = tid + k * kCompThreads;
+      if (e < len) sm.u.c.slots[e] = sl[k];
     }
-    if (__syncthreads_count(done) == kCompThreads) break;
   }
 
-  if (inside) {
-    const size_t f = (size_t)(a.f0 + fl);
-    const size_t plane = (size_t)a.width * a.height;
-    const size_t p = (size_t)py * a.width + px;
-    float* rgb = a.out_rgb + f * 3 * plane;
-    rgb[p] = fmaf(T, a.bg0, cr);
-    rgb[plane + p] = fmaf(T, a.bg1, cg);
-    rgb[2 * plane + p] = fmaf(T, a.bg2, cb);
-    if (a.out_depth) a.out_depth[f * plane + p] = dep;
+  float T0 = 1.f, r0c = 0.f, g0c = 0.f, b0c = 0.f, d0 = 0.f;
+  float T1 = 1.f, r1c = 0.f, g1c = 0.f, b1c = 0.f, d1 = 0.f;
+  float pyc0 = in0 ? (float)py0 + 0.5f : kFar;   // out-of-image pixels never pass the alpha test
+  float pyc1 = in1 ? (float)py0 + 1.5f : kFar;
+  int ne0 = len, ne1 = len;
+  for (int b = 0; b < len; b += kBatch) {
+    __syncthreads();  // previous round's records (and the slot list writes) are complete
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = b + tid + h * kCompThreads;
+      if (k < len) {
+        const uint32_t slot = fused ? sm.u.c.slots[k] : a.sorted[start + k];
+        const float4* r = rec + (size_t)slot * 3;
+        sm.u.c.s0[tid + h * kCompThreads] = __ldg(r);
+        sm.u.c.s1[tid + h * kCompThreads] = __ldg(r + 1);
+        sm.u.c.s2[tid + h * kCompThreads] = __ldg(r + 2);
+      }
+    }
+    __syncthreads();
+    const int cnt = min(kBatch, len - b);
+    if (!__all_sync(0xffffffffu, pyc0 == kFar && pyc1 == kFar)) {
+      for (int j0 = 0; j0 < cnt; j0 += 32) {
+        const int jn = min(cnt, j0 + 32);
+#pragma unroll 4
+        for (int j = j0; j < jn; ++j) {
+          const float4 q0 = sm.u.c.s0[j];   // u, v, p, q
+          const float4 q1 = sm.u.c.s1[j];   // r, log2 o, z, id
+          const float dx = q0.x - pxc;
+          const float t1 = q0.z * dx;
+          const float m = fmaf(-t1, t1, q1.y);
+          const float qdx = q0.w * dx;
+          const float ta = fmaf(q1.x, q0.y - pyc0, qdx);
+          const float tb = fmaf(q1.x, q0.y - pyc1, qdx);
+          const float arg0 = fmaf(-ta, ta, m);
+          const float arg1 = fmaf(-tb, tb, m);
+          const bool use0 = arg0 >= kLog2AlphaMin;   // alpha >= 1/255
+          const bool use1 = arg1 >= kLog2AlphaMin;
+          if (use0 || use1) {
+            const float4 q2 = sm.u.c.s2[j];
+            blend(use0, arg0, q1, q2, T0, r0c, g0c, b0c, d0, pyc0, ne0, b + j);
+            blend(use1, arg1, q1, q2, T1, r1c, g1c, b1c, d1, pyc1, ne1, b + j);
+          }
+        }
+        if (__all_sync(0xffffffffu, pyc0 == kFar && pyc1 == kFar)) break;  // whole warp finished
+      }
+    }
+    if (__syncthreads_count(pyc0 == kFar && pyc1 == kFar) == kCompThreads) break;
+  }
+
+  const size_t f = (size_t)(a.f0 + fl);
+  const size_t plane = (size_t)a.width * a.height;
+  float* rgb = a.out_rgb + f * 3 * plane;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const bool in = h ? in1 : in0;
+    if (!in) continue;
+    const size_t p = (size_t)(py0 + h) * a.width + px;
+    const float T = h ? T1 : T0;
+    rgb[p] = fmaf(T, a.bg0, h ? r1c : r0c);
+    rgb[plane + p] = fmaf(T, a.bg1, h ? g1c : g0c);
+    rgb[2 * plane + p] = fmaf(T, a.bg2, h ? b1c : b0c);
+    if (a.out_depth) a.out_depth[f * plane + p] = h ? d1 : d0;
     if (a.out_alpha) a.out_alpha[f * plane + p] = 1.f - T;
-    if (a.out_n_eval) a.out_n_eval[f * plane + p] = n_eval;
+    if (a.out_n_eval) a.out_n_eval[f * plane + p] = h ? ne1 : ne0;
   }
   if (a.stat_pairs) {
-    unsigned long long v = inside ? (unsigned long long)n_eval : 0ull;
+    unsigned long long v = (in0 ? (unsigned long long)ne0 : 0ull) + (in1 ? (unsigned long long)ne1 : 0ull);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((tid & 31) == 0) red[tid >> 5] = v;
+    if ((tid & 31) == 0) sm.red[tid >> 5] = v;
     __syncthreads();
     if (tid == 0) {
       unsigned long long s = 0;
-      for (int w = 0; w < kCompThreads / 32; ++w) s += red[w];
+      for (int w = 0; w < kCompThreads / 32; ++w) s += sm.red[w];
       if (s) atomicAdd(a.stat_pairs, s);
     }
   }
@@ -113,7 +195,12 @@ __global__ void __launch_bounds__(kCompThreads) k4_composite(CompositeArgs a) {
 void launch_k4_composite(const CompositeArgs& a, cudaStream_t s) {
   const int nf = a.fe - a.fs;
   if (nf <= 0) return;
-  k4_composite<<<(unsigned)nf * a.n_tiles, kCompThreads, 0, s>>>(a);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k4_composite, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K4Shared));
+    attr = true;
+  }
+  k4_composite<<<(unsigned)nf * a.n_tiles, kCompThreads, sizeof(K4Shared), s>>>(a);
 }
 
 }  // namespace gsb

@@ -75,8 +75,10 @@ def compare_frame(gout, f_env, f_cam, ref: oracle.FrameResult, W, H, pix=None, g
         rgb, dep, alp, nev = rgb[py, px], dep[py, px], alp[py, px], nev[py, px]
         ref_rgb, ref_dep, ref_alp, ref_term = ref.rgb, ref.depth, ref.alpha, ref.term_id
         masked = ref.masked
+        tnear = ref.term_near
     else:
         ref_rgb, ref_dep, ref_alp, ref_term, masked = ref.rgb, ref.depth, ref.alpha, ref.term_id, ref.masked
+        tnear = ref.term_near
     ok = ~masked
     d_rgb = np.abs(rgb - ref_rgb).max(axis=-1)
     d_dep = np.abs(dep - ref_dep)
@@ -91,6 +93,10 @@ def compare_frame(gout, f_env, f_cam, ref: oracle.FrameResult, W, H, pix=None, g
         dep_fail=int((d_dep > oracle.TOL_DEPTH_REL * np.abs(ref_dep) + oracle.TOL_DEPTH_ABS)[ok].sum()),
         alp_fail=int((d_alp[ok] > oracle.TOL_RGB).sum()),
         n_pix=int(ok.size),
+        # information only: how far apart are the MASKED pixels?
+        masked_max_rgb=float(d_rgb[~ok].max()) if (~ok).any() else 0.0,
+        masked_over_tol=int((d_rgb[~ok] > oracle.TOL_RGB).sum() + (d_dep > oracle.TOL_DEPTH_REL * np.abs(ref_dep)
+                                                                   + oracle.TOL_DEPTH_ABS)[~ok].sum()),
     )
     if gpu_rec is not None:
         # n_eval: oracle termination id located in the GPU's own (bit-exact) tile list
@@ -102,14 +108,15 @@ def compare_frame(gout, f_env, f_cam, ref: oracle.FrameResult, W, H, pix=None, g
             px, py = px.reshape(-1), py.reshape(-1)
             term = ref_term.reshape(-1)
             nv = nev.reshape(-1)
-            okf = ok.reshape(-1)
+            okf = (ok & ~tnear).reshape(-1)
         else:
             px, py = pix
-            term, nv, okf = ref_term, nev, ok
+            term, nv, okf = ref_term, nev, ok & ~tnear
         bad = 0
         for k in np.nonzero(okf)[0]:
             t = (py[k] // 16) * tw + px[k] // 16
             e = expected_n_eval(int(term[k]), ids[offs[t]:offs[t + 1]])
             bad += int(e != nv[k])
         res["n_eval_fail"] = bad
+        res["n_eval_unchecked_frac"] = float((~okf).mean())
     return res

@@ -43,7 +43,17 @@ def test_k1_projection_matches_oracle(name):
             proj, ozb, ovalid = oracle.project(sc, b.poses[e], b.intrinsics[e, c], b.w2c[e, c], prm)
             assert np.array_equal(zb[f], ozb), "depth-key bits (R11) must be bit-exact"
             assert np.array_equal(valid[f], ovalid)
-            v = ovalid
+            # regular = in front of the camera by >= 0.1 m and within 2 image sizes of the
+            # principal point; the rest (near-plane, far off-screen) is checked relatively:
+            # there u = f x / z suffers fp32 cancellation in z (|u| up to 1e5 px).
+            cx, cy = b.intrinsics[e, c, 2], b.intrinsics[e, c, 3]
+            regular = ovalid & (proj[:, oracle.F_Z64] >= 0.1) & \
+                (np.abs(proj[:, oracle.F_U] - cx) <= 2 * cfg.width) & (np.abs(proj[:, oracle.F_V] - cy) <= 2 * cfg.height)
+            other = ovalid & ~regular
+            for k, fk in ((0, oracle.F_U), (1, oracle.F_V)):
+                rel = np.abs(rec[f][other][:, k] - proj[other][:, fk]) / np.maximum(np.abs(proj[other][:, fk]), 1.0)
+                assert rel.size == 0 or rel.max() <= 1e-3
+            v = regular
             r = rec[f][v]
             p = proj[v]
             assert np.abs(r[:, 0] - p[:, oracle.F_U]).max() <= 1e-3
@@ -196,7 +206,7 @@ def test_batch_slicing_and_chunking_bit_identical():
             assert np.array_equal(full[k][lo:hi], part[k]), k
     ch = gu.gpu_render(sc, b, cfg.width, cfg.height, chunk_frames=4)
     st = gu.gpu_render(sc, b, cfg.width, cfg.height, stats=True)
-    small_cap = int(st["stats"]["K"] // 6 + 1)
+    small_cap = int(st["stats"]["K"] * 0.4)   # 6-frame chunk -> at least 3 passes
     sp = gu.gpu_render(sc, b, cfg.width, cfg.height, chunk_frames=6, key_capacity=small_cap)
     for k in ("rgb", "depth", "alpha", "n_eval"):
         assert np.array_equal(full[k], ch[k]), k
@@ -276,7 +286,8 @@ def test_invalid_arguments_rejected_before_enqueue():
                  gu.to_dev(b.w2c[:1].repeat(4, 0)), gsb.RenderParams(cfg.width, cfg.height), out)
     assert ei.value.status == 2
     with pytest.raises(gsb.GsbError) as ei:
-        g.render(None, gu.to_dev(b.intrinsics), gu.to_dev(b.w2c), gsb.RenderParams(cfg.width, cfg.height, near=0), out)
+        g.render(None, gu.to_dev(b.intrinsics[:2]), gu.to_dev(b.w2c[:2]), gsb.RenderParams(cfg.width, cfg.height, near=0),
+                 out[:2])
     assert ei.value.status == 1
     bad = synth.Scene(sc.means, sc.scales, sc.quats, sc.opacities, sc.sh, sc.sh_degree, sc.body_id.copy(), 0)
     bad.body_id[0] = 3
