@@ -321,7 +321,8 @@ def main():
                                        f"(B200_PROFILING.md unit counts; clock from MEASURED_PEAKS.json, {peaks_kind})"},
             "stage_ms_per_step": tsum,
             "counters": {"V_per_frame": st["V"] / (B * C), "K_per_frame": st["K"] / (B * C),
-                         "P_per_frame": st["P"] / (B * C)},
+                         "P_per_frame": st["P"] / (B * C), "long_lists_per_step": kern[-1]["long_lists"],
+                         "max_tile_list": kern[-1]["max_list"], "chunks_per_step": kern[-1]["chunks"]},
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -145,6 +145,8 @@ typedef struct {
   int64_t launches;    /* kernels launched by libgsb in the last render */
   int64_t composite_launches;
   int64_t chunks;
+  int64_t long_lists;  /* tile lists longer than K4's fused-sort capacity (sorted by K3) */
+  int64_t max_list;    /* longest tile list of the render */
 } gsb_timings;
 gsb_status gsb_get_timings(gsb_scene scene, gsb_timings* out);
 

@@ -46,7 +46,8 @@ class gsb_render_params(ctypes.Structure):
 class gsb_timings(ctypes.Structure):
     _fields_ = [("setup_ms", ctypes.c_double), ("project_ms", ctypes.c_double), ("scan_ms", ctypes.c_double),
                 ("emit_ms", ctypes.c_double), ("sort_ms", ctypes.c_double), ("composite_ms", ctypes.c_double),
-                ("launches", ctypes.c_int64), ("composite_launches", ctypes.c_int64), ("chunks", ctypes.c_int64)]
+                ("launches", ctypes.c_int64), ("composite_launches", ctypes.c_int64), ("chunks", ctypes.c_int64),
+                ("long_lists", ctypes.c_int64), ("max_list", ctypes.c_int64)]
 
 
 _lib = None

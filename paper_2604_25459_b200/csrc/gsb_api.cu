@@ -86,6 +86,7 @@ struct gsb_scene_t {
   // template (K5)
   float4 *d_mean = nullptr, *d_L0 = nullptr, *d_L1 = nullptr, *d_L2 = nullptr, *d_sh = nullptr;
   int2* d_ids = nullptr;  // internal (Morton) index -> (creation index = id of reading R10, body)
+  int* d_inv = nullptr;   // id -> internal index
   // reservation
   bool reserved = false;
   int max_frames = 0, res_w = 0, res_h = 0, chunk = 0;
@@ -97,6 +98,9 @@ struct gsb_scene_t {
   float4* rec[2] = {nullptr, nullptr};
   int* vcount[2] = {nullptr, nullptr};
   uint32_t* vis_bits[2] = {nullptr, nullptr};
+  uint32_t* long_list[2] = {nullptr, nullptr};   // lists too long for K4's fused sort
+  uint32_t* long_cnt[2] = {nullptr, nullptr};
+  uint32_t* h_lc[2] = {nullptr, nullptr};        // pinned
   int64_t vis_words = 0;
   int* hist[2] = {nullptr, nullptr};
   uint32_t* off[2] = {nullptr, nullptr};
@@ -118,7 +122,7 @@ struct gsb_scene_t {
   // last-render bookkeeping
   cudaStream_t last_stream = nullptr;
   bool stats_valid = false;
-  int64_t stat_V = 0, stat_K = 0;
+  int64_t stat_V = 0, stat_K = 0, stat_long = 0, stat_maxseg = 0;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<std::pair<int, size_t>> ev_marks;  // (class, index of begin event)
@@ -132,7 +136,9 @@ struct gsb_scene_t {
     cudaFree(table); cudaFree(cams);
     for (int s = 0; s < 2; ++s) {
       cudaFree(rec[s]); cudaFree(vcount[s]); cudaFree(hist[s]); cudaFree(off[s]); cudaFree(vis_bits[s]);
-      vis_bits[s] = nullptr;
+      cudaFree(long_list[s]); cudaFree(long_cnt[s]);
+      if (h_lc[s]) cudaFreeHost(h_lc[s]);
+      vis_bits[s] = nullptr; long_list[s] = nullptr; long_cnt[s] = nullptr; h_lc[s] = nullptr;
       cudaFree(frame_base[s]);
       if (h_fb[s]) cudaFreeHost(h_fb[s]);
       if (h_vc[s]) cudaFreeHost(h_vc[s]);
@@ -230,6 +236,7 @@ struct Pipeline {
   gsb_status project_chunk(int c, int f0, int nf) {
     const int sl = c & 1;
     CUDA_TRY(cudaMemsetAsync(s->vcount[sl], 0, sizeof(int) * nf, st));
+    CUDA_TRY(cudaMemsetAsync(s->long_cnt[sl], 0, sizeof(uint32_t), st));
     CUDA_TRY(cudaMemsetAsync(s->hist[sl], 0, sizeof(int) * s->hist_stride * nf, st));
     K1Args a{};
     a.g_mean = s->d_mean; a.g_L0 = s->d_L0; a.g_L1 = s->d_L1; a.g_L2 = s->d_L2; a.g_sh = s->d_sh;
@@ -245,31 +252,33 @@ struct Pipeline {
     LAUNCH_CHECK();
     tm.end();
     tm.begin(KC_SCAN);
-    launch_k2_scan(s->hist[sl], s->off[sl], s->hist_stride, nf, n_tiles, s->frame_base[sl], st);
+    launch_k2_scan(s->hist[sl], s->off[sl], s->hist_stride, nf, n_tiles, s->frame_base[sl], s->long_list[sl],
+                   s->long_cnt[sl], kFusedSortCap, st);
     s->launches += 2;
     LAUNCH_CHECK();
     tm.end();
     CUDA_TRY(cudaMemcpyAsync(s->h_fb[sl], s->frame_base[sl], sizeof(uint64_t) * (nf + 2), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(s->h_vc[sl], s->vcount[sl], sizeof(int) * nf, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(s->h_lc[sl], s->long_cnt[sl], sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaEventRecord(s->ev_counts[sl], st));
     return GSB_OK;
   }
 
-  gsb_status pass(int sl, int f0, int fs, int fe, uint64_t key_base, uint64_t max_seg) {
+  gsb_status pass(int sl, int f0, int fs, int fe, uint64_t key_base, uint32_t n_long) {
     ChunkArgs a{};
     a.rec = s->rec[sl]; a.n = s->n; a.vis_bits = s->vis_bits[sl]; a.vis_words = s->vis_words; a.hist = s->hist[sl];
     a.hist_stride = s->hist_stride; a.off = s->off[sl]; a.frame_base = s->frame_base[sl];
     a.n_tiles = n_tiles; a.tiles_x = tiles_x; a.fs = fs; a.fe = fe; a.key_base = key_base;
     a.keys = s->keys; a.keys_alt = s->keys_alt; a.sorted = s->sorted;
-    a.min_n = kFusedSortCap + 1;
+    a.long_list = s->long_list[sl];
     tm.begin(KC_EMIT);
     launch_k2_emit(a, st);
     if (s->n > 0) s->launches++;
     LAUNCH_CHECK();
     tm.end();
-    if (max_seg > (uint64_t)kFusedSortCap) {  // only lists too long for K4's fused sort
+    if (n_long > 0) {  // only the lists too long for K4's fused sort
       tm.begin(KC_SORT);
-      launch_k3_sort(a, st);
+      launch_k3_sort(a, n_long, st);
       s->launches++;
       LAUNCH_CHECK();
       tm.end();
@@ -277,6 +286,7 @@ struct Pipeline {
     CompositeArgs c{};
     c.rec = s->rec[sl]; c.n = s->n; c.off = s->off[sl]; c.frame_base = s->frame_base[sl];
     c.hist_stride = s->hist_stride; c.sorted = s->sorted; c.keys = s->keys; c.key_base = key_base;
+    c.inv = s->d_inv;
     c.fs = fs; c.fe = fe; c.f0 = f0; c.width = W; c.height = H; c.tiles_x = tiles_x; c.n_tiles = n_tiles;
     c.bg0 = p->background[0]; c.bg1 = p->background[1]; c.bg2 = p->background[2];
     c.out_rgb = out_rgb; c.out_depth = out_depth; c.out_alpha = out_alpha; c.out_n_eval = out_neval;
@@ -314,8 +324,10 @@ struct Pipeline {
     for (int i = 0; i < nf; ++i) s->stat_V += s->h_vc[sl][i];
     s->stat_K += (int64_t)fb[nf];
     s->chunks++;
-    const uint64_t max_seg = fb[nf + 1];
-    if (fb[nf] <= (uint64_t)s->cap) return pass(sl, f0, 0, nf, 0, max_seg);
+    const uint32_t n_long = *s->h_lc[sl];
+    s->stat_long += n_long;
+    s->stat_maxseg = std::max<int64_t>(s->stat_maxseg, (int64_t)fb[nf + 1]);
+    if (fb[nf] <= (uint64_t)s->cap) return pass(sl, f0, 0, nf, 0, n_long);
     // split the chunk's frames into passes that fit the key workspace
     int fs = 0;
     while (fs < nf) {
@@ -324,7 +336,7 @@ struct Pipeline {
       if (fe == fs)
         return fail(GSB_ERR_CAPACITY, "frame %d needs %llu tile keys > key capacity %lld", f0 + fs,
                     (unsigned long long)(fb[fs + 1] - fb[fs]), (long long)s->cap);
-      gsb_status r = pass(sl, f0, fs, fe, fb[fs], max_seg);
+      gsb_status r = pass(sl, f0, fs, fe, fb[fs], n_long);
       if (r != GSB_OK) return r;
       fs = fe;
     }
@@ -361,7 +373,7 @@ gsb_status render_impl(gsb_scene s, const float* poses, int n_envs, int n_cams, 
                        float* out_alpha, int32_t* out_neval, cudaStream_t st) {
   const int F = n_envs * n_cams;
   s->last_stream = st;
-  s->stat_V = s->stat_K = 0;
+  s->stat_V = s->stat_K = s->stat_long = s->stat_maxseg = 0;
   s->launches = s->comp_launches = s->chunks = 0;
   s->ev_used = 0;
   s->ev_marks.clear();
@@ -453,10 +465,12 @@ gsb_status gsb_create_scene(const float* means, const float* scales, const float
   }
   std::vector<float4> hm(n), h0(n), h1(n), h2(n), hs((size_t)np * n);
   std::vector<int2> hids(n);
+  std::vector<int> hinv(n);
   for (int64_t j = 0; j < n; ++j) {
     const int64_t i = perm[j];
     const int b = body_id[i];
     hids[j] = make_int2((int)i, b);
+    hinv[i] = (int)j;
     const double o = opacities[i];
     if (!(o > 0.0 && o <= 1.0)) return fail(GSB_ERR_INVALID_ARGUMENT, "opacity[%lld] = %g not in (0,1]", (long long)i, o);
     double q[4] = {quats[4 * i], quats[4 * i + 1], quats[4 * i + 2], quats[4 * i + 3]};
@@ -506,6 +520,8 @@ gsb_status gsb_create_scene(const float* means, const float* scales, const float
   if (e == cudaSuccess) e = up(&s->d_sh, hs);
   if (e == cudaSuccess) e = dalloc(&s->d_ids, (size_t)n);
   if (e == cudaSuccess && n > 0) e = cudaMemcpy(s->d_ids, hids.data(), sizeof(int2) * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = dalloc(&s->d_inv, (size_t)n);
+  if (e == cudaSuccess && n > 0) e = cudaMemcpy(s->d_inv, hinv.data(), sizeof(int) * n, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     gsb_destroy_scene(s);
     return fail(e == cudaErrorMemoryAllocation ? GSB_ERR_OUT_OF_MEMORY : GSB_ERR_CUDA, "upload: %s", cudaGetErrorString(e));
@@ -545,6 +561,9 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
     CUDA_TRY(dalloc(&s->rec[sl], (size_t)E * std::max<int64_t>(s->n, 1) * 3));
     CUDA_TRY(dalloc(&s->vcount[sl], (size_t)E));
     CUDA_TRY(dalloc(&s->vis_bits[sl], (size_t)E * std::max<int64_t>(s->vis_words, 1)));
+    CUDA_TRY(dalloc(&s->long_list[sl], (size_t)E * s->n_tiles));
+    CUDA_TRY(dalloc(&s->long_cnt[sl], 1));
+    CUDA_TRY(cudaMallocHost((void**)&s->h_lc[sl], sizeof(uint32_t)));
     CUDA_TRY(dalloc(&s->hist[sl], (size_t)E * s->hist_stride));
     CUDA_TRY(dalloc(&s->off[sl], (size_t)E * s->hist_stride));
     CUDA_TRY(dalloc(&s->frame_base[sl], (size_t)E + 2));
@@ -639,6 +658,7 @@ gsb_status gsb_get_timings(gsb_scene s, gsb_timings* out) {
   out->setup_ms = ms[KC_SETUP]; out->project_ms = ms[KC_PROJECT]; out->scan_ms = ms[KC_SCAN];
   out->emit_ms = ms[KC_EMIT]; out->sort_ms = ms[KC_SORT]; out->composite_ms = ms[KC_COMPOSITE];
   out->launches = s->launches; out->composite_launches = s->comp_launches; out->chunks = s->chunks;
+  out->long_lists = s->stat_long; out->max_list = s->stat_maxseg;
   return GSB_OK;
 }
 
@@ -649,6 +669,7 @@ gsb_status gsb_destroy_scene(gsb_scene s) {
   s->free_workspace();
   cudaFree(s->d_mean); cudaFree(s->d_L0); cudaFree(s->d_L1); cudaFree(s->d_L2); cudaFree(s->d_sh);
   cudaFree(s->d_ids);
+  cudaFree(s->d_inv);
   delete s;
   return GSB_OK;
 }
@@ -718,7 +739,7 @@ gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, 
   DBG_TRY(cudaMemsetAsync(hist, 0, sizeof(int) * F * stride, st));
   launch_k1_external(u, v, sxx, syy, kappa, zbits, valid, n, 0, F, width, height, tiles_x, rec, vbits, vwords,
                      vcount, hist, stride, st);
-  launch_k2_scan(hist, off, stride, F, n_tiles, fbase, st);
+  launch_k2_scan(hist, off, stride, F, n_tiles, fbase, nullptr, nullptr, 0, st);
   DBG_TRY(cudaGetLastError());
   std::vector<uint64_t> hfb(F + 2);
   DBG_TRY(cudaMemcpyAsync(hfb.data(), fbase, sizeof(uint64_t) * (F + 2), cudaMemcpyDeviceToHost, st));
@@ -735,11 +756,11 @@ gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, 
   ChunkArgs a{};
   a.rec = rec; a.n = n; a.vis_bits = vbits; a.vis_words = vwords; a.hist = hist; a.hist_stride = stride; a.off = off;
   a.frame_base = fbase; a.n_tiles = n_tiles; a.tiles_x = tiles_x; a.fs = 0; a.fe = F; a.key_base = 0;
-  a.min_n = 0;  // K3 sorts every list here
+  a.long_list = nullptr;  // K3 sorts every list here
   a.keys = keys; a.keys_alt = keys_alt; a.sorted = sorted;
   launch_k2_emit(a, st);
-  launch_k3_sort(a, st);
-  if (K > 0) launch_slots_to_ids(a, out_ids, K, st);
+  launch_k3_sort(a, 0, st);
+  if (K > 0) DBG_TRY(cudaMemcpyAsync(out_ids, sorted, sizeof(uint32_t) * K, cudaMemcpyDeviceToDevice, st));
   DBG_TRY(cudaGetLastError());
   std::vector<uint32_t> hoff((size_t)F * stride);
   DBG_TRY(cudaMemcpyAsync(hoff.data(), off, sizeof(uint32_t) * hoff.size(), cudaMemcpyDeviceToHost, st));

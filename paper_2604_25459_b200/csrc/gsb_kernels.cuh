@@ -52,10 +52,11 @@ struct ChunkArgs {
   int n_tiles, tiles_x;
   int fs, fe;             // frame range [fs, fe) of this pass (relative to the chunk)
   uint64_t key_base;      // frame_base[fs]: keys of this pass start at key index 0
-  int min_n;              // K3 sorts only segments with n >= min_n (smaller ones: inside K4)
-  uint64_t* keys;         // [cap]   (zbits << 32) | slot
+  const uint32_t* long_list;  // (frame << 16 | tile) of lists longer than kFusedSortCap (K3), or
+                              // nullptr: K3 sorts every list (gsb_debug_bin_sort)
+  uint64_t* keys;         // [cap]   (zbits << 32) | id
   uint64_t* keys_alt;     // [cap]   scratch for oversize segments
-  uint32_t* sorted;       // [cap]   sorted slots
+  uint32_t* sorted;       // [cap]   sorted ids of the lists K3 sorted
 };
 
 struct CompositeArgs {
@@ -64,8 +65,9 @@ struct CompositeArgs {
   const uint32_t* off;
   const uint64_t* frame_base;
   int64_t hist_stride;
-  const uint32_t* sorted;   // sorted slots of segments longer than kFusedSortCap (K3)
+  const uint32_t* sorted;   // sorted ids of segments longer than kFusedSortCap (K3)
   const uint64_t* keys;     // unsorted keys: segments up to kFusedSortCap are sorted in K4
+  const int* inv;           // id -> internal index (record slot)
   uint64_t key_base;
   int fs, fe;             // relative frames of this pass
   int f0;                 // absolute frame index of chunk frame 0
@@ -92,11 +94,13 @@ void launch_k1_external(const float* u, const float* v, const float* sxx, const 
 
 // off[f][T] = K_f, off[f][T+1] = longest tile list of frame f; frame_base[E] = total keys,
 // frame_base[E+1] = longest tile list of the chunk
+// Lists longer than long_thresh are appended to long_list (frame << 16 | tile), counted in
+// *long_count (both may be null).
 void launch_k2_scan(int* hist, uint32_t* off, int64_t hist_stride, int n_frames, int n_tiles,
-                    uint64_t* frame_base, cudaStream_t s);
+                    uint64_t* frame_base, uint32_t* long_list, uint32_t* long_count, int long_thresh,
+                    cudaStream_t s);
 void launch_k2_emit(const ChunkArgs& a, cudaStream_t s);
-void launch_k3_sort(const ChunkArgs& a, cudaStream_t s);
+void launch_k3_sort(const ChunkArgs& a, uint32_t n_long, cudaStream_t s);
 void launch_k4_composite(const CompositeArgs& a, cudaStream_t s);
-void launch_slots_to_ids(const ChunkArgs& a, uint32_t* ids, uint64_t count, cudaStream_t s);
 
 }  // namespace gsb

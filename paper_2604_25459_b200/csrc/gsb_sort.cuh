@@ -4,8 +4,8 @@
 // north_star (3): hand-written segmented radix sort, deterministic tie-break on Gaussian id;
 // reading R10: a tile list is ordered by (bits(z_f32), id).  LSD radix (8-bit digits) over the
 // top 16 varying depth bits; every pass is a stable counting scatter ranked per warp with
-// __match_any_sync; runs equal on those bits are finished by (zbits, id) (ids read from the
-// records), so the result is unique whatever order the keys arrived in.
+// __match_any_sync; runs equal on those bits are finished by the full key (zbits, id), so the
+// result is unique whatever order the keys arrived in.
 #pragma once
 #include "gsb_common.cuh"
 
@@ -90,11 +90,10 @@ __device__ __forceinline__ void radix_pass(const Ptr src, Ptr dst, int n, int sh
 // Sort keys[0..n) into (bits(z), id) order.  Two stable 8-bit LSD passes order the keys by
 // the 16 highest bits of z that vary over the segment (bits above them are constant); runs
 // that agree on those bits (rare: it takes two depths within 2^-16 of the segment's depth
-// range) are then insertion-sorted by the full (zbits, id).  The id of a key is read from
-// its record (key low 32 bits = record slot).  Returns true if the result ended in `b`.
+// range) are then insertion-sorted by the full 64-bit key (zbits << 32 | id).  Returns true
+// if the result ended in `b`.
 template <int NT, typename Ptr>
-__device__ __forceinline__ bool segment_sort(Ptr a, Ptr b, int n, const float4* __restrict__ rec,
-                                             SortShared<NT>& sm) {
+__device__ __forceinline__ bool segment_sort(Ptr a, Ptr b, int n, SortShared<NT>& sm) {
   constexpr int kWarps = SortShared<NT>::kWarps;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // which depth bits vary over the segment?
@@ -123,7 +122,7 @@ __device__ __forceinline__ bool segment_sort(Ptr a, Ptr b, int n, const float4* 
     }
   }
   Ptr r = in_b ? b : a;
-  // runs equal on the sorted bits: finish them by (zbits, id) (reading R10 tie-break on id)
+  // runs equal on the sorted bits: finish them by the full key (zbits, id) — reading R10
   int dup = 0;
   for (int e = tid + 1; e < n; e += NT) dup |= (hi32(r[e]) >> lo) == (hi32(r[e - 1]) >> lo);
   if (__syncthreads_or(dup)) {
@@ -133,15 +132,11 @@ __device__ __forceinline__ bool segment_sort(Ptr a, Ptr b, int n, const float4* 
       if (!start) continue;
       int end = e + 1;
       while (end < n && (hi32(r[end]) >> lo) == h) ++end;
-      for (int x = e + 1; x < end; ++x) {  // insertion sort of the run by (zbits, id)
+      for (int x = e + 1; x < end; ++x) {  // insertion sort of the run by the 64-bit key
         const uint64_t kx = r[x];
-        const uint64_t fx = ((uint64_t)hi32(kx) << 32) | (uint32_t)__float_as_int(rec[(size_t)(uint32_t)kx * 3 + 1].w);
         int y = x - 1;
-        while (y >= e) {
-          const uint64_t ky = r[y];
-          const uint64_t fy = ((uint64_t)hi32(ky) << 32) | (uint32_t)__float_as_int(rec[(size_t)(uint32_t)ky * 3 + 1].w);
-          if (fy <= fx) break;
-          r[y + 1] = ky;
+        while (y >= e && r[y] > kx) {
+          r[y + 1] = r[y];
           --y;
         }
         r[y + 1] = kx;

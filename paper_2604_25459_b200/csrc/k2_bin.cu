@@ -2,7 +2,7 @@
 // built by K1) and emission of one 64-bit key per (visible Gaussian, overlapped tile).
 //
 // 3DGS tile binning [3DGS-conv, cited P:212]; keys are unique (reading R10):
-//   key = bits(z_f32) << 32 | slot        (slot -> record -> Gaussian id)
+//   key = bits(z_f32) << 32 | id          (id = creation index of the Gaussian)
 // and land directly in their (frame, tile) bucket, so K3 only sorts within a bucket.
 // The tile coordinate is implied by the bucket; the frame by the chunk's frame_base.
 #include "gsb_common.cuh"
@@ -26,7 +26,10 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
 // emission cursor).  One block per frame.
 __global__ void __launch_bounds__(kScanThreads) k2_scan_tiles(int* __restrict__ hist,
                                                               uint32_t* __restrict__ off,
-                                                              int64_t stride, int n_tiles) {
+                                                              int64_t stride, int n_tiles,
+                                                              uint32_t* __restrict__ long_list,
+                                                              uint32_t* __restrict__ long_count,
+                                                              int long_thresh) {
   __shared__ uint32_t wsum[kScanThreads / 32];
   __shared__ uint32_t carry_s, max_s;
   const int f = blockIdx.x;
@@ -53,6 +56,7 @@ __global__ void __launch_bounds__(kScanThreads) k2_scan_tiles(int* __restrict__ 
     if (t < n_tiles) {
       o[t] = carry + wsum[warp] + inc - x;
       h[t] = 0;
+      if (long_list && x > (uint32_t)long_thresh) long_list[atomicAdd(long_count, 1u)] = ((uint32_t)f << 16) | (uint32_t)t;
     }
     __syncthreads();
     if (tid == kScanThreads - 1) carry_s = carry + wsum[warp] + inc;
@@ -82,8 +86,10 @@ __global__ void k2_scan_frames(const uint32_t* __restrict__ off, int64_t stride,
 }
 
 void launch_k2_scan(int* hist, uint32_t* off, int64_t hist_stride, int n_frames, int n_tiles,
-                    uint64_t* frame_base, cudaStream_t s) {
-  k2_scan_tiles<<<n_frames, kScanThreads, 0, s>>>(hist, off, hist_stride, n_tiles);
+                    uint64_t* frame_base, uint32_t* long_list, uint32_t* long_count, int long_thresh,
+                    cudaStream_t s) {
+  k2_scan_tiles<<<n_frames, kScanThreads, 0, s>>>(hist, off, hist_stride, n_tiles, long_list, long_count,
+                                                  long_thresh);
   k2_scan_frames<<<1, 32, 0, s>>>(off, hist_stride, n_tiles, n_frames, frame_base);
 }
 
@@ -101,13 +107,15 @@ __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
   if (word == 0) return;  // warp-uniform
   const int lane = threadIdx.x & 31;
   const bool has = (word >> lane) & 1u;
-  uint32_t rect = 0, zb = 0;
+  uint32_t rect = 0, zb = 0, id = 0;
   if (has) {
     const float4* r = a.rec + ((size_t)fl * a.n + i) * 3;
-    zb = __float_as_uint(__ldg(&r[1].z));
+    const float4 r1 = __ldg(r + 1);
+    zb = __float_as_uint(r1.z);
+    id = __float_as_uint(r1.w);
     rect = __float_as_uint(__ldg(&r[2].w));
   }
-  const uint64_t key = ((uint64_t)zb << 32) | (uint64_t)i;
+  const uint64_t key = ((uint64_t)zb << 32) | (uint64_t)id;   // unique (reading R10)
   int* cur = a.hist + (size_t)fl * a.hist_stride;
   const uint32_t* off = a.off + (size_t)fl * a.hist_stride;
   uint64_t* keys = a.keys + (a.frame_base[fl] - a.key_base);
@@ -191,24 +199,6 @@ void launch_k1_external(const float* u, const float* v, const float* sxx, const 
   k1_external<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(u, v, sxx, syy, kappa, zbits, valid, n, f0,
                                                           n_frames, width, height, tiles_x, rec, vis_bits,
                                                           vis_words, vcount, hist, hist_stride);
-}
-
-// sorted slots -> Gaussian ids (debug_bin_sort output)
-__global__ void k_slots_to_ids(ChunkArgs a, uint32_t* __restrict__ ids) {
-  const int fl = a.fs + blockIdx.y;
-  const uint64_t b = a.frame_base[fl] - a.key_base, e = a.frame_base[fl + 1] - a.key_base;
-  for (uint64_t k = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < e;
-       k += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t slot = a.sorted[k];
-    ids[k] = (uint32_t)__float_as_int(a.rec[((size_t)fl * a.n + slot) * 3 + 1].w);
-  }
-}
-
-void launch_slots_to_ids(const ChunkArgs& a, uint32_t* ids, uint64_t count, cudaStream_t s) {
-  (void)count;
-  const int nf = a.fe - a.fs;
-  if (nf <= 0) return;
-  k_slots_to_ids<<<dim3(64, (unsigned)nf), 256, 0, s>>>(a, ids);
 }
 
 }  // namespace gsb

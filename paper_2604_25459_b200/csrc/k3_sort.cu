@@ -17,13 +17,20 @@ __global__ void __launch_bounds__(kSortThreads) k3_sort(ChunkArgs a) {
   uint64_t* sa = reinterpret_cast<uint64_t*>(smem_raw + sizeof(SortShared<kSortThreads>));
   uint64_t* sb = sa + kSmemCap;
 
-  const int fl = a.fs + blockIdx.x / a.n_tiles;
-  const int t = blockIdx.x % a.n_tiles;
+  int fl, t;
+  if (a.long_list) {  // render path: only the lists too long for K4's fused sort
+    const uint32_t e = a.long_list[blockIdx.x];
+    fl = (int)(e >> 16);
+    t = (int)(e & 0xffffu);
+    if (fl < a.fs || fl >= a.fe) return;
+  } else {
+    fl = a.fs + blockIdx.x / a.n_tiles;
+    t = blockIdx.x % a.n_tiles;
+  }
   const uint32_t* off = a.off + (size_t)fl * a.hist_stride;
   const uint64_t start = a.frame_base[fl] - a.key_base + off[t];
   const int n = (int)(off[t + 1] - off[t]);
-  if (n == 0 || n < a.min_n) return;
-  const float4* rec = a.rec + (size_t)fl * a.n * 3;
+  if (n == 0) return;
   if (n == 1) {
     if (threadIdx.x == 0) a.sorted[start] = (uint32_t)a.keys[start];
     return;
@@ -31,29 +38,31 @@ __global__ void __launch_bounds__(kSortThreads) k3_sort(ChunkArgs a) {
   if (n <= kSmemCap) {
     for (int e = threadIdx.x; e < n; e += kSortThreads) sa[e] = a.keys[start + e];
     __syncthreads();
-    const bool in_b = segment_sort(sa, sb, n, rec, sm);
+    const bool in_b = segment_sort(sa, sb, n, sm);
     const uint64_t* r = in_b ? sb : sa;
     for (int e = threadIdx.x; e < n; e += kSortThreads) a.sorted[start + e] = (uint32_t)r[e];
   } else {
     uint64_t* ga = a.keys + start;
     uint64_t* gb = a.keys_alt + start;
-    const bool in_b = segment_sort(ga, gb, n, rec, sm);
+    const bool in_b = segment_sort(ga, gb, n, sm);
     __syncthreads();
     const uint64_t* r = in_b ? gb : ga;
     for (int e = threadIdx.x; e < n; e += kSortThreads) a.sorted[start + e] = (uint32_t)r[e];
   }
 }
 
-void launch_k3_sort(const ChunkArgs& a, cudaStream_t s) {
+void launch_k3_sort(const ChunkArgs& a, uint32_t n_long, cudaStream_t s) {
   const int nf = a.fe - a.fs;
   if (nf <= 0) return;
+  const unsigned grid = a.long_list ? n_long : (unsigned)nf * a.n_tiles;
+  if (grid == 0) return;
   const size_t smem = sizeof(SortShared<kSortThreads>) + 2 * kSmemCap * sizeof(uint64_t);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k3_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k3_sort<<<(unsigned)nf * a.n_tiles, kSortThreads, smem, s>>>(a);
+  k3_sort<<<grid, kSortThreads, smem, s>>>(a);
 }
 
 }  // namespace gsb

@@ -35,7 +35,7 @@ struct K4Shared {
   union {
     uint64_t keys[2][kFusedSortCap];
     struct {
-      uint32_t slots[kFusedSortCap];
+      uint32_t slots[kFusedSortCap];   // sorted ids
       float4 s0[kBatch], s1[kBatch], s2[kBatch];
     } c;
   } u;
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kCompThreads, 6) k4_composite(CompositeArgs a)
   if (fused && len > 0) {
     for (int e = tid; e < len; e += kCompThreads) sm.u.keys[0][e] = a.keys[start + e];
     __syncthreads();
-    const bool in_b = len > 1 && segment_sort(sm.u.keys[0], sm.u.keys[1], len, rec, sm.sort);
+    const bool in_b = len > 1 && segment_sort(sm.u.keys[0], sm.u.keys[1], len, sm.sort);
     uint32_t sl[kFusedSortCap / kCompThreads];
 #pragma unroll
     for (int k = 0; k < kFusedSortCap / kCompThreads; ++k) {
@@ -118,14 +118,14 @@ __global__ void __launch_bounds__(kCompThreads, 6) k4_composite(CompositeArgs a)
   float pyc0 = in0 ? (float)py0 + 0.5f : kFar;   // out-of-image pixels never pass the alpha test
   float pyc1 = in1 ? (float)py0 + 1.5f : kFar;
   int ne0 = len, ne1 = len;
+  __syncthreads();  // the sorted id list is complete
   for (int b = 0; b < len; b += kBatch) {
-    __syncthreads();  // previous round's records (and the slot list writes) are complete
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int k = b + tid + h * kCompThreads;
       if (k < len) {
-        const uint32_t slot = fused ? sm.u.c.slots[k] : a.sorted[start + k];
-        const float4* r = rec + (size_t)slot * 3;
+        const uint32_t id = fused ? sm.u.c.slots[k] : a.sorted[start + k];
+        const float4* r = rec + (size_t)__ldg(a.inv + id) * 3;
         sm.u.c.s0[tid + h * kCompThreads] = __ldg(r);
         sm.u.c.s1[tid + h * kCompThreads] = __ldg(r + 1);
         sm.u.c.s2[tid + h * kCompThreads] = __ldg(r + 2);
@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(kCompThreads, 6) k4_composite(CompositeArgs a)
         if (__all_sync(0xffffffffu, pyc0 == kFar && pyc1 == kFar)) break;  // whole warp finished
       }
     }
+    // also the barrier that frees the staging buffers for the next round
     if (__syncthreads_count(pyc0 == kFar && pyc1 == kFar) == kCompThreads) break;
   }
 

@@ -74,4 +74,4 @@ def test_host_side_validation_without_gpu():
 
 def test_render_params_layout_matches_header():
     assert ctypes.sizeof(gsb.gsb_render_params) == 4 * 9
-    assert ctypes.sizeof(gsb.gsb_timings) == 8 * 9
+    assert ctypes.sizeof(gsb.gsb_timings) == 8 * 11
