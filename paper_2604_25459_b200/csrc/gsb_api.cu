@@ -276,16 +276,11 @@ struct Pipeline {
     if (s->n > 0) s->launches++;
     LAUNCH_CHECK();
     tm.end();
-    if (n_long > 0) {  // only the lists too long for K4's fused sort
-      tm.begin(KC_SORT);
-      launch_k3_sort(a, n_long, st);
-      s->launches++;
-      LAUNCH_CHECK();
-      tm.end();
-    }
+    (void)n_long;  // long lists are sorted in HBM by their K4 CTA (K3 serves gsb_debug_bin_sort)
     CompositeArgs c{};
     c.rec = s->rec[sl]; c.n = s->n; c.off = s->off[sl]; c.frame_base = s->frame_base[sl];
-    c.hist_stride = s->hist_stride; c.sorted = s->sorted; c.keys = s->keys; c.key_base = key_base;
+    c.hist_stride = s->hist_stride; c.sorted = s->sorted; c.keys = s->keys; c.keys_alt = s->keys_alt;
+    c.key_base = key_base;
     c.inv = s->d_inv;
     c.fs = fs; c.fe = fe; c.f0 = f0; c.width = W; c.height = H; c.tiles_x = tiles_x; c.n_tiles = n_tiles;
     c.bg0 = p->background[0]; c.bg1 = p->background[1]; c.bg2 = p->background[2];

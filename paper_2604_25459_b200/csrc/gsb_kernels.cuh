@@ -65,8 +65,9 @@ struct CompositeArgs {
   const uint32_t* off;
   const uint64_t* frame_base;
   int64_t hist_stride;
-  const uint32_t* sorted;   // sorted ids of segments longer than kFusedSortCap (K3)
-  const uint64_t* keys;     // unsorted keys: segments up to kFusedSortCap are sorted in K4
+  uint32_t* sorted;         // sorted ids of segments longer than kFusedSortCap
+  const uint64_t* keys;     // unsorted keys (K2b); K4 sorts every tile list itself
+  uint64_t* keys_alt;       // scratch twin of keys for the HBM sort of long lists
   const int* inv;           // id -> internal index (record slot)
   uint64_t key_base;
   int fs, fe;             // relative frames of this pass

@@ -37,11 +37,12 @@ struct K4Shared {
     struct {
       uint32_t slots[kFusedSortCap];   // sorted ids
       float4 s0[kBatch], s1[kBatch], s2[kBatch];
+      float2 box[kBatch];              // half-extents of the alpha >= 1/255 box (R8), inflated
     } c;
   } u;
   unsigned long long red[kCompThreads / 32];
 };
-static_assert(sizeof(uint32_t) * kFusedSortCap + 3 * 16 * kBatch <= 2 * 8 * kFusedSortCap, "union layout");
+static_assert(sizeof(uint32_t) * kFusedSortCap + 3 * 16 * kBatch + 8 * kBatch <= 2 * 8 * kFusedSortCap, "union layout");
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -78,13 +79,16 @@ __device__ __forceinline__ void blend(bool use, float arg, const float4& r1, con
 __global__ void __launch_bounds__(kCompThreads, 6) k4_composite(CompositeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K4Shared& sm = *reinterpret_cast<K4Shared*>(smem_raw);
+  const unsigned FULL = 0xffffffffu;
   const int fl = a.fs + blockIdx.x / a.n_tiles;
   const int t = blockIdx.x % a.n_tiles;
   const int tx = t % a.tiles_x, ty = t / a.tiles_x;
-  const int tid = threadIdx.x;
-  // thread -> pixels (px, py0) and (px, py0 + 1): a warp covers 16 x 4 pixels
-  const int px = tx * kTile + (tid & 15);
-  const int py0 = ty * kTile + 2 * (tid >> 4);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // warp w owns the 8x8 block (w & 1, w >> 1) of the tile; a thread owns two vertically
+  // adjacent pixels (px, py0) and (px, py0 + 1) of it
+  const int bx0 = tx * kTile + 8 * (warp & 1), by0 = ty * kTile + 8 * (warp >> 1);
+  const int px = bx0 + (lane & 7);
+  const int py0 = by0 + 2 * (lane >> 3);
   const bool in_x = px < a.width;
   const bool in0 = in_x && py0 < a.height, in1 = in_x && py0 + 1 < a.height;
   const uint32_t* off = a.off + (size_t)fl * a.hist_stride;
@@ -92,24 +96,38 @@ __global__ void __launch_bounds__(kCompThreads, 6) k4_composite(CompositeArgs a)
   const int len = (int)(off[t + 1] - off[t]);
   const float4* rec = a.rec + (size_t)fl * a.n * 3;
   const float pxc = (float)px + 0.5f;
+  const float bcx = (float)bx0 + 4.0f, bcy = (float)by0 + 4.0f;  // block centre (pixel centres +-3.5)
 
-  // depth order of this tile's list (reading R10): sorted here, or by K3 if too long
+  // depth order of this tile's list (reading R10): in shared memory, or in HBM (key buffer and
+  // its scratch twin) for the rare lists longer than kFusedSortCap
   const bool fused = len <= kFusedSortCap;
-  if (fused && len > 0) {
-    for (int e = tid; e < len; e += kCompThreads) sm.u.keys[0][e] = a.keys[start + e];
-    __syncthreads();
-    const bool in_b = len > 1 && segment_sort(sm.u.keys[0], sm.u.keys[1], len, sm.sort);
-    uint32_t sl[kFusedSortCap / kCompThreads];
+  const uint32_t* ids_g = nullptr;
+  if (len > 0) {
+    if (fused) {
+      for (int e = tid; e < len; e += kCompThreads) sm.u.keys[0][e] = a.keys[start + e];
+      __syncthreads();
+      const bool in_b = len > 1 && segment_sort(sm.u.keys[0], sm.u.keys[1], len, sm.sort);
+      uint32_t sl[kFusedSortCap / kCompThreads];
 #pragma unroll
-    for (int k = 0; k < kFusedSortCap / kCompThreads; ++k) {
-      const int e = tid + k * kCompThreads;
-      if (e < len) sl[k] = (uint32_t)sm.u.keys[in_b ? 1 : 0][e];
-    }
-    __syncthreads();
+      for (int k = 0; k < kFusedSortCap / kCompThreads; ++k) {
+        const int e = tid + k * kCompThreads;
+        if (e < len) sl[k] = (uint32_t)sm.u.keys[in_b ? 1 : 0][e];
+      }
+      __syncthreads();
 #pragma unroll
-    for (int k = 0; k < kFusedSortCap / kCompThreads; ++k) {
-      const int e = tid + k * kCompThreads;
-      if (e < len) sm.u.c.slots[e] = sl[k];
+      for (int k = 0; k < kFusedSortCap / kCompThreads; ++k) {
+        const int e = tid + k * kCompThreads;
+        if (e < len) sm.u.c.slots[e] = sl[k];
+      }
+    } else {
+      uint64_t* ga = const_cast<uint64_t*>(a.keys) + start;
+      uint64_t* gb = a.keys_alt + start;
+      const bool in_b = segment_sort(ga, gb, len, sm.sort);
+      uint32_t* dst = a.sorted + start;
+      const uint64_t* r = in_b ? gb : ga;
+      for (int e = tid; e < len; e += kCompThreads) dst[e] = (uint32_t)r[e];
+      ids_g = dst;
+      __threadfence_block();
     }
   }
 
@@ -122,32 +140,57 @@ __global__ void __launch_bounds__(kCompThreads, 6) k4_composite(CompositeArgs a)
   for (int b = 0; b < len; b += kBatch) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int k = b + tid + h * kCompThreads;
+      const int e = tid + h * kCompThreads;
+      const int k = b + e;
       if (k < len) {
-        const uint32_t id = fused ? sm.u.c.slots[k] : a.sorted[start + k];
+        const uint32_t id = fused ? sm.u.c.slots[k] : ids_g[k];
         const float4* r = rec + (size_t)__ldg(a.inv + id) * 3;
-        sm.u.c.s0[tid + h * kCompThreads] = __ldg(r);
-        sm.u.c.s1[tid + h * kCompThreads] = __ldg(r + 1);
-        sm.u.c.s2[tid + h * kCompThreads] = __ldg(r + 2);
+        const float4 q0 = __ldg(r), q1 = __ldg(r + 1);
+        sm.u.c.s0[e] = q0;
+        sm.u.c.s1[e] = q1;
+        sm.u.c.s2[e] = __ldg(r + 2);
+        // extents of {arg >= log2(1/255)} = {Q' <= kappa'} for Q' = (p dx)^2 + (q dx + r dy)^2:
+        // ex = sqrt(kappa') / p, ey = sqrt(kappa' (p^2 + q^2)) / (p r); inflated by 1% + 0.01 px so
+        // that skipping a block outside it never changes a per-pixel decision
+        const float kap = fmaxf(q1.y - kLog2AlphaMin, 0.f);
+        const float sk = sqrtf(kap);
+        const float ex = __fdividef(sk, q0.z);
+        const float ey = __fdividef(sk * sqrtf(fmaf(q0.z, q0.z, q0.w * q0.w)), q0.z * q1.x);
+        sm.u.c.box[e] = make_float2(fmaf(ex, 1.01f, 0.01f), fmaf(ey, 1.01f, 0.01f));
       }
     }
     __syncthreads();
     const int cnt = min(kBatch, len - b);
-    if (!__all_sync(0xffffffffu, pyc0 == kFar && pyc1 == kFar)) {
-      for (int j0 = 0; j0 < cnt; j0 += 32) {
-        const int jn = min(cnt, j0 + 32);
-#pragma unroll 4
-        for (int j = j0; j < jn; ++j) {
+    if (!__all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) {
+      // which of this batch's records can reach this warp's 8x8 block?
+      uint32_t hit[kBatch / 32];
+#pragma unroll
+      for (int k = 0; k < kBatch / 32; ++k) {
+        const int j = 32 * k + lane;
+        bool ov = false;
+        if (j < cnt) {
+          const float2 uv = make_float2(sm.u.c.s0[j].x, sm.u.c.s0[j].y);
+          const float2 bx = sm.u.c.box[j];
+          ov = fabsf(uv.x - bcx) <= bx.x + 3.5f && fabsf(uv.y - bcy) <= bx.y + 3.5f;
+        }
+        hit[k] = __ballot_sync(FULL, ov);
+      }
+#pragma unroll
+      for (int k = 0; k < kBatch / 32; ++k) {
+        uint32_t m = hit[k];
+        while (m) {
+          const int j = 32 * k + __ffs(m) - 1;
+          m &= m - 1;
           const float4 q0 = sm.u.c.s0[j];   // u, v, p, q
           const float4 q1 = sm.u.c.s1[j];   // r, log2 o, z, id
           const float dx = q0.x - pxc;
           const float t1 = q0.z * dx;
-          const float m = fmaf(-t1, t1, q1.y);
+          const float mm = fmaf(-t1, t1, q1.y);
           const float qdx = q0.w * dx;
           const float ta = fmaf(q1.x, q0.y - pyc0, qdx);
           const float tb = fmaf(q1.x, q0.y - pyc1, qdx);
-          const float arg0 = fmaf(-ta, ta, m);
-          const float arg1 = fmaf(-tb, tb, m);
+          const float arg0 = fmaf(-ta, ta, mm);
+          const float arg1 = fmaf(-tb, tb, mm);
           const bool use0 = arg0 >= kLog2AlphaMin;   // alpha >= 1/255
           const bool use1 = arg1 >= kLog2AlphaMin;
           if (use0 || use1) {
@@ -156,7 +199,7 @@ __global__ void __launch_bounds__(kCompThreads, 6) k4_composite(CompositeArgs a)
             blend(use1, arg1, q1, q2, T1, r1c, g1c, b1c, d1, pyc1, ne1, b + j);
           }
         }
-        if (__all_sync(0xffffffffu, pyc0 == kFar && pyc1 == kFar)) break;  // whole warp finished
+        if (__all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) break;  // whole warp finished
       }
     }
     // also the barrier that frees the staging buffers for the next round
@@ -182,8 +225,8 @@ __global__ void __launch_bounds__(kCompThreads, 6) k4_composite(CompositeArgs a)
   if (a.stat_pairs) {
     unsigned long long v = (in0 ? (unsigned long long)ne0 : 0ull) + (in1 ? (unsigned long long)ne1 : 0ull);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((tid & 31) == 0) sm.red[tid >> 5] = v;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    if (lane == 0) sm.red[warp] = v;
     __syncthreads();
     if (tid == 0) {
       unsigned long long s = 0;
