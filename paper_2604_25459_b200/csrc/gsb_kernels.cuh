@@ -7,7 +7,7 @@
 
 namespace gsb {
 
-constexpr int kFusedSortCap = 1920;  // tile lists up to this length are sorted inside K4 (6 CTAs/SM)
+constexpr int kFusedSortCap = 1024;  // tile lists up to this length are sorted in K4 smem (8 CTAs/SM)
 
 struct K1Args {
   // template (K5: shared read-only buffer, one copy for every env)

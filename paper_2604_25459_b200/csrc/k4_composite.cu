@@ -28,8 +28,8 @@ constexpr int kCompThreads = 128;          // 2 pixels per thread: a 16x16 tile 
 constexpr int kBatch = 256;                // records staged per shared-memory round
 static_assert(kBatch == 2 * kCompThreads, "each thread stages two records per round");
 
-// Shared memory: the sort's two key buffers are dead once the tile list is ordered, so the
-// sorted slots (u32) and the record staging area reuse them (6 CTAs = 24 warps per SM).
+// Shared memory (~23 KB -> 8 CTAs = 32 warps per SM): the sort's two key buffers are dead once
+// the tile list is ordered, so the sorted ids (u32) and the record staging area reuse them.
 struct K4Shared {
   SortShared<kCompThreads> sort;
   union {
@@ -42,7 +42,6 @@ struct K4Shared {
   } u;
   unsigned long long red[kCompThreads / 32];
 };
-static_assert(sizeof(uint32_t) * kFusedSortCap + 3 * 16 * kBatch + 8 * kBatch <= 2 * 8 * kFusedSortCap, "union layout");
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -76,7 +75,7 @@ __device__ __forceinline__ void blend(bool use, float arg, const float4& r1, con
   }
 }
 
-__global__ void __launch_bounds__(kCompThreads, 6) k4_composite(CompositeArgs a) {
+__global__ void __launch_bounds__(kCompThreads, 8) k4_composite(CompositeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K4Shared& sm = *reinterpret_cast<K4Shared*>(smem_raw);
   const unsigned FULL = 0xffffffffu;
