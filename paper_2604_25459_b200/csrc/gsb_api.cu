@@ -553,7 +553,7 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
   CUDA_TRY(dalloc(&s->table, (size_t)F * nb1 * 4));
   CUDA_TRY(dalloc(&s->cams, (size_t)F));
   for (int sl = 0; sl < 2; ++sl) {
-    CUDA_TRY(dalloc(&s->rec[sl], (size_t)E * std::max<int64_t>(s->n, 1) * 3));
+    CUDA_TRY(dalloc(&s->rec[sl], (size_t)E * std::max<int64_t>(s->n, 1) * kRecQuads));
     CUDA_TRY(dalloc(&s->vcount[sl], (size_t)E));
     CUDA_TRY(dalloc(&s->vis_bits[sl], (size_t)E * std::max<int64_t>(s->vis_words, 1)));
     CUDA_TRY(dalloc(&s->long_list[sl], (size_t)E * s->n_tiles));
@@ -724,7 +724,7 @@ gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, 
       return fail(GSB_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_));          \
     }                                                                              \
   } while (0)
-  DBG_TRY(dalloc(&rec, (size_t)F * std::max<int64_t>(n, 1) * 3));
+  DBG_TRY(dalloc(&rec, (size_t)F * std::max<int64_t>(n, 1) * kRecQuads));
   DBG_TRY(dalloc(&vcount, (size_t)F));
   DBG_TRY(dalloc(&vbits, (size_t)F * std::max<int64_t>(vwords, 1)));
   DBG_TRY(dalloc(&hist, (size_t)F * stride));

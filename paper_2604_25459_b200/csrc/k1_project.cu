@@ -243,10 +243,18 @@ __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
     }
     const uint32_t rect = pack_rect(tx0, tx1, ty0, ty1);
     if (vis) {
-      float4* r = a.rec + ((size_t)fl * a.n + i) * 3;
+      // half-extents of {arg >= log2(1/255)} = {Q' <= kappa'}, Q' = (p dx)^2 + (q dx + r dy)^2:
+      // ex = sqrt(kappa') / p, ey = sqrt(kappa' (p^2 + q^2)) / (p r) (the R8 box in the whitened
+      // metric), inflated by 1% + 0.01 px: K4 skips a pixel block only when it is outside it
+      const float kap = fmaxf(log2o - kLog2AlphaMin, 0.f);
+      const float sk = sqrtf(kap);
+      const float ex = fmaf(sk / pw, 1.01f, 0.01f);
+      const float ey = fmaf(sk * sqrtf(fmaf(pw, pw, qw * qw)) / (pw * rw), 1.01f, 0.01f);
+      float4* r = a.rec + ((size_t)fl * a.n + i) * kRecQuads;
       r[0] = make_float4(u, v, pw, qw);
-      r[1] = make_float4(rw, log2o, z, __int_as_float(id));
-      r[2] = make_float4(rgb.x, rgb.y, rgb.z, __uint_as_float(rect));
+      r[1] = make_float4(rw, log2o, ex, ey);
+      r[2] = make_float4(rgb.x, rgb.y, rgb.z, z);
+      r[3] = make_float4(__int_as_float(id), __uint_as_float(rect), 0.f, 0.f);
     }
     warp_tile_count(vis, rect, a.tiles_x, a.hist + (size_t)fl * a.hist_stride);
   }

@@ -109,11 +109,11 @@ __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
   const bool has = (word >> lane) & 1u;
   uint32_t rect = 0, zb = 0, id = 0;
   if (has) {
-    const float4* r = a.rec + ((size_t)fl * a.n + i) * 3;
-    const float4 r1 = __ldg(r + 1);
-    zb = __float_as_uint(r1.z);
-    id = __float_as_uint(r1.w);
-    rect = __float_as_uint(__ldg(&r[2].w));
+    const float4* r = a.rec + ((size_t)fl * a.n + i) * kRecQuads;
+    zb = __float_as_uint(__ldg(&r[2].w));
+    const float2 r3 = __ldg(reinterpret_cast<const float2*>(r + 3));
+    id = __float_as_uint(r3.x);
+    rect = __float_as_uint(r3.y);
   }
   const uint64_t key = ((uint64_t)zb << 32) | (uint64_t)id;   // unique (reading R10)
   int* cur = a.hist + (size_t)fl * a.hist_stride;
@@ -181,10 +181,9 @@ __global__ void __launch_bounds__(128) k1_external(const float* __restrict__ u, 
     }
     const uint32_t rect = pack_rect(tx0, tx1, ty0, ty1);
     if (vis) {
-      float4* r = rec + ((size_t)fl * n + i) * 3;
-      r[0] = make_float4(u[o], v[o], 0.f, 0.f);
-      r[1] = make_float4(0.f, 0.f, __uint_as_float(zbits[o]), __int_as_float((int)i));
-      r[2] = make_float4(0.f, 0.f, 0.f, __uint_as_float(rect));
+      float4* r = rec + ((size_t)fl * n + i) * kRecQuads;
+      r[2] = make_float4(0.f, 0.f, 0.f, __uint_as_float(zbits[o]));
+      r[3] = make_float4(__int_as_float((int)i), __uint_as_float(rect), 0.f, 0.f);
     }
     warp_tile_count(vis, rect, tiles_x, hist + (size_t)fl * hist_stride);
   }

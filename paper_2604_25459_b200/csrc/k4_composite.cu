@@ -25,23 +25,23 @@
 namespace gsb {
 
 constexpr int kCompThreads = 128;          // 2 pixels per thread: a 16x16 tile per CTA
-constexpr int kBatch = 256;                // records staged per shared-memory round
-static_assert(kBatch == 2 * kCompThreads, "each thread stages two records per round");
+constexpr int kBatch = kCompThreads;       // records staged per round (one cp.async set per thread)
 
-// Shared memory (~23 KB -> 8 CTAs = 32 warps per SM): the sort's two key buffers are dead once
-// the tile list is ordered, so the sorted ids (u32) and the record staging area reuse them.
+// Shared memory (~21.5 KB -> 8 CTAs = 32 warps per SM): the sort's two key buffers are dead once
+// the tile list is ordered, so the list of record slots and the double-buffered record staging
+// reuse them.
 struct K4Shared {
   SortShared<kCompThreads> sort;
   union {
     uint64_t keys[2][kFusedSortCap];
     struct {
-      uint32_t slots[kFusedSortCap];   // sorted ids
-      float4 s0[kBatch], s1[kBatch], s2[kBatch];
-      float2 box[kBatch];              // half-extents of the alpha >= 1/255 box (R8), inflated
+      uint32_t slots[kFusedSortCap];        // record slot of each list entry, in (z, id) order
+      float4 rec[2][3][kBatch];             // [buffer][R0, R1, R2][entry]
     } c;
   } u;
   unsigned long long red[kCompThreads / 32];
 };
+static_assert(sizeof(uint32_t) * kFusedSortCap + 2 * 3 * 16 * kBatch <= 2 * 8 * kFusedSortCap, "union layout");
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -49,15 +49,21 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // Front-to-back blend of one list entry into one pixel (readings R12-R14), predicated on
 // `use` (alpha >= 1/255 for a live pixel).  A pixel that terminates gets its centre moved to
 // kFar: every later quadratic form is then huge and every later entry fails the alpha test
 // without any per-pixel "done" test in the hot loop.
 constexpr float kFar = 1e20f;
 
-__device__ __forceinline__ void blend(bool use, float arg, const float4& r1, const float4& r2, float& T,
-                                      float& cr, float& cg, float& cb, float& dep, float& pyc, int& n_eval,
-                                      int idx) {
+__device__ __forceinline__ void blend(bool use, float arg, const float4& r2, float& T, float& cr, float& cg,
+                                      float& cb, float& dep, float& pyc, int& n_eval, int idx) {
   const float alpha = fminf(kAlphaMax, ex2_approx(arg));
   const float w = alpha * T;
   const float tT = T - w;                       // T (1 - alpha)
@@ -67,7 +73,7 @@ __device__ __forceinline__ void blend(bool use, float arg, const float4& r1, con
   cr = fmaf(wa, r2.x, cr);
   cg = fmaf(wa, r2.y, cg);
   cb = fmaf(wa, r2.z, cb);
-  dep = fmaf(wa, r1.z, dep);
+  dep = fmaf(wa, r2.w, dep);
   T = add ? tT : T;
   if (term) {
     n_eval = idx + 1;
@@ -93,14 +99,14 @@ __global__ void __launch_bounds__(kCompThreads, 8) k4_composite(CompositeArgs a)
   const uint32_t* off = a.off + (size_t)fl * a.hist_stride;
   const uint64_t start = a.frame_base[fl] - a.key_base + off[t];
   const int len = (int)(off[t + 1] - off[t]);
-  const float4* rec = a.rec + (size_t)fl * a.n * 3;
+  const float4* rec = a.rec + (size_t)fl * a.n * kRecQuads;
   const float pxc = (float)px + 0.5f;
   const float bcx = (float)bx0 + 4.0f, bcy = (float)by0 + 4.0f;  // block centre (pixel centres +-3.5)
 
   // depth order of this tile's list (reading R10): in shared memory, or in HBM (key buffer and
-  // its scratch twin) for the rare lists longer than kFusedSortCap
+  // its scratch twin) for the rare lists longer than kFusedSortCap; then id -> record slot
   const bool fused = len <= kFusedSortCap;
-  const uint32_t* ids_g = nullptr;
+  uint32_t* slots = sm.u.c.slots;
   if (len > 0) {
     if (fused) {
       for (int e = tid; e < len; e += kCompThreads) sm.u.keys[0][e] = a.keys[start + e];
@@ -110,13 +116,13 @@ __global__ void __launch_bounds__(kCompThreads, 8) k4_composite(CompositeArgs a)
 #pragma unroll
       for (int k = 0; k < kFusedSortCap / kCompThreads; ++k) {
         const int e = tid + k * kCompThreads;
-        if (e < len) sl[k] = (uint32_t)sm.u.keys[in_b ? 1 : 0][e];
+        if (e < len) sl[k] = (uint32_t)__ldg(a.inv + (uint32_t)sm.u.keys[in_b ? 1 : 0][e]);
       }
       __syncthreads();
 #pragma unroll
       for (int k = 0; k < kFusedSortCap / kCompThreads; ++k) {
         const int e = tid + k * kCompThreads;
-        if (e < len) sm.u.c.slots[e] = sl[k];
+        if (e < len) slots[e] = sl[k];
       }
     } else {
       uint64_t* ga = const_cast<uint64_t*>(a.keys) + start;
@@ -124,52 +130,53 @@ __global__ void __launch_bounds__(kCompThreads, 8) k4_composite(CompositeArgs a)
       const bool in_b = segment_sort(ga, gb, len, sm.sort);
       uint32_t* dst = a.sorted + start;
       const uint64_t* r = in_b ? gb : ga;
-      for (int e = tid; e < len; e += kCompThreads) dst[e] = (uint32_t)r[e];
-      ids_g = dst;
-      __threadfence_block();
+      for (int e = tid; e < len; e += kCompThreads) dst[e] = (uint32_t)__ldg(a.inv + (uint32_t)r[e]);
+      slots = dst;
     }
   }
+  __syncthreads();  // the slot list is complete
+
+  // stage round b's records into buffer (b & 1): one record (3 x 16 B cp.async) per thread
+  auto stage = [&](int b) {
+    const int k = b * kBatch + tid;
+    if (k < len) {
+      const float4* r = rec + (size_t)slots[k] * kRecQuads;
+      float4 (*buf)[kBatch] = sm.u.c.rec[b & 1];
+      cp_async16(&buf[0][tid], r);
+      cp_async16(&buf[1][tid], r + 1);
+      cp_async16(&buf[2][tid], r + 2);
+    }
+    cp_async_commit();
+  };
 
   float T0 = 1.f, r0c = 0.f, g0c = 0.f, b0c = 0.f, d0 = 0.f;
   float T1 = 1.f, r1c = 0.f, g1c = 0.f, b1c = 0.f, d1 = 0.f;
   float pyc0 = in0 ? (float)py0 + 0.5f : kFar;   // out-of-image pixels never pass the alpha test
   float pyc1 = in1 ? (float)py0 + 1.5f : kFar;
   int ne0 = len, ne1 = len;
-  __syncthreads();  // the sorted id list is complete
-  for (int b = 0; b < len; b += kBatch) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int e = tid + h * kCompThreads;
-      const int k = b + e;
-      if (k < len) {
-        const uint32_t id = fused ? sm.u.c.slots[k] : ids_g[k];
-        const float4* r = rec + (size_t)__ldg(a.inv + id) * 3;
-        const float4 q0 = __ldg(r), q1 = __ldg(r + 1);
-        sm.u.c.s0[e] = q0;
-        sm.u.c.s1[e] = q1;
-        sm.u.c.s2[e] = __ldg(r + 2);
-        // extents of {arg >= log2(1/255)} = {Q' <= kappa'} for Q' = (p dx)^2 + (q dx + r dy)^2:
-        // ex = sqrt(kappa') / p, ey = sqrt(kappa' (p^2 + q^2)) / (p r); inflated by 1% + 0.01 px so
-        // that skipping a block outside it never changes a per-pixel decision
-        const float kap = fmaxf(q1.y - kLog2AlphaMin, 0.f);
-        const float sk = sqrtf(kap);
-        const float ex = __fdividef(sk, q0.z);
-        const float ey = __fdividef(sk * sqrtf(fmaf(q0.z, q0.z, q0.w * q0.w)), q0.z * q1.x);
-        sm.u.c.box[e] = make_float2(fmaf(ex, 1.01f, 0.01f), fmaf(ey, 1.01f, 0.01f));
-      }
-    }
+  const int rounds = (len + kBatch - 1) / kBatch;
+  if (rounds > 0) {
+    stage(0);
+    cp_async_wait_all();
     __syncthreads();
-    const int cnt = min(kBatch, len - b);
+  }
+  for (int b = 0; b < rounds; ++b) {
+    if (b + 1 < rounds) stage(b + 1);   // overlaps this round's compositing
+    const float4* R0 = sm.u.c.rec[b & 1][0];
+    const float4* R1 = sm.u.c.rec[b & 1][1];
+    const float4* R2 = sm.u.c.rec[b & 1][2];
+    const int base = b * kBatch;
+    const int cnt = min(kBatch, len - base);
     if (!__all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) {
-      // which of this batch's records can reach this warp's 8x8 block?
+      // which of this round's records can reach this warp's 8x8 block?
       uint32_t hit[kBatch / 32];
 #pragma unroll
       for (int k = 0; k < kBatch / 32; ++k) {
         const int j = 32 * k + lane;
         bool ov = false;
         if (j < cnt) {
-          const float2 uv = make_float2(sm.u.c.s0[j].x, sm.u.c.s0[j].y);
-          const float2 bx = sm.u.c.box[j];
+          const float2 uv = *reinterpret_cast<const float2*>(&R0[j]);
+          const float2 bx = *reinterpret_cast<const float2*>(&R1[j].z);
           ov = fabsf(uv.x - bcx) <= bx.x + 3.5f && fabsf(uv.y - bcy) <= bx.y + 3.5f;
         }
         hit[k] = __ballot_sync(FULL, ov);
@@ -180,8 +187,8 @@ __global__ void __launch_bounds__(kCompThreads, 8) k4_composite(CompositeArgs a)
         while (m) {
           const int j = 32 * k + __ffs(m) - 1;
           m &= m - 1;
-          const float4 q0 = sm.u.c.s0[j];   // u, v, p, q
-          const float4 q1 = sm.u.c.s1[j];   // r, log2 o, z, id
+          const float4 q0 = R0[j];                                   // u, v, p, q
+          const float2 q1 = *reinterpret_cast<const float2*>(&R1[j]);  // r, log2 o
           const float dx = q0.x - pxc;
           const float t1 = q0.z * dx;
           const float mm = fmaf(-t1, t1, q1.y);
@@ -193,17 +200,19 @@ __global__ void __launch_bounds__(kCompThreads, 8) k4_composite(CompositeArgs a)
           const bool use0 = arg0 >= kLog2AlphaMin;   // alpha >= 1/255
           const bool use1 = arg1 >= kLog2AlphaMin;
           if (use0 || use1) {
-            const float4 q2 = sm.u.c.s2[j];
-            blend(use0, arg0, q1, q2, T0, r0c, g0c, b0c, d0, pyc0, ne0, b + j);
-            blend(use1, arg1, q1, q2, T1, r1c, g1c, b1c, d1, pyc1, ne1, b + j);
+            const float4 q2 = R2[j];                                 // r, g, b, z
+            blend(use0, arg0, q2, T0, r0c, g0c, b0c, d0, pyc0, ne0, base + j);
+            blend(use1, arg1, q2, T1, r1c, g1c, b1c, d1, pyc1, ne1, base + j);
           }
         }
         if (__all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) break;  // whole warp finished
       }
     }
-    // also the barrier that frees the staging buffers for the next round
+    cp_async_wait_all();
+    // round b+1 visible to every warp, round b's buffer free; stop when every pixel is done
     if (__syncthreads_count(pyc0 == kFar && pyc1 == kFar) == kCompThreads) break;
   }
+  cp_async_wait_all();
 
   const size_t f = (size_t)(a.f0 + fl);
   const size_t plane = (size_t)a.width * a.height;
