@@ -46,15 +46,16 @@ __device__ __forceinline__ void bins_excl_scan(SortShared<NT>& sm) {
   __syncthreads();
 }
 
-// one stable counting pass on digit (hi32(key) >> shift) & 0xff: src -> dst
+// one stable counting pass on digit ((hi32(key) - zmin) >> shift) & 0xff: src -> dst
 template <int NT, typename Ptr>
-__device__ __forceinline__ void radix_pass(const Ptr src, Ptr dst, int n, int shift, SortShared<NT>& sm) {
+__device__ __forceinline__ void radix_pass(const Ptr src, Ptr dst, int n, int shift, uint32_t zmin,
+                                           SortShared<NT>& sm) {
   constexpr int kWarps = SortShared<NT>::kWarps;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // digit histogram
   for (int b = tid; b < 256; b += NT) sm.base[b] = 0;
   __syncthreads();
-  for (int e = tid; e < n; e += NT) atomicAdd(&sm.base[(hi32(src[e]) >> shift) & 0xffu], 1u);
+  for (int e = tid; e < n; e += NT) atomicAdd(&sm.base[((hi32(src[e]) - zmin) >> shift) & 0xffu], 1u);
   __syncthreads();
   bins_excl_scan(sm);
   // chunked stable scatter
@@ -62,7 +63,7 @@ __device__ __forceinline__ void radix_pass(const Ptr src, Ptr dst, int n, int sh
     const int e = c + tid;
     const bool valid = e < n;
     const uint64_t key = valid ? src[e] : 0ull;
-    const uint32_t d = valid ? ((hi32(key) >> shift) & 0xffu) : 256u + lane;
+    const uint32_t d = valid ? (((hi32(key) - zmin) >> shift) & 0xffu) : 256u + lane;
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     const uint32_t rank = __popc(peers & lanemask_lt());
     for (int b = tid; b < 256; b += NT)
@@ -87,19 +88,27 @@ __device__ __forceinline__ void radix_pass(const Ptr src, Ptr dst, int n, int sh
   }
 }
 
-// Sort keys[0..n) into (bits(z), id) order.  Two stable 8-bit LSD passes order the keys by
-// the 16 highest bits of z that vary over the segment (bits above them are constant); runs
-// that agree on those bits (rare: it takes two depths within 2^-16 of the segment's depth
-// range) are then insertion-sorted by the full 64-bit key (zbits << 32 | id).  Returns true
-// if the result ended in `b`.
+// Sort keys[0..n) into (bits(z), id) order.  Two stable 8-bit LSD passes order the keys by the
+// 16 highest varying bits of (zbits - zmin) (monotone in z; bits above are zero); runs that agree
+// on those bits (two depths within ~2^-16 of the segment's depth range) are then
+// insertion-sorted by the full 64-bit key (zbits << 32 | id).  Returns true if the result ended
+// in `b`.
 template <int NT, typename Ptr>
 __device__ __forceinline__ bool segment_sort(Ptr a, Ptr b, int n, SortShared<NT>& sm) {
   constexpr int kWarps = SortShared<NT>::kWarps;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // which depth bits vary over the segment?
-  const uint32_t first = hi32(a[0]);
+  // depth range of the segment: sort on (zbits - zmin), whose highest set bit bounds the
+  // number of varying bits (unlike zbits itself, whose exponent bits flip at powers of two)
+  uint32_t zmin = 0xffffffffu;
+  for (int e = tid; e < n; e += NT) zmin = min(zmin, hi32(a[e]));
+  zmin = __reduce_min_sync(0xffffffffu, zmin);
+  if (lane == 0) sm.wred[warp] = zmin;
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) zmin = min(zmin, sm.wred[w]);
+  __syncthreads();
   uint32_t orx = 0;
-  for (int e = tid; e < n; e += NT) orx |= hi32(a[e]) ^ first;
+  for (int e = tid; e < n; e += NT) orx |= hi32(a[e]) - zmin;
   orx = __reduce_or_sync(0xffffffffu, orx);
   if (lane == 0) sm.wred[warp] = orx;
   __syncthreads();
@@ -107,31 +116,32 @@ __device__ __forceinline__ bool segment_sort(Ptr a, Ptr b, int n, SortShared<NT>
 #pragma unroll
   for (int w = 0; w < kWarps; ++w) orx |= sm.wred[w];
   __syncthreads();
-  const int hb = orx ? 31 - __clz(orx) : -1;       // highest varying bit
-  const int lo = hb >= 16 ? hb - 15 : 0;           // sort bits [lo, lo + 16)
+  const int hb = orx ? 31 - __clz(orx) : -1;       // highest varying bit of (zbits - zmin)
+  const int lo = hb >= 16 ? hb - 15 : 0;           // sort bits [lo, lo + 16) of (zbits - zmin)
   bool in_b = false;
   if (hb >= 0) {
     if (((orx >> lo) & 0xffu) != 0) {
-      radix_pass(a, b, n, lo, sm);
+      radix_pass(a, b, n, lo, zmin, sm);
       in_b = true;
     }
     if (((orx >> (lo + 8)) & 0xffu) != 0) {
-      if (in_b) radix_pass(b, a, n, lo + 8, sm);
-      else radix_pass(a, b, n, lo + 8, sm);
+      if (in_b) radix_pass(b, a, n, lo + 8, zmin, sm);
+      else radix_pass(a, b, n, lo + 8, zmin, sm);
       in_b = !in_b;
     }
   }
   Ptr r = in_b ? b : a;
   // runs equal on the sorted bits: finish them by the full key (zbits, id) — reading R10
   int dup = 0;
-  for (int e = tid + 1; e < n; e += NT) dup |= (hi32(r[e]) >> lo) == (hi32(r[e - 1]) >> lo);
+  for (int e = tid + 1; e < n; e += NT) dup |= ((hi32(r[e]) - zmin) >> lo) == ((hi32(r[e - 1]) - zmin) >> lo);
   if (__syncthreads_or(dup)) {
     for (int e = tid; e < n; e += NT) {
-      const uint32_t h = hi32(r[e]) >> lo;
-      const bool start = (e == 0 || (hi32(r[e - 1]) >> lo) != h) && (e + 1 < n && (hi32(r[e + 1]) >> lo) == h);
+      const uint32_t h = (hi32(r[e]) - zmin) >> lo;
+      const bool start = (e == 0 || ((hi32(r[e - 1]) - zmin) >> lo) != h) &&
+                         (e + 1 < n && ((hi32(r[e + 1]) - zmin) >> lo) == h);
       if (!start) continue;
       int end = e + 1;
-      while (end < n && (hi32(r[end]) >> lo) == h) ++end;
+      while (end < n && ((hi32(r[end]) - zmin) >> lo) == h) ++end;
       for (int x = e + 1; x < end; ++x) {  // insertion sort of the run by the 64-bit key
         const uint64_t kx = r[x];
         int y = x - 1;

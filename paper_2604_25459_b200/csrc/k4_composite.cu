@@ -40,6 +40,7 @@ struct K4Shared {
     } c;
   } u;
   unsigned long long red[kCompThreads / 32];
+  uint8_t wlist[kCompThreads / 32][kBatch];   // per-warp compacted record indices of a round
 };
 static_assert(sizeof(uint32_t) * kFusedSortCap + 2 * 3 * 16 * kBatch <= 2 * 8 * kFusedSortCap, "union layout");
 
@@ -56,32 +57,31 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// Front-to-back blend of one list entry into one pixel (readings R12-R14), predicated on
-// `use` (alpha >= 1/255 for a live pixel).  A pixel that terminates gets its centre moved to
-// kFar: every later quadratic form is then huge and every later entry fails the alpha test
-// without any per-pixel "done" test in the hot loop.
+// Front-to-back blend of one list entry into one pixel (readings R12-R14).  alpha is 0 unless
+// `use` (alpha >= 1/255 for a live pixel); then T never drops below 1e-4 without terminating,
+// so an unused entry leaves every accumulator unchanged.  A pixel that terminates gets its
+// centre moved to kFar: every later quadratic form is huge and every later entry fails the
+// alpha test, without a per-pixel "done" test in the hot loop.
 constexpr float kFar = 1e20f;
 
 __device__ __forceinline__ void blend(bool use, float arg, const float4& r2, float& T, float& cr, float& cg,
                                       float& cb, float& dep, float& pyc, int& n_eval, int idx) {
-  const float alpha = fminf(kAlphaMax, ex2_approx(arg));
+  const float alpha = use ? fminf(kAlphaMax, ex2_approx(arg)) : 0.f;
   const float w = alpha * T;
   const float tT = T - w;                       // T (1 - alpha)
-  const bool term = use && tT < kTermT;         // stop before blending (R13)
-  const bool add = use && !term;
-  const float wa = add ? w : 0.f;
-  cr = fmaf(wa, r2.x, cr);
-  cg = fmaf(wa, r2.y, cg);
-  cb = fmaf(wa, r2.z, cb);
-  dep = fmaf(wa, r2.w, dep);
-  T = add ? tT : T;
-  if (term) {
+  if (tT >= kTermT) {
+    cr = fmaf(w, r2.x, cr);
+    cg = fmaf(w, r2.y, cg);
+    cb = fmaf(w, r2.z, cb);
+    dep = fmaf(w, r2.w, dep);
+    T = tT;
+  } else {                                      // stop before blending (R13)
     n_eval = idx + 1;
     pyc = kFar;
   }
 }
 
-__global__ void __launch_bounds__(kCompThreads, 8) k4_composite(CompositeArgs a) {
+__global__ void __launch_bounds__(kCompThreads, 10) k4_composite(CompositeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K4Shared& sm = *reinterpret_cast<K4Shared*>(smem_raw);
   const unsigned FULL = 0xffffffffu;
@@ -168,8 +168,9 @@ __global__ void __launch_bounds__(kCompThreads, 8) k4_composite(CompositeArgs a)
     const int base = b * kBatch;
     const int cnt = min(kBatch, len - base);
     if (!__all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) {
-      // which of this round's records can reach this warp's 8x8 block?
-      uint32_t hit[kBatch / 32];
+      // this warp's list of the round's records that can reach its 8x8 block (u8 indices)
+      uint8_t* wl = sm.wlist[warp];
+      int nsel = 0;
 #pragma unroll
       for (int k = 0; k < kBatch / 32; ++k) {
         const int j = 32 * k + lane;
@@ -179,14 +180,16 @@ __global__ void __launch_bounds__(kCompThreads, 8) k4_composite(CompositeArgs a)
           const float2 bx = *reinterpret_cast<const float2*>(&R1[j].z);
           ov = fabsf(uv.x - bcx) <= bx.x + 3.5f && fabsf(uv.y - bcy) <= bx.y + 3.5f;
         }
-        hit[k] = __ballot_sync(FULL, ov);
+        const unsigned hit = __ballot_sync(FULL, ov);
+        if (ov) wl[nsel + __popc(hit & lanemask_lt())] = (uint8_t)j;
+        nsel += __popc(hit);
       }
-#pragma unroll
-      for (int k = 0; k < kBatch / 32; ++k) {
-        uint32_t m = hit[k];
-        while (m) {
-          const int j = 32 * k + __ffs(m) - 1;
-          m &= m - 1;
+      __syncwarp();
+      for (int i0 = 0; i0 < nsel; i0 += 16) {
+        const int i1 = min(nsel, i0 + 16);
+#pragma unroll 2
+        for (int i = i0; i < i1; ++i) {
+          const int j = wl[i];
           const float4 q0 = R0[j];                                   // u, v, p, q
           const float2 q1 = *reinterpret_cast<const float2*>(&R1[j]);  // r, log2 o
           const float dx = q0.x - pxc;
@@ -207,6 +210,7 @@ __global__ void __launch_bounds__(kCompThreads, 8) k4_composite(CompositeArgs a)
         }
         if (__all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) break;  // whole warp finished
       }
+      __syncwarp();
     }
     cp_async_wait_all();
     // round b+1 visible to every warp, round b's buffer free; stop when every pixel is done
