@@ -81,7 +81,7 @@ __device__ __forceinline__ void blend(bool use, float arg, const float4& r2, flo
   }
 }
 
-__global__ void __launch_bounds__(kCompThreads, 10) k4_composite(CompositeArgs a) {
+__global__ void __launch_bounds__(kCompThreads, 9) k4_composite(CompositeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K4Shared& sm = *reinterpret_cast<K4Shared*>(smem_raw);
   const unsigned FULL = 0xffffffffu;
@@ -176,9 +176,21 @@ __global__ void __launch_bounds__(kCompThreads, 10) k4_composite(CompositeArgs a
         const int j = 32 * k + lane;
         bool ov = false;
         if (j < cnt) {
-          const float2 uv = *reinterpret_cast<const float2*>(&R0[j]);
-          const float2 bx = *reinterpret_cast<const float2*>(&R1[j].z);
-          ov = fabsf(uv.x - bcx) <= bx.x + 3.5f && fabsf(uv.y - bcy) <= bx.y + 3.5f;
+          // lower bound of Q' = (p dx)^2 + (q dx + r dy)^2 over the block's pixel centres
+          // (dx = u - x in [xa, xb], dy = v - y in [ya, yb]): each term minimised on its own;
+          // keep the record unless LB > kappa' with a 2% margin (so no per-pixel decision changes)
+          const float4 q0 = R0[j];                                     // u, v, p, q
+          const float2 q1 = *reinterpret_cast<const float2*>(&R1[j]);  // r, log2 o
+          const float xa = q0.x - (bcx + 3.5f), xb = q0.x - (bcx - 3.5f);
+          const float ya = q0.y - (bcy + 3.5f), yb = q0.y - (bcy - 3.5f);
+          const float dxm = fmaxf(fmaxf(xa, -xb), 0.f);              // distance of 0 to [xa, xb]
+          const float lmin = fmaf(q0.w, q0.w >= 0.f ? xa : xb, q1.x * ya);
+          const float lmax = fmaf(q0.w, q0.w >= 0.f ? xb : xa, q1.x * yb);
+          const float lm = fmaxf(fmaxf(lmin, -lmax), 0.f);           // distance of 0 to [lmin, lmax]
+          const float px_ = q0.z * dxm;
+          const float lb = fmaf(px_, px_, lm * lm);
+          const float kap = q1.y - kLog2AlphaMin;                    // kappa' = log2(255 o)
+          ov = lb <= fmaf(kap, 1.02f, 0.02f);
         }
         const unsigned hit = __ballot_sync(FULL, ov);
         if (ov) wl[nsel + __popc(hit & lanemask_lt())] = (uint8_t)j;
