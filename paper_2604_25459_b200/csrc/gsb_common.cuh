@@ -114,15 +114,16 @@ __device__ __forceinline__ void warp_tile_count(bool has, uint32_t rect, int til
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int tx0 = rect & 0xff, tx1 = (rect >> 8) & 0xff, ty0 = (rect >> 16) & 0xff, ty1 = rect >> 24;
-  const int w = tx1 - tx0 + 1;
-  const int nt = has ? w * (ty1 - ty0 + 1) : 0;
+  const int nt = has ? (tx1 - tx0 + 1) * (ty1 - ty0 + 1) : 0;
   const bool big = nt > kBigRect;
   const int rounds = __reduce_max_sync(FULL, big ? 0 : nt);
+  int tx = tx0, ty = ty0;  // this lane's r-th tile, stepped row-major (no division)
   for (int r = 0; r < rounds; ++r) {
     const bool act = !big && r < nt;
-    const int t = act ? (ty0 + r / w) * tiles_x + tx0 + r % w : -1 - lane;
+    const int t = act ? ty * tiles_x + tx : -1 - lane;
     const unsigned peers = __match_any_sync(FULL, t);
     if (act && lane == __ffs(peers) - 1) atomicAdd(counter + t, __popc(peers));
+    if (++tx > tx1) { tx = tx0; ++ty; }
   }
   unsigned bm = __ballot_sync(FULL, big);
   while (bm) {
@@ -130,8 +131,10 @@ __device__ __forceinline__ void warp_tile_count(bool has, uint32_t rect, int til
     bm &= bm - 1;
     const uint32_t rj = __shfl_sync(FULL, rect, j);
     const int jx0 = rj & 0xff, jx1 = (rj >> 8) & 0xff, jy0 = (rj >> 16) & 0xff, jy1 = rj >> 24;
-    const int jw = jx1 - jx0 + 1, jn = jw * (jy1 - jy0 + 1);
-    for (int k = lane; k < jn; k += 32) atomicAdd(counter + (jy0 + k / jw) * tiles_x + jx0 + k % jw, 1);
+    const int jw = jx1 - jx0 + 1;
+    for (int y = jy0; y <= jy1; ++y)
+      for (int x = jx0 + lane; x <= jx1; x += 32) atomicAdd(counter + y * tiles_x + x, 1);
+    (void)jw;
   }
 }
 

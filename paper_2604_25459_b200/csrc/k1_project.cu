@@ -131,7 +131,10 @@ __device__ __forceinline__ float det2(float a, float b, float c, float d) {
 }
 
 // ------------------------------------------------------------------------------ K1
-template <int D>
+// fast sqrt for conservative bounds (x > 0; x * rsqrt(x), ~2 ulp)
+__device__ __forceinline__ float sqrt_approx(float x) { return x * rsqrtf(x); }
+
+template <int D, bool DEBUG>
 __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool in = i < a.n;
@@ -152,7 +155,7 @@ __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
   const float opac = l2.y, kappa = l2.z, log2o = l2.w;
   // reading R5: o < 1/255 is never visible (binary32 compare == the exact compare)
   const bool o_ok = in && (opac >= 1.0f / 255.0f);
-  const bool debug = a.dbg_rec != nullptr;
+  constexpr bool debug = DEBUG;
   const float wscale = 0.84932180028801904f;  // sqrt(log2(e) / 2)
   const float fw = (float)a.width, fh = (float)a.height;
 
@@ -179,8 +182,8 @@ __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
       // Conservative screen cull: Sigma2D_xx <= jx^2 (1 + limx^2) smax^2 + 0.3 (rows of M are
       // orthonormal, |t/z| <= lim after the clamp), so the exact R9 extents are inside
       // bx, by; a Gaussian whose bound box misses the image has an empty R9 rect as well.
-      const float bx = 1.02f * sqrtf(kappa * fmaf(jx * jx * (1.f + cam.limx * cam.limx), smax2, 0.3f)) + 1.f;
-      const float by = 1.02f * sqrtf(kappa * fmaf(jy * jy * (1.f + cam.limy * cam.limy), smax2, 0.3f)) + 1.f;
+      const float bx = 1.02f * sqrt_approx(kappa * fmaf(jx * jx * (1.f + cam.limx * cam.limx), smax2, 0.3f)) + 1.f;
+      const float by = 1.02f * sqrt_approx(kappa * fmaf(jy * jy * (1.f + cam.limy * cam.limy), smax2, 0.3f)) + 1.f;
       const bool offscreen = (u + bx < 0.f) || (u - bx > fw) || (v + by < 0.f) || (v - by > fh);
       if (!offscreen || debug) {
         // EWA Jacobian with the 1.3 frustum clamp (reading R6), applied to M: rows of J M
@@ -247,9 +250,10 @@ __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
       // ex = sqrt(kappa') / p, ey = sqrt(kappa' (p^2 + q^2)) / (p r) (the R8 box in the whitened
       // metric), inflated by 1% + 0.01 px: K4 skips a pixel block only when it is outside it
       const float kap = fmaxf(log2o - kLog2AlphaMin, 0.f);
-      const float sk = sqrtf(kap);
-      const float ex = fmaf(sk / pw, 1.01f, 0.01f);
-      const float ey = fmaf(sk * sqrtf(fmaf(pw, pw, qw * qw)) / (pw * rw), 1.01f, 0.01f);
+      const float sk = sqrt_approx(fmaxf(kap, 1e-30f));
+      const float ipw = __fdividef(1.f, pw);
+      const float ex = fmaf(sk * ipw, 1.01f, 0.01f);
+      const float ey = fmaf(sk * sqrt_approx(fmaf(pw, pw, qw * qw)) * __fdividef(ipw, rw), 1.01f, 0.01f);
       float4* r = a.rec + ((size_t)fl * a.n + i) * kRecQuads;
       r[0] = make_float4(u, v, pw, qw);
       r[1] = make_float4(rw, log2o, ex, ey);
@@ -272,12 +276,21 @@ void launch_k0(const float* poses, const float* intr, const float* w2c, int n_fr
 void launch_k1(const K1Args& a, int sh_degree, cudaStream_t s) {
   if (a.n == 0) return;
   const unsigned grid = (unsigned)((a.n + 127) / 128);
+  const bool dbg = a.dbg_rec != nullptr;
+#define K1_CASE(D)                                            \
+  case D:                                                     \
+    if (dbg) k1_project<D, true><<<grid, 128, 0, s>>>(a);     \
+    else k1_project<D, false><<<grid, 128, 0, s>>>(a);        \
+    break;
   switch (sh_degree) {
-    case 0: k1_project<0><<<grid, 128, 0, s>>>(a); break;
-    case 1: k1_project<1><<<grid, 128, 0, s>>>(a); break;
-    case 2: k1_project<2><<<grid, 128, 0, s>>>(a); break;
-    default: k1_project<3><<<grid, 128, 0, s>>>(a); break;
+    K1_CASE(0)
+    K1_CASE(1)
+    K1_CASE(2)
+    default:
+      if (dbg) k1_project<3, true><<<grid, 128, 0, s>>>(a);
+      else k1_project<3, false><<<grid, 128, 0, s>>>(a);
   }
+#undef K1_CASE
 }
 
 }  // namespace gsb

@@ -120,19 +120,20 @@ __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
   const uint32_t* off = a.off + (size_t)fl * a.hist_stride;
   uint64_t* keys = a.keys + (a.frame_base[fl] - a.key_base);
   const int tx0 = rect & 0xff, tx1 = (rect >> 8) & 0xff, ty0 = (rect >> 16) & 0xff, ty1 = rect >> 24;
-  const int w = tx1 - tx0 + 1;
-  const int nt = has ? w * (ty1 - ty0 + 1) : 0;
+  const int nt = has ? (tx1 - tx0 + 1) * (ty1 - ty0 + 1) : 0;
   const bool big = nt > kBigRect;
   const int rounds = __reduce_max_sync(FULL, big ? 0 : nt);
+  int tx = tx0, ty = ty0;  // this lane's r-th tile, stepped row-major (no division)
   for (int r = 0; r < rounds; ++r) {
     const bool act = !big && r < nt;
-    const int t = act ? (ty0 + r / w) * a.tiles_x + tx0 + r % w : -1 - lane;
+    const int t = act ? ty * a.tiles_x + tx : -1 - lane;
     const unsigned peers = __match_any_sync(FULL, t);
     const int leader = __ffs(peers) - 1;
     int base = 0;
     if (act && lane == leader) base = atomicAdd(cur + t, __popc(peers));
     base = __shfl_sync(FULL, base, leader);
     if (act) keys[off[t] + base + __popc(peers & lanemask_lt())] = key;
+    if (++tx > tx1) { tx = tx0; ++ty; }
   }
   unsigned bm = __ballot_sync(FULL, big);
   while (bm) {
@@ -141,11 +142,11 @@ __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
     const uint32_t rj = __shfl_sync(FULL, rect, j);
     const uint64_t kj = __shfl_sync(FULL, key, j);
     const int jx0 = rj & 0xff, jx1 = (rj >> 8) & 0xff, jy0 = (rj >> 16) & 0xff, jy1 = rj >> 24;
-    const int jw = jx1 - jx0 + 1, jn = jw * (jy1 - jy0 + 1);
-    for (int k = lane; k < jn; k += 32) {
-      const int t = (jy0 + k / jw) * a.tiles_x + jx0 + k % jw;
-      keys[off[t] + atomicAdd(cur + t, 1)] = kj;
-    }
+    for (int y = jy0; y <= jy1; ++y)
+      for (int x = jx0 + lane; x <= jx1; x += 32) {
+        const int t = y * a.tiles_x + x;
+        keys[off[t] + atomicAdd(cur + t, 1)] = kj;
+      }
   }
 }
 
