@@ -118,15 +118,12 @@ __device__ __forceinline__ void warp_tile_count(bool has, uint32_t rect, int til
   const bool big = nt > kBigRect;
   const int rounds = __reduce_max_sync(FULL, big ? 0 : nt);
   int tx = tx0, ty = ty0;  // this lane's r-th tile, stepped row-major (no division)
-#pragma unroll
-  for (int r = 0; r < kBigRect; ++r) {  // unrolled: the rounds' match/atomics overlap
-    if (r < rounds) {
-      const bool act = !big && r < nt;
-      const int t = act ? ty * tiles_x + tx : -1 - lane;
-      const unsigned peers = __match_any_sync(FULL, t);
-      if (act && lane == __ffs(peers) - 1) atomicAdd(counter + t, __popc(peers));
-      if (++tx > tx1) { tx = tx0; ++ty; }
-    }
+  for (int r = 0; r < rounds; ++r) {
+    const bool act = !big && r < nt;
+    const int t = act ? ty * tiles_x + tx : -1 - lane;
+    const unsigned peers = __match_any_sync(FULL, t);
+    if (act && lane == __ffs(peers) - 1) atomicAdd(counter + t, __popc(peers));
+    if (++tx > tx1) { tx = tx0; ++ty; }
   }
   unsigned bm = __ballot_sync(FULL, big);
   while (bm) {

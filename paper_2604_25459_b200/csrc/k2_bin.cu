@@ -123,29 +123,17 @@ __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
   const int nt = has ? (tx1 - tx0 + 1) * (ty1 - ty0 + 1) : 0;
   const bool big = nt > kBigRect;
   const int rounds = __reduce_max_sync(FULL, big ? 0 : nt);
-  // phase 1: every round's tile, peer group and (for group leaders) cursor atomic, issued back
-  // to back so up to kBigRect atomics per warp are in flight; phase 2: scatter the keys
-  int tt[kBigRect];
-  unsigned pp[kBigRect];
-  int bb[kBigRect];
   int tx = tx0, ty = ty0;  // this lane's r-th tile, stepped row-major (no division)
-#pragma unroll
-  for (int r = 0; r < kBigRect; ++r) {
-    if (r < rounds) {
-      const bool act = !big && r < nt;
-      tt[r] = act ? ty * a.tiles_x + tx : -1 - lane;
-      pp[r] = __match_any_sync(FULL, tt[r]);
-      bb[r] = 0;
-      if (act && lane == __ffs(pp[r]) - 1) bb[r] = atomicAdd(cur + tt[r], __popc(pp[r]));
-      if (++tx > tx1) { tx = tx0; ++ty; }
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < kBigRect; ++r) {
-    if (r < rounds) {
-      const int base = __shfl_sync(FULL, bb[r], __ffs(pp[r]) - 1);
-      if (tt[r] >= 0) keys[off[tt[r]] + base + __popc(pp[r] & lanemask_lt())] = key;
-    }
+  for (int r = 0; r < rounds; ++r) {
+    const bool act = !big && r < nt;
+    const int t = act ? ty * a.tiles_x + tx : -1 - lane;
+    const unsigned peers = __match_any_sync(FULL, t);
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (act && lane == leader) base = atomicAdd(cur + t, __popc(peers));
+    base = __shfl_sync(FULL, base, leader);
+    if (act) keys[off[t] + base + __popc(peers & lanemask_lt())] = key;
+    if (++tx > tx1) { tx = tx0; ++ty; }
   }
   unsigned bm = __ballot_sync(FULL, big);
   while (bm) {
