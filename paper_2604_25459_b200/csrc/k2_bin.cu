@@ -150,82 +150,12 @@ __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
   }
 }
 
-// Variant for frames with at most kSmemTiles tiles: the CTA's 256 Gaussians (Morton-ordered
-// neighbours, so few distinct tiles) first rank their keys per tile with shared-memory atomics,
-// then claim one range per touched tile with a single global atomic each (issued in parallel),
-// and finally scatter.  The keys are unique, so the arbitrary order inside a bucket is fine.
-constexpr int kSmemTiles = 4096;
-
-__global__ void __launch_bounds__(256) k2_emit_cta(ChunkArgs a) {
-  __shared__ int cnt[kSmemTiles];
-  const int fl = a.fs + blockIdx.y;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t w = i >> 5;
-  unsigned word = 0;
-  if (i < a.n) word = a.vis_bits[(size_t)fl * a.vis_words + w];
-  if (__syncthreads_or(word != 0) == 0) return;  // no visible Gaussian in this CTA
-  for (int t = threadIdx.x; t < a.n_tiles; t += blockDim.x) cnt[t] = 0;
-  const int lane = threadIdx.x & 31;
-  const bool has = (word >> lane) & 1u;
-  uint32_t rect = 0, zb = 0, id = 0;
-  if (has) {
-    const float4* r = a.rec + ((size_t)fl * a.n + i) * kRecQuads;
-    zb = __float_as_uint(__ldg(&r[2].w));
-    const float2 r3 = __ldg(reinterpret_cast<const float2*>(r + 3));
-    id = __float_as_uint(r3.x);
-    rect = __float_as_uint(r3.y);
-  }
-  const uint64_t key = ((uint64_t)zb << 32) | (uint64_t)id;
-  const int tx0 = rect & 0xff, tx1 = (rect >> 8) & 0xff, ty0 = (rect >> 16) & 0xff, ty1 = rect >> 24;
-  const int nt = has ? (tx1 - tx0 + 1) * (ty1 - ty0 + 1) : 0;
-  __syncthreads();
-  // local ranks (small rects; bigger ones take the global atomic directly below)
-  constexpr int kLocal = 8;
-  int lr[kLocal];
-  if (nt <= kLocal) {
-    int tx = tx0, ty = ty0;
-#pragma unroll
-    for (int r = 0; r < kLocal; ++r)
-      if (r < nt) {
-        lr[r] = atomicAdd(&cnt[ty * a.tiles_x + tx], 1);
-        if (++tx > tx1) { tx = tx0; ++ty; }
-      }
-  }
-  __syncthreads();
-  int* cur = a.hist + (size_t)fl * a.hist_stride;
-  for (int t = threadIdx.x; t < a.n_tiles; t += blockDim.x) {
-    const int c = cnt[t];
-    if (c) cnt[t] = atomicAdd(cur + t, c);   // this CTA's base inside the tile's bucket
-  }
-  __syncthreads();
-  const uint32_t* off = a.off + (size_t)fl * a.hist_stride;
-  uint64_t* keys = a.keys + (a.frame_base[fl] - a.key_base);
-  if (nt <= kLocal) {
-    int tx = tx0, ty = ty0;
-#pragma unroll
-    for (int r = 0; r < kLocal; ++r)
-      if (r < nt) {
-        const int t = ty * a.tiles_x + tx;
-        keys[off[t] + cnt[t] + lr[r]] = key;
-        if (++tx > tx1) { tx = tx0; ++ty; }
-      }
-  } else {
-    for (int ty = ty0; ty <= ty1; ++ty)
-      for (int tx = tx0; tx <= tx1; ++tx) {
-        const int t = ty * a.tiles_x + tx;
-        keys[off[t] + atomicAdd(cur + t, 1)] = key;
-      }
-  }
-}
-
 void launch_k2_emit(const ChunkArgs& a, cudaStream_t s) {
   const int nf = a.fe - a.fs;
   if (nf <= 0 || a.n == 0) return;
   dim3 grid((unsigned)((a.n + 255) / 256), (unsigned)nf);
-  if (a.n_tiles <= kSmemTiles) k2_emit_cta<<<grid, 256, 0, s>>>(a);
-  else k2_emit<<<grid, 256, 0, s>>>(a);
+  k2_emit<<<grid, 256, 0, s>>>(a);
 }
-
 
 // ------------------------------------------------- records from external fp32 projections
 __global__ void __launch_bounds__(128) k1_external(const float* __restrict__ u, const float* __restrict__ v,
