@@ -12,6 +12,9 @@ OUT = os.path.join(HERE, "libgsb.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
+# shared cudart: one runtime instance per process (torch loads libcudart.so.12 too), so host
+# memory pinned by the caller is recognised as pinned by libgsb's async copies
+LINK = ["-cudart", "shared", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
 
 
 def sources():
@@ -33,7 +36,7 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
-    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", OUT, *sources()]
+    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", OUT, *sources(), *LINK]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     print(" ".join(cmd), file=sys.stderr)

@@ -75,6 +75,8 @@ cudaError_t dalloc(T** p, size_t count) {
 
 enum KClass { KC_SETUP = 0, KC_PROJECT, KC_SCAN, KC_EMIT, KC_SORT, KC_COMPOSITE, KC_N };
 
+constexpr int kMaxChunk = 1024;  // frames per pipeline chunk (upper bound)
+
 }  // namespace
 
 struct gsb_scene_t {
@@ -100,13 +102,12 @@ struct gsb_scene_t {
   uint32_t* vis_bits[2] = {nullptr, nullptr};
   uint32_t* long_list[2] = {nullptr, nullptr};   // lists too long for K4's fused sort
   uint32_t* long_cnt[2] = {nullptr, nullptr};
-  uint32_t* h_lc[2] = {nullptr, nullptr};        // pinned
   int64_t vis_words = 0;
   int* hist[2] = {nullptr, nullptr};
   uint32_t* off[2] = {nullptr, nullptr};
   uint64_t* frame_base[2] = {nullptr, nullptr};
-  uint64_t* h_fb[2] = {nullptr, nullptr};   // pinned
-  int* h_vc[2] = {nullptr, nullptr};        // pinned
+  uint64_t* h_rb[2] = {nullptr, nullptr};   // mapped pinned readback: fb[E+2], vcount[E], n_long
+  uint64_t* d_rb[2] = {nullptr, nullptr};   // its device view
   cudaEvent_t ev_counts[2] = {nullptr, nullptr};
   uint64_t *keys = nullptr, *keys_alt = nullptr;
   uint32_t* sorted = nullptr;
@@ -137,14 +138,12 @@ struct gsb_scene_t {
     for (int s = 0; s < 2; ++s) {
       cudaFree(rec[s]); cudaFree(vcount[s]); cudaFree(hist[s]); cudaFree(off[s]); cudaFree(vis_bits[s]);
       cudaFree(long_list[s]); cudaFree(long_cnt[s]);
-      if (h_lc[s]) cudaFreeHost(h_lc[s]);
-      vis_bits[s] = nullptr; long_list[s] = nullptr; long_cnt[s] = nullptr; h_lc[s] = nullptr;
+      vis_bits[s] = nullptr; long_list[s] = nullptr; long_cnt[s] = nullptr;
       cudaFree(frame_base[s]);
-      if (h_fb[s]) cudaFreeHost(h_fb[s]);
-      if (h_vc[s]) cudaFreeHost(h_vc[s]);
+      if (h_rb[s]) cudaFreeHost(h_rb[s]);
       if (ev_counts[s]) cudaEventDestroy(ev_counts[s]);
       rec[s] = nullptr; vcount[s] = nullptr; hist[s] = nullptr; off[s] = nullptr;
-      frame_base[s] = nullptr; h_fb[s] = nullptr; h_vc[s] = nullptr; ev_counts[s] = nullptr;
+      frame_base[s] = nullptr; h_rb[s] = nullptr; d_rb[s] = nullptr; ev_counts[s] = nullptr;
     }
     cudaFree(keys); cudaFree(keys_alt); cudaFree(sorted); cudaFree(d_pairs);
     cudaFree(st_poses); cudaFree(st_intr); cudaFree(st_w2c);
@@ -253,13 +252,10 @@ struct Pipeline {
     tm.end();
     tm.begin(KC_SCAN);
     launch_k2_scan(s->hist[sl], s->off[sl], s->hist_stride, nf, n_tiles, s->frame_base[sl], s->long_list[sl],
-                   s->long_cnt[sl], kFusedSortCap, st);
+                   s->long_cnt[sl], kFusedSortCap, s->vcount[sl], s->d_rb[sl], st);
     s->launches += 2;
     LAUNCH_CHECK();
     tm.end();
-    CUDA_TRY(cudaMemcpyAsync(s->h_fb[sl], s->frame_base[sl], sizeof(uint64_t) * (nf + 2), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(s->h_vc[sl], s->vcount[sl], sizeof(int) * nf, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(s->h_lc[sl], s->long_cnt[sl], sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaEventRecord(s->ev_counts[sl], st));
     return GSB_OK;
   }
@@ -315,11 +311,13 @@ struct Pipeline {
   gsb_status finish_chunk(int c, int f0, int nf) {
     const int sl = c & 1;
     CUDA_TRY(cudaEventSynchronize(s->ev_counts[sl]));
-    const uint64_t* fb = s->h_fb[sl];
-    for (int i = 0; i < nf; ++i) s->stat_V += s->h_vc[sl][i];
+    const volatile uint64_t* rb = s->h_rb[sl];
+    uint64_t fb[kMaxChunk + 2];
+    for (int i = 0; i < nf + 2; ++i) fb[i] = rb[i];
+    for (int i = 0; i < nf; ++i) s->stat_V += (int64_t)rb[nf + 2 + i];
     s->stat_K += (int64_t)fb[nf];
     s->chunks++;
-    const uint32_t n_long = *s->h_lc[sl];
+    const uint32_t n_long = (uint32_t)rb[2 * nf + 2];
     s->stat_long += n_long;
     s->stat_maxseg = std::max<int64_t>(s->stat_maxseg, (int64_t)fb[nf + 1]);
     if (fb[nf] <= (uint64_t)s->cap) return pass(sl, f0, 0, nf, 0, n_long);
@@ -543,7 +541,7 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
   s->tiles_y = (height + kTile - 1) / kTile;
   s->n_tiles = s->tiles_x * s->tiles_y;
   s->hist_stride = ((int64_t)s->n_tiles + 2 + 31) / 32 * 32;
-  const int E = chunk_frames > 0 ? std::min<int64_t>(chunk_frames, F) : (int)std::min<int64_t>(64, F);
+  const int E = (int)std::min<int64_t>(chunk_frames > 0 ? std::min(chunk_frames, kMaxChunk) : 64, F);
   s->chunk = E;
   int64_t cap = key_capacity;
   if (cap == 0) cap = std::max<int64_t>((int64_t)1 << 22, std::min<int64_t>(3 * (int64_t)E * std::max<int64_t>(s->n, 1), ((int64_t)1 << 32) - 1));
@@ -558,12 +556,11 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
     CUDA_TRY(dalloc(&s->vis_bits[sl], (size_t)E * std::max<int64_t>(s->vis_words, 1)));
     CUDA_TRY(dalloc(&s->long_list[sl], (size_t)E * s->n_tiles));
     CUDA_TRY(dalloc(&s->long_cnt[sl], 1));
-    CUDA_TRY(cudaMallocHost((void**)&s->h_lc[sl], sizeof(uint32_t)));
     CUDA_TRY(dalloc(&s->hist[sl], (size_t)E * s->hist_stride));
     CUDA_TRY(dalloc(&s->off[sl], (size_t)E * s->hist_stride));
     CUDA_TRY(dalloc(&s->frame_base[sl], (size_t)E + 2));
-    CUDA_TRY(cudaMallocHost((void**)&s->h_fb[sl], sizeof(uint64_t) * (E + 2)));
-    CUDA_TRY(cudaMallocHost((void**)&s->h_vc[sl], sizeof(int) * E));
+    CUDA_TRY(cudaHostAlloc((void**)&s->h_rb[sl], sizeof(uint64_t) * (2 * E + 3), cudaHostAllocMapped));
+    CUDA_TRY(cudaHostGetDevicePointer((void**)&s->d_rb[sl], s->h_rb[sl], 0));
     CUDA_TRY(cudaEventCreateWithFlags(&s->ev_counts[sl], cudaEventDisableTiming));
   }
   CUDA_TRY(dalloc(&s->keys, (size_t)cap));
@@ -734,7 +731,7 @@ gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, 
   DBG_TRY(cudaMemsetAsync(hist, 0, sizeof(int) * F * stride, st));
   launch_k1_external(u, v, sxx, syy, kappa, zbits, valid, n, 0, F, width, height, tiles_x, rec, vbits, vwords,
                      vcount, hist, stride, st);
-  launch_k2_scan(hist, off, stride, F, n_tiles, fbase, nullptr, nullptr, 0, st);
+  launch_k2_scan(hist, off, stride, F, n_tiles, fbase, nullptr, nullptr, 0, nullptr, nullptr, st);
   DBG_TRY(cudaGetLastError());
   std::vector<uint64_t> hfb(F + 2);
   DBG_TRY(cudaMemcpyAsync(hfb.data(), fbase, sizeof(uint64_t) * (F + 2), cudaMemcpyDeviceToHost, st));

@@ -97,9 +97,11 @@ void launch_k1_external(const float* u, const float* v, const float* sxx, const 
 // frame_base[E+1] = longest tile list of the chunk
 // Lists longer than long_thresh are appended to long_list (frame << 16 | tile), counted in
 // *long_count (both may be null).
+// host_mapped (device view of mapped pinned memory, may be null) receives
+// [frame_base[0..E+1], vcount[0..E), long_count] as u64.
 void launch_k2_scan(int* hist, uint32_t* off, int64_t hist_stride, int n_frames, int n_tiles,
                     uint64_t* frame_base, uint32_t* long_list, uint32_t* long_count, int long_thresh,
-                    cudaStream_t s);
+                    const int* vcount, uint64_t* host_mapped, cudaStream_t s);
 void launch_k2_emit(const ChunkArgs& a, cudaStream_t s);
 void launch_k3_sort(const ChunkArgs& a, uint32_t n_long, cudaStream_t s);
 void launch_k4_composite(const CompositeArgs& a, cudaStream_t s);

@@ -71,26 +71,39 @@ __global__ void __launch_bounds__(kScanThreads) k2_scan_tiles(int* __restrict__ 
   }
 }
 
-// frame_base[0..E] = exclusive prefix of K_f = off[f][T] (single block)
+// frame_base[0..E] = exclusive prefix of K_f = off[f][T] (single block).  When `host` is set
+// (mapped pinned memory) the values the host needs to size the binning — frame bases, longest
+// list, visible counts, long-list count — are also written straight to host memory, so the
+// readback never queues behind output copies on the copy engine.
 __global__ void k2_scan_frames(const uint32_t* __restrict__ off, int64_t stride, int n_tiles,
-                               int n_frames, uint64_t* __restrict__ frame_base) {
+                               int n_frames, uint64_t* __restrict__ frame_base, const int* __restrict__ vcount,
+                               const uint32_t* __restrict__ long_count, volatile uint64_t* __restrict__ host) {
   if (threadIdx.x != 0) return;
   uint64_t acc = 0, mx = 0;
   for (int f = 0; f < n_frames; ++f) {
     frame_base[f] = acc;
+    if (host) host[f] = acc;
     acc += off[(size_t)f * stride + n_tiles];
     mx = max(mx, (uint64_t)off[(size_t)f * stride + n_tiles + 1]);
   }
   frame_base[n_frames] = acc;
   frame_base[n_frames + 1] = mx;
+  if (host) {
+    host[n_frames] = acc;
+    host[n_frames + 1] = mx;
+    for (int f = 0; f < n_frames; ++f) host[n_frames + 2 + f] = vcount ? (uint64_t)vcount[f] : 0ull;
+    host[2 * n_frames + 2] = long_count ? (uint64_t)*long_count : 0ull;
+    __threadfence_system();
+  }
 }
 
 void launch_k2_scan(int* hist, uint32_t* off, int64_t hist_stride, int n_frames, int n_tiles,
                     uint64_t* frame_base, uint32_t* long_list, uint32_t* long_count, int long_thresh,
-                    cudaStream_t s) {
+                    const int* vcount, uint64_t* host_mapped, cudaStream_t s) {
   k2_scan_tiles<<<n_frames, kScanThreads, 0, s>>>(hist, off, hist_stride, n_tiles, long_list, long_count,
                                                   long_thresh);
-  k2_scan_frames<<<1, 32, 0, s>>>(off, hist_stride, n_tiles, n_frames, frame_base);
+  k2_scan_frames<<<1, 32, 0, s>>>(off, hist_stride, n_tiles, n_frames, frame_base, vcount, long_count,
+                                  host_mapped);
 }
 
 // ------------------------------------------------------------------------------ emission

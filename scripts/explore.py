@@ -1,0 +1,64 @@
+"""Exploration on the GPU box: pinned-copy bandwidth and device frames/s on every config."""
+import json
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import paper_2604_25459_b200 as gsb  # noqa: E402
+import synth  # noqa: E402
+
+res = {}
+# pinned copy bandwidth (the e2e ceiling)
+n = 1 << 28  # 1 GiB of fp32
+h = torch.empty(n, pin_memory=True)
+d = torch.empty(n, device="cuda")
+for name, (dst, src) in {"d2h": (h, d), "h2d": (d, h)}.items():
+    dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(3):
+        dst.copy_(src, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    res[name + "_GBps"] = 3 * 4 * n / (e0.elapsed_time(e1) / 1e3) / 1e9
+del h, d
+torch.cuda.empty_cache()
+print(json.dumps(res), flush=True)
+
+envs = {"C2": 64, "C3": 1024, "C4": 4096, "C5": 1024, "T1": 3}
+for name in sys.argv[1:] or ["C2", "C4", "C5", "C3"]:
+    cfg = synth.CONFIGS[name]
+    B = envs.get(name, cfg.n_envs)
+    sc = synth.make_scene(cfg)
+    g = gsb.Scene.from_synth(sc)
+    g.reserve(B, cfg.n_cams, cfg.width, cfg.height)
+    K, W = synth.make_cameras(cfg, np.arange(B))
+    poses = [torch.from_numpy(synth.make_poses(cfg, np.arange(B), s)).cuda() for s in range(4)]
+    K, W = torch.from_numpy(K).cuda(), torch.from_numpy(W).cuda()
+    rgb = torch.empty((B, cfg.n_cams, 3, cfg.height, cfg.width), device="cuda")
+    dep = torch.empty((B, cfg.n_cams, cfg.height, cfg.width), device="cuda")
+    g.render(poses[0], K, W, gsb.RenderParams(cfg.width, cfg.height, stats=True), rgb, dep)
+    st = g.stats()
+    prm = gsb.RenderParams(cfg.width, cfg.height, timing=True)
+    for s in range(2):
+        g.render(poses[s], K, W, prm, rgb, dep)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for s in range(3):
+        g.render(poses[(s + 1) % 4], K, W, prm, rgb, dep)
+    e1.record()
+    torch.cuda.synchronize()
+    tm = g.timings()
+    F = B * cfg.n_cams
+    out = {"config": name, "frames": F, "W": cfg.width, "H": cfg.height, "N": sc.n,
+           "fps": 3 * F / (e0.elapsed_time(e1) / 1e3), "V/f": st["V"] / F, "K/f": st["K"] / F, "P/f": st["P"] / F,
+           "stage_ms": {k: round(v, 2) for k, v in tm.items() if k.endswith("_ms")},
+           "long_lists": tm["long_lists"], "max_list": tm["max_list"]}
+    print(json.dumps(out), flush=True)
+    del g, rgb, dep
+    torch.cuda.empty_cache()
