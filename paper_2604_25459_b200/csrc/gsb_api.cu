@@ -272,7 +272,7 @@ struct Pipeline {
     if (s->n > 0) s->launches++;
     LAUNCH_CHECK();
     tm.end();
-    (void)n_long;  // long lists are sorted in HBM by their K4 CTA (K3 serves gsb_debug_bin_sort)
+    // long lists are sorted by their K4 CTA (K3 serves gsb_debug_bin_sort)
     CompositeArgs c{};
     c.rec = s->rec[sl]; c.n = s->n; c.off = s->off[sl]; c.frame_base = s->frame_base[sl];
     c.hist_stride = s->hist_stride; c.sorted = s->sorted; c.keys = s->keys; c.keys_alt = s->keys_alt;
@@ -283,7 +283,8 @@ struct Pipeline {
     c.out_rgb = out_rgb; c.out_depth = out_depth; c.out_alpha = out_alpha; c.out_n_eval = out_neval;
     c.stat_pairs = (p->flags & GSB_FLAG_STATS) ? s->d_pairs : nullptr;
     tm.begin(KC_COMPOSITE);
-    launch_k4_composite(c, st);
+    // many lists beyond the small fused-sort capacity (e.g. 128x128 views): larger variant
+    launch_k4_composite(c, (uint64_t)n_long * 16 > (uint64_t)(fe - fs) * n_tiles, st);
     s->launches++;
     s->comp_launches++;
     LAUNCH_CHECK();

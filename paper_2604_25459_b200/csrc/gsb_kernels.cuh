@@ -7,7 +7,8 @@
 
 namespace gsb {
 
-constexpr int kFusedSortCap = 1024;  // tile lists up to this length are sorted in K4 smem (8 CTAs/SM)
+constexpr int kFusedSortCap = 1024;  // tile lists up to this length are sorted in K4 smem (8 CTAs/SM);
+                                     // chunks with many longer lists use a 4x variant
 
 struct K1Args {
   // template (K5: shared read-only buffer, one copy for every env)
@@ -104,6 +105,7 @@ void launch_k2_scan(int* hist, uint32_t* off, int64_t hist_stride, int n_frames,
                     const int* vcount, uint64_t* host_mapped, cudaStream_t s);
 void launch_k2_emit(const ChunkArgs& a, cudaStream_t s);
 void launch_k3_sort(const ChunkArgs& a, uint32_t n_long, cudaStream_t s);
-void launch_k4_composite(const CompositeArgs& a, cudaStream_t s);
+// long_lists: use the variant with a 4x larger shared-memory sort (fewer CTAs per SM)
+void launch_k4_composite(const CompositeArgs& a, bool long_lists, cudaStream_t s);
 
 }  // namespace gsb

@@ -157,4 +157,113 @@ __device__ __forceinline__ bool segment_sort(Ptr a, Ptr b, int n, SortShared<NT>
   return in_b;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Packed tile sort (K4): the segment's 64-bit keys stay where K2 wrote them (HBM/L2); the sort
+// runs on 32-bit words (16 highest varying bits of zbits - zmin) << 16 | local index, so the
+// double buffer costs 8 B per key and each pass moves 4 B.  Runs equal on the 16 bits (depths
+// within ~2^-16 of the segment's range) are finished by the full key (zbits << 32 | id) read
+// back through L2.  Result: local indices in (bits(z), id) order (reading R10).
+template <int NT>
+__device__ __forceinline__ void radix_pass32(const uint32_t* src, uint32_t* dst, int n, int shift,
+                                             SortShared<NT>& sm) {
+  constexpr int kWarps = SortShared<NT>::kWarps;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int b = tid; b < 256; b += NT) sm.base[b] = 0;
+  __syncthreads();
+  for (int e = tid; e < n; e += NT) atomicAdd(&sm.base[(src[e] >> shift) & 0xffu], 1u);
+  __syncthreads();
+  bins_excl_scan(sm);
+  for (int c = 0; c < n; c += NT) {
+    const int e = c + tid;
+    const bool valid = e < n;
+    const uint32_t key = valid ? src[e] : 0u;
+    const uint32_t d = valid ? ((key >> shift) & 0xffu) : 256u + lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t rank = __popc(peers & lanemask_lt());
+    for (int b = tid; b < 256; b += NT)
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) sm.whist[w][b] = 0;
+    __syncthreads();
+    if (valid && rank == 0) sm.whist[warp][d] = __popc(peers);
+    __syncthreads();
+    for (int b = tid; b < 256; b += NT) {
+      uint32_t run = sm.base[b];
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const uint32_t t = sm.whist[w][b];
+        sm.whist[w][b] = run;
+        run += t;
+      }
+      sm.base[b] = run;
+    }
+    __syncthreads();
+    if (valid) dst[sm.whist[warp][d] + rank] = key;
+    __syncthreads();
+  }
+}
+
+// n <= 65536.  Returns true if the sorted words ended in `b` (else `a`).
+template <int NT>
+__device__ __forceinline__ bool packed_sort(const uint64_t* __restrict__ gkeys, int n, uint32_t* a, uint32_t* b,
+                                            SortShared<NT>& sm) {
+  constexpr int kWarps = SortShared<NT>::kWarps;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t zmin = 0xffffffffu;
+  for (int e = tid; e < n; e += NT) zmin = min(zmin, hi32(__ldg(gkeys + e)));
+  zmin = __reduce_min_sync(0xffffffffu, zmin);
+  if (lane == 0) sm.wred[warp] = zmin;
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) zmin = min(zmin, sm.wred[w]);
+  __syncthreads();
+  uint32_t orx = 0;
+  for (int e = tid; e < n; e += NT) orx |= hi32(__ldg(gkeys + e)) - zmin;
+  orx = __reduce_or_sync(0xffffffffu, orx);
+  if (lane == 0) sm.wred[warp] = orx;
+  __syncthreads();
+  orx = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) orx |= sm.wred[w];
+  const int hb = orx ? 31 - __clz(orx) : -1;
+  const int lo = hb >= 16 ? hb - 15 : 0;
+  const uint32_t field_or = orx >> lo;              // which of the 16 field bits vary
+  for (int e = tid; e < n; e += NT)
+    a[e] = ((((hi32(__ldg(gkeys + e)) - zmin) >> lo) & 0xffffu) << 16) | (uint32_t)e;
+  __syncthreads();
+  bool in_b = false;
+  if (field_or & 0xffu) {
+    radix_pass32(a, b, n, 16, sm);
+    in_b = true;
+  }
+  if (field_or & 0xff00u) {
+    if (in_b) radix_pass32(b, a, n, 24, sm);
+    else radix_pass32(a, b, n, 24, sm);
+    in_b = !in_b;
+  }
+  uint32_t* r = in_b ? b : a;
+  int dup = 0;
+  for (int e = tid + 1; e < n; e += NT) dup |= (r[e] >> 16) == (r[e - 1] >> 16);
+  if (__syncthreads_or(dup)) {
+    for (int e = tid; e < n; e += NT) {
+      const uint32_t h = r[e] >> 16;
+      const bool start = (e == 0 || (r[e - 1] >> 16) != h) && (e + 1 < n && (r[e + 1] >> 16) == h);
+      if (!start) continue;
+      int end = e + 1;
+      while (end < n && (r[end] >> 16) == h) ++end;
+      for (int x = e + 1; x < end; ++x) {  // insertion sort of the run by the full key
+        const uint32_t wx = r[x];
+        const uint64_t kx = __ldg(gkeys + (wx & 0xffffu));
+        int y = x - 1;
+        while (y >= e && __ldg(gkeys + (r[y] & 0xffffu)) > kx) {
+          r[y + 1] = r[y];
+          --y;
+        }
+        r[y + 1] = wx;
+      }
+    }
+    __syncthreads();
+  }
+  return in_b;
+}
+
 }  // namespace gsb

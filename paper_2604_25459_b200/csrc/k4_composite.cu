@@ -27,22 +27,21 @@ namespace gsb {
 constexpr int kCompThreads = 128;          // 2 pixels per thread: a 16x16 tile per CTA
 constexpr int kBatch = kCompThreads;       // records staged per round (one cp.async set per thread)
 
-// Shared memory (~21.5 KB -> 8 CTAs = 32 warps per SM): the sort's two key buffers are dead once
-// the tile list is ordered, so the list of record slots and the double-buffered record staging
-// reuse them.
+// Shared memory: the packed sort's two word buffers (CAP x 4 B each); after the sort the
+// result buffer's words are resolved into record slots in the other buffer, and the
+// double-buffered record staging (2 x 3 x 128 float4 = 12 KB) reuses the result buffer when
+// it is large enough (CAP >= 3072), else has its own area.
+//   CAP 1024: ~25.6 KB -> 8 CTAs/SM;  CAP 4096: ~37.6 KB -> 5 CTAs/SM (long-list configs)
+constexpr int kStageQuads = 2 * 3 * kBatch;
+template <int CAP>
 struct K4Shared {
+  static constexpr bool kOwnStage = CAP * 4 < kStageQuads * 16;
   SortShared<kCompThreads> sort;
-  union {
-    uint64_t keys[2][kFusedSortCap];
-    struct {
-      uint32_t slots[kFusedSortCap];        // record slot of each list entry, in (z, id) order
-      float4 rec[2][3][kBatch];             // [buffer][R0, R1, R2][entry]
-    } c;
-  } u;
+  uint32_t buf[2][CAP];
+  float4 stage[kOwnStage ? kStageQuads : 1];
   unsigned long long red[kCompThreads / 32];
   uint8_t wlist[kCompThreads / 32][kBatch];   // per-warp compacted record indices of a round
 };
-static_assert(sizeof(uint32_t) * kFusedSortCap + 2 * 3 * 16 * kBatch <= 2 * 8 * kFusedSortCap, "union layout");
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -81,9 +80,10 @@ __device__ __forceinline__ void blend(bool use, float arg, const float4& r2, flo
   }
 }
 
-__global__ void __launch_bounds__(kCompThreads, 9) k4_composite(CompositeArgs a) {
+template <int CAP, int MINB>
+__global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  K4Shared& sm = *reinterpret_cast<K4Shared*>(smem_raw);
+  K4Shared<CAP>& sm = *reinterpret_cast<K4Shared<CAP>*>(smem_raw);
   const unsigned FULL = 0xffffffffu;
   const int fl = a.fs + blockIdx.x / a.n_tiles;
   const int t = blockIdx.x % a.n_tiles;
@@ -103,27 +103,21 @@ __global__ void __launch_bounds__(kCompThreads, 9) k4_composite(CompositeArgs a)
   const float pxc = (float)px + 0.5f;
   const float bcx = (float)bx0 + 4.0f, bcy = (float)by0 + 4.0f;  // block centre (pixel centres +-3.5)
 
-  // depth order of this tile's list (reading R10): in shared memory, or in HBM (key buffer and
-  // its scratch twin) for the rare lists longer than kFusedSortCap; then id -> record slot
-  const bool fused = len <= kFusedSortCap;
-  uint32_t* slots = sm.u.c.slots;
+  // depth order of this tile's list (reading R10): packed sort in shared memory, or the 64-bit
+  // sort in HBM (key buffer and its scratch twin) for lists longer than CAP; then id -> slot
+  const bool fused = len <= CAP;
+  const uint32_t* slots = sm.buf[1];
+  float4* stg = K4Shared<CAP>::kOwnStage ? sm.stage : reinterpret_cast<float4*>(sm.buf[0]);
   if (len > 0) {
     if (fused) {
-      for (int e = tid; e < len; e += kCompThreads) sm.u.keys[0][e] = a.keys[start + e];
-      __syncthreads();
-      const bool in_b = len > 1 && segment_sort(sm.u.keys[0], sm.u.keys[1], len, sm.sort);
-      uint32_t sl[kFusedSortCap / kCompThreads];
-#pragma unroll
-      for (int k = 0; k < kFusedSortCap / kCompThreads; ++k) {
-        const int e = tid + k * kCompThreads;
-        if (e < len) sl[k] = (uint32_t)__ldg(a.inv + (uint32_t)sm.u.keys[in_b ? 1 : 0][e]);
-      }
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < kFusedSortCap / kCompThreads; ++k) {
-        const int e = tid + k * kCompThreads;
-        if (e < len) slots[e] = sl[k];
-      }
+      const uint64_t* gk = a.keys + start;
+      const bool in_b = packed_sort(gk, len, sm.buf[0], sm.buf[1], sm.sort);
+      const uint32_t* res = sm.buf[in_b ? 1 : 0];
+      uint32_t* sl = sm.buf[in_b ? 0 : 1];
+      for (int e = tid; e < len; e += kCompThreads)
+        sl[e] = (uint32_t)__ldg(a.inv + (uint32_t)__ldg(gk + (res[e] & 0xffffu)));
+      slots = sl;
+      if (!K4Shared<CAP>::kOwnStage) stg = reinterpret_cast<float4*>(sm.buf[in_b ? 1 : 0]);
     } else {
       uint64_t* ga = const_cast<uint64_t*>(a.keys) + start;
       uint64_t* gb = a.keys_alt + start;
@@ -134,17 +128,17 @@ __global__ void __launch_bounds__(kCompThreads, 9) k4_composite(CompositeArgs a)
       slots = dst;
     }
   }
-  __syncthreads();  // the slot list is complete
+  __syncthreads();  // the slot list is complete (and the sort buffers are free)
 
   // stage round b's records into buffer (b & 1): one record (3 x 16 B cp.async) per thread
   auto stage = [&](int b) {
     const int k = b * kBatch + tid;
     if (k < len) {
       const float4* r = rec + (size_t)slots[k] * kRecQuads;
-      float4 (*buf)[kBatch] = sm.u.c.rec[b & 1];
-      cp_async16(&buf[0][tid], r);
-      cp_async16(&buf[1][tid], r + 1);
-      cp_async16(&buf[2][tid], r + 2);
+      float4* buf = stg + (b & 1) * 3 * kBatch;
+      cp_async16(&buf[tid], r);
+      cp_async16(&buf[kBatch + tid], r + 1);
+      cp_async16(&buf[2 * kBatch + tid], r + 2);
     }
     cp_async_commit();
   };
@@ -162,9 +156,9 @@ __global__ void __launch_bounds__(kCompThreads, 9) k4_composite(CompositeArgs a)
   }
   for (int b = 0; b < rounds; ++b) {
     if (b + 1 < rounds) stage(b + 1);   // overlaps this round's compositing
-    const float4* R0 = sm.u.c.rec[b & 1][0];
-    const float4* R1 = sm.u.c.rec[b & 1][1];
-    const float4* R2 = sm.u.c.rec[b & 1][2];
+    const float4* R0 = stg + (b & 1) * 3 * kBatch;
+    const float4* R1 = R0 + kBatch;
+    const float4* R2 = R1 + kBatch;
     const int base = b * kBatch;
     const int cnt = min(kBatch, len - base);
     if (!__all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) {
@@ -260,15 +254,23 @@ __global__ void __launch_bounds__(kCompThreads, 9) k4_composite(CompositeArgs a)
   }
 }
 
-void launch_k4_composite(const CompositeArgs& a, cudaStream_t s) {
-  const int nf = a.fe - a.fs;
-  if (nf <= 0) return;
+template <int CAP, int MINB>
+static void launch_k4_variant(const CompositeArgs& a, unsigned grid, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k4_composite, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K4Shared));
+    cudaFuncSetAttribute(k4_composite<CAP, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(K4Shared<CAP>));
     attr = true;
   }
-  k4_composite<<<(unsigned)nf * a.n_tiles, kCompThreads, sizeof(K4Shared), s>>>(a);
+  k4_composite<CAP, MINB><<<grid, kCompThreads, sizeof(K4Shared<CAP>), s>>>(a);
+}
+
+void launch_k4_composite(const CompositeArgs& a, bool long_lists, cudaStream_t s) {
+  const int nf = a.fe - a.fs;
+  if (nf <= 0) return;
+  const unsigned grid = (unsigned)nf * a.n_tiles;
+  if (long_lists) launch_k4_variant<4 * kFusedSortCap, 5>(a, grid, s);
+  else launch_k4_variant<kFusedSortCap, 8>(a, grid, s);
 }
 
 }  // namespace gsb

@@ -167,6 +167,8 @@ CONFIGS: Dict[str, Config] = {
     "T3": Config("T3", 13, 4, 1, 48, 40, 3000, 0, 0, 0),
     "T4": Config("T4", 14, 2, 2, 64, 64, 8000, 10, 200, 1, fov60=True),
     "T5": Config("T5", 15, 2, 1, 160, 120, 12000, 10, 200, 2),
+    # long tile lists (C4-like density at parity size): exercises K4's large-capacity variant
+    "T6": Config("T6", 16, 2, 2, 64, 64, 40000, 10, 200, 3, fov60=True),
 }
 
 
