@@ -27,21 +27,30 @@ namespace gsb {
 constexpr int kCompThreads = 128;          // 2 pixels per thread: a 16x16 tile per CTA
 constexpr int kBatch = kCompThreads;       // records staged per round (one cp.async set per thread)
 
-// Shared memory: the packed sort's two word buffers (CAP x 4 B each); after the sort the
-// result buffer's words are resolved into record slots in the other buffer, and the
-// double-buffered record staging (2 x 3 x 128 float4 = 12 KB) reuses the result buffer when
-// it is large enough (CAP >= 3072), else has its own area.
-//   CAP 1024: ~25.6 KB -> 8 CTAs/SM;  CAP 4096: ~37.6 KB -> 5 CTAs/SM (long-list configs)
+// Shared memory.  Small variant (CAP = kFusedSortCap, ~21.5 KB -> 9 CTAs/SM): the tile's
+// 64-bit keys are loaded once and radix-sorted in smem; the key buffers are then reused for
+// the slot list and the double-buffered record staging (2 x 3 x 128 float4 = 12 KB).
+// Large variant (CAP = 4 kFusedSortCap, ~37.6 KB -> 5 CTAs/SM, for views whose tile lists are
+// mostly long): the keys stay in L2 and a packed 32-bit sort runs on 8 B per key; the result
+// buffer then holds the staging and the other buffer the slot list.
 constexpr int kStageQuads = 2 * 3 * kBatch;
 template <int CAP>
 struct K4Shared {
-  static constexpr bool kOwnStage = CAP * 4 < kStageQuads * 16;
+  static constexpr bool kPacked = CAP > kFusedSortCap;
   SortShared<kCompThreads> sort;
-  uint32_t buf[2][CAP];
-  float4 stage[kOwnStage ? kStageQuads : 1];
+  union {
+    uint64_t keys[kPacked ? 1 : 2][kPacked ? 1 : CAP];         // small variant: 64-bit sort
+    struct {
+      uint32_t slots[kPacked ? 1 : CAP];
+      float4 stage[kStageQuads];
+    } c;
+    uint32_t buf[2][kPacked ? CAP : 1];                          // large variant: packed sort
+  } u;
   unsigned long long red[kCompThreads / 32];
   uint8_t wlist[kCompThreads / 32][kBatch];   // per-warp compacted record indices of a round
 };
+static_assert(sizeof(uint32_t) * kFusedSortCap + 16 * kStageQuads <= 2 * 8 * kFusedSortCap, "small union");
+static_assert(4 * 4 * kFusedSortCap >= 16 * kStageQuads, "large variant stages in the result buffer");
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -103,30 +112,52 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
   const float pxc = (float)px + 0.5f;
   const float bcx = (float)bx0 + 4.0f, bcy = (float)by0 + 4.0f;  // block centre (pixel centres +-3.5)
 
-  // depth order of this tile's list (reading R10): packed sort in shared memory, or the 64-bit
-  // sort in HBM (key buffer and its scratch twin) for lists longer than CAP; then id -> slot
+  // depth order of this tile's list (reading R10), then id -> record slot.  Lists longer than
+  // CAP are sorted as 64-bit keys in HBM (key buffer and its scratch twin).
   const bool fused = len <= CAP;
-  const uint32_t* slots = sm.buf[1];
-  float4* stg = K4Shared<CAP>::kOwnStage ? sm.stage : reinterpret_cast<float4*>(sm.buf[0]);
-  if (len > 0) {
-    if (fused) {
+  const uint32_t* slots = nullptr;
+  float4* stg = nullptr;
+  if constexpr (K4Shared<CAP>::kPacked) {
+    stg = reinterpret_cast<float4*>(sm.u.buf[0]);
+    if (fused && len > 0) {
       const uint64_t* gk = a.keys + start;
-      const bool in_b = packed_sort(gk, len, sm.buf[0], sm.buf[1], sm.sort);
-      const uint32_t* res = sm.buf[in_b ? 1 : 0];
-      uint32_t* sl = sm.buf[in_b ? 0 : 1];
+      const bool in_b = packed_sort(gk, len, sm.u.buf[0], sm.u.buf[1], sm.sort);
+      const uint32_t* res = sm.u.buf[in_b ? 1 : 0];
+      uint32_t* sl = sm.u.buf[in_b ? 0 : 1];
       for (int e = tid; e < len; e += kCompThreads)
         sl[e] = (uint32_t)__ldg(a.inv + (uint32_t)__ldg(gk + (res[e] & 0xffffu)));
       slots = sl;
-      if (!K4Shared<CAP>::kOwnStage) stg = reinterpret_cast<float4*>(sm.buf[in_b ? 1 : 0]);
-    } else {
-      uint64_t* ga = const_cast<uint64_t*>(a.keys) + start;
-      uint64_t* gb = a.keys_alt + start;
-      const bool in_b = segment_sort(ga, gb, len, sm.sort);
-      uint32_t* dst = a.sorted + start;
-      const uint64_t* r = in_b ? gb : ga;
-      for (int e = tid; e < len; e += kCompThreads) dst[e] = (uint32_t)__ldg(a.inv + (uint32_t)r[e]);
-      slots = dst;
+      stg = reinterpret_cast<float4*>(sm.u.buf[in_b ? 1 : 0]);
     }
+  } else {
+    stg = sm.u.c.stage;
+    slots = sm.u.c.slots;
+    if (fused && len > 0) {
+      for (int e = tid; e < len; e += kCompThreads) sm.u.keys[0][e] = a.keys[start + e];
+      __syncthreads();
+      const bool in_b = len > 1 && segment_sort(sm.u.keys[0], sm.u.keys[1], len, sm.sort);
+      uint32_t sl[CAP / kCompThreads];
+#pragma unroll
+      for (int k = 0; k < CAP / kCompThreads; ++k) {
+        const int e = tid + k * kCompThreads;
+        if (e < len) sl[k] = (uint32_t)__ldg(a.inv + (uint32_t)sm.u.keys[in_b ? 1 : 0][e]);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < CAP / kCompThreads; ++k) {
+        const int e = tid + k * kCompThreads;
+        if (e < len) sm.u.c.slots[e] = sl[k];
+      }
+    }
+  }
+  if (!fused) {
+    uint64_t* ga = const_cast<uint64_t*>(a.keys) + start;
+    uint64_t* gb = a.keys_alt + start;
+    const bool in_b = segment_sort(ga, gb, len, sm.sort);
+    uint32_t* dst = a.sorted + start;
+    const uint64_t* r = in_b ? gb : ga;
+    for (int e = tid; e < len; e += kCompThreads) dst[e] = (uint32_t)__ldg(a.inv + (uint32_t)r[e]);
+    slots = dst;
   }
   __syncthreads();  // the slot list is complete (and the sort buffers are free)
 
@@ -270,7 +301,7 @@ void launch_k4_composite(const CompositeArgs& a, bool long_lists, cudaStream_t s
   if (nf <= 0) return;
   const unsigned grid = (unsigned)nf * a.n_tiles;
   if (long_lists) launch_k4_variant<4 * kFusedSortCap, 5>(a, grid, s);
-  else launch_k4_variant<kFusedSortCap, 8>(a, grid, s);
+  else launch_k4_variant<kFusedSortCap, 9>(a, grid, s);
 }
 
 }  // namespace gsb
