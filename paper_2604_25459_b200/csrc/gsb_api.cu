@@ -542,7 +542,10 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
   s->tiles_y = (height + kTile - 1) / kTile;
   s->n_tiles = s->tiles_x * s->tiles_y;
   s->hist_stride = ((int64_t)s->n_tiles + 2 + 31) / 32 * 32;
-  const int E = (int)std::min<int64_t>(chunk_frames > 0 ? std::min(chunk_frames, kMaxChunk) : 64, F);
+  // automatic chunk: >= 64 frames and ~64k tiles per chunk (small views get bigger chunks so
+  // every K4 launch has many waves of CTAs)
+  const int auto_e = (int)std::min<int64_t>(512, std::max<int64_t>(64, (65536 + s->n_tiles - 1) / s->n_tiles));
+  const int E = (int)std::min<int64_t>(chunk_frames > 0 ? std::min(chunk_frames, kMaxChunk) : auto_e, F);
   s->chunk = E;
   int64_t cap = key_capacity;
   if (cap == 0) cap = std::max<int64_t>((int64_t)1 << 22, std::min<int64_t>(3 * (int64_t)E * std::max<int64_t>(s->n, 1), ((int64_t)1 << 32) - 1));

@@ -13,6 +13,8 @@
 // K1 is Gaussian-major: one thread owns one template Gaussian (its parameters stay in
 // registers) and loops over the E frames of a chunk, so the shared read-only template (K5)
 // is read from HBM once per chunk, not once per frame.
+#include <algorithm>
+
 #include "gsb_common.cuh"
 #include "gsb_kernels.cuh"
 
@@ -159,7 +161,11 @@ __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
   const float wscale = 0.84932180028801904f;  // sqrt(log2(e) / 2)
   const float fw = (float)a.width, fh = (float)a.height;
 
-  for (int fl = 0; fl < a.n_frames; ++fl) {
+  // frames of the chunk handled by this block row (gridDim.y rows split the frame loop so the
+  // grid has enough CTAs when N is small)
+  const int fpr = (a.n_frames + gridDim.y - 1) / gridDim.y;
+  const int fl_lo = blockIdx.y * fpr, fl_hi = min(a.n_frames, fl_lo + fpr);
+  for (int fl = fl_lo; fl < fl_hi; ++fl) {
     const int f = a.f0 + fl;
     const float4* tb = a.table + ((size_t)f * a.nb1 + (body + 1)) * 4;
     const float4 r2 = __ldg(tb + 2);
@@ -275,7 +281,10 @@ void launch_k0(const float* poses, const float* intr, const float* w2c, int n_fr
 
 void launch_k1(const K1Args& a, int sh_degree, cudaStream_t s) {
   if (a.n == 0) return;
-  const unsigned grid = (unsigned)((a.n + 127) / 128);
+  // >= ~4 waves of 8 CTAs x 148 SMs: split the frame loop over gridDim.y when N is small
+  const unsigned gx = (unsigned)((a.n + 127) / 128);
+  const unsigned gy = (unsigned)std::max(1, std::min(a.n_frames, (int)((4736 + gx - 1) / gx)));
+  const dim3 grid(gx, gy);
   const bool dbg = a.dbg_rec != nullptr;
 #define K1_CASE(D)                                            \
   case D:                                                     \

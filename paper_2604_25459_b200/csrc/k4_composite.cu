@@ -187,7 +187,8 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
   }
   for (int b = 0; b < rounds; ++b) {
     if (b + 1 < rounds) stage(b + 1);   // overlaps this round's compositing
-    const float4* R0 = stg + (b & 1) * 3 * kBatch;
+    const float4* R0 = reinterpret_cast<const float4*>(
+        reinterpret_cast<const char*>(K4Shared<CAP>::kPacked ? stg : sm.u.c.stage) + (b & 1) * (3 * kBatch * 16));
     const float4* R1 = R0 + kBatch;
     const float4* R2 = R1 + kBatch;
     const int base = b * kBatch;
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
         const int i1 = min(nsel, i0 + 16);
 #pragma unroll 2
         for (int i = i0; i < i1; ++i) {
-          const int j = wl[i];
+          const uint32_t j = wl[i];
           const float4 q0 = R0[j];                                   // u, v, p, q
           const float2 q1 = *reinterpret_cast<const float2*>(&R1[j]);  // r, log2 o
           const float dx = q0.x - pxc;
