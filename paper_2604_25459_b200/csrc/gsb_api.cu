@@ -284,7 +284,7 @@ struct Pipeline {
     c.stat_pairs = (p->flags & GSB_FLAG_STATS) ? s->d_pairs : nullptr;
     tm.begin(KC_COMPOSITE);
     // many lists beyond the small fused-sort capacity (e.g. 128x128 views): larger variant
-    launch_k4_composite(c, (uint64_t)n_long * 16 > (uint64_t)(fe - fs) * n_tiles, st);
+    launch_k4_composite(c, (uint64_t)n_long * 4 > (uint64_t)(fe - fs) * n_tiles, st);
     s->launches++;
     s->comp_launches++;
     LAUNCH_CHECK();
