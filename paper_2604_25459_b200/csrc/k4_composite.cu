@@ -73,21 +73,21 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 constexpr float kFar = 1e20f;
 
 __device__ __forceinline__ void blend(bool use, float arg, const float4& r2, float& T, float& cr, float& cg,
-                                      float& cb, float& dep, float& pyc, int& n_eval, int idx1) {
+                                      float& cb, float& dep, float& pyc, int& n_eval, int idx) {
   const float alpha = use ? fminf(kAlphaMax, ex2_approx(arg)) : 0.f;
   const float w = alpha * T;
   const float tT = T - w;                       // T (1 - alpha)
-  const bool keep = tT >= kTermT;               // false only when this entry terminates (R13)
-  const float wk = keep ? w : 0.f;
-  cr = fmaf(wk, r2.x, cr);
-  cg = fmaf(wk, r2.y, cg);
-  cb = fmaf(wk, r2.z, cb);
-  dep = fmaf(wk, r2.w, dep);
-  T = keep ? tT : T;
-  n_eval = keep ? n_eval : idx1;
-  pyc = keep ? pyc : kFar;
+  if (tT >= kTermT) {
+    cr = fmaf(w, r2.x, cr);
+    cg = fmaf(w, r2.y, cg);
+    cb = fmaf(w, r2.z, cb);
+    dep = fmaf(w, r2.w, dep);
+    T = tT;
+  } else {                                      // stop before blending (R13)
+    n_eval = idx + 1;
+    pyc = kFar;
+  }
 }
-
 
 template <int CAP, int MINB>
 __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs a) {
@@ -242,9 +242,8 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
           const bool use1 = arg1 >= kLog2AlphaMin;
           if (use0 || use1) {
             const float4 q2 = R2[j];                                 // r, g, b, z
-            const int idx1 = base + (int)j + 1;
-            blend(use0, arg0, q2, T0, r0c, g0c, b0c, d0, pyc0, ne0, idx1);
-            blend(use1, arg1, q2, T1, r1c, g1c, b1c, d1, pyc1, ne1, idx1);
+            blend(use0, arg0, q2, T0, r0c, g0c, b0c, d0, pyc0, ne0, base + j);
+            blend(use1, arg1, q2, T1, r1c, g1c, b1c, d1, pyc1, ne1, base + j);
           }
         }
         if (__all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) break;  // whole warp finished
