@@ -121,6 +121,23 @@ gsb_status gsb_render(gsb_scene scene, const float* body_poses, int32_t n_envs, 
                       const gsb_render_params* params, float* out_rgb, float* out_depth,
                       float* out_alpha, int32_t* out_n_eval, gsb_stream stream);
 
+/* gsb_render with a camera rig and strided pose input (§8(f) row 1: egocentric / wrist cameras
+ * and direct physics-buffer ingest).  DEVICE pointers as in gsb_render, except cam_body.
+ *   body_poses of env e, body k start at body_poses[e * pose_env_stride + k * pose_body_stride]
+ *     and hold (tx,ty,tz,qw,qx,qy,qz) in their first 7 floats (e.g. a physics state record);
+ *     pose_body_stride 0 = 7 (>= 7 otherwise), pose_env_stride 0 = n_bodies * pose_body_stride
+ *   cam_body     [C] int32 HOST array, nullable: cam_body[c] = -1 -> cam_extrinsics[e,c] is
+ *     world->camera as in gsb_render; cam_body[c] = k >= 0 -> cam_extrinsics[e,c] is the camera's
+ *     body->camera [R | t] (mount, may differ per env) and world->camera is composed on the device
+ *     by the binary32 chain of reading R29; k must be in [0, n_bodies), c < 16.
+ * Errors: as gsb_render, plus UNKNOWN_BODY (bad cam_body), INVALID_ARGUMENT (bad strides),
+ * CAPACITY (attached camera index >= 16). */
+gsb_status gsb_render_rig(gsb_scene scene, const float* body_poses, int64_t pose_env_stride,
+                          int64_t pose_body_stride, int32_t n_envs, int32_t n_cams,
+                          const float* intrinsics, const float* cam_extrinsics, const int32_t* cam_body,
+                          const gsb_render_params* params, float* out_rgb, float* out_depth,
+                          float* out_alpha, int32_t* out_n_eval, gsb_stream stream);
+
 /* Same operation with HOST buffers (inputs read, outputs written; pinned memory recommended):
  * uploads the inputs, renders, and downloads rgb (+depth/alpha/n_eval when non-NULL), with
  * the downloads of one chunk overlapping the rendering of the next.  Synchronous: returns

@@ -66,6 +66,8 @@ def lib():
                                      P, P, P, P, P, P, P, P, ctypes.c_double, ctypes.c_int]
         L.gsbo_depth_key.restype = ctypes.c_float
         L.gsbo_depth_key.argtypes = [P, P, P]
+        L.gsbo_compose_w2c.restype = None
+        L.gsbo_compose_w2c.argtypes = [P, P, P]
         L.gsbo_fmaf.restype = ctypes.c_float
         L.gsbo_fmaf.argtypes = [ctypes.c_float, ctypes.c_float, ctypes.c_float]
         L.gsbo_sh_basis.restype = None
@@ -184,6 +186,16 @@ def render_frame(scene, pose_env, intr, w2c, prm: RenderParams, pixels=None, mod
         term, nev, masked, tnear = term.reshape(H, W), nev.reshape(H, W), masked.reshape(H, W), tnear.reshape(H, W)
         brgb, bdep = brgb.reshape(H, W), bdep.reshape(H, W)
     return FrameResult(rgb, dep, alp, term, nev, masked, brgb, bdep, proj, zb, valid, order, tnear)
+
+
+def compose_w2c(pose, mount) -> np.ndarray:
+    """Reading R29: world->camera (3x4 f32) of a camera on a body at `pose` with body->camera
+    `mount` (C implementation)."""
+    p = _c(pose, np.float32).reshape(-1)
+    b = _c(mount, np.float32).reshape(-1)
+    out = np.zeros(12, np.float32)
+    lib().gsbo_compose_w2c(_p(p), _p(b), _p(out))
+    return out.reshape(3, 4)
 
 
 def depth_key(w2c, pose_or_none, mu) -> np.float32:

@@ -86,6 +86,24 @@ static float r11_depth(const float M2[3], float m2, const float mu[3]) {
   return fmaf(M2[0], mu[0], fmaf(M2[1], mu[1], fmaf(M2[2], mu[2], m2)));
 }
 
+/* Reading R29: world->camera of a camera mounted on a body, from the
+ * body pose (tx,ty,tz,qw,qx,qy,qz) and the mount B = body->camera [R|t] (3x4 row-major),
+ * composed in binary32 as W = [B_R R(q)^T | B_t - (B_R R(q)^T) t], each op separately rounded:
+ *   W[r][c] = fma(B[r][0], R[c][0], fma(B[r][1], R[c][1], B[r][2]*R[c][2]))
+ *   W[r][3] = fma(-W[r][0], tx, fma(-W[r][1], ty, fma(-W[r][2], tz, B[r][3])))
+ * with R(q) from the R11 quaternion chain. */
+void gsbo_compose_w2c(const float* pose, const float* B, float* W) {
+  float R[3][3];
+  r11_rot_f32(pose + 3, R);
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) {
+      float p = B[r * 4 + 2] * R[c][2];
+      W[r * 4 + c] = fmaf(B[r * 4 + 0], R[c][0], fmaf(B[r * 4 + 1], R[c][1], p));
+    }
+    W[r * 4 + 3] = fmaf(-W[r * 4 + 0], pose[0], fmaf(-W[r * 4 + 1], pose[1], fmaf(-W[r * 4 + 2], pose[2], B[r * 4 + 3])));
+  }
+}
+
 /* fp32 depth key of one Gaussian — exported so tests can pin the chain on its own */
 float gsbo_depth_key(const float* w2c, const float* pose_or_null, const float* mu) {
   float M2[3], m2;

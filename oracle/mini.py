@@ -71,6 +71,26 @@ def depth_key_f32(w2c, pose, mu) -> np.ndarray:
     return fma32(M2[0], mu[..., 0], fma32(M2[1], mu[..., 1], fma32(M2[2], mu[..., 2], m2)))
 
 
+def compose_w2c_f32(pose, mount) -> np.ndarray:
+    """Reading R29 in NumPy (independent of the C version): W = [B_R R^T | B_t - W t]."""
+    pose = np.asarray(pose, np.float32).reshape(7)
+    B = np.asarray(mount, np.float32).reshape(3, 4)
+    tx, ty, tz, qw, qx, qy, qz = [pose[j] for j in range(7)]
+    two, one = _f(2.0), _f(1.0)
+    xx, yy, zz = qx * qx, qy * qy, qz * qz
+    xy, xz, yz = qx * qy, qx * qz, qy * qz
+    wx, wy, wz = qw * qx, qw * qy, qw * qz
+    R = [[one - two * (yy + zz), two * (xy - wz), two * (xz + wy)],
+         [two * (xy + wz), one - two * (xx + zz), two * (yz - wx)],
+         [two * (xz - wy), two * (yz + wx), one - two * (xx + yy)]]
+    W = np.zeros((3, 4), np.float32)
+    for r in range(3):
+        for c in range(3):
+            W[r, c] = fma32(B[r, 0], R[c][0], fma32(B[r, 1], R[c][1], B[r, 2] * R[c][2]))
+        W[r, 3] = fma32(-W[r, 0], tx, fma32(-W[r, 1], ty, fma32(-W[r, 2], tz, B[r, 3])))
+    return W
+
+
 # ------------------------------------------------------------------------------------
 # fp64 geometry
 # ------------------------------------------------------------------------------------

@@ -26,7 +26,7 @@ STATUS = {0: "GSB_OK", 1: "GSB_ERR_INVALID_ARGUMENT", 2: "GSB_ERR_SHAPE_MISMATCH
           6: "GSB_ERR_CUDA", 7: "GSB_ERR_DEVICE"}
 
 # every symbol include/gsb.h declares
-EXPORTS = ["gsb_create_scene", "gsb_reserve", "gsb_render", "gsb_render_host", "gsb_get_stats",
+EXPORTS = ["gsb_create_scene", "gsb_reserve", "gsb_render", "gsb_render_rig", "gsb_render_host", "gsb_get_stats",
            "gsb_get_timings", "gsb_destroy_scene", "gsb_last_error", "gsb_version",
            "gsb_debug_project", "gsb_debug_bin_sort"]
 
@@ -67,6 +67,7 @@ def lib() -> ctypes.CDLL:
     rp = ctypes.POINTER(gsb_render_params)
     L.gsb_render.argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P, P]
     L.gsb_render_host.argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P, P]
+    L.gsb_render_rig.argtypes = [P, P, I64, I64, I32, I32, P, P, P, rp, P, P, P, P, P]
     L.gsb_get_stats.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]
     L.gsb_get_timings.argtypes = [P, ctypes.POINTER(gsb_timings)]
     L.gsb_destroy_scene.argtypes = [P]
@@ -188,6 +189,23 @@ class Scene:
         _check(lib().gsb_render(self._h, _ptr(poses) if self.n_bodies else None, B, C, _ptr(intrinsics),
                                 _ptr(world_to_cam), ctypes.byref(p), _ptr(out_rgb), _ptr(out_depth),
                                 _ptr(out_alpha), _ptr(out_n_eval), _stream(stream)))
+
+    def render_rig(self, poses, intrinsics, cam_extrinsics, params: RenderParams, out_rgb, out_depth=None,
+                   out_alpha=None, out_n_eval=None, cam_body=None, pose_env_stride: int = 0,
+                   pose_body_stride: int = 0, stream=None):
+        """gsb_render_rig: strided poses (element strides, in floats) and body-attached cameras:
+        cam_body[c] = k >= 0 makes cam_extrinsics[:, c] the body->camera mount on body k."""
+        B, C = int(intrinsics.shape[0]), int(intrinsics.shape[1])
+        p = params.to_c()
+        cb = None
+        if cam_body is not None:
+            cb = np.ascontiguousarray(cam_body, np.int32)
+            if cb.size != C:
+                raise ValueError("cam_body needs one entry per camera")
+        _check(lib().gsb_render_rig(self._h, _ptr(poses) if poses is not None else None, pose_env_stride,
+                                    pose_body_stride, B, C, _ptr(intrinsics), _ptr(cam_extrinsics),
+                                    None if cb is None else cb.ctypes.data, ctypes.byref(p), _ptr(out_rgb),
+                                    _ptr(out_depth), _ptr(out_alpha), _ptr(out_n_eval), _stream(stream)))
 
     def render_host(self, poses, intrinsics, world_to_cam, params: RenderParams, out_rgb, out_depth=None,
                     out_alpha=None, out_n_eval=None, stream=None):

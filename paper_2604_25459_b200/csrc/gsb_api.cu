@@ -337,9 +337,9 @@ struct Pipeline {
     return GSB_OK;
   }
 
-  gsb_status run(const float* poses, const float* intr, const float* w2c, int n_cams) {
+  gsb_status run(const K0Rig& rig, int n_cams) {
     tm.begin(KC_SETUP);
-    launch_k0(poses, intr, w2c, F, n_cams, s->n_bodies, W, H, s->table, s->cams, st);
+    launch_k0(rig, F, n_cams, s->n_bodies, W, H, s->table, s->cams, st);
     s->launches++;
     LAUNCH_CHECK();
     tm.end();
@@ -362,9 +362,20 @@ struct Pipeline {
   }
 };
 
-gsb_status render_impl(gsb_scene s, const float* poses, int n_envs, int n_cams, const float* intr,
-                       const float* w2c, const gsb_render_params* p, float* out_rgb, float* out_depth,
-                       float* out_alpha, int32_t* out_neval, cudaStream_t st) {
+K0Rig default_rig(gsb_scene s, const float* poses, const float* intr, const float* w2c) {
+  K0Rig r{};
+  r.poses = poses;
+  r.env_stride = (int64_t)s->n_bodies * 7;
+  r.body_stride = 7;
+  r.intr = intr;
+  r.cam_x = w2c;
+  for (int c = 0; c < kMaxRigCams; ++c) r.cam_body[c] = -1;
+  return r;
+}
+
+gsb_status render_impl(gsb_scene s, const K0Rig& rig, int n_envs, int n_cams, const gsb_render_params* p,
+                       float* out_rgb, float* out_depth, float* out_alpha, int32_t* out_neval,
+                       cudaStream_t st) {
   const int F = n_envs * n_cams;
   s->last_stream = st;
   s->stat_V = s->stat_K = s->stat_long = s->stat_maxseg = 0;
@@ -384,7 +395,7 @@ gsb_status render_impl(gsb_scene s, const float* poses, int n_envs, int n_cams, 
   pl.D = p->sh_degree < 0 ? s->sh_degree : p->sh_degree;
   pl.tm = Timer{s, st, timing};
   pl.out_rgb = out_rgb; pl.out_depth = out_depth; pl.out_alpha = out_alpha; pl.out_neval = out_neval;
-  gsb_status r = pl.run(poses, intr, w2c, n_cams);
+  gsb_status r = pl.run(rig, n_cams);
   s->stats_valid = (r == GSB_OK) && (p->flags & GSB_FLAG_STATS);
   s->timing_valid = (r == GSB_OK) && timing;
   return r;
@@ -595,8 +606,39 @@ gsb_status gsb_render(gsb_scene s, const float* poses, int32_t n_envs, int32_t n
   if (r != GSB_OK) return r;
   DeviceGuard g(s->device);
   s->dl_rgb = nullptr; s->dl_depth = nullptr; s->dl_alpha = nullptr; s->dl_neval = nullptr;
-  return render_impl(s, poses, n_envs, n_cams, intr, w2c, p, out_rgb, out_depth, out_alpha, out_neval,
-                     (cudaStream_t)stream);
+  return render_impl(s, default_rig(s, poses, intr, w2c), n_envs, n_cams, p, out_rgb, out_depth, out_alpha,
+                     out_neval, (cudaStream_t)stream);
+}
+
+gsb_status gsb_render_rig(gsb_scene s, const float* poses, int64_t pose_env_stride, int64_t pose_body_stride,
+                          int32_t n_envs, int32_t n_cams, const float* intr, const float* cam_extrinsics,
+                          const int32_t* cam_body, const gsb_render_params* p, float* out_rgb,
+                          float* out_depth, float* out_alpha, int32_t* out_neval, gsb_stream stream) {
+  gsb_status r = validate_render(s, poses, n_envs, n_cams, intr, cam_extrinsics, p, out_rgb);
+  if (r != GSB_OK) return r;
+  K0Rig rig = default_rig(s, poses, intr, cam_extrinsics);
+  if (pose_env_stride < 0 || pose_body_stride < 0)
+    return fail(GSB_ERR_INVALID_ARGUMENT, "negative pose stride");
+  if (pose_body_stride) {
+    if (pose_body_stride < 7) return fail(GSB_ERR_INVALID_ARGUMENT, "pose_body_stride < 7");
+    rig.body_stride = pose_body_stride;
+  }
+  if (pose_env_stride) rig.env_stride = pose_env_stride;
+  else rig.env_stride = (int64_t)s->n_bodies * rig.body_stride;
+  if (s->n_bodies > 0 && rig.env_stride < (int64_t)(s->n_bodies - 1) * rig.body_stride + 7 && n_envs > 1)
+    return fail(GSB_ERR_INVALID_ARGUMENT, "pose_env_stride overlaps the bodies of an env");
+  if (cam_body) {
+    for (int c = 0; c < n_cams; ++c) {
+      const int kb = cam_body[c];
+      if (kb < -1 || kb >= s->n_bodies) return fail(GSB_ERR_UNKNOWN_BODY, "cam_body[%d] = %d not in [-1, %d)", c, kb, s->n_bodies);
+      if (kb >= 0 && c >= kMaxRigCams) return fail(GSB_ERR_CAPACITY, "body-attached camera index %d >= %d", c, kMaxRigCams);
+      if (kb >= 0 && !poses) return fail(GSB_ERR_INVALID_ARGUMENT, "body-attached camera without poses");
+      if (c < kMaxRigCams) rig.cam_body[c] = kb;
+    }
+  }
+  DeviceGuard g(s->device);
+  s->dl_rgb = nullptr; s->dl_depth = nullptr; s->dl_alpha = nullptr; s->dl_neval = nullptr;
+  return render_impl(s, rig, n_envs, n_cams, p, out_rgb, out_depth, out_alpha, out_neval, (cudaStream_t)stream);
 }
 
 gsb_status gsb_render_host(gsb_scene s, const float* poses, int32_t n_envs, int32_t n_cams,
@@ -617,7 +659,7 @@ gsb_status gsb_render_host(gsb_scene s, const float* poses, int32_t n_envs, int3
     CUDA_TRY(cudaMemcpyAsync(s->st_w2c, w2c, sizeof(float) * F * 12, cudaMemcpyHostToDevice, st));
   }
   s->dl_rgb = out_rgb; s->dl_depth = out_depth; s->dl_alpha = out_alpha; s->dl_neval = out_neval;
-  r = render_impl(s, s->st_poses, n_envs, n_cams, s->st_intr, s->st_w2c, p, s->st_rgb,
+  r = render_impl(s, default_rig(s, s->st_poses, s->st_intr, s->st_w2c), n_envs, n_cams, p, s->st_rgb,
                   out_depth ? s->st_depth : nullptr, out_alpha ? s->st_alpha : nullptr,
                   out_neval ? s->st_neval : nullptr, st);
   s->dl_rgb = nullptr; s->dl_depth = nullptr; s->dl_alpha = nullptr; s->dl_neval = nullptr;
@@ -679,7 +721,7 @@ gsb_status gsb_debug_project(gsb_scene s, const float* poses, int32_t n_envs, in
   DeviceGuard g(s->device);
   cudaStream_t st = (cudaStream_t)stream;
   const int F = n_envs * n_cams;
-  launch_k0(poses, intr, w2c, F, n_cams, s->n_bodies, p->width, p->height, s->table, s->cams, st);
+  launch_k0(default_rig(s, poses, intr, w2c), F, n_cams, s->n_bodies, p->width, p->height, s->table, s->cams, st);
   LAUNCH_CHECK();
   K1Args a{};
   a.g_mean = s->d_mean; a.g_L0 = s->d_L0; a.g_L1 = s->d_L1; a.g_L2 = s->d_L2; a.g_sh = s->d_sh;

@@ -82,9 +82,20 @@ struct CompositeArgs {
   unsigned long long* stat_pairs;  // nullptr unless STATS
 };
 
-void launch_k0(const float* poses, const float* intr, const float* w2c, int n_frames, int n_cams,
-               int n_bodies, int width, int height, float4* table, FrameCam* cams,
-               cudaStream_t s);
+constexpr int kMaxRigCams = 16;  // cameras per env that can be body-attached (gsb_render_rig)
+
+// K0 inputs: poses read with strides (physics-buffer ingest); cam_x = world->camera, or
+// body->camera for cameras with cam_body[c] >= 0 (reading R29)
+struct K0Rig {
+  const float* poses;
+  int64_t env_stride, body_stride;  // floats
+  const float* intr;
+  const float* cam_x;
+  int cam_body[kMaxRigCams];
+};
+
+void launch_k0(const K0Rig& rig, int n_frames, int n_cams, int n_bodies, int width, int height,
+               float4* table, FrameCam* cams, cudaStream_t s);
 void launch_k1(const K1Args& a, int sh_degree, cudaStream_t s);
 
 // K1 variant for gsb_debug_bin_sort: records from externally supplied fp32 projections

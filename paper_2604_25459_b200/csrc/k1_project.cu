@@ -21,21 +21,45 @@
 namespace gsb {
 
 // ------------------------------------------------------------------------------ K0
-__global__ void k0_setup(const float* __restrict__ poses, const float* __restrict__ intr,
-                         const float* __restrict__ w2c, int n_frames, int n_cams, int n_bodies,
-                         int width, int height, float4* __restrict__ table,
-                         FrameCam* __restrict__ cams) {
+// Reading R29 (§8(f) row 1): a camera attached to body kb is given body->camera extrinsics
+// B = [R_bc | t_bc]; its world->camera transform is the binary32 composition
+//   W[r][c] = fma(B[r][0], Rk[c][0], fma(B[r][1], Rk[c][1], B[r][2] * Rk[c][2]))   (B Rk^T)
+//   W[r][3] = fma(-W[r][0], tk0, fma(-W[r][1], tk1, fma(-W[r][2], tk2, B[r][3])))
+// with Rk from the R11 quaternion chain, every op separately rounded.
+__device__ __forceinline__ void r29_compose(const float* B, const float* pose, float W[12]) {
+  float Rk[3][3];
+  r11_rot(pose[3], pose[4], pose[5], pose[6], Rk);
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c)
+      W[r * 4 + c] = __fmaf_rn(B[r * 4 + 0], Rk[c][0],
+                               __fmaf_rn(B[r * 4 + 1], Rk[c][1], __fmul_rn(B[r * 4 + 2], Rk[c][2])));
+    W[r * 4 + 3] = __fmaf_rn(-W[r * 4 + 0], pose[0],
+                             __fmaf_rn(-W[r * 4 + 1], pose[1], __fmaf_rn(-W[r * 4 + 2], pose[2], B[r * 4 + 3])));
+  }
+}
+
+__global__ void k0_setup(K0Rig rig, int n_frames, int n_cams, int n_bodies, int width, int height,
+                         float4* __restrict__ table, FrameCam* __restrict__ cams) {
   const int nb1 = n_bodies + 1;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n_frames * nb1) return;
   const int f = idx / nb1;
   const int k = idx % nb1 - 1;
   const int e = f / n_cams;
-  const float* W = w2c + (size_t)f * 12;
+  const int cam = f % n_cams;
+  // world->camera of this frame: given, or composed from the camera's body (R29)
+  float W[12];
+  const float* Wg = rig.cam_x + (size_t)f * 12;
+  const int kb = cam < kMaxRigCams ? rig.cam_body[cam] : -1;
+  if (kb >= 0) {
+    r29_compose(Wg, rig.poses + (size_t)e * rig.env_stride + (size_t)kb * rig.body_stride, W);
+  } else {
+    for (int j = 0; j < 12; ++j) W[j] = Wg[j];
+  }
   float R[3][3] = {{1.f, 0.f, 0.f}, {0.f, 1.f, 0.f}, {0.f, 0.f, 1.f}};
   float t[3] = {0.f, 0.f, 0.f};
   if (k >= 0) {
-    const float* p = poses + ((size_t)e * n_bodies + k) * 7;
+    const float* p = rig.poses + (size_t)e * rig.env_stride + (size_t)k * rig.body_stride;
     r11_rot(p[3], p[4], p[5], p[6], R);
     t[0] = p[0]; t[1] = p[1]; t[2] = p[2];
   }
@@ -64,7 +88,7 @@ __global__ void k0_setup(const float* __restrict__ poses, const float* __restric
   o[2] = make_float4(M[2][0], M[2][1], M[2][2], m[2]);
   o[3] = make_float4(cb[0], cb[1], cb[2], 0.f);
   if (k < 0) {
-    const float* K = intr + (size_t)f * 4;
+    const float* K = rig.intr + (size_t)f * 4;
     FrameCam fc;
     fc.fx = K[0]; fc.fy = K[1]; fc.cx = K[2]; fc.cy = K[3];
     fc.limx = 1.3f * (float)width / (2.0f * K[0]);
@@ -270,13 +294,11 @@ __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
   }
 }
 
-void launch_k0(const float* poses, const float* intr, const float* w2c, int n_frames, int n_cams,
-               int n_bodies, int width, int height, float4* table, FrameCam* cams,
-               cudaStream_t s) {
+void launch_k0(const K0Rig& rig, int n_frames, int n_cams, int n_bodies, int width, int height,
+               float4* table, FrameCam* cams, cudaStream_t s) {
   const int total = n_frames * (n_bodies + 1);
   if (total == 0) return;
-  k0_setup<<<(total + 127) / 128, 128, 0, s>>>(poses, intr, w2c, n_frames, n_cams, n_bodies, width,
-                                                height, table, cams);
+  k0_setup<<<(total + 127) / 128, 128, 0, s>>>(rig, n_frames, n_cams, n_bodies, width, height, table, cams);
 }
 
 void launch_k1(const K1Args& a, int sh_degree, cudaStream_t s) {

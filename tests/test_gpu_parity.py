@@ -295,3 +295,66 @@ def test_invalid_arguments_rejected_before_enqueue():
     with pytest.raises(gsb.GsbError) as ei:
         gsb.Scene.from_synth(bad)
     assert ei.value.status == 3
+
+
+# --------------------------------------------------------------------------- §8(f) row 1
+def _wrist_mounts(b, rng):
+    """Per-env body->camera mounts looking along the link (+x) from its tip, with small DR."""
+    B, C = b.intrinsics.shape[:2]
+    c2b = np.array([[0.0, 0.0, 1.0], [-1.0, 0.0, 0.0], [0.0, -1.0, 0.0]])  # columns: right, down, fwd
+    mounts = np.zeros((B, C, 3, 4), np.float32)
+    for e in range(B):
+        for c in range(C):
+            ang = np.radians(rng.uniform(0, 5))
+            ax = rng.normal(size=3)
+            R = synth._quat_to_mat(synth._axis_angle_quat(ax, ang)) @ c2b
+            p = np.array([0.33, 0.0, 0.06]) + rng.uniform(-0.02, 0.02, 3)
+            mounts[e, c, :, :3] = R.T
+            mounts[e, c, :, 3] = -R.T @ p
+    return mounts
+
+
+def test_rig_body_cameras_and_strided_poses_bit_identical_and_match_oracle():
+    """Cameras mounted on bodies (reading R29) and poses read from a strided physics-state
+    buffer give bit-identical frames to world cameras composed by the oracle's R29 chain, and
+    the egocentric frames match the oracle."""
+    cfg = synth.CONFIGS["T1"]
+    sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
+    rng = np.random.default_rng(8)
+    mounts = _wrist_mounts(b, rng)
+    cam_body = np.array([-1, 2], np.int32)
+    ext = b.w2c.copy()
+    ext[:, 1] = mounts[:, 1]
+    w2c_eff = b.w2c.copy()
+    for e in range(cfg.n_envs):
+        w2c_eff[e, 1] = oracle.compose_w2c(b.poses[e, 2], mounts[e, 1])
+    ref = gu.gpu_render(sc, synth.Batch(b.poses, b.intrinsics, w2c_eff), cfg.width, cfg.height)
+    # physics-state buffer: 13 floats per body (pose + velocities), junk after the pose
+    nb = cfg.n_bodies
+    state = rng.normal(size=(cfg.n_envs, nb, 13)).astype(np.float32)
+    state[..., :7] = b.poses
+    g = ref["scene"]
+    B, C, H, W = cfg.n_envs, cfg.n_cams, cfg.height, cfg.width
+    rgb = torch.full((B, C, 3, H, W), float("nan"), device="cuda")
+    dep = torch.full((B, C, H, W), float("nan"), device="cuda")
+    nev = torch.full((B, C, H, W), -7, dtype=torch.int32, device="cuda")
+    g.render_rig(gu.to_dev(state), gu.to_dev(b.intrinsics), gu.to_dev(ext), gsb.RenderParams(W, H), rgb, dep,
+                 None, nev, cam_body=cam_body, pose_env_stride=nb * 13, pose_body_stride=13)
+    torch.cuda.synchronize()
+    assert np.array_equal(rgb.cpu().numpy(), ref["rgb"])
+    assert np.array_equal(dep.cpu().numpy(), ref["depth"])
+    assert np.array_equal(nev.cpu().numpy(), ref["n_eval"])
+    for e in range(cfg.n_envs):
+        o = oracle.render_frame(sc, b.poses[e], b.intrinsics[e, 1], w2c_eff[e, 1], oracle.RenderParams(W, H))
+        r = gu.compare_frame(ref, e, 1, o, W, H)
+        print("egocentric", e, r)
+        assert r["rgb_fail"] == 0 and r["dep_fail"] == 0, r
+    # the composition itself is bit-exact on the device: render the rig with a camera whose
+    # mount is identity on a static pose... covered by the bit-identity above; bad inputs:
+    with pytest.raises(gsb.GsbError) as ei:
+        g.render_rig(gu.to_dev(state), gu.to_dev(b.intrinsics), gu.to_dev(ext), gsb.RenderParams(W, H), rgb,
+                     cam_body=np.array([-1, nb], np.int32), pose_env_stride=nb * 13, pose_body_stride=13)
+    assert ei.value.status == 3
+    with pytest.raises(gsb.GsbError):
+        g.render_rig(gu.to_dev(state), gu.to_dev(b.intrinsics), gu.to_dev(ext), gsb.RenderParams(W, H), rgb,
+                     cam_body=cam_body, pose_env_stride=nb * 13, pose_body_stride=5)
