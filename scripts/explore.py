@@ -62,3 +62,39 @@ for name in sys.argv[1:] or ["C2", "C4", "C5", "C3"]:
     print(json.dumps(out), flush=True)
     del g, rgb, dep
     torch.cuda.empty_cache()
+
+# §8(f) row 1 measurement: C4 with camera 1 wrist-mounted on body 9, poses from a 13-float
+# physics-state buffer, through gsb_render_rig
+if "rig" in sys.argv[1:] or not sys.argv[1:]:
+    cfg = synth.CONFIGS["C4"]
+    B = 4096
+    sc = synth.make_scene(cfg)
+    g = gsb.Scene.from_synth(sc)
+    g.reserve(B, cfg.n_cams, cfg.width, cfg.height)
+    K, W = synth.make_cameras(cfg, np.arange(B))
+    c2b = np.array([[0.0, 0.0, 1.0], [-1.0, 0.0, 0.0], [0.0, -1.0, 0.0]])
+    W[:, 1, :, :3] = c2b.T
+    W[:, 1, :, 3] = -c2b.T @ np.array([0.33, 0.0, 0.06])
+    nb = cfg.n_bodies
+    states = []
+    for s in range(4):
+        st = np.zeros((B, nb, 13), np.float32)
+        st[..., :7] = synth.make_poses(cfg, np.arange(B), s)
+        states.append(torch.from_numpy(st).cuda())
+    K, W = torch.from_numpy(K).cuda(), torch.from_numpy(W).cuda()
+    rgb = torch.empty((B, cfg.n_cams, 3, cfg.height, cfg.width), device="cuda")
+    dep = torch.empty((B, cfg.n_cams, cfg.height, cfg.width), device="cuda")
+    cam_body = np.array([-1, 9], np.int32)
+    prm = gsb.RenderParams(cfg.width, cfg.height)
+    for s in range(2):
+        g.render_rig(states[s], K, W, prm, rgb, dep, cam_body=cam_body, pose_env_stride=nb * 13, pose_body_stride=13)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for s in range(3):
+        g.render_rig(states[(s + 1) % 4], K, W, prm, rgb, dep, cam_body=cam_body, pose_env_stride=nb * 13,
+                     pose_body_stride=13)
+    e1.record()
+    torch.cuda.synchronize()
+    print(json.dumps({"config": "C4-rig (cam 1 on body 9, strided 13-float states)", "frames": B * 2,
+                      "fps": 3 * B * 2 / (e0.elapsed_time(e1) / 1e3)}), flush=True)
