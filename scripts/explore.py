@@ -30,7 +30,7 @@ torch.cuda.empty_cache()
 print(json.dumps(res), flush=True)
 
 envs = {"C2": 64, "C3": 1024, "C4": 4096, "C5": 1024, "T1": 3}
-for name in sys.argv[1:] or ["C2", "C4", "C5", "C3"]:
+for name in [n for n in sys.argv[1:] if n in synth.CONFIGS] or ["C2", "C4", "C5", "C3"]:
     cfg = synth.CONFIGS[name]
     B = envs.get(name, cfg.n_envs)
     sc = synth.make_scene(cfg)
