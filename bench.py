@@ -99,9 +99,9 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        backend = os.environ.get("GSB_DIST_BACKEND", "nccl" if torch.cuda.is_available() else "gloo")
         if torch.cuda.is_available():
-            torch.cuda.set_device(local)
+            torch.cuda.set_device(local % torch.cuda.device_count())
         dist.init_process_group(backend=backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
@@ -113,7 +113,8 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    on_gpu = torch.cuda.is_available() and dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if on_gpu else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -197,7 +198,7 @@ def main():
     import paper_2604_25459_b200 as gsb
 
     world, rank, local = dist_setup(args)
-    dev = torch.device("cuda", local if world > 1 else 0)
+    dev = torch.device("cuda", local % torch.cuda.device_count() if world > 1 else 0)
     peaks, peaks_kind = load_peaks()
 
     # weak scaling: every rank renders its own cfg.n_envs envs (global ids rank*B + [0, B))
