@@ -20,6 +20,47 @@ struct SortShared {
   uint32_t wred[kWarps];
 };
 
+// Exact fix-up of runs that tie on the sorted field, race-free: the array is walked in blocks of
+// NT*KPT elements; in each block every run starting there is found with reads only (its end kept
+// in a register by the thread owning the start), a barrier, then the owners insertion-sort their
+// runs by `less` (disjoint ranges), and a barrier before the next block reads.
+template <int NT, typename Ptr, typename Field, typename Less>
+__device__ __forceinline__ void fix_runs(Ptr r, int n, Field field, Less less) {
+  constexpr int KPT = 8;
+  for (int base = 0; base < n; base += NT * KPT) {
+    int end[KPT];
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+      const int e = base + k * NT + (int)threadIdx.x;
+      end[k] = -1;
+      if (e + 1 < n) {
+        const uint32_t h = field(r[e]);
+        if ((e == 0 || field(r[e - 1]) != h) && field(r[e + 1]) == h) {
+          int x = e + 2;
+          while (x < n && field(r[x]) == h) ++x;
+          end[k] = x;
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+      if (end[k] < 0) continue;
+      const int e = base + k * NT + (int)threadIdx.x;
+      for (int x = e + 1; x < end[k]; ++x) {
+        const auto kx = r[x];
+        int y = x - 1;
+        while (y >= e && less(kx, r[y])) {
+          r[y + 1] = r[y];
+          --y;
+        }
+        r[y + 1] = kx;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __device__ __forceinline__ uint32_t hi32(uint64_t k) { return (uint32_t)(k >> 32); }
 
 // exclusive scan over the block of one value per bin (256 bins, NT threads)
@@ -134,26 +175,9 @@ __device__ __forceinline__ bool segment_sort(Ptr a, Ptr b, int n, SortShared<NT>
   // runs equal on the sorted bits: finish them by the full key (zbits, id) — reading R10
   int dup = 0;
   for (int e = tid + 1; e < n; e += NT) dup |= ((hi32(r[e]) - zmin) >> lo) == ((hi32(r[e - 1]) - zmin) >> lo);
-  if (__syncthreads_or(dup)) {
-    for (int e = tid; e < n; e += NT) {
-      const uint32_t h = (hi32(r[e]) - zmin) >> lo;
-      const bool start = (e == 0 || ((hi32(r[e - 1]) - zmin) >> lo) != h) &&
-                         (e + 1 < n && ((hi32(r[e + 1]) - zmin) >> lo) == h);
-      if (!start) continue;
-      int end = e + 1;
-      while (end < n && ((hi32(r[end]) - zmin) >> lo) == h) ++end;
-      for (int x = e + 1; x < end; ++x) {  // insertion sort of the run by the 64-bit key
-        const uint64_t kx = r[x];
-        int y = x - 1;
-        while (y >= e && r[y] > kx) {
-          r[y + 1] = r[y];
-          --y;
-        }
-        r[y + 1] = kx;
-      }
-    }
-    __syncthreads();
-  }
+  if (__syncthreads_or(dup))
+    fix_runs<NT>(r, n, [&](uint64_t k) { return (hi32(k) - zmin) >> lo; },
+                 [](uint64_t x, uint64_t y) { return x < y; });
   return in_b;
 }
 
@@ -243,26 +267,9 @@ __device__ __forceinline__ bool packed_sort(const uint64_t* __restrict__ gkeys, 
   uint32_t* r = in_b ? b : a;
   int dup = 0;
   for (int e = tid + 1; e < n; e += NT) dup |= (r[e] >> 16) == (r[e - 1] >> 16);
-  if (__syncthreads_or(dup)) {
-    for (int e = tid; e < n; e += NT) {
-      const uint32_t h = r[e] >> 16;
-      const bool start = (e == 0 || (r[e - 1] >> 16) != h) && (e + 1 < n && (r[e + 1] >> 16) == h);
-      if (!start) continue;
-      int end = e + 1;
-      while (end < n && (r[end] >> 16) == h) ++end;
-      for (int x = e + 1; x < end; ++x) {  // insertion sort of the run by the full key
-        const uint32_t wx = r[x];
-        const uint64_t kx = __ldg(gkeys + (wx & 0xffffu));
-        int y = x - 1;
-        while (y >= e && __ldg(gkeys + (r[y] & 0xffffu)) > kx) {
-          r[y + 1] = r[y];
-          --y;
-        }
-        r[y + 1] = wx;
-      }
-    }
-    __syncthreads();
-  }
+  if (__syncthreads_or(dup))
+    fix_runs<NT>(r, n, [](uint32_t w) { return w >> 16; },
+                 [gkeys](uint32_t x, uint32_t y) { return __ldg(gkeys + (x & 0xffffu)) < __ldg(gkeys + (y & 0xffffu)); });
   return in_b;
 }
 
