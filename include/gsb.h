@@ -147,6 +147,30 @@ gsb_status gsb_render_host(gsb_scene scene, const float* body_poses, int32_t n_e
                            const gsb_render_params* params, float* out_rgb, float* out_depth,
                            float* out_alpha, int32_t* out_n_eval, gsb_stream stream);
 
+/* Static-camera background pre-binning (§8(f) row 2; exploits RLGK's static/dynamic split,
+ * PAPER.md App. B.2: static Gaussians never move, so with cameras fixed in the world
+ * their projection, binning and depth sort are the same for every env and every step).
+ * gsb_prebin_static projects, bins and sorts the static (body -1) Gaussians once for the C
+ * cameras given (DEVICE or HOST pointers: intrinsics [C,4], world_to_cam [C,3,4]), and keeps
+ * the sorted per-(camera, tile) lists and their records in the scene (replacing any previous
+ * pre-binning; synchronous).  Call gsb_reserve (again) afterwards if the scene was reserved
+ * before, so the merge workspace exists.
+ * gsb_render_static then renders B envs x those C cameras (frame f = e*C + c): per frame only
+ * the robot Gaussians are projected, binned and sorted, and K4 merges each tile's robot list
+ * with the camera's background list in (zbits, id) order (keys are unique, reading R10).
+ * Outputs, layout and determinism as gsb_render with intrinsics/world_to_cam broadcast over
+ * the envs — bit-identical to it.  params must equal the pre-binning's in width, height,
+ * near/far and SH degree (background and flags may differ).
+ * Errors: INVALID_ARGUMENT (no pre-binning / reservation, bad params), SHAPE_MISMATCH
+ * (params differ from the pre-binning's, B*C beyond the reservation), CAPACITY, CUDA,
+ * OUT_OF_MEMORY. */
+gsb_status gsb_prebin_static(gsb_scene scene, int32_t n_cams, const float* intrinsics,
+                             const float* world_to_cam, const gsb_render_params* params,
+                             gsb_stream stream);
+gsb_status gsb_render_static(gsb_scene scene, const float* body_poses, int32_t n_envs,
+                             const gsb_render_params* params, float* out_rgb, float* out_depth,
+                             float* out_alpha, int32_t* out_n_eval, gsb_stream stream);
+
 /* Counters of the last render made with GSB_FLAG_STATS (synchronises with it). */
 gsb_status gsb_get_stats(gsb_scene scene, int64_t* visible_V, int64_t* keys_K, int64_t* pairs_P);
 

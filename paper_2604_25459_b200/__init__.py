@@ -26,7 +26,8 @@ STATUS = {0: "GSB_OK", 1: "GSB_ERR_INVALID_ARGUMENT", 2: "GSB_ERR_SHAPE_MISMATCH
           6: "GSB_ERR_CUDA", 7: "GSB_ERR_DEVICE"}
 
 # every symbol include/gsb.h declares
-EXPORTS = ["gsb_create_scene", "gsb_reserve", "gsb_render", "gsb_render_rig", "gsb_render_host", "gsb_get_stats",
+EXPORTS = ["gsb_create_scene", "gsb_reserve", "gsb_render", "gsb_render_rig", "gsb_render_host",
+           "gsb_prebin_static", "gsb_render_static", "gsb_get_stats",
            "gsb_get_timings", "gsb_destroy_scene", "gsb_last_error", "gsb_version",
            "gsb_debug_project", "gsb_debug_bin_sort"]
 
@@ -68,9 +69,13 @@ def lib() -> ctypes.CDLL:
     L.gsb_render.argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P, P]
     L.gsb_render_host.argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P, P]
     L.gsb_render_rig.argtypes = [P, P, I64, I64, I32, I32, P, P, P, rp, P, P, P, P, P]
+    L.gsb_prebin_static.argtypes = [P, I32, P, P, rp, P]
+    L.gsb_render_static.argtypes = [P, P, I32, rp, P, P, P, P, P]
     L.gsb_get_stats.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]
     L.gsb_get_timings.argtypes = [P, ctypes.POINTER(gsb_timings)]
     L.gsb_destroy_scene.argtypes = [P]
+    L.gsb_last_error.argtypes = []
+    L.gsb_version.argtypes = []
     L.gsb_last_error.restype = ctypes.c_char_p
     L.gsb_version.restype = ctypes.c_char_p
     L.gsb_debug_project.argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P]
@@ -95,6 +100,13 @@ def _ptr(t) -> Optional[int]:
     if not t.is_contiguous():
         raise ValueError("tensor must be contiguous")
     return t.data_ptr()
+
+
+def _anyptr(a) -> Optional[int]:
+    """Pointer of a CUDA tensor, a CPU tensor or a numpy array (for calls that accept either)."""
+    if isinstance(a, np.ndarray) or (a is not None and not a.is_cuda):
+        return _hptr(a)
+    return _ptr(a)
 
 
 def _hptr(a) -> Optional[int]:
@@ -215,6 +227,23 @@ class Scene:
         _check(lib().gsb_render_host(self._h, _hptr(poses) if self.n_bodies else None, B, C,
                                      _hptr(intrinsics), _hptr(world_to_cam), ctypes.byref(p), _hptr(out_rgb),
                                      _hptr(out_depth), _hptr(out_alpha), _hptr(out_n_eval), _stream(stream)))
+
+    def prebin_static(self, intrinsics, world_to_cam, params: RenderParams, stream=None):
+        """gsb_prebin_static: pre-bin the static background for C fixed cameras (intrinsics [C,4],
+        world_to_cam [C,3,4], CUDA or CPU tensors).  Call reserve() afterwards."""
+        C = int(intrinsics.shape[0])
+        p = params.to_c()
+        _check(lib().gsb_prebin_static(self._h, C, _anyptr(intrinsics), _anyptr(world_to_cam), ctypes.byref(p),
+                                       _stream(stream)))
+
+    def render_static(self, poses, params: RenderParams, out_rgb, out_depth=None, out_alpha=None,
+                      out_n_eval=None, stream=None):
+        """gsb_render_static: B envs x the pre-binned cameras; out_rgb [B,C,3,H,W]."""
+        B = int(out_rgb.shape[0])
+        p = params.to_c()
+        _check(lib().gsb_render_static(self._h, _ptr(poses) if self.n_bodies else None, B, ctypes.byref(p),
+                                       _ptr(out_rgb), _ptr(out_depth), _ptr(out_alpha), _ptr(out_n_eval),
+                                       _stream(stream)))
 
     def stats(self):
         V, K, P = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()

@@ -82,6 +82,7 @@ constexpr int kMaxChunk = 1024;  // frames per pipeline chunk (upper bound)
 struct gsb_scene_t {
   int device = 0;
   int64_t n = 0;
+  int64_t n_bg = 0;   // static Gaussians (body -1): the prefix [0, n_bg) of the internal order
   int n_bodies = 0;
   int sh_degree = 0;
   int sh_planes = 1;
@@ -129,6 +130,20 @@ struct gsb_scene_t {
   std::vector<std::pair<int, size_t>> ev_marks;  // (class, index of begin event)
   bool timing_valid = false;
   int64_t launches = 0, comp_launches = 0, chunks = 0;
+  // static-camera pre-binning (gsb_prebin_static, §8(f) row 2)
+  int sb_cams = 0, sb_w = 0, sb_h = 0, sb_D = 0;
+  float sb_near = 0.f, sb_far = 0.f;
+  float *sb_intr = nullptr, *sb_w2c = nullptr;   // [C][4], [C][12]
+  uint64_t* bg_off = nullptr;                     // [C][T+1]
+  uint64_t* bg_keys = nullptr;                    // [K_bg]
+  float4* bg_rec = nullptr;                       // [K_bg][3]
+  std::vector<int64_t> sb_V, sb_K;                // per camera
+  uint32_t* qpos = nullptr;                       // [cap] (workspace, while pre-binned)
+  void free_prebin() {
+    cudaFree(sb_intr); cudaFree(sb_w2c); cudaFree(bg_off); cudaFree(bg_keys); cudaFree(bg_rec);
+    sb_intr = sb_w2c = nullptr; bg_off = bg_keys = nullptr; bg_rec = nullptr;
+    sb_cams = 0; sb_V.clear(); sb_K.clear();
+  }
   // host-io: where to download outputs of each pass
   float *dl_rgb = nullptr, *dl_depth = nullptr, *dl_alpha = nullptr;
   int32_t* dl_neval = nullptr;
@@ -145,7 +160,8 @@ struct gsb_scene_t {
       rec[s] = nullptr; vcount[s] = nullptr; hist[s] = nullptr; off[s] = nullptr;
       frame_base[s] = nullptr; h_rb[s] = nullptr; d_rb[s] = nullptr; ev_counts[s] = nullptr;
     }
-    cudaFree(keys); cudaFree(keys_alt); cudaFree(sorted); cudaFree(d_pairs);
+    cudaFree(keys); cudaFree(keys_alt); cudaFree(sorted); cudaFree(d_pairs); cudaFree(qpos);
+    qpos = nullptr;
     cudaFree(st_poses); cudaFree(st_intr); cudaFree(st_w2c);
     cudaFree(st_rgb); cudaFree(st_depth); cudaFree(st_alpha); cudaFree(st_neval);
     if (copy_stream) cudaStreamDestroy(copy_stream);
@@ -231,6 +247,8 @@ struct Pipeline {
   float* out_depth;
   float* out_alpha;
   int32_t* out_neval;
+  int64_t first = 0, count = 0;   // Gaussian range [first, first + count) of the internal order
+  bool merge = false;             // static cameras: merge with the pre-binned background lists
 
   gsb_status project_chunk(int c, int f0, int nf) {
     const int sl = c & 1;
@@ -238,16 +256,17 @@ struct Pipeline {
     CUDA_TRY(cudaMemsetAsync(s->long_cnt[sl], 0, sizeof(uint32_t), st));
     CUDA_TRY(cudaMemsetAsync(s->hist[sl], 0, sizeof(int) * s->hist_stride * nf, st));
     K1Args a{};
-    a.g_mean = s->d_mean; a.g_L0 = s->d_L0; a.g_L1 = s->d_L1; a.g_L2 = s->d_L2; a.g_sh = s->d_sh;
-    a.g_ids = s->d_ids;
-    a.n = s->n; a.table = s->table; a.cams = s->cams; a.nb1 = s->n_bodies + 1;
+    a.g_mean = s->d_mean + first; a.g_L0 = s->d_L0 + first; a.g_L1 = s->d_L1 + first;
+    a.g_L2 = s->d_L2 + first; a.g_sh = s->d_sh + first;
+    a.g_ids = s->d_ids + first;
+    a.n = count; a.sh_stride = s->n; a.table = s->table; a.cams = s->cams; a.nb1 = s->n_bodies + 1;
     a.f0 = f0; a.n_frames = nf; a.width = W; a.height = H; a.tiles_x = tiles_x;
     a.near_plane = p->near_plane; a.far_plane = p->far_plane;
     a.rec = s->rec[sl]; a.vcount = s->vcount[sl]; a.hist = s->hist[sl]; a.hist_stride = s->hist_stride;
     a.vis_bits = s->vis_bits[sl]; a.vis_words = s->vis_words;
     tm.begin(KC_PROJECT);
     launch_k1(a, D, st);
-    if (s->n > 0) s->launches++;
+    if (count > 0) s->launches++;
     LAUNCH_CHECK();
     tm.end();
     tm.begin(KC_SCAN);
@@ -262,22 +281,27 @@ struct Pipeline {
 
   gsb_status pass(int sl, int f0, int fs, int fe, uint64_t key_base, uint32_t n_long) {
     ChunkArgs a{};
-    a.rec = s->rec[sl]; a.n = s->n; a.vis_bits = s->vis_bits[sl]; a.vis_words = s->vis_words; a.hist = s->hist[sl];
+    a.rec = s->rec[sl]; a.n = count; a.vis_bits = s->vis_bits[sl]; a.vis_words = s->vis_words; a.hist = s->hist[sl];
     a.hist_stride = s->hist_stride; a.off = s->off[sl]; a.frame_base = s->frame_base[sl];
     a.n_tiles = n_tiles; a.tiles_x = tiles_x; a.fs = fs; a.fe = fe; a.key_base = key_base;
     a.keys = s->keys; a.keys_alt = s->keys_alt; a.sorted = s->sorted;
     a.long_list = s->long_list[sl];
     tm.begin(KC_EMIT);
     launch_k2_emit(a, st);
-    if (s->n > 0) s->launches++;
+    if (count > 0) s->launches++;
     LAUNCH_CHECK();
     tm.end();
     // long lists are sorted by their K4 CTA (K3 serves gsb_debug_bin_sort)
     CompositeArgs c{};
-    c.rec = s->rec[sl]; c.n = s->n; c.off = s->off[sl]; c.frame_base = s->frame_base[sl];
+    c.rec = s->rec[sl]; c.n = count; c.off = s->off[sl]; c.frame_base = s->frame_base[sl];
     c.hist_stride = s->hist_stride; c.sorted = s->sorted; c.keys = s->keys; c.keys_alt = s->keys_alt;
     c.key_base = key_base;
     c.inv = s->d_inv;
+    c.slot_base = (int)first;
+    if (merge) {
+      c.bg_off = s->bg_off; c.bg_keys = s->bg_keys; c.bg_rec = s->bg_rec; c.n_static_cams = s->sb_cams;
+      c.qpos_g = s->qpos;
+    }
     c.fs = fs; c.fe = fe; c.f0 = f0; c.width = W; c.height = H; c.tiles_x = tiles_x; c.n_tiles = n_tiles;
     c.bg0 = p->background[0]; c.bg1 = p->background[1]; c.bg2 = p->background[2];
     c.out_rgb = out_rgb; c.out_depth = out_depth; c.out_alpha = out_alpha; c.out_n_eval = out_neval;
@@ -317,6 +341,12 @@ struct Pipeline {
     for (int i = 0; i < nf + 2; ++i) fb[i] = rb[i];
     for (int i = 0; i < nf; ++i) s->stat_V += (int64_t)rb[nf + 2 + i];
     s->stat_K += (int64_t)fb[nf];
+    if (merge)  // the pre-binned background pairs of these frames
+      for (int i = 0; i < nf; ++i) {
+        const int cam = (f0 + i) % s->sb_cams;
+        s->stat_V += s->sb_V[cam];
+        s->stat_K += s->sb_K[cam];
+      }
     s->chunks++;
     const uint32_t n_long = (uint32_t)rb[2 * nf + 2];
     s->stat_long += n_long;
@@ -375,7 +405,7 @@ K0Rig default_rig(gsb_scene s, const float* poses, const float* intr, const floa
 
 gsb_status render_impl(gsb_scene s, const K0Rig& rig, int n_envs, int n_cams, const gsb_render_params* p,
                        float* out_rgb, float* out_depth, float* out_alpha, int32_t* out_neval,
-                       cudaStream_t st) {
+                       cudaStream_t st, bool merge = false) {
   const int F = n_envs * n_cams;
   s->last_stream = st;
   s->stat_V = s->stat_K = s->stat_long = s->stat_maxseg = 0;
@@ -395,6 +425,9 @@ gsb_status render_impl(gsb_scene s, const K0Rig& rig, int n_envs, int n_cams, co
   pl.D = p->sh_degree < 0 ? s->sh_degree : p->sh_degree;
   pl.tm = Timer{s, st, timing};
   pl.out_rgb = out_rgb; pl.out_depth = out_depth; pl.out_alpha = out_alpha; pl.out_neval = out_neval;
+  pl.merge = merge;
+  pl.first = merge ? s->n_bg : 0;      // static cameras: only the robot Gaussians per frame
+  pl.count = s->n - pl.first;
   gsb_status r = pl.run(rig, n_cams);
   s->stats_valid = (r == GSB_OK) && (p->flags & GSB_FLAG_STATS);
   s->timing_valid = (r == GSB_OK) && timing;
@@ -510,7 +543,8 @@ gsb_status gsb_create_scene(const float* means, const float* scales, const float
   }
   DeviceGuard g(device);
   gsb_scene_t* s = new gsb_scene_t();
-  s->device = device; s->n = n; s->n_bodies = n_bodies; s->sh_degree = sh_degree; s->sh_planes = np;
+  s->device = device; s->n = n; s->n_bodies = n_bodies;
+  for (int64_t i = 0; i < n; ++i) s->n_bg += (body_id[i] < 0); s->sh_degree = sh_degree; s->sh_planes = np;
   auto up = [&](float4** d, const std::vector<float4>& h) -> cudaError_t {
     cudaError_t e = dalloc(d, h.size());
     if (e != cudaSuccess) return e;
@@ -582,6 +616,7 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
   CUDA_TRY(dalloc(&s->keys_alt, (size_t)cap));
   CUDA_TRY(dalloc(&s->sorted, (size_t)cap));
   CUDA_TRY(dalloc(&s->d_pairs, 1));
+  if (s->sb_cams > 0) CUDA_TRY(dalloc(&s->qpos, (size_t)cap));
   s->host_io = (flags & GSB_RESERVE_HOST_IO) != 0;
   if (s->host_io) {
     const size_t plane = (size_t)width * height;
@@ -669,6 +704,143 @@ gsb_status gsb_render_host(gsb_scene s, const float* poses, int32_t n_envs, int3
   return GSB_OK;
 }
 
+gsb_status gsb_prebin_static(gsb_scene s, int32_t n_cams, const float* intr, const float* w2c,
+                             const gsb_render_params* p, gsb_stream stream) {
+  if (!s) return fail(GSB_ERR_INVALID_ARGUMENT, "scene is NULL");
+  if (!p || !intr || !w2c) return fail(GSB_ERR_INVALID_ARGUMENT, "NULL params/intrinsics/world_to_cam");
+  if (n_cams < 1 || n_cams > 4096) return fail(GSB_ERR_INVALID_ARGUMENT, "n_cams=%d not in 1..4096", n_cams);
+  if (p->width < 1 || p->height < 1 || p->width > kMaxDim || p->height > kMaxDim)
+    return fail(GSB_ERR_INVALID_ARGUMENT, "image %dx%d outside 1..%d", p->width, p->height, kMaxDim);
+  if (!(p->near_plane > 0.f) || !(p->far_plane > p->near_plane))
+    return fail(GSB_ERR_INVALID_ARGUMENT, "need 0 < near < far");
+  if (p->sh_degree > s->sh_degree || p->sh_degree < -1)
+    return fail(GSB_ERR_INVALID_ARGUMENT, "sh_degree %d not in [-1, %d]", p->sh_degree, s->sh_degree);
+  DeviceGuard g(s->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaStreamSynchronize(st));
+  s->free_prebin();
+  const int C = n_cams, W = p->width, H = p->height;
+  const int tiles_x = (W + kTile - 1) / kTile;
+  const int n_tiles = tiles_x * ((H + kTile - 1) / kTile);
+  const int64_t stride = ((int64_t)n_tiles + 2 + 31) / 32 * 32;
+  const int64_t nbg = s->n_bg, vwords = (nbg + 31) / 32;
+  const int nb1 = s->n_bodies + 1;
+  const int D = p->sh_degree < 0 ? s->sh_degree : p->sh_degree;
+  float* poses = nullptr; float4* table = nullptr; FrameCam* cams = nullptr; float4* rec = nullptr;
+  int* vcount = nullptr; int* hist = nullptr; uint32_t* off = nullptr; uint32_t* vbits = nullptr;
+  uint64_t* fbase = nullptr; uint64_t* keys = nullptr; uint64_t* keys_alt = nullptr; uint32_t* sorted = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(poses); cudaFree(table); cudaFree(cams); cudaFree(rec); cudaFree(vcount); cudaFree(hist);
+    cudaFree(off); cudaFree(vbits); cudaFree(fbase); cudaFree(keys); cudaFree(keys_alt); cudaFree(sorted);
+  };
+#define PB_TRY(expr)                                                                            \
+  do {                                                                                          \
+    cudaError_t e_ = (expr);                                                                    \
+    if (e_ != cudaSuccess) {                                                                    \
+      cleanup();                                                                                \
+      s->free_prebin();                                                                         \
+      return fail(e_ == cudaErrorMemoryAllocation ? GSB_ERR_OUT_OF_MEMORY : GSB_ERR_CUDA, "%s: %s", #expr, \
+                  cudaGetErrorString(e_));                                                      \
+    }                                                                                           \
+  } while (0)
+  // the camera set, kept for gsb_render_static's K0
+  PB_TRY(dalloc(&s->sb_intr, (size_t)C * 4));
+  PB_TRY(dalloc(&s->sb_w2c, (size_t)C * 12));
+  PB_TRY(cudaMemcpyAsync(s->sb_intr, intr, sizeof(float) * C * 4, cudaMemcpyDefault, st));
+  PB_TRY(cudaMemcpyAsync(s->sb_w2c, w2c, sizeof(float) * C * 12, cudaMemcpyDefault, st));
+  // K0 for the C cameras (body rows unused: identity poses)
+  std::vector<float> idp((size_t)std::max(s->n_bodies, 1) * 7, 0.f);
+  for (size_t k = 0; k < idp.size() / 7; ++k) idp[k * 7 + 3] = 1.f;
+  PB_TRY(dalloc(&poses, idp.size()));
+  PB_TRY(cudaMemcpyAsync(poses, idp.data(), sizeof(float) * idp.size(), cudaMemcpyHostToDevice, st));
+  PB_TRY(dalloc(&table, (size_t)C * nb1 * 4));
+  PB_TRY(dalloc(&cams, (size_t)C));
+  K0Rig rig = default_rig(s, poses, s->sb_intr, s->sb_w2c);
+  rig.env_stride = 0;
+  launch_k0(rig, C, C, s->n_bodies, W, H, table, cams, st);
+  PB_TRY(cudaGetLastError());
+  // K1 over the background prefix, K2 scan
+  PB_TRY(dalloc(&rec, (size_t)C * std::max<int64_t>(nbg, 1) * kRecQuads));
+  PB_TRY(dalloc(&vcount, (size_t)C));
+  PB_TRY(dalloc(&vbits, (size_t)C * std::max<int64_t>(vwords, 1)));
+  PB_TRY(dalloc(&hist, (size_t)C * stride));
+  PB_TRY(dalloc(&off, (size_t)C * stride));
+  PB_TRY(dalloc(&fbase, (size_t)C + 2));
+  PB_TRY(cudaMemsetAsync(vcount, 0, sizeof(int) * C, st));
+  PB_TRY(cudaMemsetAsync(hist, 0, sizeof(int) * C * stride, st));
+  K1Args a{};
+  a.g_mean = s->d_mean; a.g_L0 = s->d_L0; a.g_L1 = s->d_L1; a.g_L2 = s->d_L2; a.g_sh = s->d_sh;
+  a.g_ids = s->d_ids;
+  a.n = nbg; a.sh_stride = s->n; a.table = table; a.cams = cams; a.nb1 = nb1;
+  a.f0 = 0; a.n_frames = C; a.width = W; a.height = H; a.tiles_x = tiles_x;
+  a.near_plane = p->near_plane; a.far_plane = p->far_plane;
+  a.rec = rec; a.vcount = vcount; a.hist = hist; a.hist_stride = stride; a.vis_bits = vbits; a.vis_words = vwords;
+  launch_k1(a, D, st);
+  launch_k2_scan(hist, off, stride, C, n_tiles, fbase, nullptr, nullptr, 0, nullptr, nullptr, st);
+  PB_TRY(cudaGetLastError());
+  std::vector<uint64_t> hfb(C + 2);
+  std::vector<int> hv(C);
+  PB_TRY(cudaMemcpyAsync(hfb.data(), fbase, sizeof(uint64_t) * (C + 2), cudaMemcpyDeviceToHost, st));
+  PB_TRY(cudaMemcpyAsync(hv.data(), vcount, sizeof(int) * C, cudaMemcpyDeviceToHost, st));
+  PB_TRY(cudaStreamSynchronize(st));
+  const uint64_t K = hfb[C];
+  uint64_t maxk = 0;
+  for (int c = 0; c < C; ++c) maxk = std::max<uint64_t>(maxk, hfb[c + 1] - hfb[c]);
+  // K2 emission, K3 sort of every list, gather into list order
+  PB_TRY(dalloc(&keys, std::max<uint64_t>(K, 1)));
+  PB_TRY(dalloc(&keys_alt, std::max<uint64_t>(K, 1)));
+  PB_TRY(dalloc(&sorted, std::max<uint64_t>(K, 1)));
+  PB_TRY(dalloc(&s->bg_keys, std::max<uint64_t>(K, 1)));
+  PB_TRY(dalloc(&s->bg_rec, std::max<uint64_t>(K, 1) * 3));
+  ChunkArgs ca{};
+  ca.rec = rec; ca.n = nbg; ca.vis_bits = vbits; ca.vis_words = vwords; ca.hist = hist; ca.hist_stride = stride;
+  ca.off = off; ca.frame_base = fbase; ca.n_tiles = n_tiles; ca.tiles_x = tiles_x; ca.fs = 0; ca.fe = C;
+  ca.key_base = 0; ca.long_list = nullptr; ca.keys = keys; ca.keys_alt = keys_alt; ca.sorted = sorted;
+  launch_k2_emit(ca, st);
+  launch_k3_sort(ca, 0, st);
+  launch_k3_prebin_gather(sorted, fbase, rec, nbg, s->d_inv, C, maxk, s->bg_keys, s->bg_rec, st);
+  PB_TRY(cudaGetLastError());
+  std::vector<uint32_t> hoff((size_t)C * stride);
+  PB_TRY(cudaMemcpyAsync(hoff.data(), off, sizeof(uint32_t) * hoff.size(), cudaMemcpyDeviceToHost, st));
+  PB_TRY(cudaStreamSynchronize(st));
+  std::vector<uint64_t> bo((size_t)C * (n_tiles + 1));
+  for (int c = 0; c < C; ++c)
+    for (int t = 0; t <= n_tiles; ++t) bo[(size_t)c * (n_tiles + 1) + t] = hfb[c] + hoff[(size_t)c * stride + t];
+  PB_TRY(dalloc(&s->bg_off, bo.size()));
+  PB_TRY(cudaMemcpyAsync(s->bg_off, bo.data(), sizeof(uint64_t) * bo.size(), cudaMemcpyHostToDevice, st));
+  if (s->reserved && !s->qpos) PB_TRY(dalloc(&s->qpos, (size_t)s->cap));
+  PB_TRY(cudaStreamSynchronize(st));
+  cleanup();
+#undef PB_TRY
+  s->sb_cams = C; s->sb_w = W; s->sb_h = H; s->sb_D = D; s->sb_near = p->near_plane; s->sb_far = p->far_plane;
+  s->sb_V.resize(C); s->sb_K.resize(C);
+  for (int c = 0; c < C; ++c) {
+    s->sb_V[c] = hv[c];
+    s->sb_K[c] = (int64_t)(hfb[c + 1] - hfb[c]);
+  }
+  return GSB_OK;
+}
+
+gsb_status gsb_render_static(gsb_scene s, const float* poses, int32_t n_envs, const gsb_render_params* p,
+                             float* out_rgb, float* out_depth, float* out_alpha, int32_t* out_neval,
+                             gsb_stream stream) {
+  if (!s) return fail(GSB_ERR_INVALID_ARGUMENT, "scene is NULL");
+  if (s->sb_cams < 1) return fail(GSB_ERR_INVALID_ARGUMENT, "gsb_prebin_static was not called");
+  gsb_status r = validate_render(s, poses, n_envs, s->sb_cams, s->sb_intr, s->sb_w2c, p, out_rgb);
+  if (r != GSB_OK) return r;
+  const int D = p->sh_degree < 0 ? s->sh_degree : p->sh_degree;
+  if (p->width != s->sb_w || p->height != s->sb_h || p->near_plane != s->sb_near || p->far_plane != s->sb_far ||
+      D != s->sb_D)
+    return fail(GSB_ERR_SHAPE_MISMATCH, "params differ from gsb_prebin_static's (image, near/far, sh_degree)");
+  if (!s->qpos) return fail(GSB_ERR_INVALID_ARGUMENT, "gsb_reserve was not called after gsb_prebin_static");
+  DeviceGuard g(s->device);
+  s->dl_rgb = nullptr; s->dl_depth = nullptr; s->dl_alpha = nullptr; s->dl_neval = nullptr;
+  K0Rig rig = default_rig(s, poses, s->sb_intr, s->sb_w2c);
+  rig.cams_shared = 1;
+  return render_impl(s, rig, n_envs, s->sb_cams, p, out_rgb, out_depth, out_alpha, out_neval, (cudaStream_t)stream,
+                     true);
+}
+
 gsb_status gsb_get_stats(gsb_scene s, int64_t* V, int64_t* K, int64_t* P) {
   if (!s) return fail(GSB_ERR_INVALID_ARGUMENT, "scene is NULL");
   if (!s->stats_valid) return fail(GSB_ERR_INVALID_ARGUMENT, "last render had no GSB_FLAG_STATS");
@@ -705,6 +877,7 @@ gsb_status gsb_destroy_scene(gsb_scene s) {
   DeviceGuard g(s->device);
   cudaDeviceSynchronize();
   s->free_workspace();
+  s->free_prebin();
   cudaFree(s->d_mean); cudaFree(s->d_L0); cudaFree(s->d_L1); cudaFree(s->d_L2); cudaFree(s->d_sh);
   cudaFree(s->d_ids);
   cudaFree(s->d_inv);

@@ -18,7 +18,8 @@ struct K1Args {
   const float4* g_L2;
   const float4* g_sh;
   const int2* g_ids;   // (creation index = id, body) per internal index
-  int64_t n;
+  int64_t n;           // Gaussians of this launch (the pointers may start inside the template)
+  int64_t sh_stride;   // SH plane stride = template size N
   // per-frame transforms (K0)
   const float4* table;
   const FrameCam* cams;
@@ -69,7 +70,15 @@ struct CompositeArgs {
   uint32_t* sorted;         // sorted ids of segments longer than kFusedSortCap
   const uint64_t* keys;     // unsorted keys (K2b); K4 sorts every tile list itself
   uint64_t* keys_alt;       // scratch twin of keys for the HBM sort of long lists
-  const int* inv;           // id -> internal index (record slot)
+  const int* inv;           // id -> internal index; record slot = inv[id] - slot_base
+  int slot_base;            // first internal index of the launch's Gaussian range
+  // static-camera merge (gsb_render_static, §8(f) row 2), all nullptr otherwise: the
+  // pre-binned background list of (camera, tile) is merged with the frame's robot list
+  const uint64_t* bg_off;   // [C][T+1] absolute offsets into bg_keys / bg_rec
+  const uint64_t* bg_keys;  // sorted (zbits << 32 | id) of each background list
+  const float4* bg_rec;     // [K_bg][3] records (u,v,p,q | r,log2o,ex,ey | rgb,z) in list order
+  int n_static_cams;
+  uint32_t* qpos_g;         // [cap] merged positions of robot entries of lists sorted in HBM
   uint64_t key_base;
   int fs, fe;             // relative frames of this pass
   int f0;                 // absolute frame index of chunk frame 0
@@ -91,6 +100,7 @@ struct K0Rig {
   int64_t env_stride, body_stride;  // floats
   const float* intr;
   const float* cam_x;
+  int cams_shared;  // intr / cam_x hold one [C] camera set shared by all envs
   int cam_body[kMaxRigCams];
 };
 
@@ -116,6 +126,10 @@ void launch_k2_scan(int* hist, uint32_t* off, int64_t hist_stride, int n_frames,
                     const int* vcount, uint64_t* host_mapped, cudaStream_t s);
 void launch_k2_emit(const ChunkArgs& a, cudaStream_t s);
 void launch_k3_sort(const ChunkArgs& a, uint32_t n_long, cudaStream_t s);
+// gather K3-sorted background lists (ids in `sorted`) into list-ordered keys + 3-quad records
+void launch_k3_prebin_gather(const uint32_t* sorted, const uint64_t* frame_base, const float4* rec, int64_t n,
+                             const int* inv, int n_frames, uint64_t max_keys, uint64_t* bg_keys, float4* bg_rec,
+                             cudaStream_t s);
 // long_lists: use the variant with a 4x larger shared-memory sort (fewer CTAs per SM)
 void launch_k4_composite(const CompositeArgs& a, bool long_lists, cudaStream_t s);
 

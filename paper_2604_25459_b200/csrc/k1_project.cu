@@ -49,7 +49,8 @@ __global__ void k0_setup(K0Rig rig, int n_frames, int n_cams, int n_bodies, int 
   const int cam = f % n_cams;
   // world->camera of this frame: given, or composed from the camera's body (R29)
   float W[12];
-  const float* Wg = rig.cam_x + (size_t)f * 12;
+  const int crow = rig.cams_shared ? cam : f;   // static cameras: one camera set for every env
+  const float* Wg = rig.cam_x + (size_t)crow * 12;
   const int kb = cam < kMaxRigCams ? rig.cam_body[cam] : -1;
   if (kb >= 0) {
     r29_compose(Wg, rig.poses + (size_t)e * rig.env_stride + (size_t)kb * rig.body_stride, W);
@@ -88,7 +89,7 @@ __global__ void k0_setup(K0Rig rig, int n_frames, int n_cams, int n_bodies, int 
   o[2] = make_float4(M[2][0], M[2][1], M[2][2], m[2]);
   o[3] = make_float4(cb[0], cb[1], cb[2], 0.f);
   if (k < 0) {
-    const float* K = rig.intr + (size_t)f * 4;
+    const float* K = rig.intr + (size_t)crow * 4;
     FrameCam fc;
     fc.fx = K[0]; fc.fy = K[1]; fc.cx = K[2]; fc.cy = K[3];
     fc.limx = 1.3f * (float)width / (2.0f * K[0]);
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
           const float4 cb = __ldg(tb + 3);
           const float dx = mean.x - cb.x, dy = mean.y - cb.y, dz = mean.z - cb.z;
           const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
-          rgb = sh_colour<D>(a.g_sh, a.n, in ? i : 0, dx * inv, dy * inv, dz * inv);
+          rgb = sh_colour<D>(a.g_sh, a.sh_stride, in ? i : 0, dx * inv, dy * inv, dz * inv);
         }
         if (debug && in) {
           const size_t o = (size_t)f * a.n + id;

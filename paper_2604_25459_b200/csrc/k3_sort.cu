@@ -2,6 +2,8 @@
 // shared-memory sort (and for every list in gsb_debug_bin_sort).  One CTA per (frame, tile)
 // segment; lists up to kSmemCap keys are sorted in shared memory, longer ones ping-pong
 // between the key buffer and its scratch twin in HBM with the same code (gsb_sort.cuh).
+#include <algorithm>
+
 #include "gsb_common.cuh"
 #include "gsb_kernels.cuh"
 #include "gsb_sort.cuh"
@@ -49,6 +51,36 @@ __global__ void __launch_bounds__(kSortThreads) k3_sort(ChunkArgs a) {
     const uint64_t* r = in_b ? gb : ga;
     for (int e = threadIdx.x; e < n; e += kSortThreads) a.sorted[start + e] = (uint32_t)r[e];
   }
+}
+
+// gsb_prebin_static: background lists of the C static cameras, K3-sorted, gathered into list
+// order — keys (zbits << 32 | id) for K4's merge ranks and the 48 B of record K4 stages.
+__global__ void __launch_bounds__(256) k3_prebin_gather(const uint32_t* __restrict__ sorted,
+                                                        const uint64_t* __restrict__ frame_base,
+                                                        const float4* __restrict__ rec, int64_t n,
+                                                        const int* __restrict__ inv,
+                                                        uint64_t* __restrict__ bg_keys,
+                                                        float4* __restrict__ bg_rec) {
+  const int f = blockIdx.y;
+  const uint64_t b = frame_base[f], K = frame_base[f + 1] - b;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < K; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t id = sorted[b + e];
+    const float4* r = rec + ((size_t)f * n + (uint32_t)inv[id]) * kRecQuads;
+    const float4 q0 = r[0], q1 = r[1], q2 = r[2];
+    bg_keys[b + e] = ((uint64_t)__float_as_uint(q2.w) << 32) | id;
+    float4* o = bg_rec + (b + e) * 3;
+    o[0] = q0;
+    o[1] = q1;
+    o[2] = q2;
+  }
+}
+
+void launch_k3_prebin_gather(const uint32_t* sorted, const uint64_t* frame_base, const float4* rec, int64_t n,
+                             const int* inv, int n_frames, uint64_t max_keys, uint64_t* bg_keys, float4* bg_rec,
+                             cudaStream_t s) {
+  if (n_frames <= 0 || max_keys == 0) return;
+  const unsigned gx = (unsigned)std::min<uint64_t>((max_keys + 255) / 256, 4096);
+  k3_prebin_gather<<<dim3(gx, (unsigned)n_frames), 256, 0, s>>>(sorted, frame_base, rec, n, inv, bg_keys, bg_rec);
 }
 
 void launch_k3_sort(const ChunkArgs& a, uint32_t n_long, cudaStream_t s) {

@@ -34,7 +34,7 @@ constexpr int kBatch = kCompThreads;       // records staged per round (one cp.a
 // mostly long): the keys stay in L2 and a packed 32-bit sort runs on 8 B per key; the result
 // buffer then holds the staging and the other buffer the slot list.
 constexpr int kStageQuads = 2 * 3 * kBatch;
-template <int CAP>
+template <int CAP, bool MERGE = false>
 struct K4Shared {
   static constexpr bool kPacked = CAP > kFusedSortCap;
   SortShared<kCompThreads> sort;
@@ -48,6 +48,7 @@ struct K4Shared {
   } u;
   unsigned long long red[kCompThreads / 32];
   uint8_t wlist[kCompThreads / 32][kBatch];   // per-warp compacted record indices of a round
+  uint32_t qpos[MERGE ? CAP : 1];             // merge variant: merged position of robot entry j
 };
 static_assert(sizeof(uint32_t) * kFusedSortCap + 16 * kStageQuads <= 2 * 8 * kFusedSortCap, "small union");
 static_assert(4 * 4 * kFusedSortCap >= 16 * kStageQuads, "large variant stages in the result buffer");
@@ -89,10 +90,30 @@ __device__ __forceinline__ void blend(bool use, float arg, const float4& r2, flo
   }
 }
 
-template <int CAP, int MINB>
+// first index in sorted k[0..n) whose value is >= x
+template <typename T, typename P>
+__device__ __forceinline__ int lower_bound(P k, int n, T x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (k[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// MERGE (gsb_render_static, §8(f) row 2): the CTA's list is the (zbits, id) merge of the
+// pre-binned, pre-sorted background list of its (camera, tile) with the frame's robot list
+// (sorted here as usual).  Keys are unique (R10), so the merge is the full sort of the union
+// and every output is bit-identical to gsb_render with the same cameras.  Robot entry j goes
+// to merged position qpos[j] = j + #(background keys below it) (binary search in the L2-
+// resident background keys); a merged position d is robot entry k = lower_bound(qpos, d) if
+// qpos[k] == d, else background entry d - k.
+template <int CAP, int MINB, bool MERGE>
 __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  K4Shared<CAP>& sm = *reinterpret_cast<K4Shared<CAP>*>(smem_raw);
+  using Sh = K4Shared<CAP, MERGE>;
+  Sh& sm = *reinterpret_cast<Sh*>(smem_raw);
   const unsigned FULL = 0xffffffffu;
   const int fl = a.fs + blockIdx.x / a.n_tiles;
   const int t = blockIdx.x % a.n_tiles;
@@ -109,6 +130,17 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
   const uint64_t start = a.frame_base[fl] - a.key_base + off[t];
   const int len = (int)(off[t + 1] - off[t]);
   const float4* rec = a.rec + (size_t)fl * a.n * kRecQuads;
+  // merge variant: this frame's camera's background list
+  uint64_t bo = 0;
+  int lb = 0;
+  if constexpr (MERGE) {
+    const int cam = (a.f0 + fl) % a.n_static_cams;
+    const uint64_t* bof = a.bg_off + (size_t)cam * (a.n_tiles + 1);
+    bo = bof[t];
+    lb = (int)(bof[t + 1] - bo);
+  }
+  const uint64_t* bkeys = a.bg_keys + bo;
+  const uint32_t* qpos = nullptr;
   const float pxc = (float)px + 0.5f;
   const float bcx = (float)bx0 + 4.0f, bcy = (float)by0 + 4.0f;  // block centre (pixel centres +-3.5)
 
@@ -117,7 +149,7 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
   const bool fused = len <= CAP;
   const uint32_t* slots = nullptr;
   float4* stg = nullptr;
-  if constexpr (K4Shared<CAP>::kPacked) {
+  if constexpr (Sh::kPacked) {
     stg = reinterpret_cast<float4*>(sm.u.buf[0]);
     if (fused && len > 0) {
       const uint64_t* gk = a.keys + start;
@@ -125,7 +157,7 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
       const uint32_t* res = sm.u.buf[in_b ? 1 : 0];
       uint32_t* sl = sm.u.buf[in_b ? 0 : 1];
       for (int e = tid; e < len; e += kCompThreads)
-        sl[e] = (uint32_t)__ldg(a.inv + (uint32_t)__ldg(gk + (res[e] & 0xffffu)));
+        sl[e] = (uint32_t)(__ldg(a.inv + (uint32_t)__ldg(gk + (res[e] & 0xffffu))) - a.slot_base);
       slots = sl;
       stg = reinterpret_cast<float4*>(sm.u.buf[in_b ? 1 : 0]);
     }
@@ -140,8 +172,13 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
 #pragma unroll
       for (int k = 0; k < CAP / kCompThreads; ++k) {
         const int e = tid + k * kCompThreads;
-        if (e < len) sl[k] = (uint32_t)__ldg(a.inv + (uint32_t)sm.u.keys[in_b ? 1 : 0][e]);
+        if (e < len) {
+          const uint64_t key = sm.u.keys[in_b ? 1 : 0][e];
+          sl[k] = (uint32_t)(__ldg(a.inv + (uint32_t)key) - a.slot_base);
+          if constexpr (MERGE) sm.qpos[e] = (uint32_t)(e + lower_bound(bkeys, lb, key));
+        }
       }
+      if constexpr (MERGE) qpos = sm.qpos;
       __syncthreads();
 #pragma unroll
       for (int k = 0; k < CAP / kCompThreads; ++k) {
@@ -156,16 +193,29 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
     const bool in_b = segment_sort(ga, gb, len, sm.sort);
     uint32_t* dst = a.sorted + start;
     const uint64_t* r = in_b ? gb : ga;
-    for (int e = tid; e < len; e += kCompThreads) dst[e] = (uint32_t)__ldg(a.inv + (uint32_t)r[e]);
+    for (int e = tid; e < len; e += kCompThreads) dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)r[e]) - a.slot_base);
     slots = dst;
+    if constexpr (MERGE) {
+      uint32_t* qg = a.qpos_g + start;
+      for (int e = tid; e < len; e += kCompThreads) qg[e] = (uint32_t)(e + lower_bound(bkeys, lb, r[e]));
+      qpos = qg;
+    }
   }
   __syncthreads();  // the slot list is complete (and the sort buffers are free)
 
   // stage round b's records into buffer (b & 1): one record (3 x 16 B cp.async) per thread
+  const int total = len + lb;   // merged list length (lb = 0 unless MERGE)
   auto stage = [&](int b) {
     const int k = b * kBatch + tid;
-    if (k < len) {
-      const float4* r = rec + (size_t)slots[k] * kRecQuads;
+    if (k < total) {
+      const float4* r;
+      if constexpr (MERGE) {
+        const int j = len > 0 ? lower_bound(qpos, len, (uint32_t)k) : 0;
+        if (j < len && qpos[j] == (uint32_t)k) r = rec + (size_t)slots[j] * kRecQuads;
+        else r = a.bg_rec + (bo + (uint64_t)(k - j)) * 3;
+      } else {
+        r = rec + (size_t)slots[k] * kRecQuads;
+      }
       float4* buf = stg + (b & 1) * 3 * kBatch;
       cp_async16(&buf[tid], r);
       cp_async16(&buf[kBatch + tid], r + 1);
@@ -178,8 +228,8 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
   float T1 = 1.f, r1c = 0.f, g1c = 0.f, b1c = 0.f, d1 = 0.f;
   float pyc0 = in0 ? (float)py0 + 0.5f : kFar;   // out-of-image pixels never pass the alpha test
   float pyc1 = in1 ? (float)py0 + 1.5f : kFar;
-  int ne0 = len, ne1 = len;
-  const int rounds = (len + kBatch - 1) / kBatch;
+  int ne0 = total, ne1 = total;
+  const int rounds = (total + kBatch - 1) / kBatch;
   if (rounds > 0) {
     stage(0);
     cp_async_wait_all();
@@ -188,11 +238,11 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
   for (int b = 0; b < rounds; ++b) {
     if (b + 1 < rounds) stage(b + 1);   // overlaps this round's compositing
     const float4* R0 = reinterpret_cast<const float4*>(
-        reinterpret_cast<const char*>(K4Shared<CAP>::kPacked ? stg : sm.u.c.stage) + (b & 1) * (3 * kBatch * 16));
+        reinterpret_cast<const char*>(Sh::kPacked ? stg : sm.u.c.stage) + (b & 1) * (3 * kBatch * 16));
     const float4* R1 = R0 + kBatch;
     const float4* R2 = R1 + kBatch;
     const int base = b * kBatch;
-    const int cnt = min(kBatch, len - base);
+    const int cnt = min(kBatch, total - base);
     if (!__all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) {
       // this warp's list of the round's records that can reach its 8x8 block (u8 indices)
       uint8_t* wl = sm.wlist[warp];
@@ -286,23 +336,24 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
   }
 }
 
-template <int CAP, int MINB>
+template <int CAP, int MINB, bool MERGE>
 static void launch_k4_variant(const CompositeArgs& a, unsigned grid, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k4_composite<CAP, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(K4Shared<CAP>));
+    cudaFuncSetAttribute(k4_composite<CAP, MINB, MERGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(K4Shared<CAP, MERGE>));
     attr = true;
   }
-  k4_composite<CAP, MINB><<<grid, kCompThreads, sizeof(K4Shared<CAP>), s>>>(a);
+  k4_composite<CAP, MINB, MERGE><<<grid, kCompThreads, sizeof(K4Shared<CAP, MERGE>), s>>>(a);
 }
 
 void launch_k4_composite(const CompositeArgs& a, bool long_lists, cudaStream_t s) {
   const int nf = a.fe - a.fs;
   if (nf <= 0) return;
   const unsigned grid = (unsigned)nf * a.n_tiles;
-  if (long_lists) launch_k4_variant<4 * kFusedSortCap, 5>(a, grid, s);
-  else launch_k4_variant<kFusedSortCap, 9>(a, grid, s);
+  if (a.bg_off) launch_k4_variant<kFusedSortCap, 8, true>(a, grid, s);
+  else if (long_lists) launch_k4_variant<4 * kFusedSortCap, 5, false>(a, grid, s);
+  else launch_k4_variant<kFusedSortCap, 9, false>(a, grid, s);
 }
 
 }  // namespace gsb

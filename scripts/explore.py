@@ -30,7 +30,10 @@ torch.cuda.empty_cache()
 print(json.dumps(res), flush=True)
 
 envs = {"C2": 64, "C3": 1024, "C4": 4096, "C5": 1024, "T1": 3}
-for name in [n for n in sys.argv[1:] if n in synth.CONFIGS] or ["C2", "C4", "C5", "C3"]:
+MODES = ("rig", "static")
+_named = [n for n in sys.argv[1:] if n in synth.CONFIGS]
+_modes_only = bool(sys.argv[1:]) and all(a in MODES for a in sys.argv[1:])
+for name in ([] if _modes_only or ("static" in sys.argv[1:]) else (_named or ["C2", "C4", "C5", "C3"])):
     cfg = synth.CONFIGS[name]
     B = envs.get(name, cfg.n_envs)
     sc = synth.make_scene(cfg)
@@ -98,3 +101,51 @@ if "rig" in sys.argv[1:] or not sys.argv[1:]:
     torch.cuda.synchronize()
     print(json.dumps({"config": "C4-rig (cam 1 on body 9, strided 13-float states)", "frames": B * 2,
                       "fps": 3 * B * 2 / (e0.elapsed_time(e1) / 1e3)}), flush=True)
+
+# §8(f) row 2 measurement: C3 with cameras fixed in the world (env 0's camera for every env):
+# gsb_render with the camera broadcast vs gsb_prebin_static + gsb_render_static (bit-identical)
+if "static" in sys.argv[1:] or not sys.argv[1:]:
+    for name in [n for n in sys.argv[1:] if n in synth.CONFIGS] or ["C3"]:
+        cfg = synth.CONFIGS[name]
+        B = envs.get(name, cfg.n_envs)
+        sc = synth.make_scene(cfg)
+        g = gsb.Scene.from_synth(sc)
+        Ks, Ws = synth.static_cameras(cfg)
+        prm0 = gsb.RenderParams(cfg.width, cfg.height)
+        torch.cuda.synchronize()
+        t0 = time.time()
+        g.prebin_static(Ks, Ws, prm0)
+        t_prebin = time.time() - t0
+        g.reserve(B, cfg.n_cams, cfg.width, cfg.height)
+        K = torch.from_numpy(np.broadcast_to(Ks, (B,) + Ks.shape).copy()).cuda()
+        W = torch.from_numpy(np.broadcast_to(Ws, (B,) + Ws.shape).copy()).cuda()
+        poses = [torch.from_numpy(synth.make_poses(cfg, np.arange(B), s)).cuda() for s in range(4)]
+        rgb = torch.empty((B, cfg.n_cams, 3, cfg.height, cfg.width), device="cuda")
+        dep = torch.empty((B, cfg.n_cams, cfg.height, cfg.width), device="cuda")
+        res = {}
+        for mode in ("render", "render_static"):
+            def call(s, prm):
+                if mode == "render":
+                    g.render(poses[s], K, W, prm, rgb, dep)
+                else:
+                    g.render_static(poses[s], prm, rgb, dep)
+            prm = gsb.RenderParams(cfg.width, cfg.height, timing=True)
+            call(0, gsb.RenderParams(cfg.width, cfg.height, stats=True))
+            st = g.stats()
+            for s in range(2):
+                call(s, prm)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            e0.record()
+            for s in range(3):
+                call((s + 1) % 4, prm)
+            e1.record()
+            torch.cuda.synchronize()
+            tm = g.timings()
+            F = B * cfg.n_cams
+            res[mode] = {"fps": 3 * F / (e0.elapsed_time(e1) / 1e3), "P/f": st["P"] / F, "K/f": st["K"] / F,
+                         "stage_ms": {k: round(v, 2) for k, v in tm.items() if k.endswith("_ms")}}
+        print(json.dumps({"config": name + "-static (env 0 cameras for all envs)", "frames": B * cfg.n_cams,
+                          "prebin_s": round(t_prebin, 3), **res}), flush=True)
+        del g, rgb, dep
+        torch.cuda.empty_cache()

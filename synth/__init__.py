@@ -169,6 +169,9 @@ CONFIGS: Dict[str, Config] = {
     "T5": Config("T5", 15, 2, 1, 160, 120, 12000, 10, 200, 2),
     # long tile lists (C4-like density at parity size): exercises K4's large-capacity variant
     "T6": Config("T6", 16, 2, 2, 64, 64, 40000, 10, 200, 3, fov60=True),
+    # robot-dominated tile lists (thousands of robot Gaussians in a few tiles): the static-camera
+    # merge path with robot lists beyond K4's fused-sort capacity
+    "T7": Config("T7", 17, 3, 1, 64, 64, 2000, 2, 3000, 1, fov60=True),
 }
 
 
@@ -409,6 +412,13 @@ def make_cameras(cfg: Config, env_ids) -> Tuple[np.ndarray, np.ndarray]:
             W2C[bi, c, :, :3] = R
             W2C[bi, c, :, 3] = -R @ eye
     return K, W2C.astype(np.float32)
+
+
+def static_cameras(cfg: Config) -> Tuple[np.ndarray, np.ndarray]:
+    """Cameras fixed in the world (§8(f) row 2): env 0's cameras, shared by every env.
+    (intrinsics [C,4] f32, world_to_cam [C,3,4] f32)."""
+    K, W2C = make_cameras(cfg, [0])
+    return K[0].copy(), W2C[0].copy()
 
 
 @dataclasses.dataclass

@@ -30,6 +30,20 @@ def test_library_builds_and_exports_header_symbols():
     assert gsb.version().startswith("gsb")
 
 
+def test_binding_declares_every_prototype():
+    """Every exported function has ctypes argtypes matching the header's parameter count (an
+    undeclared function would pass 64-bit pointers as C int)."""
+    src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "gsb.h")).read(), flags=re.S)
+    L = gsb.lib()
+    protos = dict(re.findall(r"\b(gsb_[a-z_]+)\s*\(([^;{]*?)\)\s*;", src))
+    assert sorted(protos) == sorted(gsb.EXPORTS)
+    for name, params in protos.items():
+        params = params.strip()
+        n = 0 if params in ("", "void") else params.count(",") + 1
+        assert getattr(L, name).argtypes is not None, name
+        assert len(getattr(L, name).argtypes) == n, (name, n)
+
+
 def test_sm100a_only_cubin():
     """The library carries sm_100a SASS (no other arch, no PTX JIT fallback)."""
     import subprocess
