@@ -63,7 +63,8 @@ def lib():
         L.gsbo_composite.restype = ctypes.c_int
         L.gsbo_composite.argtypes = [P, P, ctypes.c_int64, P, P, ctypes.c_int64, P, ctypes.c_int,
                                      ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
-                                     P, P, P, P, P, P, P, P, ctypes.c_double, ctypes.c_int]
+                                     P, P, P, P, P, P, P, P, ctypes.c_double, ctypes.c_int,
+                                     ctypes.c_int64, P, P, P, P]
         L.gsbo_depth_key.restype = ctypes.c_float
         L.gsbo_depth_key.argtypes = [P, P, P]
         L.gsbo_compose_w2c.restype = None
@@ -140,8 +141,11 @@ class FrameResult:
 
 
 def composite(proj, order, px, py, prm: RenderParams, mode: str = "box", nthreads: Optional[int] = None,
-              delta_alpha: float = DELTA_ALPHA, delta_T: float = DELTA_T, valid=None):
-    """Step 7-9 for the listed pixel coordinates (see gsb_oracle.c)."""
+              delta_alpha: float = DELTA_ALPHA, delta_T: float = DELTA_T, valid=None, scores: Optional[dict] = None):
+    """Step 7-9 for the listed pixel coordinates (see gsb_oracle.c).
+    scores: if a dict, also accumulate the reading-R30 pruning scores of these pixels into it:
+    w_sum / w_max [N] (f64, by Gaussian id) and, when it holds "mask_in" ([npix] bool), the
+    flag "touched" [N] of Gaussians whose exact R8 box holds a masked pixel."""
     L = lib()
     px = _c(px, np.int32).reshape(-1)
     py = _c(py, np.int32).reshape(-1)
@@ -160,10 +164,24 @@ def composite(proj, order, px, py, prm: RenderParams, mode: str = "box", nthread
     if nthreads is None:
         nthreads = os.cpu_count() or 1
     proj = _c(proj, np.float64)
-    L.gsbo_composite(_p(proj), _p(order), order.size, _p(px), _p(py), npix, _p(bg),
-                     1 if mode == "box" else 0, delta_alpha, delta_T, cmax, zmax,
-                     _p(rgb), _p(dep), _p(alp), _p(term), _p(nev), _p(brgb), _p(bdep), _p(tnear),
-                     DELTA_T_INT, int(nthreads))
+    n_gauss = proj.shape[0]
+    ws = wm = mk = tch = None
+    if scores is not None:
+        ws, wm = np.zeros(n_gauss), np.zeros(n_gauss)
+        if scores.get("mask_in") is not None:
+            mk = _c(np.asarray(scores["mask_in"]).reshape(-1), np.uint8)
+            tch = np.zeros(n_gauss, np.uint8)
+    rc = L.gsbo_composite(_p(proj), _p(order), order.size, _p(px), _p(py), npix, _p(bg),
+                          1 if mode == "box" else 0, delta_alpha, delta_T, cmax, zmax,
+                          _p(rgb), _p(dep), _p(alp), _p(term), _p(nev), _p(brgb), _p(bdep), _p(tnear),
+                          DELTA_T_INT, int(nthreads), n_gauss, _p(ws) if ws is not None else None,
+                          _p(wm) if wm is not None else None, _p(mk) if mk is not None else None,
+                          _p(tch) if tch is not None else None)
+    if rc != 0:
+        raise MemoryError("oracle composite: allocation failed")
+    if scores is not None:
+        scores["w_sum"], scores["w_max"] = ws, wm
+        scores["touched"] = tch.astype(bool) if tch is not None else None
     masked = (brgb > 0.5 * TOL_RGB) | (bdep > 0.5 * (TOL_DEPTH_REL * dep + TOL_DEPTH_ABS))
     return rgb, dep, alp, term, nev, masked, brgb, bdep, tnear.astype(bool)
 
@@ -186,6 +204,19 @@ def render_frame(scene, pose_env, intr, w2c, prm: RenderParams, pixels=None, mod
         term, nev, masked, tnear = term.reshape(H, W), nev.reshape(H, W), masked.reshape(H, W), tnear.reshape(H, W)
         brgb, bdep = brgb.reshape(H, W), bdep.reshape(H, W)
     return FrameResult(rgb, dep, alp, term, nev, masked, brgb, bdep, proj, zb, valid, order, tnear)
+
+
+def frame_scores(scene, pose_env, intr, w2c, prm: RenderParams, nthreads: Optional[int] = None):
+    """Reading R30 (§8(f) row 3; pruning by rendering importance): for one full frame,
+    per Gaussian id the sum and the max over pixels of the blend weight w = alpha T of every
+    blended entry (step 7), plus the R28 "touched" flag (the Gaussian's R8 box holds a pixel in
+    the threshold margin, where either side of a flip is correct) and the frame's alpha.
+    Returns (w_sum [N], w_max [N], touched [N] bool, alpha [H,W])."""
+    fr = render_frame(scene, pose_env, intr, w2c, prm, nthreads=nthreads)
+    py, px = np.meshgrid(np.arange(prm.height), np.arange(prm.width), indexing="ij")
+    sc = {"mask_in": fr.masked.reshape(-1)}
+    composite(fr.proj, fr.order, px.reshape(-1), py.reshape(-1), prm, nthreads=nthreads, scores=sc)
+    return sc["w_sum"], sc["w_max"], sc["touched"], fr.alpha
 
 
 def compose_w2c(pose, mount) -> np.ndarray:

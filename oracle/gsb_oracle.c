@@ -319,6 +319,12 @@ typedef struct {
   double* out_budget_depth;
   uint8_t* out_term_near;
   double delta_T_int;
+  /* pruning scores (§8(f) row 3, reading R30), all NULL unless requested; per-thread arrays
+   * indexed by Gaussian id, merged after the join */
+  double* w_sum;            /* sum of blend weights w = alpha T over the pixels */
+  double* w_max;            /* max of w */
+  const uint8_t* mask_in;   /* [npix] pixels in the R28 margin */
+  uint8_t* touched;         /* Gaussians whose R8 box holds a masked pixel */
 } comp_job;
 
 static void composite_pixel(const comp_job* jb, int64_t p) {
@@ -360,6 +366,10 @@ static void composite_pixel(const comp_job* jb, int64_t p) {
       break;
     }
     const double w = alpha * T; /* R14 */
+    if (jb->w_sum) {
+      jb->w_sum[i] += w;
+      if (w > jb->w_max[i]) jb->w_max[i] = w;
+    }
     C[0] += w * g[F_R];
     C[1] += w * g[F_G];
     C[2] += w * g[F_BL];
@@ -374,6 +384,15 @@ static void composite_pixel(const comp_job* jb, int64_t p) {
   jb->out_budget_rgb[p] = brgb;
   jb->out_budget_depth[p] = bdep;
   jb->out_term_near[p] = term_near;
+  if (jb->touched && jb->mask_in && jb->mask_in[p]) {
+    /* a masked pixel may blend any Gaussian whose exact box holds it on either side of a flip */
+    for (int64_t j = 0; j < jb->n_order; ++j) {
+      const uint32_t i = jb->order[j];
+      const double* g = jb->proj + (int64_t)i * GSBO_NF;
+      const double rx = sqrt(g[F_KAPPA] * g[F_SXX]), ry = sqrt(g[F_KAPPA] * g[F_SYY]);
+      if (pxc >= g[F_U] - rx && pxc <= g[F_U] + rx && pyc >= g[F_V] - ry && pyc <= g[F_V] + ry) jb->touched[i] = 1;
+    }
+  }
 }
 
 static void* composite_worker(void* arg) {
@@ -387,7 +406,8 @@ int gsbo_composite(const double* proj, const uint32_t* order, int64_t n_order, c
                    double delta_T, double cmax, double zmax, double* out_rgb, double* out_depth,
                    double* out_alpha, int64_t* out_term_id, int64_t* out_n_eval,
                    double* out_budget_rgb, double* out_budget_depth, uint8_t* out_term_near,
-                   double delta_T_int, int nthreads) {
+                   double delta_T_int, int nthreads, int64_t n_gauss, double* out_w_sum, double* out_w_max,
+                   const uint8_t* mask_in, uint8_t* out_touched) {
   if (nthreads < 1) nthreads = 1;
   if (nthreads > 256) nthreads = 256;
   if ((int64_t)nthreads > npix) nthreads = npix > 0 ? (int)npix : 1;
@@ -406,13 +426,33 @@ int gsbo_composite(const double* proj, const uint32_t* order, int64_t n_order, c
     jb->out_term_id = out_term_id; jb->out_n_eval = out_n_eval;
     jb->out_budget_rgb = out_budget_rgb; jb->out_budget_depth = out_budget_depth;
     jb->out_term_near = out_term_near; jb->delta_T_int = delta_T_int;
+    jb->w_sum = jb->w_max = NULL; jb->mask_in = mask_in; jb->touched = NULL;
+    if (out_w_sum && out_w_max) {
+      jb->w_sum = (double*)calloc((size_t)n_gauss + 1, sizeof(double));
+      jb->w_max = (double*)calloc((size_t)n_gauss + 1, sizeof(double));
+      if (!jb->w_sum || !jb->w_max) return 1;
+    }
+    if (out_touched && mask_in) {
+      jb->touched = (uint8_t*)calloc((size_t)n_gauss + 1, 1);
+      if (!jb->touched) return 1;
+    }
   }
   if (nthreads == 1) {
     composite_worker(&jobs[0]);
-    return 0;
+  } else {
+    for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, composite_worker, &jobs[t]);
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
   }
-  for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, composite_worker, &jobs[t]);
-  for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+  /* merge the per-thread score arrays: sums added, maxima maxed, flags or-ed */
+  for (int t = 0; t < nthreads; ++t) {
+    comp_job* jb = &jobs[t];
+    for (int64_t i = 0; i < n_gauss && jb->w_sum; ++i) {
+      out_w_sum[i] += jb->w_sum[i];
+      if (jb->w_max[i] > out_w_max[i]) out_w_max[i] = jb->w_max[i];
+    }
+    for (int64_t i = 0; i < n_gauss && jb->touched; ++i) out_touched[i] |= jb->touched[i];
+    free(jb->w_sum); free(jb->w_max); free(jb->touched);
+  }
   return 0;
 }
 

@@ -543,3 +543,56 @@ def test_r29_egocentric_view_of_own_body_is_pose_invariant():
         ok = ~(r.masked | imgs[0].masked)
         assert np.abs(r.rgb - imgs[0].rgb)[ok].max() < 1e-4
         assert ok.mean() > 0.99
+
+
+# ---------------------------------------------------------------- pruning scores (R30)
+def test_scores_single_gaussian_closed_form():
+    """One isotropic on-axis Gaussian (pin 1 geometry): its blend weight at pixel p is its alpha
+    there (T = 1), so w_sum = sum over pixels of min(0.99, o exp(-(dx^2/Sxx + dy^2/Syy)/2)) over
+    the pixels where that is >= 1/255, and w_max = min(0.99, o) at the pixel centre on (u, v)
+    (reading R30 on top of R12-R14)."""
+    z, s, o = 3.0, 0.05, 0.8
+    sc = scene_from([0, 0, z], s, opac=o)
+    K, W = identity_cam(fx=100.0, fy=120.0, cx=32.5, cy=24.5)
+    prm = oracle.RenderParams(64, 48)
+    ws, wm, touched, alpha = oracle.frame_scores(sc, np.zeros((0, 7), np.float32), K, W, prm)
+    s32, o32 = float(np.float32(s)), float(np.float32(o))
+    sxx, syy = s32 * s32 * 100.0 ** 2 / z ** 2 + 0.3, s32 * s32 * 120.0 ** 2 / z ** 2 + 0.3
+    py, px = np.mgrid[0:48, 0:64]
+    a = o32 * np.exp(-0.5 * (((px + 0.5) - 32.5) ** 2 / sxx + ((py + 0.5) - 24.5) ** 2 / syy))
+    a = np.minimum(0.99, a)
+    exp_sum = a[a >= 1.0 / 255.0].sum()
+    assert ws[0] == pytest.approx(exp_sum, rel=1e-12)
+    assert wm[0] == pytest.approx(min(0.99, o32), rel=1e-12)
+    assert not touched.any()
+
+
+def test_scores_two_layers_and_partition_identity():
+    """Front-to-back 'over': the back Gaussian's weight at the shared centre pixel is
+    (1 - a1) a2, and summed over all Gaussians the weights of a pixel are its alpha = 1 - T, so
+    sum_i w_sum_i = sum_p alpha_p (pin 9 identity, here per Gaussian) — on a two-layer scene and
+    on random tiny scenes with bodies; scores do not depend on the R8 acceleration (pin 10)."""
+    K, W = identity_cam()
+    prm = oracle.RenderParams(64, 48)
+    sc = scene_from([[0, 0, 2.0], [0, 0, 3.0]], [[0.001, 0.001, 0.001], [0.001, 0.001, 0.001]], opac=[0.6, 0.7])
+    ws, wm, _, alpha = oracle.frame_scores(sc, np.zeros((0, 7), np.float32), K, W, prm)
+    a1, a2 = float(np.float32(0.6)), float(np.float32(0.7))
+    # tiny footprint: the centre pixel is the only one above 1/255 for the front Gaussian
+    assert wm[0] == pytest.approx(a1, rel=1e-12)
+    assert wm[1] == pytest.approx((1 - a1) * a2, rel=1e-12)
+    assert ws.sum() == pytest.approx(alpha.sum(), rel=1e-12)
+    rng = np.random.default_rng(31)
+    for trial in range(4):
+        sc = random_tiny_scene(rng, 40, n_bodies=2, sh_degree=1)
+        pose = random_pose(rng, 2)
+        ws, wm, _, alpha = oracle.frame_scores(sc, pose, K, W, prm)
+        assert ws.sum() == pytest.approx(alpha.sum(), rel=1e-12, abs=1e-12)
+        assert (wm <= 0.99).all() and (wm >= 0).all()
+        assert ((ws > 0) == (wm > 0)).all()
+        # pure brute force gives the same scores (the R8 box only skips alpha < 1/255)
+        fr = oracle.render_frame(sc, pose, K, W, prm)
+        py, px = np.meshgrid(np.arange(48), np.arange(64), indexing="ij")
+        sp = {}
+        oracle.composite(fr.proj, fr.order, px.reshape(-1), py.reshape(-1), prm, mode="pure", scores=sp)
+        np.testing.assert_array_equal(sp["w_sum"], ws)
+        np.testing.assert_array_equal(sp["w_max"], wm)
