@@ -63,6 +63,8 @@ typedef enum {
                                evaluations) for gsb_get_stats */
 #define GSB_FLAG_TIMING 2u  /* record CUDA events around every kernel class on the render
                                stream for gsb_get_timings */
+#define GSB_FLAG_SCORES 4u  /* also accumulate the pruning scores of reading R30 into the
+                               scene (gsb_get_scores); not with gsb_render_static */
 
 /* reserve flags */
 #define GSB_RESERVE_HOST_IO 1u /* also reserve device staging for gsb_render_host */
@@ -190,6 +192,25 @@ typedef struct {
   int64_t max_list;    /* longest tile list of the render */
 } gsb_timings;
 gsb_status gsb_get_timings(gsb_scene scene, gsb_timings* out);
+
+/* Renderer-driven pruning scores (§8(f) row 3; "efficient pruning strategy",
+ * after the rendering-importance scores of its citations; reading R30 in DESIGN.md).  Every
+ * render made with GSB_FLAG_SCORES adds, for each Gaussian, the blend weights w = alpha T it
+ * received (step 7 of the oracle; terminating and skipped entries receive none) over all pixels
+ * of all its frames: sum and max.  fp32; the sum's order of addition is not fixed (atomics), the
+ * max is exact.  Accumulators live in the scene (8 B per Gaussian, zero at creation).
+ * gsb_scores_reset zeroes them (enqueued on stream).  gsb_get_scores copies them, by creation
+ * index, into DEVICE arrays w_sum [N] / w_max [N] (either may be NULL), enqueued on stream. */
+gsb_status gsb_scores_reset(gsb_scene scene, gsb_stream stream);
+gsb_status gsb_get_scores(gsb_scene scene, float* w_sum, float* w_max, gsb_stream stream);
+
+/* filter_template semantics: a new scene, on the same device, holding the
+ * Gaussians with keep[id] != 0 (keep: HOST uint8 [N], by creation index) in creation order,
+ * re-indexed 0..M-1 (ids, and so the R10 tie-break, follow the original order); bodies and all
+ * parameters are preserved.  Rendering the result equals rendering a scene created from the
+ * kept Gaussians directly.  The new scene is unreserved and has no pre-binning or scores.
+ * Synchronous.  Errors: INVALID_ARGUMENT, OUT_OF_MEMORY, CUDA. */
+gsb_status gsb_filter_scene(gsb_scene scene, const uint8_t* keep, gsb_scene* out);
 
 gsb_status gsb_destroy_scene(gsb_scene scene);
 

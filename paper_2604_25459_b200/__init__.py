@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libgsb.so")
 
 GSB_FLAG_STATS = 1
 GSB_FLAG_TIMING = 2
+GSB_FLAG_SCORES = 4
 GSB_RESERVE_HOST_IO = 1
 
 STATUS = {0: "GSB_OK", 1: "GSB_ERR_INVALID_ARGUMENT", 2: "GSB_ERR_SHAPE_MISMATCH",
@@ -27,7 +28,8 @@ STATUS = {0: "GSB_OK", 1: "GSB_ERR_INVALID_ARGUMENT", 2: "GSB_ERR_SHAPE_MISMATCH
 
 # every symbol include/gsb.h declares
 EXPORTS = ["gsb_create_scene", "gsb_reserve", "gsb_render", "gsb_render_rig", "gsb_render_host",
-           "gsb_prebin_static", "gsb_render_static", "gsb_get_stats",
+           "gsb_prebin_static", "gsb_render_static",
+           "gsb_scores_reset", "gsb_get_scores", "gsb_filter_scene", "gsb_get_stats",
            "gsb_get_timings", "gsb_destroy_scene", "gsb_last_error", "gsb_version",
            "gsb_debug_project", "gsb_debug_bin_sort"]
 
@@ -71,6 +73,9 @@ def lib() -> ctypes.CDLL:
     L.gsb_render_rig.argtypes = [P, P, I64, I64, I32, I32, P, P, P, rp, P, P, P, P, P]
     L.gsb_prebin_static.argtypes = [P, I32, P, P, rp, P]
     L.gsb_render_static.argtypes = [P, P, I32, rp, P, P, P, P, P]
+    L.gsb_scores_reset.argtypes = [P, P]
+    L.gsb_get_scores.argtypes = [P, P, P, P]
+    L.gsb_filter_scene.argtypes = [P, P, ctypes.POINTER(P)]
     L.gsb_get_stats.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]
     L.gsb_get_timings.argtypes = [P, ctypes.POINTER(gsb_timings)]
     L.gsb_destroy_scene.argtypes = [P]
@@ -139,6 +144,7 @@ class RenderParams:
     sh_degree: int = -1
     stats: bool = False
     timing: bool = False
+    scores: bool = False   # accumulate the reading-R30 pruning scores into the scene
 
     def to_c(self) -> gsb_render_params:
         p = gsb_render_params()
@@ -146,8 +152,21 @@ class RenderParams:
         for k in range(3):
             p.background[k] = float(self.background[k])
         p.sh_degree = self.sh_degree
-        p.flags = (GSB_FLAG_STATS if self.stats else 0) | (GSB_FLAG_TIMING if self.timing else 0)
+        p.flags = ((GSB_FLAG_STATS if self.stats else 0) | (GSB_FLAG_TIMING if self.timing else 0)
+                   | (GSB_FLAG_SCORES if self.scores else 0))
         return p
+
+
+def prune_mask(w_sum, keep_fraction: float) -> np.ndarray:
+    """Host-side pruning policy over reading-R30 scores: keep the ceil(keep_fraction * N)
+    Gaussians of largest w_sum (ties by lower creation index); returns bool [N] by id."""
+    w = np.asarray(w_sum.cpu() if hasattr(w_sum, "cpu") else w_sum, np.float64).reshape(-1)
+    n = w.size
+    k = int(np.ceil(keep_fraction * n))
+    order = np.lexsort((np.arange(n), -w))
+    keep = np.zeros(n, bool)
+    keep[order[:k]] = True
+    return keep
 
 
 class Scene:
@@ -170,6 +189,12 @@ class Scene:
                                   ctypes.byref(h)))
         self._h = h
         self._keep = None
+
+    @classmethod
+    def _wrap(cls, handle, n: int, n_bodies: int, sh_degree: int, device: int) -> "Scene":
+        obj = cls.__new__(cls)
+        obj._h, obj.n, obj.n_bodies, obj.sh_degree, obj.device, obj._keep = handle, n, n_bodies, sh_degree, device, None
+        return obj
 
     @classmethod
     def from_synth(cls, scene, device: int = 0) -> "Scene":
@@ -244,6 +269,28 @@ class Scene:
         _check(lib().gsb_render_static(self._h, _ptr(poses) if self.n_bodies else None, B, ctypes.byref(p),
                                        _ptr(out_rgb), _ptr(out_depth), _ptr(out_alpha), _ptr(out_n_eval),
                                        _stream(stream)))
+
+    def scores_reset(self, stream=None):
+        """gsb_scores_reset: zero the pruning-score accumulators."""
+        _check(lib().gsb_scores_reset(self._h, _stream(stream)))
+
+    def scores(self, stream=None):
+        """gsb_get_scores: (w_sum, w_max) float32 CUDA tensors [N] by creation index."""
+        import torch
+        ws = torch.empty(self.n, dtype=torch.float32, device=f"cuda:{self.device}")
+        wm = torch.empty(self.n, dtype=torch.float32, device=f"cuda:{self.device}")
+        _check(lib().gsb_get_scores(self._h, _ptr(ws), _ptr(wm), _stream(stream)))
+        return ws, wm
+
+    def filter(self, keep) -> "Scene":
+        """gsb_filter_scene (filter_template semantics): a new Scene of the Gaussians with
+        keep[id] true, re-indexed in creation order."""
+        k = np.ascontiguousarray(np.asarray(keep, bool).astype(np.uint8))
+        if k.size != self.n:
+            raise ValueError("keep needs one entry per Gaussian")
+        h = ctypes.c_void_p()
+        _check(lib().gsb_filter_scene(self._h, k.ctypes.data, ctypes.byref(h)))
+        return Scene._wrap(h, int(k.sum()), self.n_bodies, self.sh_degree, self.device)
 
     def stats(self):
         V, K, P = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()

@@ -90,6 +90,8 @@ struct gsb_scene_t {
   float4 *d_mean = nullptr, *d_L0 = nullptr, *d_L1 = nullptr, *d_L2 = nullptr, *d_sh = nullptr;
   int2* d_ids = nullptr;  // internal (Morton) index -> (creation index = id of reading R10, body)
   int* d_inv = nullptr;   // id -> internal index
+  float* d_wsum = nullptr;     // pruning scores (reading R30), by internal index
+  uint32_t* d_wmax = nullptr;  // float bits
   // reservation
   bool reserved = false;
   int max_frames = 0, res_w = 0, res_h = 0, chunk = 0;
@@ -306,6 +308,10 @@ struct Pipeline {
     c.bg0 = p->background[0]; c.bg1 = p->background[1]; c.bg2 = p->background[2];
     c.out_rgb = out_rgb; c.out_depth = out_depth; c.out_alpha = out_alpha; c.out_n_eval = out_neval;
     c.stat_pairs = (p->flags & GSB_FLAG_STATS) ? s->d_pairs : nullptr;
+    if (p->flags & GSB_FLAG_SCORES) {
+      c.score_sum = s->d_wsum;
+      c.score_max = s->d_wmax;
+    }
     tm.begin(KC_COMPOSITE);
     // many lists beyond the small fused-sort capacity (e.g. 128x128 views): larger variant
     launch_k4_composite(c, (uint64_t)n_long * 4 > (uint64_t)(fe - fs) * n_tiles, st);
@@ -561,6 +567,10 @@ gsb_status gsb_create_scene(const float* means, const float* scales, const float
   if (e == cudaSuccess && n > 0) e = cudaMemcpy(s->d_ids, hids.data(), sizeof(int2) * n, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = dalloc(&s->d_inv, (size_t)n);
   if (e == cudaSuccess && n > 0) e = cudaMemcpy(s->d_inv, hinv.data(), sizeof(int) * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = dalloc(&s->d_wsum, (size_t)n);
+  if (e == cudaSuccess) e = dalloc(&s->d_wmax, (size_t)n);
+  if (e == cudaSuccess && n > 0) e = cudaMemset(s->d_wsum, 0, sizeof(float) * n);
+  if (e == cudaSuccess && n > 0) e = cudaMemset(s->d_wmax, 0, sizeof(uint32_t) * n);
   if (e != cudaSuccess) {
     gsb_destroy_scene(s);
     return fail(e == cudaErrorMemoryAllocation ? GSB_ERR_OUT_OF_MEMORY : GSB_ERR_CUDA, "upload: %s", cudaGetErrorString(e));
@@ -833,6 +843,7 @@ gsb_status gsb_render_static(gsb_scene s, const float* poses, int32_t n_envs, co
       D != s->sb_D)
     return fail(GSB_ERR_SHAPE_MISMATCH, "params differ from gsb_prebin_static's (image, near/far, sh_degree)");
   if (!s->qpos) return fail(GSB_ERR_INVALID_ARGUMENT, "gsb_reserve was not called after gsb_prebin_static");
+  if (p->flags & GSB_FLAG_SCORES) return fail(GSB_ERR_INVALID_ARGUMENT, "GSB_FLAG_SCORES is not supported by gsb_render_static");
   DeviceGuard g(s->device);
   s->dl_rgb = nullptr; s->dl_depth = nullptr; s->dl_alpha = nullptr; s->dl_neval = nullptr;
   K0Rig rig = default_rig(s, poses, s->sb_intr, s->sb_w2c);
@@ -872,6 +883,91 @@ gsb_status gsb_get_timings(gsb_scene s, gsb_timings* out) {
   return GSB_OK;
 }
 
+gsb_status gsb_scores_reset(gsb_scene s, gsb_stream stream) {
+  if (!s) return fail(GSB_ERR_INVALID_ARGUMENT, "scene is NULL");
+  DeviceGuard g(s->device);
+  if (s->n > 0) {
+    CUDA_TRY(cudaMemsetAsync(s->d_wsum, 0, sizeof(float) * s->n, (cudaStream_t)stream));
+    CUDA_TRY(cudaMemsetAsync(s->d_wmax, 0, sizeof(uint32_t) * s->n, (cudaStream_t)stream));
+  }
+  return GSB_OK;
+}
+
+gsb_status gsb_get_scores(gsb_scene s, float* w_sum, float* w_max, gsb_stream stream) {
+  if (!s) return fail(GSB_ERR_INVALID_ARGUMENT, "scene is NULL");
+  DeviceGuard g(s->device);
+  launch_k4_scores_export(s->d_wsum, s->d_wmax, s->d_ids, s->n, w_sum, w_max, (cudaStream_t)stream);
+  LAUNCH_CHECK();
+  return GSB_OK;
+}
+
+gsb_status gsb_filter_scene(gsb_scene s, const uint8_t* keep, gsb_scene* out) {
+  if (!out) return fail(GSB_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (!s) return fail(GSB_ERR_INVALID_ARGUMENT, "scene is NULL");
+  if (s->n > 0 && !keep) return fail(GSB_ERR_INVALID_ARGUMENT, "keep is NULL");
+  DeviceGuard g(s->device);
+  const int64_t n = s->n;
+  const int np = s->sh_planes;
+  std::vector<float4> hm(n), h0(n), h1(n), h2(n), hs((size_t)np * n);
+  std::vector<int2> hids(n);
+  if (n > 0) {
+    CUDA_TRY(cudaMemcpy(hm.data(), s->d_mean, sizeof(float4) * n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(h0.data(), s->d_L0, sizeof(float4) * n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(h1.data(), s->d_L1, sizeof(float4) * n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(h2.data(), s->d_L2, sizeof(float4) * n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(hs.data(), s->d_sh, sizeof(float4) * np * n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(hids.data(), s->d_ids, sizeof(int2) * n, cudaMemcpyDeviceToHost));
+  }
+  // new id = rank of the old id among the kept ones (creation order preserved)
+  std::vector<int> newid(n, -1);
+  int64_t m = 0;
+  for (int64_t i = 0; i < n; ++i)
+    if (keep[i]) newid[i] = (int)m++;
+  // kept Gaussians in the parent's internal order (still grouped by body, background first)
+  std::vector<float4> km, k0, k1, k2, ks((size_t)np * m);
+  std::vector<int2> kids;
+  std::vector<int> kinv(m);
+  km.reserve(m); k0.reserve(m); k1.reserve(m); k2.reserve(m); kids.reserve(m);
+  int64_t nbg = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    const int id = hids[j].x;
+    if (!keep[id]) continue;
+    const int64_t jj = (int64_t)km.size();
+    km.push_back(hm[j]); k0.push_back(h0[j]); k1.push_back(h1[j]); k2.push_back(h2[j]);
+    for (int pl = 0; pl < np; ++pl) ks[(size_t)pl * m + jj] = hs[(size_t)pl * n + j];
+    kids.push_back(make_int2(newid[id], hids[j].y));
+    kinv[newid[id]] = (int)jj;
+    nbg += hids[j].y < 0;
+  }
+  gsb_scene_t* t = new gsb_scene_t();
+  t->device = s->device; t->n = m; t->n_bg = nbg; t->n_bodies = s->n_bodies; t->sh_degree = s->sh_degree;
+  t->sh_planes = np;
+  auto up = [&](auto** d, const auto& h) -> cudaError_t {
+    cudaError_t e = dalloc(d, h.size());
+    if (e != cudaSuccess || h.empty()) return e;
+    return cudaMemcpy(*d, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice);
+  };
+  cudaError_t e = up(&t->d_mean, km);
+  if (e == cudaSuccess) e = up(&t->d_L0, k0);
+  if (e == cudaSuccess) e = up(&t->d_L1, k1);
+  if (e == cudaSuccess) e = up(&t->d_L2, k2);
+  if (e == cudaSuccess) e = up(&t->d_sh, ks);
+  if (e == cudaSuccess) e = up(&t->d_ids, kids);
+  if (e == cudaSuccess) e = up(&t->d_inv, kinv);
+  if (e == cudaSuccess) e = dalloc(&t->d_wsum, (size_t)m);
+  if (e == cudaSuccess) e = dalloc(&t->d_wmax, (size_t)m);
+  if (e == cudaSuccess && m > 0) e = cudaMemset(t->d_wsum, 0, sizeof(float) * m);
+  if (e == cudaSuccess && m > 0) e = cudaMemset(t->d_wmax, 0, sizeof(uint32_t) * m);
+  if (e != cudaSuccess) {
+    gsb_destroy_scene(t);
+    return fail(e == cudaErrorMemoryAllocation ? GSB_ERR_OUT_OF_MEMORY : GSB_ERR_CUDA, "filter upload: %s",
+                cudaGetErrorString(e));
+  }
+  *out = t;
+  return GSB_OK;
+}
+
 gsb_status gsb_destroy_scene(gsb_scene s) {
   if (!s) return GSB_OK;
   DeviceGuard g(s->device);
@@ -881,6 +977,8 @@ gsb_status gsb_destroy_scene(gsb_scene s) {
   cudaFree(s->d_mean); cudaFree(s->d_L0); cudaFree(s->d_L1); cudaFree(s->d_L2); cudaFree(s->d_sh);
   cudaFree(s->d_ids);
   cudaFree(s->d_inv);
+  cudaFree(s->d_wsum);
+  cudaFree(s->d_wmax);
   delete s;
   return GSB_OK;
 }

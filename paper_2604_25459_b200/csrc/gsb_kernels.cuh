@@ -89,6 +89,8 @@ struct CompositeArgs {
   float* out_alpha;
   int32_t* out_n_eval;
   unsigned long long* stat_pairs;  // nullptr unless STATS
+  float* score_sum;         // [N] by internal index, nullptr unless GSB_FLAG_SCORES (reading R30)
+  uint32_t* score_max;      // [N] float bits of the max weight
 };
 
 constexpr int kMaxRigCams = 16;  // cameras per env that can be body-attached (gsb_render_rig)
@@ -132,5 +134,7 @@ void launch_k3_prebin_gather(const uint32_t* sorted, const uint64_t* frame_base,
                              cudaStream_t s);
 // long_lists: use the variant with a 4x larger shared-memory sort (fewer CTAs per SM)
 void launch_k4_composite(const CompositeArgs& a, bool long_lists, cudaStream_t s);
+void launch_k4_scores_export(const float* wsum, const uint32_t* wmax, const int2* ids, int64_t n, float* out_sum,
+                             float* out_max, cudaStream_t s);
 
 }  // namespace gsb

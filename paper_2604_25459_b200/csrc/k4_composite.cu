@@ -34,7 +34,7 @@ constexpr int kBatch = kCompThreads;       // records staged per round (one cp.a
 // mostly long): the keys stay in L2 and a packed 32-bit sort runs on 8 B per key; the result
 // buffer then holds the staging and the other buffer the slot list.
 constexpr int kStageQuads = 2 * 3 * kBatch;
-template <int CAP, bool MERGE = false>
+template <int CAP, bool MERGE = false, bool SCORE = false>
 struct K4Shared {
   static constexpr bool kPacked = CAP > kFusedSortCap;
   SortShared<kCompThreads> sort;
@@ -49,6 +49,8 @@ struct K4Shared {
   unsigned long long red[kCompThreads / 32];
   uint8_t wlist[kCompThreads / 32][kBatch];   // per-warp compacted record indices of a round
   uint32_t qpos[MERGE ? CAP : 1];             // merge variant: merged position of robot entry j
+  float ssum[SCORE ? 2 : 1][SCORE ? kBatch : 1];     // score variant: per-round sum of w per record
+  uint32_t smax[SCORE ? 2 : 1][SCORE ? kBatch : 1];  // and max of w (float bits, w >= 0)
 };
 static_assert(sizeof(uint32_t) * kFusedSortCap + 16 * kStageQuads <= 2 * 8 * kFusedSortCap, "small union");
 static_assert(4 * 4 * kFusedSortCap >= 16 * kStageQuads, "large variant stages in the result buffer");
@@ -72,9 +74,10 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // centre moved to kFar: every later quadratic form is huge and every later entry fails the
 // alpha test, without a per-pixel "done" test in the hot loop.
 constexpr float kFar = 1e20f;
+constexpr float kScoreFix = 67108864.f;  // 2^26: warp-level fixed point of the score sums
 
-__device__ __forceinline__ void blend(bool use, float arg, const float4& r2, float& T, float& cr, float& cg,
-                                      float& cb, float& dep, float& pyc, int& n_eval, int idx) {
+__device__ __forceinline__ float blend(bool use, float arg, const float4& r2, float& T, float& cr, float& cg,
+                                       float& cb, float& dep, float& pyc, int& n_eval, int idx) {
   const float alpha = use ? fminf(kAlphaMax, ex2_approx(arg)) : 0.f;
   const float w = alpha * T;
   const float tT = T - w;                       // T (1 - alpha)
@@ -84,10 +87,11 @@ __device__ __forceinline__ void blend(bool use, float arg, const float4& r2, flo
     cb = fmaf(w, r2.z, cb);
     dep = fmaf(w, r2.w, dep);
     T = tT;
-  } else {                                      // stop before blending (R13)
-    n_eval = idx + 1;
-    pyc = kFar;
+    return w;                                   // blended weight (reading R30 scores)
   }
+  n_eval = idx + 1;                             // stop before blending (R13)
+  pyc = kFar;
+  return 0.f;
 }
 
 // first index in sorted k[0..n) whose value is >= x
@@ -109,10 +113,14 @@ __device__ __forceinline__ int lower_bound(P k, int n, T x) {
 // to merged position qpos[j] = j + #(background keys below it) (binary search in the L2-
 // resident background keys); a merged position d is robot entry k = lower_bound(qpos, d) if
 // qpos[k] == d, else background entry d - k.
-template <int CAP, int MINB, bool MERGE>
+// SCORE (GSB_FLAG_SCORES, §8(f) row 3, reading R30): every blended weight w = alpha T is also
+// accumulated per Gaussian — sum and max over the warp (REDUX), then per record of the round
+// in shared memory, then one global atomic per (CTA, record) into the scene's accumulators
+// (by internal index).
+template <int CAP, int MINB, bool MERGE, bool SCORE>
 __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  using Sh = K4Shared<CAP, MERGE>;
+  using Sh = K4Shared<CAP, MERGE, SCORE>;
   Sh& sm = *reinterpret_cast<Sh*>(smem_raw);
   const unsigned FULL = 0xffffffffu;
   const int fl = a.fs + blockIdx.x / a.n_tiles;
@@ -200,6 +208,10 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
       for (int e = tid; e < len; e += kCompThreads) qg[e] = (uint32_t)(e + lower_bound(bkeys, lb, r[e]));
       qpos = qg;
     }
+  }
+  if constexpr (SCORE) {
+    sm.ssum[0][tid] = 0.f; sm.ssum[1][tid] = 0.f;
+    sm.smax[0][tid] = 0u; sm.smax[1][tid] = 0u;
   }
   __syncthreads();  // the slot list is complete (and the sort buffers are free)
 
@@ -290,10 +302,22 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
           const float arg1 = fmaf(-tb, tb, mm);
           const bool use0 = arg0 >= kLog2AlphaMin;   // alpha >= 1/255
           const bool use1 = arg1 >= kLog2AlphaMin;
+          float wb0 = 0.f, wb1 = 0.f;
           if (use0 || use1) {
             const float4 q2 = R2[j];                                 // r, g, b, z
-            blend(use0, arg0, q2, T0, r0c, g0c, b0c, d0, pyc0, ne0, base + j);
-            blend(use1, arg1, q2, T1, r1c, g1c, b1c, d1, pyc1, ne1, base + j);
+            wb0 = blend(use0, arg0, q2, T0, r0c, g0c, b0c, d0, pyc0, ne0, base + j);
+            wb1 = blend(use1, arg1, q2, T1, r1c, g1c, b1c, d1, pyc1, ne1, base + j);
+          }
+          if constexpr (SCORE) {
+            // warp sum in 6.26 fixed point (|error| <= 2^-27 per pixel weight; 64 pixels x 0.99
+            // < 2^6) and exact max of the float bits (w >= 0): two REDUX instructions
+            const uint32_t q = __float2uint_rn((wb0 + wb1) * kScoreFix);
+            const uint32_t tot = __reduce_add_sync(FULL, q);
+            const uint32_t mx = __reduce_max_sync(FULL, __float_as_uint(fmaxf(wb0, wb1)));
+            if (lane == 0 && tot) {
+              atomicAdd(&sm.ssum[b & 1][j], (float)tot * (1.f / kScoreFix));
+              atomicMax(&sm.smax[b & 1][j], mx);
+            }
           }
         }
         if (__all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) break;  // whole warp finished
@@ -302,7 +326,18 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
     }
     cp_async_wait_all();
     // round b+1 visible to every warp, round b's buffer free; stop when every pixel is done
-    if (__syncthreads_count(pyc0 == kFar && pyc1 == kFar) == kCompThreads) break;
+    const int n_done = __syncthreads_count(pyc0 == kFar && pyc1 == kFar);
+    if constexpr (SCORE) {  // flush round b's per-record scores (thread tid owns record tid)
+      const float ws = sm.ssum[b & 1][tid];
+      if (ws > 0.f) {
+        const uint32_t g = slots[base + tid] + (uint32_t)a.slot_base;
+        atomicAdd(a.score_sum + g, ws);
+        atomicMax(a.score_max + g, sm.smax[b & 1][tid]);
+      }
+      sm.ssum[b & 1][tid] = 0.f;
+      sm.smax[b & 1][tid] = 0u;
+    }
+    if (n_done == kCompThreads) break;
   }
   cp_async_wait_all();
 
@@ -336,24 +371,48 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
   }
 }
 
-template <int CAP, int MINB, bool MERGE>
+template <int CAP, int MINB, bool MERGE, bool SCORE>
 static void launch_k4_variant(const CompositeArgs& a, unsigned grid, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k4_composite<CAP, MINB, MERGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(K4Shared<CAP, MERGE>));
+    cudaFuncSetAttribute(k4_composite<CAP, MINB, MERGE, SCORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(K4Shared<CAP, MERGE, SCORE>));
     attr = true;
   }
-  k4_composite<CAP, MINB, MERGE><<<grid, kCompThreads, sizeof(K4Shared<CAP, MERGE>), s>>>(a);
+  k4_composite<CAP, MINB, MERGE, SCORE><<<grid, kCompThreads, sizeof(K4Shared<CAP, MERGE, SCORE>), s>>>(a);
 }
 
 void launch_k4_composite(const CompositeArgs& a, bool long_lists, cudaStream_t s) {
   const int nf = a.fe - a.fs;
   if (nf <= 0) return;
   const unsigned grid = (unsigned)nf * a.n_tiles;
-  if (a.bg_off) launch_k4_variant<kFusedSortCap, 8, true>(a, grid, s);
-  else if (long_lists) launch_k4_variant<4 * kFusedSortCap, 5, false>(a, grid, s);
-  else launch_k4_variant<kFusedSortCap, 9, false>(a, grid, s);
+  if (a.score_sum) {
+    if (long_lists) launch_k4_variant<4 * kFusedSortCap, 5, false, true>(a, grid, s);
+    else launch_k4_variant<kFusedSortCap, 8, false, true>(a, grid, s);
+  } else if (a.bg_off) {
+    launch_k4_variant<kFusedSortCap, 8, true, false>(a, grid, s);
+  } else if (long_lists) {
+    launch_k4_variant<4 * kFusedSortCap, 5, false, false>(a, grid, s);
+  } else {
+    launch_k4_variant<kFusedSortCap, 9, false, false>(a, grid, s);
+  }
+}
+
+// gsb_get_scores: accumulators (internal order) -> creation-id order
+__global__ void k4_scores_export(const float* __restrict__ wsum, const uint32_t* __restrict__ wmax,
+                                 const int2* __restrict__ ids, int64_t n, float* __restrict__ out_sum,
+                                 float* __restrict__ out_max) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int id = ids[j].x;
+  if (out_sum) out_sum[id] = wsum[j];
+  if (out_max) out_max[id] = __uint_as_float(wmax[j]);
+}
+
+void launch_k4_scores_export(const float* wsum, const uint32_t* wmax, const int2* ids, int64_t n, float* out_sum,
+                             float* out_max, cudaStream_t s) {
+  if (n <= 0) return;
+  k4_scores_export<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(wsum, wmax, ids, n, out_sum, out_max);
 }
 
 }  // namespace gsb

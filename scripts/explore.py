@@ -30,7 +30,7 @@ torch.cuda.empty_cache()
 print(json.dumps(res), flush=True)
 
 envs = {"C2": 64, "C3": 1024, "C4": 4096, "C5": 1024, "T1": 3}
-MODES = ("rig", "static")
+MODES = ("rig", "static", "scores")
 _named = [n for n in sys.argv[1:] if n in synth.CONFIGS]
 _modes_only = bool(sys.argv[1:]) and all(a in MODES for a in sys.argv[1:])
 for name in ([] if _modes_only or ("static" in sys.argv[1:]) else (_named or ["C2", "C4", "C5", "C3"])):
@@ -149,3 +149,33 @@ if "static" in sys.argv[1:] or not sys.argv[1:]:
                           "prebin_s": round(t_prebin, 3), **res}), flush=True)
         del g, rgb, dep
         torch.cuda.empty_cache()
+
+# §8(f) row 3 measurement: C3 render with GSB_FLAG_SCORES (pruning-score accumulation) vs plain
+if "scores" in sys.argv[1:] or not sys.argv[1:]:
+    cfg = synth.CONFIGS["C3"]
+    B = 1024
+    sc = synth.make_scene(cfg)
+    g = gsb.Scene.from_synth(sc)
+    g.reserve(B, cfg.n_cams, cfg.width, cfg.height)
+    K, W = synth.make_cameras(cfg, np.arange(B))
+    K, W = torch.from_numpy(K).cuda(), torch.from_numpy(W).cuda()
+    poses = [torch.from_numpy(synth.make_poses(cfg, np.arange(B), s)).cuda() for s in range(4)]
+    rgb = torch.empty((B, cfg.n_cams, 3, cfg.height, cfg.width), device="cuda")
+    dep = torch.empty((B, cfg.n_cams, cfg.height, cfg.width), device="cuda")
+    res = {}
+    for mode in ("plain", "scores"):
+        prm = gsb.RenderParams(cfg.width, cfg.height, timing=True, scores=(mode == "scores"))
+        for s in range(2):
+            g.render(poses[s], K, W, prm, rgb, dep)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        for s in range(3):
+            g.render(poses[(s + 1) % 4], K, W, prm, rgb, dep)
+        e1.record()
+        torch.cuda.synchronize()
+        tm = g.timings()
+        res[mode] = {"fps": 3 * B / (e0.elapsed_time(e1) / 1e3), "composite_ms": round(tm["composite_ms"], 2)}
+    ws, wm = g.scores()
+    res["scored_gaussians"] = int((ws > 0).sum().item())
+    print(json.dumps({"config": "C3 with GSB_FLAG_SCORES", **res}), flush=True)

@@ -89,3 +89,11 @@ def test_host_side_validation_without_gpu():
 def test_render_params_layout_matches_header():
     assert ctypes.sizeof(gsb.gsb_render_params) == 4 * 9
     assert ctypes.sizeof(gsb.gsb_timings) == 8 * 11
+
+
+def test_prune_mask_policy():
+    """Host-side pruning policy: top ceil(f N) by score, ties broken by lower creation index."""
+    w = np.array([0.5, 0.1, 0.5, 0.0, 0.9, 0.1])
+    np.testing.assert_array_equal(gsb.prune_mask(w, 0.5), [True, False, True, False, True, False])
+    np.testing.assert_array_equal(gsb.prune_mask(w, 0.6), [True, True, True, False, True, False])
+    assert gsb.prune_mask(w, 0.0).sum() == 0 and gsb.prune_mask(w, 1.0).all()
