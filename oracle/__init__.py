@@ -9,8 +9,9 @@ Layout:
                 per-pixel brute force over all Gaussians in (z_f32 bits, id) order.
   mini.py       independent NumPy re-implementation (fp64) for small frames (pin 11).
   binning.py    integer-path oracle: fp32 tile rects (R9) and per-tile (zbits, id) lists (R10).
+  obs.py        observation epilogue of reading R31 (image DR, uint8 / fp16 encoding), numpy fp32.
 
-Each function cites the passage it follows; DESIGN.md §2 lists every reading (R1-R28).
+Each function cites the passage it follows; DESIGN.md §2 lists every reading (R1-R31).
 """
 from __future__ import annotations
 

@@ -596,3 +596,52 @@ def test_scores_two_layers_and_partition_identity():
         oracle.composite(fr.proj, fr.order, px.reshape(-1), py.reshape(-1), prm, mode="pure", scores=sp)
         np.testing.assert_array_equal(sp["w_sum"], ws)
         np.testing.assert_array_equal(sp["w_max"], wm)
+
+
+# ---------------------------------------------------------------- observation epilogue (R31)
+def test_obs_epilogue_identity_brightness_contrast_and_clamps():
+    """Reading R31 with identity DR is the textbook 8-bit encoding rint(clamp(c)*255); an
+    additive brightness of m/255 shifts codes by m; contrast pivots about 0.5; gain scales;
+    NaN / negative / >1 map to 0 / 0 / 255; depth goes to IEEE half by round-to-nearest-even."""
+    from oracle import obs
+    codes = np.arange(256)
+    c = (codes / 255.0).astype(np.float32).reshape(1, 1, 16, 16).repeat(3, 1)
+    q, _ = obs.epilogue(c, None, None)
+    np.testing.assert_array_equal(q[0, 0].reshape(-1), codes)
+    q, _ = obs.epilogue(c, None, np.float32([[1.0, 1.0, 10 / 255.0, 0.0]]))
+    np.testing.assert_array_equal(q[0, 1].reshape(-1), np.minimum(codes + 10, 255))
+    half = np.full((1, 3, 2, 2), 0.5, np.float32)
+    for k in (0.0, 0.3, 2.0, 7.5):
+        q, _ = obs.epilogue(half, None, np.float32([[1.0, k, 0.0, 0.0]]))
+        assert (q == 128).all()   # rint(127.5) = 128 (half to even)
+    q, _ = obs.epilogue(np.full((1, 3, 1, 1), 0.25, np.float32), None, np.float32([[2.0, 1.0, 0.0, 0.0]]))
+    assert (q == 128).all()
+    odd = np.float32([np.nan, -0.5, 1.5, 1.0]).reshape(1, 1, 2, 2).repeat(3, 1)
+    q, _ = obs.epilogue(odd, None, None)
+    np.testing.assert_array_equal(q[0, 0].reshape(-1), [0, 0, 255, 255])
+    _, d = obs.epilogue(np.zeros((1, 3, 1, 4), np.float32), np.float32([[[1.0, 2049.0, 3.0e-8, 65520.0]]]), None)
+    np.testing.assert_array_equal(d.view(np.uint16).reshape(-1), [0x3C00, 0x6800, 0x0001, 0x7C00])
+
+
+def test_obs_noise_is_unit_variance_irwin_hall_and_counter_based():
+    """The R31 noise: Irwin-Hall(4) of 22-bit hashed uniforms scaled by sqrt(3)/2^22 has mean 0,
+    variance 1 and support within 2 sqrt(3) (closed forms); it depends only on (seed, step,
+    global frame, pixel, channel) — so env slicing with frame offsets reproduces it — and
+    neighbouring channels/pixels are uncorrelated."""
+    from oracle import obs
+    H, W = 64, 64
+    f, ch, y, x = np.meshgrid(np.arange(64), np.arange(3), np.arange(H), np.arange(W), indexing="ij")
+    z = obs.noise_z(7, 3, f, y, x, ch, H, W).astype(np.float64) * float(obs.S3)
+    assert abs(z.mean()) < 5e-3 and abs(z.std() - 1.0) < 5e-3
+    assert np.abs(z).max() <= 2 * np.sqrt(3) + 1e-6
+    assert abs(np.corrcoef(z[:, 0].ravel(), z[:, 1].ravel())[0, 1]) < 5e-3
+    assert abs(np.corrcoef(z[..., :-1].ravel(), z[..., 1:].ravel())[0, 1]) < 5e-3
+    # slicing: frames 10..19 of a batch == frames 0..9 of a slice with offset 10
+    rgb = np.random.default_rng(0).uniform(0, 1, (20, 3, 8, 8)).astype(np.float32)
+    dr = np.tile(np.float32([1.1, 0.9, 0.02, 0.05]), (20, 1))
+    full, _ = obs.epilogue(rgb, None, dr, seed=5, step=9)
+    part, _ = obs.epilogue(rgb[10:], None, dr[10:], seed=5, step=9, frame_offset=10)
+    np.testing.assert_array_equal(full[10:], part)
+    other, _ = obs.epilogue(rgb, None, dr, seed=5, step=10)
+    assert (other != full).mean() > 0.3
+    assert float(obs.S3) == pytest.approx(np.sqrt(3) / 2 ** 22, rel=1e-7)
