@@ -149,6 +149,40 @@ gsb_status gsb_render_host(gsb_scene scene, const float* body_poses, int32_t n_e
                            const gsb_render_params* params, float* out_rgb, float* out_depth,
                            float* out_alpha, int32_t* out_n_eval, gsb_stream stream);
 
+/* Observation epilogue (§8(f) row 4; reading R31 in DESIGN.md / oracle/obs.py): the policy-
+ * facing encoding fused into K4's store — image domain randomisation ("brightness, contrast
+ * and exposure"; "image noise") and 8-bit RGB (+ fp16 depth), so a batch leaves
+ * HBM (and crosses PCIe) at 3-5 B per pixel instead of 16.  Per frame f with
+ * (gain, contrast, brightness, noise_std) = image_dr[f] and c = C + T*bg (binary32, RN):
+ *   v = ((c*gain - 0.5)*contrast + 0.5) + brightness [+ (z*sqrt(3)/2^22)*noise_std]
+ *   rgb8 = rint(clamp(v, 0, 1) * 255)            (NaN -> 0)
+ * z = Irwin-Hall(4) counter-based noise keyed by (seed, step, global frame
+ * (env_offset + e)*C + c, pixel, channel) — identical under any env slicing.  Motion blur is
+ * not part of the epilogue. */
+#define GSB_OBS_DEPTH_F16 1u  /* out_depth holds IEEE half bits (uint16), else fp32 */
+typedef struct {
+  const float* image_dr;  /* [B, C, 4] fp32 (gain, contrast, brightness, noise_std) per frame, or
+                             NULL = identity (1, 1, 0, 0); DEVICE for gsb_render_obs, HOST for
+                             gsb_render_obs_host */
+  uint32_t seed, step;    /* noise stream */
+  int64_t env_offset;     /* global index of env 0 of this call (sharded runs), >= 0 */
+  uint32_t flags;         /* GSB_OBS_* */
+} gsb_obs_params;
+
+/* gsb_render with the observation epilogue: out_rgb8 [B, C, 3, H, W] uint8 (required),
+ * out_depth [B, C, H, W] fp16 bits or fp32 per GSB_OBS_DEPTH_F16 (nullable).  DEVICE buffers.
+ * Errors as gsb_render, plus INVALID_ARGUMENT for bad obs params. */
+gsb_status gsb_render_obs(gsb_scene scene, const float* body_poses, int32_t n_envs, int32_t n_cams,
+                          const float* intrinsics, const float* world_to_cam,
+                          const gsb_render_params* params, const gsb_obs_params* obs,
+                          uint8_t* out_rgb8, void* out_depth, gsb_stream stream);
+/* The same with HOST buffers (inputs incl. image_dr read, outputs written; pinned memory
+ * recommended), downloads overlapping the next chunk, synchronous; needs GSB_RESERVE_HOST_IO. */
+gsb_status gsb_render_obs_host(gsb_scene scene, const float* body_poses, int32_t n_envs,
+                               int32_t n_cams, const float* intrinsics, const float* world_to_cam,
+                               const gsb_render_params* params, const gsb_obs_params* obs,
+                               uint8_t* out_rgb8, void* out_depth, gsb_stream stream);
+
 /* Static-camera background pre-binning (§8(f) row 2; exploits RLGK's static/dynamic split,
  * PAPER.md App. B.2: static Gaussians never move, so with cameras fixed in the world
  * their projection, binning and depth sort are the same for every env and every step).

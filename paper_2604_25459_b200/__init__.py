@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(_HERE, "libgsb.so")
 GSB_FLAG_STATS = 1
 GSB_FLAG_TIMING = 2
 GSB_FLAG_SCORES = 4
+GSB_OBS_DEPTH_F16 = 1
 GSB_RESERVE_HOST_IO = 1
 
 STATUS = {0: "GSB_OK", 1: "GSB_ERR_INVALID_ARGUMENT", 2: "GSB_ERR_SHAPE_MISMATCH",
@@ -29,7 +30,7 @@ STATUS = {0: "GSB_OK", 1: "GSB_ERR_INVALID_ARGUMENT", 2: "GSB_ERR_SHAPE_MISMATCH
 # every symbol include/gsb.h declares
 EXPORTS = ["gsb_create_scene", "gsb_reserve", "gsb_render", "gsb_render_rig", "gsb_render_host",
            "gsb_prebin_static", "gsb_render_static",
-           "gsb_scores_reset", "gsb_get_scores", "gsb_filter_scene", "gsb_get_stats",
+           "gsb_scores_reset", "gsb_get_scores", "gsb_filter_scene", "gsb_render_obs", "gsb_render_obs_host", "gsb_get_stats",
            "gsb_get_timings", "gsb_destroy_scene", "gsb_last_error", "gsb_version",
            "gsb_debug_project", "gsb_debug_bin_sort"]
 
@@ -38,6 +39,11 @@ class GsbError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{STATUS.get(status, status)}: {msg}")
         self.status = status
+
+
+class gsb_obs_params(ctypes.Structure):
+    _fields_ = [("image_dr", ctypes.c_void_p), ("seed", ctypes.c_uint32), ("step", ctypes.c_uint32),
+                ("env_offset", ctypes.c_int64), ("flags", ctypes.c_uint32)]
 
 
 class gsb_render_params(ctypes.Structure):
@@ -74,6 +80,9 @@ def lib() -> ctypes.CDLL:
     L.gsb_prebin_static.argtypes = [P, I32, P, P, rp, P]
     L.gsb_render_static.argtypes = [P, P, I32, rp, P, P, P, P, P]
     L.gsb_scores_reset.argtypes = [P, P]
+    op = ctypes.POINTER(gsb_obs_params)
+    L.gsb_render_obs.argtypes = [P, P, I32, I32, P, P, rp, op, P, P, P]
+    L.gsb_render_obs_host.argtypes = [P, P, I32, I32, P, P, rp, op, P, P, P]
     L.gsb_get_scores.argtypes = [P, P, P, P]
     L.gsb_filter_scene.argtypes = [P, P, ctypes.POINTER(P)]
     L.gsb_get_stats.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]
@@ -269,6 +278,37 @@ class Scene:
         _check(lib().gsb_render_static(self._h, _ptr(poses) if self.n_bodies else None, B, ctypes.byref(p),
                                        _ptr(out_rgb), _ptr(out_depth), _ptr(out_alpha), _ptr(out_n_eval),
                                        _stream(stream)))
+
+    @staticmethod
+    def _obs(image_dr, seed, step, env_offset, depth_f16, host):
+        o = gsb_obs_params()
+        o.image_dr = None if image_dr is None else (_hptr(image_dr) if host else _ptr(image_dr))
+        o.seed, o.step, o.env_offset = int(seed) & 0xFFFFFFFF, int(step) & 0xFFFFFFFF, int(env_offset)
+        o.flags = GSB_OBS_DEPTH_F16 if depth_f16 else 0
+        return o
+
+    def render_obs(self, poses, intrinsics, world_to_cam, params: RenderParams, out_rgb8, out_depth=None,
+                   image_dr=None, seed: int = 0, step: int = 0, env_offset: int = 0, depth_f16: bool = True,
+                   stream=None):
+        """gsb_render_obs: uint8 RGB [B,C,3,H,W] (+ depth [B,C,H,W] as float16 or float32) with the
+        reading-R31 image DR (image_dr [B,C,4] CUDA float32: gain, contrast, brightness, noise_std)."""
+        B, C = int(intrinsics.shape[0]), int(intrinsics.shape[1])
+        p = params.to_c()
+        o = self._obs(image_dr, seed, step, env_offset, depth_f16, False)
+        _check(lib().gsb_render_obs(self._h, _ptr(poses) if self.n_bodies else None, B, C, _ptr(intrinsics),
+                                    _ptr(world_to_cam), ctypes.byref(p), ctypes.byref(o), _ptr(out_rgb8),
+                                    _ptr(out_depth), _stream(stream)))
+
+    def render_obs_host(self, poses, intrinsics, world_to_cam, params: RenderParams, out_rgb8, out_depth=None,
+                        image_dr=None, seed: int = 0, step: int = 0, env_offset: int = 0, depth_f16: bool = True,
+                        stream=None):
+        """gsb_render_obs_host on host (pinned) buffers; synchronous."""
+        B, C = int(intrinsics.shape[0]), int(intrinsics.shape[1])
+        p = params.to_c()
+        o = self._obs(image_dr, seed, step, env_offset, depth_f16, True)
+        _check(lib().gsb_render_obs_host(self._h, _hptr(poses) if self.n_bodies else None, B, C,
+                                         _hptr(intrinsics), _hptr(world_to_cam), ctypes.byref(p), ctypes.byref(o),
+                                         _hptr(out_rgb8), _hptr(out_depth), _stream(stream)))
 
     def scores_reset(self, stream=None):
         """gsb_scores_reset: zero the pruning-score accumulators."""

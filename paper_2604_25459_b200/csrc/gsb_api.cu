@@ -149,6 +149,14 @@ struct gsb_scene_t {
   // host-io: where to download outputs of each pass
   float *dl_rgb = nullptr, *dl_depth = nullptr, *dl_alpha = nullptr;
   int32_t* dl_neval = nullptr;
+  uint8_t* dl_rgb8 = nullptr;
+  uint16_t* dl_depth16 = nullptr;
+  // observation epilogue of the current render (gsb_render_obs*), nullptr otherwise
+  const gsb_obs_params* obs = nullptr;
+  uint8_t* obs_rgb8 = nullptr;
+  uint16_t* obs_depth16 = nullptr;
+  const float* obs_dr = nullptr;
+  float* st_dr = nullptr;  // host-io staging of the DR parameters
 
   void free_workspace() {
     cudaFree(table); cudaFree(cams);
@@ -165,7 +173,8 @@ struct gsb_scene_t {
     cudaFree(keys); cudaFree(keys_alt); cudaFree(sorted); cudaFree(d_pairs); cudaFree(qpos);
     qpos = nullptr;
     cudaFree(st_poses); cudaFree(st_intr); cudaFree(st_w2c);
-    cudaFree(st_rgb); cudaFree(st_depth); cudaFree(st_alpha); cudaFree(st_neval);
+    cudaFree(st_rgb); cudaFree(st_depth); cudaFree(st_alpha); cudaFree(st_neval); cudaFree(st_dr);
+    st_dr = nullptr;
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (ev_copy) cudaEventDestroy(ev_copy);
     for (auto e : ev_pool) cudaEventDestroy(e);
@@ -243,7 +252,7 @@ struct Pipeline {
   gsb_scene_t* s;
   cudaStream_t st;
   const gsb_render_params* p;
-  int F, W, H, tiles_x, n_tiles, D;
+  int F, W, H, tiles_x, n_tiles, D, n_cams;
   Timer tm;
   float* out_rgb;
   float* out_depth;
@@ -312,6 +321,11 @@ struct Pipeline {
       c.score_sum = s->d_wsum;
       c.score_max = s->d_wmax;
     }
+    if (s->obs) {
+      c.obs_rgb8 = s->obs_rgb8; c.obs_depth16 = s->obs_depth16; c.obs_dr = s->obs_dr;
+      c.obs_seed = s->obs->seed; c.obs_step = s->obs->step;
+      c.obs_frame_offset = s->obs->env_offset * (int64_t)n_cams;
+    }
     tm.begin(KC_COMPOSITE);
     // many lists beyond the small fused-sort capacity (e.g. 128x128 views): larger variant
     launch_k4_composite(c, (uint64_t)n_long * 4 > (uint64_t)(fe - fs) * n_tiles, st);
@@ -319,7 +333,20 @@ struct Pipeline {
     s->comp_launches++;
     LAUNCH_CHECK();
     tm.end();
-    if (s->dl_rgb) {  // host-io: download this pass's frames on the copy stream
+    if (s->dl_rgb8) {  // host-io observations: uint8 RGB (+ fp16 or fp32 depth)
+      CUDA_TRY(cudaEventRecord(s->ev_copy, st));
+      CUDA_TRY(cudaStreamWaitEvent(s->copy_stream, s->ev_copy, 0));
+      const size_t plane = (size_t)W * H;
+      const size_t a0 = (size_t)(f0 + fs), cnt = (size_t)(fe - fs);
+      CUDA_TRY(cudaMemcpyAsync(s->dl_rgb8 + a0 * 3 * plane, s->obs_rgb8 + a0 * 3 * plane, cnt * 3 * plane,
+                               cudaMemcpyDeviceToHost, s->copy_stream));
+      if (s->dl_depth16)
+        CUDA_TRY(cudaMemcpyAsync(s->dl_depth16 + a0 * plane, s->obs_depth16 + a0 * plane, cnt * plane * 2,
+                                 cudaMemcpyDeviceToHost, s->copy_stream));
+      if (s->dl_depth)
+        CUDA_TRY(cudaMemcpyAsync(s->dl_depth + a0 * plane, out_depth + a0 * plane, cnt * plane * 4,
+                                 cudaMemcpyDeviceToHost, s->copy_stream));
+    } else if (s->dl_rgb) {  // host-io: download this pass's frames on the copy stream
       CUDA_TRY(cudaEventRecord(s->ev_copy, st));
       CUDA_TRY(cudaStreamWaitEvent(s->copy_stream, s->ev_copy, 0));
       const size_t plane = (size_t)W * H;
@@ -432,6 +459,7 @@ gsb_status render_impl(gsb_scene s, const K0Rig& rig, int n_envs, int n_cams, co
   pl.tm = Timer{s, st, timing};
   pl.out_rgb = out_rgb; pl.out_depth = out_depth; pl.out_alpha = out_alpha; pl.out_neval = out_neval;
   pl.merge = merge;
+  pl.n_cams = n_cams;
   pl.first = merge ? s->n_bg : 0;      // static cameras: only the robot Gaussians per frame
   pl.count = s->n - pl.first;
   gsb_status r = pl.run(rig, n_cams);
@@ -637,6 +665,7 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
     CUDA_TRY(dalloc(&s->st_depth, (size_t)F * plane));
     CUDA_TRY(dalloc(&s->st_alpha, (size_t)F * plane));
     CUDA_TRY(dalloc(&s->st_neval, (size_t)F * plane));
+    CUDA_TRY(dalloc(&s->st_dr, (size_t)F * 4));
     CUDA_TRY(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&s->ev_copy, cudaEventDisableTiming));
   }
@@ -850,6 +879,77 @@ gsb_status gsb_render_static(gsb_scene s, const float* poses, int32_t n_envs, co
   rig.cams_shared = 1;
   return render_impl(s, rig, n_envs, s->sb_cams, p, out_rgb, out_depth, out_alpha, out_neval, (cudaStream_t)stream,
                      true);
+}
+
+namespace {
+struct ObsScope {  // the observation epilogue of one render call; cleared on exit
+  gsb_scene s;
+  ObsScope(gsb_scene s_, const gsb_obs_params* o, uint8_t* rgb8, uint16_t* d16, const float* dr) : s(s_) {
+    s->obs = o; s->obs_rgb8 = rgb8; s->obs_depth16 = d16; s->obs_dr = dr;
+  }
+  ~ObsScope() {
+    s->obs = nullptr; s->obs_rgb8 = nullptr; s->obs_depth16 = nullptr; s->obs_dr = nullptr;
+    s->dl_rgb = nullptr; s->dl_depth = nullptr; s->dl_alpha = nullptr; s->dl_neval = nullptr;
+    s->dl_rgb8 = nullptr; s->dl_depth16 = nullptr;
+  }
+};
+
+gsb_status validate_obs(const gsb_obs_params* o, const void* out_rgb8) {
+  if (!o) return fail(GSB_ERR_INVALID_ARGUMENT, "obs params are NULL");
+  if (!out_rgb8) return fail(GSB_ERR_INVALID_ARGUMENT, "out_rgb8 is NULL");
+  if (o->env_offset < 0) return fail(GSB_ERR_INVALID_ARGUMENT, "negative env_offset");
+  if (o->flags & ~GSB_OBS_DEPTH_F16) return fail(GSB_ERR_INVALID_ARGUMENT, "unknown obs flags 0x%x", o->flags);
+  return GSB_OK;
+}
+}  // namespace
+
+gsb_status gsb_render_obs(gsb_scene s, const float* poses, int32_t n_envs, int32_t n_cams, const float* intr,
+                          const float* w2c, const gsb_render_params* p, const gsb_obs_params* obs,
+                          uint8_t* out_rgb8, void* out_depth, gsb_stream stream) {
+  gsb_status r = validate_render(s, poses, n_envs, n_cams, intr, w2c, p, (const float*)out_rgb8);
+  if (r != GSB_OK) return r;
+  r = validate_obs(obs, out_rgb8);
+  if (r != GSB_OK) return r;
+  DeviceGuard g(s->device);
+  const bool f16 = (obs->flags & GSB_OBS_DEPTH_F16) != 0;
+  ObsScope os(s, obs, out_rgb8, f16 ? (uint16_t*)out_depth : nullptr, obs->image_dr);
+  return render_impl(s, default_rig(s, poses, intr, w2c), n_envs, n_cams, p, nullptr,
+                     f16 ? nullptr : (float*)out_depth, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+gsb_status gsb_render_obs_host(gsb_scene s, const float* poses, int32_t n_envs, int32_t n_cams, const float* intr,
+                               const float* w2c, const gsb_render_params* p, const gsb_obs_params* obs,
+                               uint8_t* out_rgb8, void* out_depth, gsb_stream stream) {
+  gsb_status r = validate_render(s, poses, n_envs, n_cams, intr, w2c, p, (const float*)out_rgb8);
+  if (r != GSB_OK) return r;
+  r = validate_obs(obs, out_rgb8);
+  if (r != GSB_OK) return r;
+  if (!s->host_io) return fail(GSB_ERR_INVALID_ARGUMENT, "reserve with GSB_RESERVE_HOST_IO for gsb_render_obs_host");
+  if (n_envs > s->max_envs) return fail(GSB_ERR_SHAPE_MISMATCH, "n_envs beyond the host-io reservation");
+  DeviceGuard g(s->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t F = (size_t)n_envs * n_cams;
+  if (s->n_bodies > 0 && n_envs > 0)
+    CUDA_TRY(cudaMemcpyAsync(s->st_poses, poses, sizeof(float) * (size_t)n_envs * s->n_bodies * 7, cudaMemcpyHostToDevice, st));
+  if (F > 0) {
+    CUDA_TRY(cudaMemcpyAsync(s->st_intr, intr, sizeof(float) * F * 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(s->st_w2c, w2c, sizeof(float) * F * 12, cudaMemcpyHostToDevice, st));
+    if (obs->image_dr) CUDA_TRY(cudaMemcpyAsync(s->st_dr, obs->image_dr, sizeof(float) * F * 4, cudaMemcpyHostToDevice, st));
+  }
+  const bool f16 = (obs->flags & GSB_OBS_DEPTH_F16) != 0;
+  // staging: uint8 RGB in st_rgb, fp16 depth in st_depth (both smaller than their fp32 sizes)
+  ObsScope os(s, obs, (uint8_t*)s->st_rgb, f16 ? (uint16_t*)s->st_depth : nullptr, obs->image_dr ? s->st_dr : nullptr);
+  s->dl_rgb8 = out_rgb8;
+  if (out_depth) {
+    if (f16) s->dl_depth16 = (uint16_t*)out_depth;
+    else s->dl_depth = (float*)out_depth;
+  }
+  r = render_impl(s, default_rig(s, s->st_poses, s->st_intr, s->st_w2c), n_envs, n_cams, p, nullptr,
+                  (out_depth && !f16) ? s->st_depth : nullptr, nullptr, nullptr, st);
+  if (r != GSB_OK) return r;
+  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaStreamSynchronize(s->copy_stream));
+  return GSB_OK;
 }
 
 gsb_status gsb_get_stats(gsb_scene s, int64_t* V, int64_t* K, int64_t* P) {

@@ -91,6 +91,12 @@ struct CompositeArgs {
   unsigned long long* stat_pairs;  // nullptr unless STATS
   float* score_sum;         // [N] by internal index, nullptr unless GSB_FLAG_SCORES (reading R30)
   uint32_t* score_max;      // [N] float bits of the max weight
+  // observation epilogue (gsb_render_obs, §8(f) row 4, reading R31); obs_rgb8 == nullptr: fp32 outputs
+  uint8_t* obs_rgb8;        // [F][3][H][W]
+  uint16_t* obs_depth16;    // [F][H][W] IEEE half bits, or nullptr (then out_depth fp32, if set)
+  const float* obs_dr;      // [F][4] (gain, contrast, brightness, noise_std) per frame, or nullptr
+  uint32_t obs_seed, obs_step;
+  int64_t obs_frame_offset; // global index of this call's frame 0 (noise streams)
 };
 
 constexpr int kMaxRigCams = 16;  // cameras per env that can be body-attached (gsb_render_rig)

@@ -30,7 +30,7 @@ torch.cuda.empty_cache()
 print(json.dumps(res), flush=True)
 
 envs = {"C2": 64, "C3": 1024, "C4": 4096, "C5": 1024, "T1": 3}
-MODES = ("rig", "static", "scores")
+MODES = ("rig", "static", "scores", "obs")
 _named = [n for n in sys.argv[1:] if n in synth.CONFIGS]
 _modes_only = bool(sys.argv[1:]) and all(a in MODES for a in sys.argv[1:])
 for name in ([] if _modes_only or ("static" in sys.argv[1:]) else (_named or ["C2", "C4", "C5", "C3"])):
@@ -179,3 +179,52 @@ if "scores" in sys.argv[1:] or not sys.argv[1:]:
     ws, wm = g.scores()
     res["scored_gaussians"] = int((ws > 0).sum().item())
     print(json.dumps({"config": "C3 with GSB_FLAG_SCORES", **res}), flush=True)
+
+# §8(f) row 4 measurement: C3 observations (uint8 RGB + fp16 depth, image DR with noise), device
+# and host (e2e: pinned host inputs/outputs) vs the fp32 outputs
+if "obs" in sys.argv[1:] or not sys.argv[1:]:
+    cfg = synth.CONFIGS["C3"]
+    B = 1024
+    sc = synth.make_scene(cfg)
+    g = gsb.Scene.from_synth(sc)
+    g.reserve(B, cfg.n_cams, cfg.width, cfg.height, host_io=True)
+    K, W = synth.make_cameras(cfg, np.arange(B))
+    Kd, Wd = torch.from_numpy(K).cuda(), torch.from_numpy(W).cuda()
+    P = [synth.make_poses(cfg, np.arange(B), s) for s in range(4)]
+    Pd = [torch.from_numpy(p).cuda() for p in P]
+    rng = np.random.default_rng(0)
+    dr = np.stack([rng.uniform(0.7, 1.4, (B, 1)), rng.uniform(0.7, 1.3, (B, 1)), rng.uniform(-0.05, 0.05, (B, 1)),
+                   np.full((B, 1), 0.02)], -1).astype(np.float32)
+    drd = torch.from_numpy(dr).cuda()
+    H_, W_ = cfg.height, cfg.width
+    q = torch.empty((B, 1, 3, H_, W_), dtype=torch.uint8, device="cuda")
+    d16 = torch.empty((B, 1, H_, W_), dtype=torch.float16, device="cuda")
+    hq = torch.empty((B, 1, 3, H_, W_), dtype=torch.uint8).pin_memory()
+    hd = torch.empty((B, 1, H_, W_), dtype=torch.float16).pin_memory()
+    hP = [torch.from_numpy(p).pin_memory() for p in P]
+    hK, hW, hdr = torch.from_numpy(K).pin_memory(), torch.from_numpy(W).pin_memory(), torch.from_numpy(dr).pin_memory()
+    prm = gsb.RenderParams(W_, H_, timing=True)
+    res = {}
+
+    def dev(s):
+        g.render_obs(Pd[s], Kd, Wd, prm, q, d16, image_dr=drd, seed=1, step=s)
+
+    def host(s):
+        g.render_obs_host(hP[s], hK, hW, prm, hq, hd, image_dr=hdr, seed=1, step=s)
+
+    for mode, fn in (("device", dev), ("host_e2e", host)):
+        for s in range(2):
+            fn(s)
+        torch.cuda.synchronize()
+        t0 = time.time()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        for s in range(3):
+            fn((s + 1) % 4)
+        e1.record()
+        torch.cuda.synchronize()
+        wall = time.time() - t0
+        res[mode] = {"fps": 3 * B / (e0.elapsed_time(e1) / 1e3), "wall_fps": 3 * B / wall,
+                     "composite_ms": round(g.timings()["composite_ms"], 2)}
+    res["d2h_bytes_per_step"] = int(hq.numel() + 2 * hd.numel())
+    print(json.dumps({"config": "C3 observations (uint8 RGB + fp16 depth, image DR)", **res}), flush=True)

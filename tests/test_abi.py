@@ -86,9 +86,26 @@ def test_host_side_validation_without_gpu():
     assert L.gsb_debug_bin_sort(None, None, None, None, None, None, None, 0, 0, 8, 8, None, None, 0, None, None) == 1
 
 
-def test_render_params_layout_matches_header():
-    assert ctypes.sizeof(gsb.gsb_render_params) == 4 * 9
-    assert ctypes.sizeof(gsb.gsb_timings) == 8 * 11
+def test_render_params_layout_matches_header(tmp_path):
+    """ctypes structs == the C compiler's layout of include/gsb.h (sizes and every offset)."""
+    import subprocess
+    structs = {"gsb_render_params": gsb.gsb_render_params, "gsb_timings": gsb.gsb_timings,
+               "gsb_obs_params": gsb.gsb_obs_params}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "gsb.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'printf("{name} %zu\\n", sizeof({name}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'printf("{name}.{fname} %zu\\n", offsetof({name}, {fname}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    got = dict(l.split() for l in subprocess.check_output([str(exe)]).decode().splitlines())
+    for name, cls in structs.items():
+        assert int(got[name]) == ctypes.sizeof(cls), name
+        for fname, _ in cls._fields_:
+            assert int(got[f"{name}.{fname}"]) == getattr(cls, fname).offset, (name, fname)
 
 
 def test_prune_mask_policy():
