@@ -29,7 +29,7 @@ del h, d
 torch.cuda.empty_cache()
 print(json.dumps(res), flush=True)
 
-envs = {"C2": 64, "C3": 1024, "C4": 4096, "C5": 1024, "T1": 3}
+envs = {"C2": 64, "C3": 1024, "C4": 4096, "C5": 1024, "C6": 4096, "C7": 256, "T1": 3}
 MODES = ("rig", "static", "scores", "obs")
 _named = [n for n in sys.argv[1:] if n in synth.CONFIGS]
 _modes_only = bool(sys.argv[1:]) and all(a in MODES for a in sys.argv[1:])

@@ -161,6 +161,10 @@ CONFIGS: Dict[str, Config] = {
     "C3": Config("C3", 3, 1024, 1, 640, 480, 500_000, 10, 2000, 3),
     "C4": Config("C4", 4, 4096, 2, 128, 128, 180_000, 10, 2000, 3, fov60=True),
     "C5": Config("C5", 5, 8192, 1, 640, 480, 980_000, 10, 2000, 3),
+    # §8(f) row 4 second workloads: 224x224 policy views (ViT input) and a 1280x720 sweep
+    # point, both on the C3 scene
+    "C6": Config("C6", 6, 4096, 1, 224, 224, 500_000, 10, 2000, 3, fov60=True),
+    "C7": Config("C7", 7, 256, 1, 1280, 720, 500_000, 10, 2000, 3),
     # parity-test configs: oracle finishes in seconds, several tiles + ragged tail
     "T1": Config("T1", 11, 3, 2, 100, 75, 6000, 10, 200, 3),
     "T2": Config("T2", 12, 2, 1, 130, 97, 20000, 10, 300, 3),

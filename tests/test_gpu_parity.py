@@ -166,10 +166,12 @@ def test_render_oversize_tile_list_matches_oracle():
 
 
 @pytest.mark.slow
-def test_render_c3_full_size_sampled_pixels():
-    """BASELINE configs[2] at full size, in the bench's launch configuration (1024 envs, one call):
-    sampled pixels of frames {0, B/2, B-1} against the oracle."""
-    cfg = synth.CONFIGS["C3"]
+@pytest.mark.parametrize("name", ["C3", "C4", "C6", "C7"])
+def test_render_full_size_sampled_pixels(name):
+    """BASELINE configs at full size, in the bench's launch configuration (all envs in one call;
+    C3 is the headline, C4 the 128x128 two-camera case, C6/C7 the 224x224 and 1280x720 §8(f)
+    row-4 workloads): sampled pixels of frames {0, B/2, B-1} against the oracle."""
+    cfg = synth.CONFIGS[name]
     sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
     gout = gu.gpu_render(sc, b, cfg.width, cfg.height, stats=True)
     kap = gu.kappa_f32(sc)
@@ -182,7 +184,7 @@ def test_render_c3_full_size_sampled_pixels():
         rec, zb, va = gu.gpu_project(gout["scene"], sub, cfg.width, cfg.height)
         r = gu.compare_frame(gout, e, 0, ref, cfg.width, cfg.height, pix=(px, py), gpu_rec=rec[0], gpu_zb=zb[0],
                              gpu_valid=va[0], kap=kap)
-        print("C3", e, r)
+        print(name, e, r)
         assert r["rgb_fail"] == 0 and r["dep_fail"] == 0 and r["alp_fail"] == 0, r
         assert r["n_eval_fail"] == 0, r
         assert r["masked_frac"] <= MASK_CAP, r
