@@ -1097,7 +1097,7 @@ gsb_status gsb_debug_project(gsb_scene s, const float* poses, int32_t n_envs, in
   K1Args a{};
   a.g_mean = s->d_mean; a.g_L0 = s->d_L0; a.g_L1 = s->d_L1; a.g_L2 = s->d_L2; a.g_sh = s->d_sh;
     a.g_ids = s->d_ids;
-  a.n = s->n; a.table = s->table; a.cams = s->cams; a.nb1 = s->n_bodies + 1;
+  a.n = s->n; a.sh_stride = s->n; a.table = s->table; a.cams = s->cams; a.nb1 = s->n_bodies + 1;
   a.f0 = 0; a.n_frames = F; a.width = p->width; a.height = p->height;
   a.tiles_x = (p->width + kTile - 1) / kTile;
   a.near_plane = p->near_plane; a.far_plane = p->far_plane;
