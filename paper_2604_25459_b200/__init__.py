@@ -15,7 +15,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgsb.so")
+LIB_PATH = os.environ.get("GSB_LIB_PATH") or os.path.join(_HERE, "libgsb.so")  # override: A/B builds (scripts/ab.py)
 
 GSB_FLAG_STATS = 1
 GSB_FLAG_TIMING = 2

@@ -101,6 +101,7 @@ struct gsb_scene_t {
   float4* table = nullptr;
   FrameCam* cams = nullptr;
   float4* rec[2] = {nullptr, nullptr};
+  uint2* emit[2] = {nullptr, nullptr};
   int* vcount[2] = {nullptr, nullptr};
   uint32_t* vis_bits[2] = {nullptr, nullptr};
   uint32_t* long_list[2] = {nullptr, nullptr};   // lists too long for K4's fused sort
@@ -161,7 +162,7 @@ struct gsb_scene_t {
   void free_workspace() {
     cudaFree(table); cudaFree(cams);
     for (int s = 0; s < 2; ++s) {
-      cudaFree(rec[s]); cudaFree(vcount[s]); cudaFree(hist[s]); cudaFree(off[s]); cudaFree(vis_bits[s]);
+      cudaFree(rec[s]); cudaFree(emit[s]); emit[s] = nullptr; cudaFree(vcount[s]); cudaFree(hist[s]); cudaFree(off[s]); cudaFree(vis_bits[s]);
       cudaFree(long_list[s]); cudaFree(long_cnt[s]);
       vis_bits[s] = nullptr; long_list[s] = nullptr; long_cnt[s] = nullptr;
       cudaFree(frame_base[s]);
@@ -273,7 +274,8 @@ struct Pipeline {
     a.n = count; a.sh_stride = s->n; a.table = s->table; a.cams = s->cams; a.nb1 = s->n_bodies + 1;
     a.f0 = f0; a.n_frames = nf; a.width = W; a.height = H; a.tiles_x = tiles_x;
     a.near_plane = p->near_plane; a.far_plane = p->far_plane;
-    a.rec = s->rec[sl]; a.vcount = s->vcount[sl]; a.hist = s->hist[sl]; a.hist_stride = s->hist_stride;
+    a.rec = s->rec[sl]; a.emit = s->emit[sl];
+    a.vcount = s->vcount[sl]; a.hist = s->hist[sl]; a.hist_stride = s->hist_stride;
     a.vis_bits = s->vis_bits[sl]; a.vis_words = s->vis_words;
     tm.begin(KC_PROJECT);
     launch_k1(a, D, st);
@@ -292,7 +294,7 @@ struct Pipeline {
 
   gsb_status pass(int sl, int f0, int fs, int fe, uint64_t key_base, uint32_t n_long) {
     ChunkArgs a{};
-    a.rec = s->rec[sl]; a.n = count; a.vis_bits = s->vis_bits[sl]; a.vis_words = s->vis_words; a.hist = s->hist[sl];
+    a.rec = s->rec[sl]; a.emit = s->emit[sl]; a.ids = s->d_ids + first; a.n = count; a.vis_bits = s->vis_bits[sl]; a.vis_words = s->vis_words; a.hist = s->hist[sl];
     a.hist_stride = s->hist_stride; a.off = s->off[sl]; a.frame_base = s->frame_base[sl];
     a.n_tiles = n_tiles; a.tiles_x = tiles_x; a.fs = fs; a.fe = fe; a.key_base = key_base;
     a.keys = s->keys; a.keys_alt = s->keys_alt; a.sorted = s->sorted;
@@ -639,6 +641,7 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
   CUDA_TRY(dalloc(&s->cams, (size_t)F));
   for (int sl = 0; sl < 2; ++sl) {
     CUDA_TRY(dalloc(&s->rec[sl], (size_t)E * std::max<int64_t>(s->n, 1) * kRecQuads));
+    CUDA_TRY(dalloc(&s->emit[sl], (size_t)E * std::max<int64_t>(s->n, 1)));
     CUDA_TRY(dalloc(&s->vcount[sl], (size_t)E));
     CUDA_TRY(dalloc(&s->vis_bits[sl], (size_t)E * std::max<int64_t>(s->vis_words, 1)));
     CUDA_TRY(dalloc(&s->long_list[sl], (size_t)E * s->n_tiles));
@@ -766,10 +769,11 @@ gsb_status gsb_prebin_static(gsb_scene s, int32_t n_cams, const float* intr, con
   const int nb1 = s->n_bodies + 1;
   const int D = p->sh_degree < 0 ? s->sh_degree : p->sh_degree;
   float* poses = nullptr; float4* table = nullptr; FrameCam* cams = nullptr; float4* rec = nullptr;
+  uint2* emit = nullptr;
   int* vcount = nullptr; int* hist = nullptr; uint32_t* off = nullptr; uint32_t* vbits = nullptr;
   uint64_t* fbase = nullptr; uint64_t* keys = nullptr; uint64_t* keys_alt = nullptr; uint32_t* sorted = nullptr;
   auto cleanup = [&]() {
-    cudaFree(poses); cudaFree(table); cudaFree(cams); cudaFree(rec); cudaFree(vcount); cudaFree(hist);
+    cudaFree(poses); cudaFree(table); cudaFree(cams); cudaFree(rec); cudaFree(emit); cudaFree(vcount); cudaFree(hist);
     cudaFree(off); cudaFree(vbits); cudaFree(fbase); cudaFree(keys); cudaFree(keys_alt); cudaFree(sorted);
   };
 #define PB_TRY(expr)                                                                            \
@@ -800,6 +804,7 @@ gsb_status gsb_prebin_static(gsb_scene s, int32_t n_cams, const float* intr, con
   PB_TRY(cudaGetLastError());
   // K1 over the background prefix, K2 scan
   PB_TRY(dalloc(&rec, (size_t)C * std::max<int64_t>(nbg, 1) * kRecQuads));
+  PB_TRY(dalloc(&emit, (size_t)C * std::max<int64_t>(nbg, 1)));
   PB_TRY(dalloc(&vcount, (size_t)C));
   PB_TRY(dalloc(&vbits, (size_t)C * std::max<int64_t>(vwords, 1)));
   PB_TRY(dalloc(&hist, (size_t)C * stride));
@@ -813,7 +818,8 @@ gsb_status gsb_prebin_static(gsb_scene s, int32_t n_cams, const float* intr, con
   a.n = nbg; a.sh_stride = s->n; a.table = table; a.cams = cams; a.nb1 = nb1;
   a.f0 = 0; a.n_frames = C; a.width = W; a.height = H; a.tiles_x = tiles_x;
   a.near_plane = p->near_plane; a.far_plane = p->far_plane;
-  a.rec = rec; a.vcount = vcount; a.hist = hist; a.hist_stride = stride; a.vis_bits = vbits; a.vis_words = vwords;
+  a.rec = rec; a.emit = emit;
+  a.vcount = vcount; a.hist = hist; a.hist_stride = stride; a.vis_bits = vbits; a.vis_words = vwords;
   launch_k1(a, D, st);
   launch_k2_scan(hist, off, stride, C, n_tiles, fbase, nullptr, nullptr, 0, nullptr, nullptr, st);
   PB_TRY(cudaGetLastError());
@@ -832,7 +838,7 @@ gsb_status gsb_prebin_static(gsb_scene s, int32_t n_cams, const float* intr, con
   PB_TRY(dalloc(&s->bg_keys, std::max<uint64_t>(K, 1)));
   PB_TRY(dalloc(&s->bg_rec, std::max<uint64_t>(K, 1) * 3));
   ChunkArgs ca{};
-  ca.rec = rec; ca.n = nbg; ca.vis_bits = vbits; ca.vis_words = vwords; ca.hist = hist; ca.hist_stride = stride;
+  ca.rec = rec; ca.emit = emit; ca.ids = s->d_ids; ca.n = nbg; ca.vis_bits = vbits; ca.vis_words = vwords; ca.hist = hist; ca.hist_stride = stride;
   ca.off = off; ca.frame_base = fbase; ca.n_tiles = n_tiles; ca.tiles_x = tiles_x; ca.fs = 0; ca.fe = C;
   ca.key_base = 0; ca.long_list = nullptr; ca.keys = keys; ca.keys_alt = keys_alt; ca.sorted = sorted;
   launch_k2_emit(ca, st);
@@ -1121,13 +1127,13 @@ gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, 
   const int tiles_x = (width + kTile - 1) / kTile;
   const int n_tiles = tiles_x * ((height + kTile - 1) / kTile);
   const int64_t stride = ((int64_t)n_tiles + 2 + 31) / 32 * 32;
-  float4* rec = nullptr; int* vcount = nullptr; int* hist = nullptr; uint32_t* off = nullptr;
+  uint2* emit = nullptr; int* vcount = nullptr; int* hist = nullptr; uint32_t* off = nullptr;
   uint32_t* vbits = nullptr;
   const int64_t vwords = (n + 31) / 32;
   uint64_t* fbase = nullptr; uint64_t* keys = nullptr; uint64_t* keys_alt = nullptr; uint32_t* sorted = nullptr;
   gsb_status result = GSB_OK;
   auto cleanup = [&]() {
-    cudaFree(rec); cudaFree(vcount); cudaFree(hist); cudaFree(off); cudaFree(fbase); cudaFree(vbits);
+    cudaFree(emit); cudaFree(vcount); cudaFree(hist); cudaFree(off); cudaFree(fbase); cudaFree(vbits);
     cudaFree(keys); cudaFree(keys_alt); cudaFree(sorted);
   };
 #define DBG_TRY(expr)                                                              \
@@ -1138,7 +1144,7 @@ gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, 
       return fail(GSB_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_));          \
     }                                                                              \
   } while (0)
-  DBG_TRY(dalloc(&rec, (size_t)F * std::max<int64_t>(n, 1) * kRecQuads));
+  DBG_TRY(dalloc(&emit, (size_t)F * std::max<int64_t>(n, 1)));
   DBG_TRY(dalloc(&vcount, (size_t)F));
   DBG_TRY(dalloc(&vbits, (size_t)F * std::max<int64_t>(vwords, 1)));
   DBG_TRY(dalloc(&hist, (size_t)F * stride));
@@ -1146,7 +1152,7 @@ gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, 
   DBG_TRY(dalloc(&fbase, (size_t)F + 2));
   DBG_TRY(cudaMemsetAsync(vcount, 0, sizeof(int) * F, st));
   DBG_TRY(cudaMemsetAsync(hist, 0, sizeof(int) * F * stride, st));
-  launch_k1_external(u, v, sxx, syy, kappa, zbits, valid, n, 0, F, width, height, tiles_x, rec, vbits, vwords,
+  launch_k1_external(u, v, sxx, syy, kappa, zbits, valid, n, 0, F, width, height, tiles_x, emit, vbits, vwords,
                      vcount, hist, stride, st);
   launch_k2_scan(hist, off, stride, F, n_tiles, fbase, nullptr, nullptr, 0, nullptr, nullptr, st);
   DBG_TRY(cudaGetLastError());
@@ -1163,7 +1169,7 @@ gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, 
   DBG_TRY(dalloc(&keys_alt, std::max<uint64_t>(K, 1)));
   DBG_TRY(dalloc(&sorted, std::max<uint64_t>(K, 1)));
   ChunkArgs a{};
-  a.rec = rec; a.n = n; a.vis_bits = vbits; a.vis_words = vwords; a.hist = hist; a.hist_stride = stride; a.off = off;
+  a.rec = nullptr; a.emit = emit; a.ids = nullptr; a.n = n; a.vis_bits = vbits; a.vis_words = vwords; a.hist = hist; a.hist_stride = stride; a.off = off;
   a.frame_base = fbase; a.n_tiles = n_tiles; a.tiles_x = tiles_x; a.fs = 0; a.fe = F; a.key_base = 0;
   a.long_list = nullptr;  // K3 sorts every list here
   a.keys = keys; a.keys_alt = keys_alt; a.sorted = sorted;

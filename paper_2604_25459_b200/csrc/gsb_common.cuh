@@ -11,12 +11,12 @@
 //     g_L2[N]    = (L22, opacity, kappa = 2 ln(255 o), log2 o)
 //     g_sh[P][N] = SH coefficients, P = ceil(3 (D+1)^2 / 4) float4 planes, coefficient-major
 //   per frame-body table (K0 -> K1): 4 float4 = M row 0 | m0, row 1 | m1, row 2 | m2, c_body
-//   projected record (K1 -> K2/K4), 64 B at [frame][internal index]:
+//   projected record (K1 -> K4), 48 B at [frame][internal index]:
 //     R0 = (u, v, p', q')          whitening factor of Sigma2D^-1 scaled by sqrt(log2(e)/2)
 //     R1 = (r', log2 o, ex, ey)    half-extents of the alpha >= 1/255 box (R8), inflated
 //     R2 = (r, g, b, z)            z = fp32 depth key (R11)
-//     R3 = (id, rect, -, -)        id as int bits; rect = tx0 | tx1 << 8 | ty0 << 16 | ty1 << 24
-//   K4 stages only R0..R2 (48 B); K2 emission reads R2.w and R3.
+//   emission entry (K1 -> K2b), 8 B at [frame][internal index]: (bits(z), rect) with
+//     rect = tx0 | tx1 << 8 | ty0 << 16 | ty1 << 24; the key's id comes from the template
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -24,7 +24,7 @@
 namespace gsb {
 
 constexpr int kTile = 16;             // reading R9: tiles fixed at 16x16 pixels
-constexpr int kRecQuads = 4;          // float4s per projected record
+constexpr int kRecQuads = 3;          // float4s per projected record
 constexpr int kMaxDim = 4096;         // width, height <= 4096 -> tile coords fit in 8 bits
 constexpr float kAlphaMax = 0.99f;    // north_star: alpha clamped at 0.99
 constexpr float kTermT = 1e-4f;       // reading R13

@@ -31,6 +31,7 @@ struct K1Args {
   float near_plane, far_plane;
   // outputs
   float4* rec;     // [E][N][3] records at the internal index, nullptr for debug-only launches
+  uint2* emit;     // [E][N] (bits(z), rect) for the key emission
   uint32_t* vis_bits;  // [E][vis_words] visibility ballot of each warp (32 internal indices)
   int64_t vis_words;   // ceil(N / 32)
   int* vcount;     // [E] visible pairs (statistics)
@@ -44,6 +45,8 @@ struct K1Args {
 
 struct ChunkArgs {
   const float4* rec;      // [E][N][3]
+  const uint2* emit;      // [E][N] (bits(z), rect) of the visible (frame, Gaussian) pairs
+  const int2* ids;        // template (id, body) of the launch's range, or nullptr: id = index
   int64_t n;              // record stride per frame (= N)
   const uint32_t* vis_bits;  // [E][vis_words]
   int64_t vis_words;
@@ -120,7 +123,7 @@ void launch_k1(const K1Args& a, int sh_degree, cudaStream_t s);
 void launch_k1_external(const float* u, const float* v, const float* sxx, const float* syy,
                         const float* kappa, const uint32_t* zbits, const uint8_t* valid,
                         int64_t n, int f0, int n_frames, int width, int height, int tiles_x,
-                        float4* rec, uint32_t* vis_bits, int64_t vis_words, int* vcount, int* hist,
+                        uint2* emit, uint32_t* vis_bits, int64_t vis_words, int* vcount, int* hist,
                         int64_t hist_stride, cudaStream_t s);
 
 // off[f][T] = K_f, off[f][T+1] = longest tile list of frame f; frame_base[E] = total keys,

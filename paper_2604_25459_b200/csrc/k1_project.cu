@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
       r[0] = make_float4(u, v, pw, qw);
       r[1] = make_float4(rw, log2o, ex, ey);
       r[2] = make_float4(rgb.x, rgb.y, rgb.z, z);
-      r[3] = make_float4(__int_as_float(id), __uint_as_float(rect), 0.f, 0.f);
+      a.emit[(size_t)fl * a.n + i] = make_uint2(__float_as_uint(z), rect);
     }
     warp_tile_count(vis, rect, a.tiles_x, a.hist + (size_t)fl * a.hist_stride);
   }

@@ -122,11 +122,10 @@ __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
   const bool has = (word >> lane) & 1u;
   uint32_t rect = 0, zb = 0, id = 0;
   if (has) {
-    const float4* r = a.rec + ((size_t)fl * a.n + i) * kRecQuads;
-    zb = __float_as_uint(__ldg(&r[2].w));
-    const float2 r3 = __ldg(reinterpret_cast<const float2*>(r + 3));
-    id = __float_as_uint(r3.x);
-    rect = __float_as_uint(r3.y);
+    const uint2 er = __ldg(a.emit + (size_t)fl * a.n + i);
+    zb = er.x;
+    rect = er.y;
+    id = a.ids ? (uint32_t)__ldg(&a.ids[i].x) : (uint32_t)i;
   }
   const uint64_t key = ((uint64_t)zb << 32) | (uint64_t)id;   // unique (reading R10)
   int* cur = a.hist + (size_t)fl * a.hist_stride;
@@ -177,7 +176,7 @@ __global__ void __launch_bounds__(128) k1_external(const float* __restrict__ u, 
                                                    const uint32_t* __restrict__ zbits,
                                                    const uint8_t* __restrict__ valid, int64_t n, int f0,
                                                    int n_frames, int width, int height, int tiles_x,
-                                                   float4* __restrict__ rec, uint32_t* __restrict__ vis_bits,
+                                                   uint2* __restrict__ emit, uint32_t* __restrict__ vis_bits,
                                                    int64_t vis_words, int* __restrict__ vcount,
                                                    int* __restrict__ hist, int64_t hist_stride) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -194,11 +193,7 @@ __global__ void __launch_bounds__(128) k1_external(const float* __restrict__ u, 
       if (bal) atomicAdd(vcount + fl, __popc(bal));
     }
     const uint32_t rect = pack_rect(tx0, tx1, ty0, ty1);
-    if (vis) {
-      float4* r = rec + ((size_t)fl * n + i) * kRecQuads;
-      r[2] = make_float4(0.f, 0.f, 0.f, __uint_as_float(zbits[o]));
-      r[3] = make_float4(__int_as_float((int)i), __uint_as_float(rect), 0.f, 0.f);
-    }
+    if (vis) emit[(size_t)fl * n + i] = make_uint2(zbits[o], rect);
     warp_tile_count(vis, rect, tiles_x, hist + (size_t)fl * hist_stride);
   }
 }
@@ -206,11 +201,11 @@ __global__ void __launch_bounds__(128) k1_external(const float* __restrict__ u, 
 void launch_k1_external(const float* u, const float* v, const float* sxx, const float* syy,
                         const float* kappa, const uint32_t* zbits, const uint8_t* valid,
                         int64_t n, int f0, int n_frames, int width, int height, int tiles_x,
-                        float4* rec, uint32_t* vis_bits, int64_t vis_words, int* vcount, int* hist,
+                        uint2* emit, uint32_t* vis_bits, int64_t vis_words, int* vcount, int* hist,
                         int64_t hist_stride, cudaStream_t s) {
   if (n == 0) return;
   k1_external<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(u, v, sxx, syy, kappa, zbits, valid, n, f0,
-                                                          n_frames, width, height, tiles_x, rec, vis_bits,
+                                                          n_frames, width, height, tiles_x, emit, vis_bits,
                                                           vis_words, vcount, hist, hist_stride);
 }
 
