@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -77,6 +78,16 @@ enum KClass { KC_SETUP = 0, KC_PROJECT, KC_SCAN, KC_EMIT, KC_SORT, KC_COMPOSITE,
 
 constexpr int kMaxChunk = 1024;  // frames per pipeline chunk (upper bound)
 
+// compositing path of plain / observation renders: split K4a + K4b (default) or the
+// one-CTA-per-tile K4 (GSB_K4=fused, for A/B comparisons)
+bool split_k4() {
+  static const int v = [] {
+    const char* e = getenv("GSB_K4");
+    return (e && std::string(e) == "fused") ? 0 : 1;
+  }();
+  return v != 0;
+}
+
 }  // namespace
 
 struct gsb_scene_t {
@@ -116,6 +127,7 @@ struct gsb_scene_t {
   uint64_t *keys = nullptr, *keys_alt = nullptr;
   uint32_t* sorted = nullptr;
   unsigned long long* d_pairs = nullptr;
+  int* d_counter = nullptr;   // K4b work-item counter
   // host-io staging
   bool host_io = false;
   int max_envs = 0, res_cams = 0;
@@ -171,7 +183,8 @@ struct gsb_scene_t {
       rec[s] = nullptr; vcount[s] = nullptr; hist[s] = nullptr; off[s] = nullptr;
       frame_base[s] = nullptr; h_rb[s] = nullptr; d_rb[s] = nullptr; ev_counts[s] = nullptr;
     }
-    cudaFree(keys); cudaFree(keys_alt); cudaFree(sorted); cudaFree(d_pairs); cudaFree(qpos);
+    cudaFree(keys); cudaFree(keys_alt); cudaFree(sorted); cudaFree(d_pairs); cudaFree(qpos); cudaFree(d_counter);
+    d_counter = nullptr;
     qpos = nullptr;
     cudaFree(st_poses); cudaFree(st_intr); cudaFree(st_w2c);
     cudaFree(st_rgb); cudaFree(st_depth); cudaFree(st_alpha); cudaFree(st_neval); cudaFree(st_dr);
@@ -330,7 +343,13 @@ struct Pipeline {
     }
     tm.begin(KC_COMPOSITE);
     // many lists beyond the small fused-sort capacity (e.g. 128x128 views): larger variant
-    launch_k4_composite(c, (uint64_t)n_long * 4 > (uint64_t)(fe - fs) * n_tiles, st);
+    const bool long_lists = (uint64_t)n_long * 4 > (uint64_t)(fe - fs) * n_tiles;
+    if (!merge && !c.score_sum && split_k4()) {
+      launch_k4_split(c, long_lists, s->d_counter, st);   // K4a sort + K4b persistent warps
+      s->launches++;
+    } else {
+      launch_k4_composite(c, long_lists, st);
+    }
     s->launches++;
     s->comp_launches++;
     LAUNCH_CHECK();
@@ -657,6 +676,7 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
   CUDA_TRY(dalloc(&s->keys_alt, (size_t)cap));
   CUDA_TRY(dalloc(&s->sorted, (size_t)cap));
   CUDA_TRY(dalloc(&s->d_pairs, 1));
+  CUDA_TRY(dalloc(&s->d_counter, 1));
   if (s->sb_cams > 0) CUDA_TRY(dalloc(&s->qpos, (size_t)cap));
   s->host_io = (flags & GSB_RESERVE_HOST_IO) != 0;
   if (s->host_io) {

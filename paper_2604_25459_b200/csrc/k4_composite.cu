@@ -18,11 +18,10 @@
 // sorting, which is barrier-bound, overlaps with the ALU-bound compositing of the other CTAs
 // resident on the SM.  Records are then staged through shared memory 256 at a time and the
 // CTA stops as soon as every pixel has terminated (__syncthreads_count vote).
-#include <cuda_fp16.h>
-
 #include "gsb_common.cuh"
 #include "gsb_kernels.cuh"
 #include "gsb_sort.cuh"
+#include "k4_common.cuh"
 
 namespace gsb {
 
@@ -56,76 +55,6 @@ struct K4Shared {
 };
 static_assert(sizeof(uint32_t) * kFusedSortCap + 16 * kStageQuads <= 2 * 8 * kFusedSortCap, "small union");
 static_assert(4 * 4 * kFusedSortCap >= 16 * kStageQuads, "large variant stages in the result buffer");
-
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
-// Front-to-back blend of one list entry into one pixel (readings R12-R14).  alpha is 0 unless
-// `use` (alpha >= 1/255 for a live pixel); then T never drops below 1e-4 without terminating,
-// so an unused entry leaves every accumulator unchanged.  A pixel that terminates gets its
-// centre moved to kFar: every later quadratic form is huge and every later entry fails the
-// alpha test, without a per-pixel "done" test in the hot loop.
-constexpr float kFar = 1e20f;
-constexpr float kScoreFix = 67108864.f;  // 2^26: warp-level fixed point of the score sums
-
-__device__ __forceinline__ float blend(bool use, float arg, const float4& r2, float& T, float& cr, float& cg,
-                                       float& cb, float& dep, float& pyc, int& n_eval, int idx) {
-  const float alpha = use ? fminf(kAlphaMax, ex2_approx(arg)) : 0.f;
-  const float w = alpha * T;
-  const float tT = T - w;                       // T (1 - alpha)
-  if (tT >= kTermT) {
-    cr = fmaf(w, r2.x, cr);
-    cg = fmaf(w, r2.y, cg);
-    cb = fmaf(w, r2.z, cb);
-    dep = fmaf(w, r2.w, dep);
-    T = tT;
-    return w;                                   // blended weight (reading R30 scores)
-  }
-  n_eval = idx + 1;                             // stop before blending (R13)
-  pyc = kFar;
-  return 0.f;
-}
-
-// Reading R31 noise: counter-based Irwin-Hall(4) of 22-bit lowbias32-hashed uniforms (exact
-// integer arithmetic, so the oracle reproduces every draw); z * sqrt(3)/2^22 has unit variance.
-__device__ __forceinline__ uint32_t mix32(uint32_t x) {
-  x ^= x >> 16;
-  x *= 0x7feb352du;
-  x ^= x >> 15;
-  x *= 0x846ca68bu;
-  x ^= x >> 16;
-  return x;
-}
-__device__ __forceinline__ float irwin_hall4(uint64_t idx, uint32_t kseed) {
-  const uint32_t base = mix32((uint32_t)idx ^ mix32((uint32_t)(idx >> 32) ^ kseed));
-  uint32_t s = 0;
-#pragma unroll
-  for (uint32_t j = 0; j < 4; ++j) s += mix32(base + j * 0x9E3779B9u) >> 10;
-  return __fsub_rn((float)s, 8388608.f);   // (float)s exact: s < 2^24
-}
-constexpr float kNoiseS3 = 1.7320508075688772f / 4194304.f;   // sqrt(3) / 2^22 (power-of-2 divisor: exact)
-
-// first index in sorted k[0..n) whose value is >= x
-template <typename T, typename P>
-__device__ __forceinline__ int lower_bound(P k, int n, T x) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (k[mid] < x) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
 
 // MERGE (gsb_render_static, §8(f) row 2): the CTA's list is the (zbits, id) merge of the
 // pre-binned, pre-sorted background list of its (camera, tile) with the frame's robot list
@@ -362,55 +291,7 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
   }
   cp_async_wait_all();
 
-  const size_t f = (size_t)(a.f0 + fl);
-  const size_t plane = (size_t)a.width * a.height;
-  if (a.obs_rgb8) {
-    // observation epilogue, reading R31: image DR + uint8 RGB (+ fp16 depth), binary32 RN ops
-    float4 dr = make_float4(1.f, 1.f, 0.f, 0.f);
-    if (a.obs_dr) dr = *reinterpret_cast<const float4*>(a.obs_dr + f * 4);
-    const uint64_t gf = (uint64_t)a.obs_frame_offset + f;
-    const uint32_t kseed = mix32(a.obs_seed ^ mix32(a.obs_step));
-    uint8_t* o8 = a.obs_rgb8 + f * 3 * plane;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const bool in = h ? in1 : in0;
-      if (!in) continue;
-      const int y = py0 + h;
-      const size_t p = (size_t)y * a.width + px;
-      const float T = h ? T1 : T0;
-      const float cc[3] = {fmaf(T, a.bg0, h ? r1c : r0c), fmaf(T, a.bg1, h ? g1c : g0c), fmaf(T, a.bg2, h ? b1c : b0c)};
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        float v = __fadd_rn(__fmul_rn(__fsub_rn(__fmul_rn(cc[ch], dr.x), 0.5f), dr.y), 0.5f);
-        v = __fadd_rn(v, dr.z);
-        if (dr.w != 0.f) {
-          const uint64_t idx = ((gf * (uint64_t)a.height + (uint64_t)y) * (uint64_t)a.width + (uint64_t)px) * 3u + ch;
-          v = __fadd_rn(v, __fmul_rn(__fmul_rn(irwin_hall4(idx, kseed), kNoiseS3), dr.w));
-        }
-        o8[ch * plane + p] = (uint8_t)__float2uint_rn(__fmul_rn(__saturatef(v), 255.f));
-      }
-      const float d = h ? d1 : d0;
-      if (a.obs_depth16) a.obs_depth16[f * plane + p] = __half_as_ushort(__float2half_rn(d));
-      else if (a.out_depth) a.out_depth[f * plane + p] = d;
-      if (a.out_alpha) a.out_alpha[f * plane + p] = 1.f - T;
-      if (a.out_n_eval) a.out_n_eval[f * plane + p] = h ? ne1 : ne0;
-    }
-  } else {
-    float* rgb = a.out_rgb + f * 3 * plane;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const bool in = h ? in1 : in0;
-      if (!in) continue;
-      const size_t p = (size_t)(py0 + h) * a.width + px;
-      const float T = h ? T1 : T0;
-      rgb[p] = fmaf(T, a.bg0, h ? r1c : r0c);
-      rgb[plane + p] = fmaf(T, a.bg1, h ? g1c : g0c);
-      rgb[2 * plane + p] = fmaf(T, a.bg2, h ? b1c : b0c);
-      if (a.out_depth) a.out_depth[f * plane + p] = h ? d1 : d0;
-      if (a.out_alpha) a.out_alpha[f * plane + p] = 1.f - T;
-      if (a.out_n_eval) a.out_n_eval[f * plane + p] = h ? ne1 : ne0;
-    }
-  }
+  store_pixels(a, (size_t)(a.f0 + fl), px, py0, in0, in1, T0, r0c, g0c, b0c, d0, ne0, T1, r1c, g1c, b1c, d1, ne1);
   if (a.stat_pairs) {
     unsigned long long v = (in0 ? (unsigned long long)ne0 : 0ull) + (in1 ? (unsigned long long)ne1 : 0ull);
 #pragma unroll

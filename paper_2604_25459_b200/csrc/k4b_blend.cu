@@ -1,0 +1,241 @@
+// k4b_blend.cu — the split compositing path (plain and observation renders):
+//
+//   K4a k4a_sort   one CTA per (frame, tile): the tile's keys in (bits(z), id) order (reading
+//                  R10, the segmented radix sort of gsb_sort.cuh), written as record slots into
+//                  the `sorted` workspace.  Barrier-bound, short.
+//   K4b k4b_blend  persistent warps: each warp takes (frame, tile, 8x8 block) work items from an
+//                  atomic counter and composites its 64 pixels front to back over the tile's
+//                  sorted list (readings R12-R16), staging 32 records per round with cp.async
+//                  into its own double buffer, culling them against its block (the same lower
+//                  bound as k4_composite.cu), and leaving the item as soon as its pixels have
+//                  terminated.
+//
+// Why split: in the one-CTA-per-tile kernel the four warps of a tile meet at a barrier every
+// round, and warps whose block terminates early idle until the slowest one finishes (35 % of
+// K4's stall samples, profiles/r04_k4_ncu_full.txt).  Here no warp ever waits for another; the
+// price is reading each record once per warp (from L2) instead of once per CTA.
+#include <algorithm>
+
+#include "gsb_sort.cuh"
+#include "k4_common.cuh"
+
+namespace gsb {
+
+constexpr int kSortThreadsA = 128;
+
+template <int CAP>
+struct K4aShared {
+  static constexpr bool kPacked = CAP > kFusedSortCap;
+  SortShared<kSortThreadsA> sort;
+  union {
+    uint64_t keys[kPacked ? 1 : 2][kPacked ? 1 : CAP];   // small variant: 64-bit keys in smem
+    uint32_t buf[2][kPacked ? CAP : 1];                   // large variant: packed sort
+  } u;
+};
+
+template <int CAP>
+__global__ void __launch_bounds__(kSortThreadsA) k4a_sort(CompositeArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  using Sh = K4aShared<CAP>;
+  Sh& sm = *reinterpret_cast<Sh*>(smem_raw);
+  const int fl = a.fs + blockIdx.x / a.n_tiles;
+  const int t = blockIdx.x % a.n_tiles;
+  const int tid = threadIdx.x;
+  const uint32_t* off = a.off + (size_t)fl * a.hist_stride;
+  const uint64_t start = a.frame_base[fl] - a.key_base + off[t];
+  const int len = (int)(off[t + 1] - off[t]);
+  if (len == 0) return;
+  uint32_t* dst = a.sorted + start;
+  const int base = a.slot_base;
+  if (len == 1) {
+    if (tid == 0) dst[0] = (uint32_t)(__ldg(a.inv + (uint32_t)a.keys[start]) - base);
+    return;
+  }
+  if (len <= CAP) {
+    if constexpr (Sh::kPacked) {
+      const uint64_t* gk = a.keys + start;
+      const bool in_b = packed_sort(gk, len, sm.u.buf[0], sm.u.buf[1], sm.sort);
+      const uint32_t* res = sm.u.buf[in_b ? 1 : 0];
+      for (int e = tid; e < len; e += kSortThreadsA)
+        dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)__ldg(gk + (res[e] & 0xffffu))) - base);
+    } else {
+      for (int e = tid; e < len; e += kSortThreadsA) sm.u.keys[0][e] = a.keys[start + e];
+      __syncthreads();
+      const bool in_b = segment_sort(sm.u.keys[0], sm.u.keys[1], len, sm.sort);
+      const uint64_t* r = sm.u.keys[in_b ? 1 : 0];
+      for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)r[e]) - base);
+    }
+  } else {  // longer than the shared-memory capacity: 64-bit keys sorted in HBM
+    uint64_t* ga = const_cast<uint64_t*>(a.keys) + start;
+    uint64_t* gb = a.keys_alt + start;
+    const bool in_b = segment_sort(ga, gb, len, sm.sort);
+    const uint64_t* r = in_b ? gb : ga;
+    for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)r[e]) - base);
+  }
+}
+
+// ------------------------------------------------------------------------------ K4b
+constexpr int kBlendWarps = 4;
+constexpr int kWarpBatch = 32;   // records staged per warp round (one per lane)
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a, int* __restrict__ counter,
+                                                                  int n_items) {
+  __shared__ __align__(16) float4 stg[kBlendWarps][2][3][kWarpBatch];   // 12 KB
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float4 (*S)[3][kWarpBatch] = stg[warp];
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(counter, 1);
+    item = __shfl_sync(FULL, item, 0);
+    if (item >= n_items) break;
+    const int blk = item & 3, ft = item >> 2;
+    const int fl = a.fs + ft / a.n_tiles;
+    const int t = ft % a.n_tiles;
+    const int tx = t % a.tiles_x, ty = t / a.tiles_x;
+    // the 8x8 block `blk` of the tile; a lane owns pixels (px, py0) and (px, py0 + 1)
+    const int bx0 = tx * kTile + 8 * (blk & 1), by0 = ty * kTile + 8 * (blk >> 1);
+    const int px = bx0 + (lane & 7);
+    const int py0 = by0 + 2 * (lane >> 3);
+    const bool in_x = px < a.width;
+    const bool in0 = in_x && py0 < a.height, in1 = in_x && py0 + 1 < a.height;
+    const uint32_t* off = a.off + (size_t)fl * a.hist_stride;
+    const uint64_t start = a.frame_base[fl] - a.key_base + off[t];
+    const int len = (int)(off[t + 1] - off[t]);
+    const float4* rec = a.rec + (size_t)fl * a.n * kRecQuads;
+    const uint32_t* slots = a.sorted + start;
+    const float pxc = (float)px + 0.5f;
+    const float bcx = (float)bx0 + 4.0f, bcy = (float)by0 + 4.0f;  // block centre (pixel centres +-3.5)
+
+    float T0 = 1.f, r0c = 0.f, g0c = 0.f, b0c = 0.f, d0 = 0.f;
+    float T1 = 1.f, r1c = 0.f, g1c = 0.f, b1c = 0.f, d1 = 0.f;
+    float pyc0 = in0 ? (float)py0 + 0.5f : kFar;   // out-of-image pixels never pass the alpha test
+    float pyc1 = in1 ? (float)py0 + 1.5f : kFar;
+    int ne0 = len, ne1 = len;
+    const int rounds = __all_sync(FULL, pyc0 == kFar && pyc1 == kFar) ? 0 : (len + kWarpBatch - 1) / kWarpBatch;
+
+    // stage round b (slot sl of this lane's record) into buffer b & 1; the slot of the round
+    // after the next is read one round ahead, so no cp.async waits on a slot load
+    auto stage = [&](int b, uint32_t sl) {
+      if (b * kWarpBatch + lane < len) {
+        const float4* r = rec + (size_t)sl * kRecQuads;
+        cp_async16(&S[b & 1][0][lane], r);
+        cp_async16(&S[b & 1][1][lane], r + 1);
+        cp_async16(&S[b & 1][2][lane], r + 2);
+      }
+      cp_async_commit();
+    };
+    auto slot_of = [&](int b) -> uint32_t {
+      const int k = b * kWarpBatch + lane;
+      return k < len ? __ldg(slots + k) : 0u;
+    };
+    uint32_t sl_next = 0;
+    if (rounds > 0) {
+      stage(0, slot_of(0));
+      sl_next = slot_of(1);
+    }
+    for (int b = 0; b < rounds; ++b) {
+      if (b + 1 < rounds) {
+        stage(b + 1, sl_next);
+        sl_next = slot_of(b + 2);
+        cp_async_wait_group<1>();
+      } else {
+        cp_async_wait_group<0>();
+      }
+      __syncwarp();
+      const float4* R0 = S[b & 1][0];
+      const float4* R1 = S[b & 1][1];
+      const float4* R2 = S[b & 1][2];
+      const int base = b * kWarpBatch;
+      // this round's records that can reach the block (lower bound of the whitened quadratic
+      // form over the block's pixel centres, 2 % margin: no per-pixel decision changes)
+      bool ov = false;
+      if (base + lane < len) {
+        const float4 q0 = R0[lane];
+        const float2 q1 = *reinterpret_cast<const float2*>(&R1[lane]);
+        const float xa = q0.x - (bcx + 3.5f), xb = q0.x - (bcx - 3.5f);
+        const float ya = q0.y - (bcy + 3.5f), yb = q0.y - (bcy - 3.5f);
+        const float dxm = fmaxf(fmaxf(xa, -xb), 0.f);
+        const float lmin = fmaf(q0.w, q0.w >= 0.f ? xa : xb, q1.x * ya);
+        const float lmax = fmaf(q0.w, q0.w >= 0.f ? xb : xa, q1.x * yb);
+        const float lm = fmaxf(fmaxf(lmin, -lmax), 0.f);
+        const float px_ = q0.z * dxm;
+        const float lbq = fmaf(px_, px_, lm * lm);
+        ov = lbq <= fmaf(q1.y - kLog2AlphaMin, 1.02f, 0.02f);
+      }
+      unsigned m = __ballot_sync(FULL, ov);
+      int it = 0;
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const float4 q0 = R0[j];                                   // u, v, p, q
+        const float2 q1 = *reinterpret_cast<const float2*>(&R1[j]);  // r, log2 o
+        const float dx = q0.x - pxc;
+        const float t1 = q0.z * dx;
+        const float mm = fmaf(-t1, t1, q1.y);
+        const float qdx = q0.w * dx;
+        const float ta = fmaf(q1.x, q0.y - pyc0, qdx);
+        const float tb = fmaf(q1.x, q0.y - pyc1, qdx);
+        const float arg0 = fmaf(-ta, ta, mm);
+        const float arg1 = fmaf(-tb, tb, mm);
+        const bool use0 = arg0 >= kLog2AlphaMin;   // alpha >= 1/255
+        const bool use1 = arg1 >= kLog2AlphaMin;
+        if (use0 || use1) {
+          const float4 q2 = R2[j];                                 // r, g, b, z
+          blend(use0, arg0, q2, T0, r0c, g0c, b0c, d0, pyc0, ne0, base + j);
+          blend(use1, arg1, q2, T1, r1c, g1c, b1c, d1, pyc1, ne1, base + j);
+        }
+        if ((++it & 15) == 0 && __all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) break;
+      }
+      __syncwarp();   // buffer b & 1 is free for round b + 2
+      if (__all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) break;
+    }
+    cp_async_wait_all();   // nothing may land in the buffers after this item
+    __syncwarp();
+    store_pixels(a, (size_t)(a.f0 + fl), px, py0, in0, in1, T0, r0c, g0c, b0c, d0, ne0, T1, r1c, g1c, b1c, d1,
+                 ne1);
+    if (a.stat_pairs) {
+      unsigned long long v = (in0 ? (unsigned long long)ne0 : 0ull) + (in1 ? (unsigned long long)ne1 : 0ull);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+      if (lane == 0 && v) atomicAdd(a.stat_pairs, v);
+    }
+  }
+}
+
+template <int CAP>
+static void launch_k4a_variant(const CompositeArgs& a, unsigned grid, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k4a_sort<CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K4aShared<CAP>));
+    attr = true;
+  }
+  k4a_sort<CAP><<<grid, kSortThreadsA, sizeof(K4aShared<CAP>), s>>>(a);
+}
+
+void launch_k4_split(const CompositeArgs& a, bool long_lists, int* counter, cudaStream_t s) {
+  const int nf = a.fe - a.fs;
+  if (nf <= 0) return;
+  const unsigned grid = (unsigned)nf * a.n_tiles;
+  if (long_lists) launch_k4a_variant<4 * kFusedSortCap>(a, grid, s);
+  else launch_k4a_variant<kFusedSortCap>(a, grid, s);
+  static int persistent = 0;
+  if (!persistent) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4b_blend, kBlendWarps * 32, 0);
+    persistent = std::max(1, sms * std::max(1, per_sm));
+  }
+  const long long items = (long long)grid * 4;
+  cudaMemsetAsync(counter, 0, sizeof(int), s);
+  const unsigned g = (unsigned)std::min<long long>(persistent, (items + kBlendWarps - 1) / kBlendWarps);
+  k4b_blend<<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
+}
+
+}  // namespace gsb

@@ -11,7 +11,7 @@ tail -c 3000 gpurun_out/bench.json
 if [ -n "$PROFILE" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 500 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo ncu_list=$?
 for k in $PROFILE; do
-  case $k in k4) re=k4_composite;; k1) re=k1_project;; k2) re=k2_emit;; k3) re=k3_sort;; esac
+  case $k in k4) re=k4_composite;; k4a) re=k4a_sort;; k4b) re=k4b_blend;; k1) re=k1_project;; k2) re=k2_emit;; k3) re=k3_sort;; esac
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$re -s 8 -c 1 -o gpurun_out/$k python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo ncu_$k=$?
 done
 fi
