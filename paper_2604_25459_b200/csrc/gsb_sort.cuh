@@ -182,6 +182,82 @@ __device__ __forceinline__ bool segment_sort(Ptr a, Ptr b, int n, SortShared<NT>
 }
 
 // ---------------------------------------------------------------------------------------------
+// Single-pass counting sort for short segments (K4a, lists up to a few thousand keys): bucket
+// = the BITS highest varying bits of (zbits - zmin); histogram with shared atomics, one block
+// scan, scatter with atomic cursors (order inside a bucket arbitrary), then the buckets holding
+// several keys are finished by the full key (zbits, id) — reading R10; the result is the unique
+// order whatever the scatter order.  Two barrier-light phases instead of two radix passes.
+template <int NT, int BITS>
+struct CountShared {
+  static constexpr int kBins = 1 << BITS;
+  static constexpr int kWarps = NT / 32;
+  uint32_t bins[kBins];
+  uint32_t wred[kWarps];
+  uint32_t dup;
+};
+
+// a -> b (a is left unchanged)
+template <int NT, int BITS>
+__device__ __forceinline__ void count_sort(const uint64_t* a, uint64_t* b, int n, CountShared<NT, BITS>& sm) {
+  using Sh = CountShared<NT, BITS>;
+  constexpr int PER = Sh::kBins / NT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t zmin = 0xffffffffu;
+  for (int e = tid; e < n; e += NT) zmin = min(zmin, hi32(a[e]));
+  zmin = __reduce_min_sync(0xffffffffu, zmin);
+  if (lane == 0) sm.wred[warp] = zmin;
+  if (tid == 0) sm.dup = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) sm.bins[tid + k * NT] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < Sh::kWarps; ++w) zmin = min(zmin, sm.wred[w]);
+  uint32_t orx = 0;
+  for (int e = tid; e < n; e += NT) orx |= hi32(a[e]) - zmin;
+  orx = __reduce_or_sync(0xffffffffu, orx);
+  __syncthreads();
+  if (lane == 0) sm.wred[warp] = orx;
+  __syncthreads();
+  orx = 0;
+#pragma unroll
+  for (int w = 0; w < Sh::kWarps; ++w) orx |= sm.wred[w];
+  const int hb = orx ? 31 - __clz(orx) : -1;          // highest varying bit of (zbits - zmin)
+  const int lo = hb >= BITS ? hb - BITS + 1 : 0;      // bucket = bits [lo, lo + BITS)
+  // histogram (a key landing in an occupied bucket marks the segment for the fix-up)
+  uint32_t dup = 0;
+  for (int e = tid; e < n; e += NT) dup |= atomicAdd(&sm.bins[(hi32(a[e]) - zmin) >> lo], 1u);
+  if (dup) sm.dup = 1;
+  __syncthreads();
+  // exclusive scan of the buckets: PER consecutive buckets per thread
+  uint32_t v[PER], sum = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) { v[k] = sm.bins[tid * PER + k]; sum += v[k]; }
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) sm.wred[warp] = inc;
+  __syncthreads();
+  uint32_t run = inc - sum;
+#pragma unroll
+  for (int w = 0; w < Sh::kWarps; ++w) run += (w < warp) ? sm.wred[w] : 0u;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) { sm.bins[tid * PER + k] = run; run += v[k]; }
+  __syncthreads();
+  // scatter
+  for (int e = tid; e < n; e += NT) {
+    const uint64_t key = a[e];
+    b[atomicAdd(&sm.bins[(hi32(key) - zmin) >> lo], 1u)] = key;
+  }
+  __syncthreads();
+  if (sm.dup)   // uniform
+    fix_runs<NT>(b, n, [&](uint64_t k) { return (hi32(k) - zmin) >> lo; },
+                 [](uint64_t x, uint64_t y) { return x < y; });
+}
+
+// ---------------------------------------------------------------------------------------------
 // Packed tile sort (K4): the segment's 64-bit keys stay where K2 wrote them (HBM/L2); the sort
 // runs on 32-bit words (16 highest varying bits of zbits - zmin) << 16 | local index, so the
 // double buffer costs 8 B per key and each pass moves 4 B.  Runs equal on the 16 bits (depths

@@ -1,8 +1,8 @@
 // k4b_blend.cu — the split compositing path (plain and observation renders):
 //
 //   K4a k4a_sort   one CTA per (frame, tile): the tile's keys in (bits(z), id) order (reading
-//                  R10, the segmented radix sort of gsb_sort.cuh), written as record slots into
-//                  the `sorted` workspace.  Barrier-bound, short.
+//                  R10; gsb_sort.cuh: a one-pass 11-bit counting sort for lists up to 1024 keys,
+//                  the radix sorts beyond), written as record slots into the `sorted` workspace.
 //   K4b k4b_blend  persistent warps: each warp takes (frame, tile, 8x8 block) work items from an
 //                  atomic counter and composites its 64 pixels front to back over the tile's
 //                  sorted list (readings R12-R16), staging 32 records per round with cp.async
@@ -23,10 +23,15 @@ namespace gsb {
 
 constexpr int kSortThreadsA = 128;
 
+constexpr int kCountBits = 11;   // K4a counting-sort buckets (2048)
+
 template <int CAP>
 struct K4aShared {
   static constexpr bool kPacked = CAP > kFusedSortCap;
-  SortShared<kSortThreadsA> sort;
+  union {   // a CTA uses one of the two sorts
+    SortShared<kSortThreadsA> sort;
+    CountShared<kSortThreadsA, kCountBits> count;
+  } s;
   union {
     uint64_t keys[kPacked ? 1 : 2][kPacked ? 1 : CAP];   // small variant: 64-bit keys in smem
     uint32_t buf[2][kPacked ? CAP : 1];                   // large variant: packed sort
@@ -54,21 +59,21 @@ __global__ void __launch_bounds__(kSortThreadsA) k4a_sort(CompositeArgs a) {
   if (len <= CAP) {
     if constexpr (Sh::kPacked) {
       const uint64_t* gk = a.keys + start;
-      const bool in_b = packed_sort(gk, len, sm.u.buf[0], sm.u.buf[1], sm.sort);
+      const bool in_b = packed_sort(gk, len, sm.u.buf[0], sm.u.buf[1], sm.s.sort);
       const uint32_t* res = sm.u.buf[in_b ? 1 : 0];
       for (int e = tid; e < len; e += kSortThreadsA)
         dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)__ldg(gk + (res[e] & 0xffffu))) - base);
     } else {
       for (int e = tid; e < len; e += kSortThreadsA) sm.u.keys[0][e] = a.keys[start + e];
       __syncthreads();
-      const bool in_b = segment_sort(sm.u.keys[0], sm.u.keys[1], len, sm.sort);
-      const uint64_t* r = sm.u.keys[in_b ? 1 : 0];
+      count_sort(sm.u.keys[0], sm.u.keys[1], len, sm.s.count);
+      const uint64_t* r = sm.u.keys[1];
       for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)r[e]) - base);
     }
   } else {  // longer than the shared-memory capacity: 64-bit keys sorted in HBM
     uint64_t* ga = const_cast<uint64_t*>(a.keys) + start;
     uint64_t* gb = a.keys_alt + start;
-    const bool in_b = segment_sort(ga, gb, len, sm.sort);
+    const bool in_b = segment_sort(ga, gb, len, sm.s.sort);
     const uint64_t* r = in_b ? gb : ga;
     for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)r[e]) - base);
   }
