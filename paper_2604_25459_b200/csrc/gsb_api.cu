@@ -341,13 +341,18 @@ struct Pipeline {
       c.obs_seed = s->obs->seed; c.obs_step = s->obs->step;
       c.obs_frame_offset = s->obs->env_offset * (int64_t)n_cams;
     }
-    tm.begin(KC_COMPOSITE);
     // many lists beyond the small fused-sort capacity (e.g. 128x128 views): larger variant
     const bool long_lists = (uint64_t)n_long * 4 > (uint64_t)(fe - fs) * n_tiles;
     if (!merge && !c.score_sum && split_k4()) {
-      launch_k4_split(c, long_lists, s->d_counter, st);   // K4a sort + K4b persistent warps
+      tm.begin(KC_SORT);
+      launch_k4a_sort(c, long_lists, st);   // K4a: tile sort -> id-ordered record slots
       s->launches++;
+      LAUNCH_CHECK();
+      tm.end();
+      tm.begin(KC_COMPOSITE);
+      launch_k4b_blend(c, s->d_counter, st);   // K4b: persistent per-warp compositing
     } else {
+      tm.begin(KC_COMPOSITE);
       launch_k4_composite(c, long_lists, st);
     }
     s->launches++;

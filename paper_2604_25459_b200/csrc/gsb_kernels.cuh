@@ -145,7 +145,8 @@ void launch_k3_prebin_gather(const uint32_t* sorted, const uint64_t* frame_base,
 void launch_k4_composite(const CompositeArgs& a, bool long_lists, cudaStream_t s);
 // split path (plain / observation renders): K4a tile sort into a.sorted, then K4b persistent
 // per-warp compositing; counter = one int of device scratch
-void launch_k4_split(const CompositeArgs& a, bool long_lists, int* counter, cudaStream_t s);
+void launch_k4a_sort(const CompositeArgs& a, bool long_lists, cudaStream_t s);
+void launch_k4b_blend(const CompositeArgs& a, int* counter, cudaStream_t s);
 void launch_k4_scores_export(const float* wsum, const uint32_t* wmax, const int2* ids, int64_t n, float* out_sum,
                              float* out_max, cudaStream_t s);
 

@@ -21,7 +21,7 @@
 
 namespace gsb {
 
-constexpr int kSortThreadsA = 128;
+constexpr int kSortThreadsA = 256;
 
 constexpr int kCountBits = 11;   // K4a counting-sort buckets (2048)
 
@@ -223,12 +223,17 @@ static void launch_k4a_variant(const CompositeArgs& a, unsigned grid, cudaStream
   k4a_sort<CAP><<<grid, kSortThreadsA, sizeof(K4aShared<CAP>), s>>>(a);
 }
 
-void launch_k4_split(const CompositeArgs& a, bool long_lists, int* counter, cudaStream_t s) {
+void launch_k4a_sort(const CompositeArgs& a, bool long_lists, cudaStream_t s) {
   const int nf = a.fe - a.fs;
   if (nf <= 0) return;
   const unsigned grid = (unsigned)nf * a.n_tiles;
   if (long_lists) launch_k4a_variant<4 * kFusedSortCap>(a, grid, s);
   else launch_k4a_variant<kFusedSortCap>(a, grid, s);
+}
+
+void launch_k4b_blend(const CompositeArgs& a, int* counter, cudaStream_t s) {
+  const int nf = a.fe - a.fs;
+  if (nf <= 0) return;
   static int persistent = 0;
   if (!persistent) {
     int dev = 0, sms = 0, per_sm = 0;
@@ -237,7 +242,7 @@ void launch_k4_split(const CompositeArgs& a, bool long_lists, int* counter, cuda
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4b_blend, kBlendWarps * 32, 0);
     persistent = std::max(1, sms * std::max(1, per_sm));
   }
-  const long long items = (long long)grid * 4;
+  const long long items = (long long)nf * a.n_tiles * 4;
   cudaMemsetAsync(counter, 0, sizeof(int), s);
   const unsigned g = (unsigned)std::min<long long>(persistent, (items + kBlendWarps - 1) / kBlendWarps);
   k4b_blend<<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);

@@ -40,7 +40,7 @@ with open(os.path.join(dst, f"{tag}_launch_shares.txt"), "w") as f:
         f.write(f"{n:60s} {c:8d} {v:10.2f} {100 * v / tot:6.1f}%\n")
 print(open(os.path.join(dst, f"{tag}_launch_shares.txt")).read())
 
-for k in ("k4", "k1", "k2", "k3"):
+for k in ("k4b", "k4a", "k4", "k1", "k2", "k3"):
     rep = os.path.join(src, f"{k}.ncu-rep")
     if not os.path.exists(rep):
         continue
@@ -51,12 +51,12 @@ for k in ("k4", "k1", "k2", "k3"):
             f.write(f"== {d.pop('kernel')}\n")
             for kk, v in d.items():
                 f.write(f"   {kk:66s} {v}\n")
-    if k == "k4":
+    if k == "k4b" or (k == "k4" and not os.path.exists(os.path.join(src, "k4b.ncu-rep"))):
         d = summary(rep)[0]
         rd = float(d["dram__bytes_read.sum"].split()[0]) * (1e6 if "Mbyte" in d["dram__bytes_read.sum"] else 1e9 if "Gbyte" in d["dram__bytes_read.sum"] else 1.0)
         wr = float(d["dram__bytes_write.sum"].split()[0]) * (1e6 if "Mbyte" in d["dram__bytes_write.sum"] else 1e9 if "Gbyte" in d["dram__bytes_write.sum"] else 1.0)
-        json.dump({"tag": tag, "kernel": "k4_composite", "dram_bytes_read": rd, "dram_bytes_write": wr,
+        json.dump({"tag": tag, "kernel": "k4b_blend" if k == "k4b" else "k4_composite", "dram_bytes_read": rd, "dram_bytes_write": wr,
                    "dram_bytes_per_launch": rd + wr, "frames_per_launch": 64,
-                   "source": f"profiles/{tag}_k4_ncu_full.txt"},
+                   "source": f"profiles/{tag}_{k}_ncu_full.txt"},
                   open(os.path.join(dst, "k4_ncu_summary.json"), "w"), indent=1)
     print("wrote", k)
