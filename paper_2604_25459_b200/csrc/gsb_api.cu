@@ -87,6 +87,7 @@ bool split_k4() {
   }();
   return v != 0;
 }
+constexpr int kSplitMinAvgList = 200;  // keys per tile (pass average) for the split path
 
 }  // namespace
 
@@ -305,7 +306,7 @@ struct Pipeline {
     return GSB_OK;
   }
 
-  gsb_status pass(int sl, int f0, int fs, int fe, uint64_t key_base, uint32_t n_long) {
+  gsb_status pass(int sl, int f0, int fs, int fe, uint64_t key_base, uint64_t n_keys, uint32_t n_long) {
     ChunkArgs a{};
     a.rec = s->rec[sl]; a.emit = s->emit[sl]; a.ids = s->d_ids + first; a.n = count; a.vis_bits = s->vis_bits[sl]; a.vis_words = s->vis_words; a.hist = s->hist[sl];
     a.hist_stride = s->hist_stride; a.off = s->off[sl]; a.frame_base = s->frame_base[sl];
@@ -343,7 +344,10 @@ struct Pipeline {
     }
     // many lists beyond the small fused-sort capacity (e.g. 128x128 views): larger variant
     const bool long_lists = (uint64_t)n_long * 4 > (uint64_t)(fe - fs) * n_tiles;
-    if (!merge && !c.score_sum && split_k4()) {
+    // split K4a + K4b unless the lists are short on average (then the one-CTA-per-tile kernel's
+    // shared staging beats per-warp record reads; measured crossover ~200-330 keys per tile)
+    const bool split = split_k4() && n_keys >= (uint64_t)kSplitMinAvgList * (uint64_t)(fe - fs) * n_tiles;
+    if (!merge && !c.score_sum && split) {
       tm.begin(KC_SORT);
       launch_k4a_sort(c, long_lists, st);   // K4a: tile sort -> id-ordered record slots
       s->launches++;
@@ -410,7 +414,7 @@ struct Pipeline {
     const uint32_t n_long = (uint32_t)rb[2 * nf + 2];
     s->stat_long += n_long;
     s->stat_maxseg = std::max<int64_t>(s->stat_maxseg, (int64_t)fb[nf + 1]);
-    if (fb[nf] <= (uint64_t)s->cap) return pass(sl, f0, 0, nf, 0, n_long);
+    if (fb[nf] <= (uint64_t)s->cap) return pass(sl, f0, 0, nf, 0, fb[nf], n_long);
     // split the chunk's frames into passes that fit the key workspace
     int fs = 0;
     while (fs < nf) {
@@ -419,7 +423,7 @@ struct Pipeline {
       if (fe == fs)
         return fail(GSB_ERR_CAPACITY, "frame %d needs %llu tile keys > key capacity %lld", f0 + fs,
                     (unsigned long long)(fb[fs + 1] - fb[fs]), (long long)s->cap);
-      gsb_status r = pass(sl, f0, fs, fe, fb[fs], n_long);
+      gsb_status r = pass(sl, f0, fs, fe, fb[fs], fb[fe] - fb[fs], n_long);
       if (r != GSB_OK) return r;
       fs = fe;
     }
