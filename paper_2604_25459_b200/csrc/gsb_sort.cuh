@@ -184,21 +184,21 @@ __device__ __forceinline__ bool segment_sort(Ptr a, Ptr b, int n, SortShared<NT>
 // ---------------------------------------------------------------------------------------------
 // Single-pass counting sort for short segments (K4a, lists up to a few thousand keys): bucket
 // = the BITS highest varying bits of (zbits - zmin); histogram with shared atomics, one block
-// scan, scatter with atomic cursors (order inside a bucket arbitrary), then the buckets holding
-// several keys are finished by the full key (zbits, id) — reading R10; the result is the unique
-// order whatever the scatter order.  Two barrier-light phases instead of two radix passes.
+// scan, scatter with atomic cursors (order inside a bucket arbitrary); then every key takes its
+// rank among the keys of its own bucket (full key (zbits, id), reading R10) and lands at
+// bucket start + rank.  Keys are unique, so the result is the unique order whatever the
+// scatter order; ranking is parallel over keys (a bucket of m keys costs m reads per key), so
+// skewed depth distributions do not serialise.  In: a; scratch: b; result: a.
 template <int NT, int BITS>
 struct CountShared {
   static constexpr int kBins = 1 << BITS;
   static constexpr int kWarps = NT / 32;
   uint32_t bins[kBins];
   uint32_t wred[kWarps];
-  uint32_t dup;
 };
 
-// a -> b (a is left unchanged)
 template <int NT, int BITS>
-__device__ __forceinline__ void count_sort(const uint64_t* a, uint64_t* b, int n, CountShared<NT, BITS>& sm) {
+__device__ __forceinline__ void count_sort(uint64_t* a, uint64_t* b, int n, CountShared<NT, BITS>& sm) {
   using Sh = CountShared<NT, BITS>;
   constexpr int PER = Sh::kBins / NT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -206,7 +206,6 @@ __device__ __forceinline__ void count_sort(const uint64_t* a, uint64_t* b, int n
   for (int e = tid; e < n; e += NT) zmin = min(zmin, hi32(a[e]));
   zmin = __reduce_min_sync(0xffffffffu, zmin);
   if (lane == 0) sm.wred[warp] = zmin;
-  if (tid == 0) sm.dup = 0;
 #pragma unroll
   for (int k = 0; k < PER; ++k) sm.bins[tid + k * NT] = 0;
   __syncthreads();
@@ -223,10 +222,7 @@ __device__ __forceinline__ void count_sort(const uint64_t* a, uint64_t* b, int n
   for (int w = 0; w < Sh::kWarps; ++w) orx |= sm.wred[w];
   const int hb = orx ? 31 - __clz(orx) : -1;          // highest varying bit of (zbits - zmin)
   const int lo = hb >= BITS ? hb - BITS + 1 : 0;      // bucket = bits [lo, lo + BITS)
-  // histogram (a key landing in an occupied bucket marks the segment for the fix-up)
-  uint32_t dup = 0;
-  for (int e = tid; e < n; e += NT) dup |= atomicAdd(&sm.bins[(hi32(a[e]) - zmin) >> lo], 1u);
-  if (dup) sm.dup = 1;
+  for (int e = tid; e < n; e += NT) atomicAdd(&sm.bins[(hi32(a[e]) - zmin) >> lo], 1u);
   __syncthreads();
   // exclusive scan of the buckets: PER consecutive buckets per thread
   uint32_t v[PER], sum = 0;
@@ -246,15 +242,22 @@ __device__ __forceinline__ void count_sort(const uint64_t* a, uint64_t* b, int n
 #pragma unroll
   for (int k = 0; k < PER; ++k) { sm.bins[tid * PER + k] = run; run += v[k]; }
   __syncthreads();
-  // scatter
+  // scatter (cursors advance: afterwards bins[k] = end of bucket k = start of bucket k + 1)
   for (int e = tid; e < n; e += NT) {
     const uint64_t key = a[e];
     b[atomicAdd(&sm.bins[(hi32(key) - zmin) >> lo], 1u)] = key;
   }
   __syncthreads();
-  if (sm.dup)   // uniform
-    fix_runs<NT>(b, n, [&](uint64_t k) { return (hi32(k) - zmin) >> lo; },
-                 [](uint64_t x, uint64_t y) { return x < y; });
+  // rank inside the bucket by the full key
+  for (int p = tid; p < n; p += NT) {
+    const uint64_t key = b[p];
+    const uint32_t bk = (hi32(key) - zmin) >> lo;
+    const int s0 = bk ? (int)sm.bins[bk - 1] : 0, s1 = (int)sm.bins[bk];
+    int rank = 0;
+    for (int q = s0; q < s1; ++q) rank += b[q] < key;
+    a[s0 + rank] = key;
+  }
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------------------------

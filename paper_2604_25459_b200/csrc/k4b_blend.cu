@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kSortThreadsA) k4a_sort(CompositeArgs a) {
       for (int e = tid; e < len; e += kSortThreadsA) sm.u.keys[0][e] = a.keys[start + e];
       __syncthreads();
       count_sort(sm.u.keys[0], sm.u.keys[1], len, sm.s.count);
-      const uint64_t* r = sm.u.keys[1];
+      const uint64_t* r = sm.u.keys[0];
       for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)r[e]) - base);
     }
   } else {  // longer than the shared-memory capacity: 64-bit keys sorted in HBM
