@@ -38,7 +38,10 @@ constexpr int kStageQuads = 2 * 3 * kBatch;
 template <int CAP, bool MERGE = false, bool SCORE = false>
 struct K4Shared {
   static constexpr bool kPacked = CAP > kFusedSortCap;
-  SortShared<kCompThreads> sort;
+  union {   // radix sort (packed / HBM lists, merge variant) or counting sort (small variant)
+    SortShared<kCompThreads> sort;
+    CountShared<kCompThreads, MERGE ? 7 : 11> count;   // (merge variant: unused, kept small)
+  } s;
   union {
     uint64_t keys[kPacked ? 1 : 2][kPacked ? 1 : CAP];         // small variant: 64-bit sort
     struct {
@@ -111,7 +114,7 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
     stg = reinterpret_cast<float4*>(sm.u.buf[0]);
     if (fused && len > 0) {
       const uint64_t* gk = a.keys + start;
-      const bool in_b = packed_sort(gk, len, sm.u.buf[0], sm.u.buf[1], sm.sort);
+      const bool in_b = packed_sort(gk, len, sm.u.buf[0], sm.u.buf[1], sm.s.sort);
       const uint32_t* res = sm.u.buf[in_b ? 1 : 0];
       uint32_t* sl = sm.u.buf[in_b ? 0 : 1];
       for (int e = tid; e < len; e += kCompThreads)
@@ -125,7 +128,12 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
     if (fused && len > 0) {
       for (int e = tid; e < len; e += kCompThreads) sm.u.keys[0][e] = a.keys[start + e];
       __syncthreads();
-      const bool in_b = len > 1 && segment_sort(sm.u.keys[0], sm.u.keys[1], len, sm.sort);
+      bool in_b = false;
+      if constexpr (MERGE) {   // shared memory is tight here (qpos): the radix sort
+        in_b = len > 1 && segment_sort(sm.u.keys[0], sm.u.keys[1], len, sm.s.sort);
+      } else if (len > 1) {
+        count_sort(sm.u.keys[0], sm.u.keys[1], len, sm.s.count);   // result in keys[0]
+      }
       uint32_t sl[CAP / kCompThreads];
 #pragma unroll
       for (int k = 0; k < CAP / kCompThreads; ++k) {
@@ -148,7 +156,7 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
   if (!fused) {
     uint64_t* ga = const_cast<uint64_t*>(a.keys) + start;
     uint64_t* gb = a.keys_alt + start;
-    const bool in_b = segment_sort(ga, gb, len, sm.sort);
+    const bool in_b = segment_sort(ga, gb, len, sm.s.sort);
     uint32_t* dst = a.sorted + start;
     const uint64_t* r = in_b ? gb : ga;
     for (int e = tid; e < len; e += kCompThreads) dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)r[e]) - a.slot_base);
