@@ -87,7 +87,15 @@ bool split_k4() {
   }();
   return v != 0;
 }
-constexpr int kSplitMinAvgList = 200;  // keys per tile (pass average) for the split path
+constexpr int kSplitMinAvgList = 200;
+
+bool two_streams() {   // GSB_STREAMS=1: everything on the caller's stream (A/B comparisons)
+  static const bool v = [] {
+    const char* e = getenv("GSB_STREAMS");
+    return !(e && e[0] == '1');
+  }();
+  return v;
+}  // keys per tile (pass average) for the split path
 
 }  // namespace
 
@@ -125,6 +133,11 @@ struct gsb_scene_t {
   uint64_t* h_rb[2] = {nullptr, nullptr};   // mapped pinned readback: fb[E+2], vcount[E], n_long
   uint64_t* d_rb[2] = {nullptr, nullptr};   // its device view
   cudaEvent_t ev_counts[2] = {nullptr, nullptr};
+  // two internal streams: projection (K1, K2a) runs one chunk ahead of binning + compositing
+  // (K2b, K4a, K4b), so the latency-bound kernels of one overlap the other's
+  cudaStream_t sp = nullptr, sc = nullptr;
+  cudaEvent_t ev_done[2] = {nullptr, nullptr};   // chunk slot free again (its compositing done)
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr;
   uint64_t *keys = nullptr, *keys_alt = nullptr;
   uint32_t* sorted = nullptr;
   unsigned long long* d_pairs = nullptr;
@@ -191,6 +204,12 @@ struct gsb_scene_t {
     cudaFree(st_rgb); cudaFree(st_depth); cudaFree(st_alpha); cudaFree(st_neval); cudaFree(st_dr);
     st_dr = nullptr;
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (sp) cudaStreamDestroy(sp);
+    if (sc) cudaStreamDestroy(sc);
+    for (auto& e : ev_done) { if (e) cudaEventDestroy(e); e = nullptr; }
+    if (ev_start) cudaEventDestroy(ev_start);
+    if (ev_end) cudaEventDestroy(ev_end);
+    sp = sc = nullptr; ev_start = ev_end = nullptr;
     if (ev_copy) cudaEventDestroy(ev_copy);
     for (auto e : ev_pool) cudaEventDestroy(e);
     ev_pool.clear();
@@ -227,16 +246,18 @@ struct Timer {
   bool on;
   size_t begin_idx = 0;
   int cls = 0;
-  void begin(int c) {
+  cudaStream_t cur = nullptr;
+  void begin(int c, cudaStream_t on_stream) {
     if (!on) return;
     if (s->ev_used + 2 > s->ev_pool.size()) { on = false; return; }
     cls = c;
+    cur = on_stream;
     begin_idx = s->ev_used;
-    cudaEventRecord(s->ev_pool[s->ev_used++], st);
+    cudaEventRecord(s->ev_pool[s->ev_used++], cur);
   }
   void end() {
     if (!on) return;
-    cudaEventRecord(s->ev_pool[s->ev_used++], st);
+    cudaEventRecord(s->ev_pool[s->ev_used++], cur);
     s->ev_marks.push_back({cls, begin_idx});
   }
 };
@@ -265,7 +286,8 @@ gsb_status validate_render(gsb_scene s, const float* poses, int n_envs, int n_ca
 
 struct Pipeline {
   gsb_scene_t* s;
-  cudaStream_t st;
+  cudaStream_t st;        // the caller's stream
+  cudaStream_t sp, sc;    // projection / compositing streams (== st when GSB_STREAMS=1)
   const gsb_render_params* p;
   int F, W, H, tiles_x, n_tiles, D, n_cams;
   Timer tm;
@@ -278,9 +300,10 @@ struct Pipeline {
 
   gsb_status project_chunk(int c, int f0, int nf) {
     const int sl = c & 1;
-    CUDA_TRY(cudaMemsetAsync(s->vcount[sl], 0, sizeof(int) * nf, st));
-    CUDA_TRY(cudaMemsetAsync(s->long_cnt[sl], 0, sizeof(uint32_t), st));
-    CUDA_TRY(cudaMemsetAsync(s->hist[sl], 0, sizeof(int) * s->hist_stride * nf, st));
+    if (c >= 2) CUDA_TRY(cudaStreamWaitEvent(sp, s->ev_done[sl], 0));   // chunk c-2 left this slot
+    CUDA_TRY(cudaMemsetAsync(s->vcount[sl], 0, sizeof(int) * nf, sp));
+    CUDA_TRY(cudaMemsetAsync(s->long_cnt[sl], 0, sizeof(uint32_t), sp));
+    CUDA_TRY(cudaMemsetAsync(s->hist[sl], 0, sizeof(int) * s->hist_stride * nf, sp));
     K1Args a{};
     a.g_mean = s->d_mean + first; a.g_L0 = s->d_L0 + first; a.g_L1 = s->d_L1 + first;
     a.g_L2 = s->d_L2 + first; a.g_sh = s->d_sh + first;
@@ -291,18 +314,18 @@ struct Pipeline {
     a.rec = s->rec[sl]; a.emit = s->emit[sl];
     a.vcount = s->vcount[sl]; a.hist = s->hist[sl]; a.hist_stride = s->hist_stride;
     a.vis_bits = s->vis_bits[sl]; a.vis_words = s->vis_words;
-    tm.begin(KC_PROJECT);
-    launch_k1(a, D, st);
+    tm.begin(KC_PROJECT, sp);
+    launch_k1(a, D, sp);
     if (count > 0) s->launches++;
     LAUNCH_CHECK();
     tm.end();
-    tm.begin(KC_SCAN);
+    tm.begin(KC_SCAN, sp);
     launch_k2_scan(s->hist[sl], s->off[sl], s->hist_stride, nf, n_tiles, s->frame_base[sl], s->long_list[sl],
-                   s->long_cnt[sl], kFusedSortCap, s->vcount[sl], s->d_rb[sl], st);
+                   s->long_cnt[sl], kFusedSortCap, s->vcount[sl], s->d_rb[sl], sp);
     s->launches += 2;
     LAUNCH_CHECK();
     tm.end();
-    CUDA_TRY(cudaEventRecord(s->ev_counts[sl], st));
+    CUDA_TRY(cudaEventRecord(s->ev_counts[sl], sp));
     return GSB_OK;
   }
 
@@ -313,8 +336,8 @@ struct Pipeline {
     a.n_tiles = n_tiles; a.tiles_x = tiles_x; a.fs = fs; a.fe = fe; a.key_base = key_base;
     a.keys = s->keys; a.keys_alt = s->keys_alt; a.sorted = s->sorted;
     a.long_list = s->long_list[sl];
-    tm.begin(KC_EMIT);
-    launch_k2_emit(a, st);
+    tm.begin(KC_EMIT, sc);
+    launch_k2_emit(a, sc);
     if (count > 0) s->launches++;
     LAUNCH_CHECK();
     tm.end();
@@ -348,23 +371,23 @@ struct Pipeline {
     // shared staging beats per-warp record reads; measured crossover ~200-330 keys per tile)
     const bool split = split_k4() && n_keys >= (uint64_t)kSplitMinAvgList * (uint64_t)(fe - fs) * n_tiles;
     if (!merge && !c.score_sum && split) {
-      tm.begin(KC_SORT);
-      launch_k4a_sort(c, long_lists, st);   // K4a: tile sort -> id-ordered record slots
+      tm.begin(KC_SORT, sc);
+      launch_k4a_sort(c, long_lists, sc);   // K4a: tile sort -> id-ordered record slots
       s->launches++;
       LAUNCH_CHECK();
       tm.end();
-      tm.begin(KC_COMPOSITE);
-      launch_k4b_blend(c, s->d_counter, st);   // K4b: persistent per-warp compositing
+      tm.begin(KC_COMPOSITE, sc);
+      launch_k4b_blend(c, s->d_counter, sc);   // K4b: persistent per-warp compositing
     } else {
-      tm.begin(KC_COMPOSITE);
-      launch_k4_composite(c, long_lists, st);
+      tm.begin(KC_COMPOSITE, sc);
+      launch_k4_composite(c, long_lists, sc);
     }
     s->launches++;
     s->comp_launches++;
     LAUNCH_CHECK();
     tm.end();
     if (s->dl_rgb8) {  // host-io observations: uint8 RGB (+ fp16 or fp32 depth)
-      CUDA_TRY(cudaEventRecord(s->ev_copy, st));
+      CUDA_TRY(cudaEventRecord(s->ev_copy, sc));
       CUDA_TRY(cudaStreamWaitEvent(s->copy_stream, s->ev_copy, 0));
       const size_t plane = (size_t)W * H;
       const size_t a0 = (size_t)(f0 + fs), cnt = (size_t)(fe - fs);
@@ -377,7 +400,7 @@ struct Pipeline {
         CUDA_TRY(cudaMemcpyAsync(s->dl_depth + a0 * plane, out_depth + a0 * plane, cnt * plane * 4,
                                  cudaMemcpyDeviceToHost, s->copy_stream));
     } else if (s->dl_rgb) {  // host-io: download this pass's frames on the copy stream
-      CUDA_TRY(cudaEventRecord(s->ev_copy, st));
+      CUDA_TRY(cudaEventRecord(s->ev_copy, sc));
       CUDA_TRY(cudaStreamWaitEvent(s->copy_stream, s->ev_copy, 0));
       const size_t plane = (size_t)W * H;
       const size_t a0 = (size_t)(f0 + fs), cnt = (size_t)(fe - fs);
@@ -399,6 +422,14 @@ struct Pipeline {
   gsb_status finish_chunk(int c, int f0, int nf) {
     const int sl = c & 1;
     CUDA_TRY(cudaEventSynchronize(s->ev_counts[sl]));
+    gsb_status r = finish_passes(c, f0, nf);
+    if (r != GSB_OK) return r;
+    CUDA_TRY(cudaEventRecord(s->ev_done[sl], sc));
+    return GSB_OK;
+  }
+
+  gsb_status finish_passes(int c, int f0, int nf) {
+    const int sl = c & 1;
     const volatile uint64_t* rb = s->h_rb[sl];
     uint64_t fb[kMaxChunk + 2];
     for (int i = 0; i < nf + 2; ++i) fb[i] = rb[i];
@@ -431,11 +462,25 @@ struct Pipeline {
   }
 
   gsb_status run(const K0Rig& rig, int n_cams) {
-    tm.begin(KC_SETUP);
+    tm.begin(KC_SETUP, st);
     launch_k0(rig, F, n_cams, s->n_bodies, W, H, s->table, s->cams, st);
     s->launches++;
     LAUNCH_CHECK();
     tm.end();
+    if (sp != st) {   // the internal streams start after everything the caller enqueued
+      CUDA_TRY(cudaEventRecord(s->ev_start, st));
+      CUDA_TRY(cudaStreamWaitEvent(sp, s->ev_start, 0));
+      CUDA_TRY(cudaStreamWaitEvent(sc, s->ev_start, 0));
+    }
+    gsb_status r = run_chunks();
+    if (sp != st) {   // and the caller's stream continues after the last composite
+      CUDA_TRY(cudaEventRecord(s->ev_end, sc));
+      CUDA_TRY(cudaStreamWaitEvent(st, s->ev_end, 0));
+    }
+    return r;
+  }
+
+  gsb_status run_chunks() {
     const int E = s->chunk;
     const int nchunks = (F + E - 1) / E;
     for (int c = 0; c < nchunks; ++c) {
@@ -482,7 +527,12 @@ gsb_status render_impl(gsb_scene s, const K0Rig& rig, int n_envs, int n_cams, co
   }
   if (p->flags & GSB_FLAG_STATS) CUDA_TRY(cudaMemsetAsync(s->d_pairs, 0, sizeof(unsigned long long), st));
   Pipeline pl{};
-  pl.s = s; pl.st = st; pl.p = p; pl.F = F; pl.W = p->width; pl.H = p->height;
+  pl.s = s; pl.st = st; pl.p = p;
+  pl.sp = pl.sc = st;
+  if (two_streams() && s->sp && s->sc) {
+    pl.sp = s->sp;
+    pl.sc = s->sc;
+  } pl.F = F; pl.W = p->width; pl.H = p->height;
   pl.tiles_x = (p->width + kTile - 1) / kTile;
   pl.n_tiles = pl.tiles_x * ((p->height + kTile - 1) / kTile);
   pl.D = p->sh_degree < 0 ? s->sh_degree : p->sh_degree;
@@ -686,6 +736,11 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
   CUDA_TRY(dalloc(&s->sorted, (size_t)cap));
   CUDA_TRY(dalloc(&s->d_pairs, 1));
   CUDA_TRY(dalloc(&s->d_counter, 1));
+  CUDA_TRY(cudaStreamCreateWithFlags(&s->sp, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&s->sc, cudaStreamNonBlocking));
+  for (auto& e : s->ev_done) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&s->ev_start, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&s->ev_end, cudaEventDisableTiming));
   if (s->sb_cams > 0) CUDA_TRY(dalloc(&s->qpos, (size_t)cap));
   s->host_io = (flags & GSB_RESERVE_HOST_IO) != 0;
   if (s->host_io) {
