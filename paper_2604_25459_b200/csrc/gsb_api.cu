@@ -95,6 +95,13 @@ bool two_streams() {   // GSB_STREAMS=1: everything on the caller's stream (A/B 
     return !(e && e[0] == '1');
   }();
   return v;
+}
+bool three_streams() {   // GSB_STREAMS=2: binning/sort on the compositing stream
+  static const bool v = [] {
+    const char* e = getenv("GSB_STREAMS");
+    return !(e && (e[0] == '1' || e[0] == '2'));
+  }();
+  return v;
 }  // keys per tile (pass average) for the split path
 
 }  // namespace
@@ -137,6 +144,13 @@ struct gsb_scene_t {
   // (K2b, K4a, K4b), so the latency-bound kernels of one overlap the other's
   cudaStream_t sp = nullptr, sc = nullptr;
   cudaEvent_t ev_done[2] = {nullptr, nullptr};   // chunk slot free again (its compositing done)
+  // third stream: binning + tile sort (K2b, K4a, fused K4) of pass q overlaps K4b of pass q-1;
+  // `sorted` is double-buffered by pass parity
+  cudaStream_t sb = nullptr;
+  uint32_t* sorted2 = nullptr;
+  cudaEvent_t ev_sorted[2] = {nullptr, nullptr};  // K4a of the pass with this parity done
+  cudaEvent_t ev_k4b[2] = {nullptr, nullptr};     // K4b of the pass with this parity done
+  cudaEvent_t ev_bin = nullptr;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr;
   uint64_t *keys = nullptr, *keys_alt = nullptr;
   uint32_t* sorted = nullptr;
@@ -206,6 +220,14 @@ struct gsb_scene_t {
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (sp) cudaStreamDestroy(sp);
     if (sc) cudaStreamDestroy(sc);
+    if (sb) cudaStreamDestroy(sb);
+    sb = nullptr;
+    cudaFree(sorted2);
+    sorted2 = nullptr;
+    for (auto& e : ev_sorted) { if (e) cudaEventDestroy(e); e = nullptr; }
+    for (auto& e : ev_k4b) { if (e) cudaEventDestroy(e); e = nullptr; }
+    if (ev_bin) cudaEventDestroy(ev_bin);
+    ev_bin = nullptr;
     for (auto& e : ev_done) { if (e) cudaEventDestroy(e); e = nullptr; }
     if (ev_start) cudaEventDestroy(ev_start);
     if (ev_end) cudaEventDestroy(ev_end);
@@ -288,6 +310,8 @@ struct Pipeline {
   gsb_scene_t* s;
   cudaStream_t st;        // the caller's stream
   cudaStream_t sp, sc;    // projection / compositing streams (== st when GSB_STREAMS=1)
+  cudaStream_t sb;        // binning + sort stream (== sc unless three streams)
+  int pass_idx = 0;       // passes so far in this render (parity selects the `sorted` buffer)
   const gsb_render_params* p;
   int F, W, H, tiles_x, n_tiles, D, n_cams;
   Timer tm;
@@ -334,17 +358,19 @@ struct Pipeline {
     a.rec = s->rec[sl]; a.emit = s->emit[sl]; a.ids = s->d_ids + first; a.n = count; a.vis_bits = s->vis_bits[sl]; a.vis_words = s->vis_words; a.hist = s->hist[sl];
     a.hist_stride = s->hist_stride; a.off = s->off[sl]; a.frame_base = s->frame_base[sl];
     a.n_tiles = n_tiles; a.tiles_x = tiles_x; a.fs = fs; a.fe = fe; a.key_base = key_base;
-    a.keys = s->keys; a.keys_alt = s->keys_alt; a.sorted = s->sorted;
+    const int q = pass_idx & 1;
+    uint32_t* sorted = (q && sb != sc) ? s->sorted2 : s->sorted;
+    a.keys = s->keys; a.keys_alt = s->keys_alt; a.sorted = sorted;
     a.long_list = s->long_list[sl];
-    tm.begin(KC_EMIT, sc);
-    launch_k2_emit(a, sc);
+    tm.begin(KC_EMIT, sb);
+    launch_k2_emit(a, sb);
     if (count > 0) s->launches++;
     LAUNCH_CHECK();
     tm.end();
     // long lists are sorted by their K4 CTA (K3 serves gsb_debug_bin_sort)
     CompositeArgs c{};
     c.rec = s->rec[sl]; c.n = count; c.off = s->off[sl]; c.frame_base = s->frame_base[sl];
-    c.hist_stride = s->hist_stride; c.sorted = s->sorted; c.keys = s->keys; c.keys_alt = s->keys_alt;
+    c.hist_stride = s->hist_stride; c.sorted = sorted; c.keys = s->keys; c.keys_alt = s->keys_alt;
     c.key_base = key_base;
     c.inv = s->d_inv;
     c.slot_base = (int)first;
@@ -370,24 +396,34 @@ struct Pipeline {
     // split K4a + K4b unless the lists are short on average (then the one-CTA-per-tile kernel's
     // shared staging beats per-warp record reads; measured crossover ~200-330 keys per tile)
     const bool split = split_k4() && n_keys >= (uint64_t)kSplitMinAvgList * (uint64_t)(fe - fs) * n_tiles;
+    // `sorted` buffer q was last read by the K4b of pass pass_idx - 2
+    if (sb != sc && pass_idx >= 2) CUDA_TRY(cudaStreamWaitEvent(sb, s->ev_k4b[q], 0));
+    cudaStream_t cs = sb;   // stream of this pass's last compositing kernel
     if (!merge && !c.score_sum && split) {
-      tm.begin(KC_SORT, sc);
-      launch_k4a_sort(c, long_lists, sc);   // K4a: tile sort -> id-ordered record slots
+      tm.begin(KC_SORT, sb);
+      launch_k4a_sort(c, long_lists, sb);   // K4a: tile sort -> id-ordered record slots
       s->launches++;
       LAUNCH_CHECK();
       tm.end();
+      if (sb != sc) {
+        CUDA_TRY(cudaEventRecord(s->ev_sorted[q], sb));
+        CUDA_TRY(cudaStreamWaitEvent(sc, s->ev_sorted[q], 0));
+      }
+      cs = sc;
       tm.begin(KC_COMPOSITE, sc);
       launch_k4b_blend(c, s->d_counter, sc);   // K4b: persistent per-warp compositing
     } else {
-      tm.begin(KC_COMPOSITE, sc);
-      launch_k4_composite(c, long_lists, sc);
+      tm.begin(KC_COMPOSITE, sb);
+      launch_k4_composite(c, long_lists, sb);
     }
     s->launches++;
     s->comp_launches++;
     LAUNCH_CHECK();
     tm.end();
+    if (sb != sc) CUDA_TRY(cudaEventRecord(s->ev_k4b[q], cs));
+    ++pass_idx;
     if (s->dl_rgb8) {  // host-io observations: uint8 RGB (+ fp16 or fp32 depth)
-      CUDA_TRY(cudaEventRecord(s->ev_copy, sc));
+      CUDA_TRY(cudaEventRecord(s->ev_copy, cs));
       CUDA_TRY(cudaStreamWaitEvent(s->copy_stream, s->ev_copy, 0));
       const size_t plane = (size_t)W * H;
       const size_t a0 = (size_t)(f0 + fs), cnt = (size_t)(fe - fs);
@@ -400,7 +436,7 @@ struct Pipeline {
         CUDA_TRY(cudaMemcpyAsync(s->dl_depth + a0 * plane, out_depth + a0 * plane, cnt * plane * 4,
                                  cudaMemcpyDeviceToHost, s->copy_stream));
     } else if (s->dl_rgb) {  // host-io: download this pass's frames on the copy stream
-      CUDA_TRY(cudaEventRecord(s->ev_copy, sc));
+      CUDA_TRY(cudaEventRecord(s->ev_copy, cs));
       CUDA_TRY(cudaStreamWaitEvent(s->copy_stream, s->ev_copy, 0));
       const size_t plane = (size_t)W * H;
       const size_t a0 = (size_t)(f0 + fs), cnt = (size_t)(fe - fs);
@@ -424,6 +460,10 @@ struct Pipeline {
     CUDA_TRY(cudaEventSynchronize(s->ev_counts[sl]));
     gsb_status r = finish_passes(c, f0, nf);
     if (r != GSB_OK) return r;
+    if (sb != sc) {   // the chunk is done when both its binning and its compositing are
+      CUDA_TRY(cudaEventRecord(s->ev_bin, sb));
+      CUDA_TRY(cudaStreamWaitEvent(sc, s->ev_bin, 0));
+    }
     CUDA_TRY(cudaEventRecord(s->ev_done[sl], sc));
     return GSB_OK;
   }
@@ -471,6 +511,7 @@ struct Pipeline {
       CUDA_TRY(cudaEventRecord(s->ev_start, st));
       CUDA_TRY(cudaStreamWaitEvent(sp, s->ev_start, 0));
       CUDA_TRY(cudaStreamWaitEvent(sc, s->ev_start, 0));
+      if (sb != sc) CUDA_TRY(cudaStreamWaitEvent(sb, s->ev_start, 0));
     }
     gsb_status r = run_chunks();
     if (sp != st) {   // and the caller's stream continues after the last composite
@@ -528,10 +569,11 @@ gsb_status render_impl(gsb_scene s, const K0Rig& rig, int n_envs, int n_cams, co
   if (p->flags & GSB_FLAG_STATS) CUDA_TRY(cudaMemsetAsync(s->d_pairs, 0, sizeof(unsigned long long), st));
   Pipeline pl{};
   pl.s = s; pl.st = st; pl.p = p;
-  pl.sp = pl.sc = st;
+  pl.sp = pl.sc = pl.sb = st;
   if (two_streams() && s->sp && s->sc) {
     pl.sp = s->sp;
-    pl.sc = s->sc;
+    pl.sc = pl.sb = s->sc;
+    if (three_streams() && s->sb) pl.sb = s->sb;
   } pl.F = F; pl.W = p->width; pl.H = p->height;
   pl.tiles_x = (p->width + kTile - 1) / kTile;
   pl.n_tiles = pl.tiles_x * ((p->height + kTile - 1) / kTile);
@@ -738,6 +780,11 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
   CUDA_TRY(dalloc(&s->d_counter, 1));
   CUDA_TRY(cudaStreamCreateWithFlags(&s->sp, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&s->sc, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&s->sb, cudaStreamNonBlocking));
+  CUDA_TRY(dalloc(&s->sorted2, (size_t)cap));
+  for (auto& e : s->ev_sorted) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : s->ev_k4b) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&s->ev_bin, cudaEventDisableTiming));
   for (auto& e : s->ev_done) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&s->ev_start, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&s->ev_end, cudaEventDisableTiming));
