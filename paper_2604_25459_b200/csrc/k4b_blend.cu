@@ -15,6 +15,7 @@
 // K4's stall samples, profiles/r04_k4_ncu_full.txt).  Here no warp ever waits for another; the
 // price is reading each record once per warp (from L2) instead of once per CTA.
 #include <algorithm>
+#include <cstdlib>
 
 #include "gsb_sort.cuh"
 #include "k4_common.cuh"
@@ -240,6 +241,7 @@ void launch_k4b_blend(const CompositeArgs& a, int* counter, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4b_blend, kBlendWarps * 32, 0);
+    if (const char* e = getenv("GSB_K4B_PER_SM")) per_sm = std::min(per_sm, atoi(e));
     persistent = std::max(1, sms * std::max(1, per_sm));
   }
   const long long items = (long long)nf * a.n_tiles * 4;
