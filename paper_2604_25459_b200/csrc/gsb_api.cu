@@ -87,7 +87,12 @@ bool split_k4() {
   }();
   return v != 0;
 }
-constexpr int kSplitMinAvgList = 200;
+// pass-average list length (keys per tile) from which the split path is used; GSB_K4_SPLIT_MIN
+// overrides it (read per pass: tests force either path)
+uint64_t split_min_avg() {
+  const char* e = getenv("GSB_K4_SPLIT_MIN");
+  return e ? (uint64_t)strtoull(e, nullptr, 10) : 200u;
+}
 
 bool two_streams() {   // GSB_STREAMS=1: everything on the caller's stream (A/B comparisons)
   static const bool v = [] {
@@ -181,10 +186,11 @@ struct gsb_scene_t {
   uint64_t* bg_keys = nullptr;                    // [K_bg]
   float4* bg_rec = nullptr;                       // [K_bg][3]
   std::vector<int64_t> sb_V, sb_K;                // per camera
+  uint64_t* d_bgcum = nullptr;                    // [C+1] prefix of sb_K (split K4 merge)
   uint32_t* qpos = nullptr;                       // [cap] (workspace, while pre-binned)
   void free_prebin() {
-    cudaFree(sb_intr); cudaFree(sb_w2c); cudaFree(bg_off); cudaFree(bg_keys); cudaFree(bg_rec);
-    sb_intr = sb_w2c = nullptr; bg_off = bg_keys = nullptr; bg_rec = nullptr;
+    cudaFree(sb_intr); cudaFree(sb_w2c); cudaFree(bg_off); cudaFree(bg_keys); cudaFree(bg_rec); cudaFree(d_bgcum);
+    sb_intr = sb_w2c = nullptr; bg_off = bg_keys = nullptr; bg_rec = nullptr; d_bgcum = nullptr;
     sb_cams = 0; sb_V.clear(); sb_K.clear();
   }
   // host-io: where to download outputs of each pass
@@ -374,9 +380,12 @@ struct Pipeline {
     c.key_base = key_base;
     c.inv = s->d_inv;
     c.slot_base = (int)first;
+    uint64_t n_entries = n_keys;   // sorted entries of the pass (merge: + background lists)
     if (merge) {
       c.bg_off = s->bg_off; c.bg_keys = s->bg_keys; c.bg_rec = s->bg_rec; c.n_static_cams = s->sb_cams;
       c.qpos_g = s->qpos;
+      c.bg_cum = s->d_bgcum;
+      for (int f = fs; f < fe; ++f) n_entries += (uint64_t)s->sb_K[(f0 + f) % s->sb_cams];
     }
     c.fs = fs; c.fe = fe; c.f0 = f0; c.width = W; c.height = H; c.tiles_x = tiles_x; c.n_tiles = n_tiles;
     c.bg0 = p->background[0]; c.bg1 = p->background[1]; c.bg2 = p->background[2];
@@ -395,13 +404,14 @@ struct Pipeline {
     const bool long_lists = (uint64_t)n_long * 4 > (uint64_t)(fe - fs) * n_tiles;
     // split K4a + K4b unless the lists are short on average (then the one-CTA-per-tile kernel's
     // shared staging beats per-warp record reads; measured crossover ~200-330 keys per tile)
-    const bool split = split_k4() && n_keys >= (uint64_t)kSplitMinAvgList * (uint64_t)(fe - fs) * n_tiles;
+    const bool split = split_k4() && n_entries >= split_min_avg() * (uint64_t)(fe - fs) * n_tiles &&
+                       n_entries <= (uint64_t)s->cap;
     // `sorted` buffer q was last read by the K4b of pass pass_idx - 2
     if (sb != sc && pass_idx >= 2) CUDA_TRY(cudaStreamWaitEvent(sb, s->ev_k4b[q], 0));
     cudaStream_t cs = sb;   // stream of this pass's last compositing kernel
-    if (!merge && !c.score_sum && split) {
+    if (!c.score_sum && split) {
       tm.begin(KC_SORT, sb);
-      launch_k4a_sort(c, long_lists, sb);   // K4a: tile sort -> id-ordered record slots
+      launch_k4a_sort(c, long_lists && !merge, sb);   // K4a: tile sort (merge) -> ordered record slots
       s->launches++;
       LAUNCH_CHECK();
       tm.end();
@@ -990,9 +1000,16 @@ gsb_status gsb_prebin_static(gsb_scene s, int32_t n_cams, const float* intr, con
 #undef PB_TRY
   s->sb_cams = C; s->sb_w = W; s->sb_h = H; s->sb_D = D; s->sb_near = p->near_plane; s->sb_far = p->far_plane;
   s->sb_V.resize(C); s->sb_K.resize(C);
+  std::vector<uint64_t> cum(C + 1, 0);
   for (int c = 0; c < C; ++c) {
     s->sb_V[c] = hv[c];
     s->sb_K[c] = (int64_t)(hfb[c + 1] - hfb[c]);
+    cum[c + 1] = cum[c] + (uint64_t)s->sb_K[c];
+  }
+  if (dalloc(&s->d_bgcum, (size_t)C + 1) != cudaSuccess ||
+      cudaMemcpy(s->d_bgcum, cum.data(), sizeof(uint64_t) * (C + 1), cudaMemcpyHostToDevice) != cudaSuccess) {
+    s->free_prebin();
+    return fail(GSB_ERR_OUT_OF_MEMORY, "prebin: background size table");
   }
   return GSB_OK;
 }

@@ -82,6 +82,7 @@ struct CompositeArgs {
   const float4* bg_rec;     // [K_bg][3] records (u,v,p,q | r,log2o,ex,ey | rgb,z) in list order
   int n_static_cams;
   uint32_t* qpos_g;         // [cap] merged positions of robot entries of lists sorted in HBM
+  const uint64_t* bg_cum;   // [C+1] prefix of the background list sizes over cameras (split path)
   uint64_t key_base;
   int fs, fe;             // relative frames of this pass
   int f0;                 // absolute frame index of chunk frame 0

@@ -39,6 +39,44 @@ struct K4aShared {
   } u;
 };
 
+// Where the (frame fl, tile t) list lives in the `sorted` buffer.  Plain: at the tile's key
+// offset.  Static-camera merge (gsb_render_static): the merged list of the tile's robot keys
+// and its camera's pre-binned background list; frame regions hold K_rb(f) + K_bg(cam(f))
+// entries, so the frame base adds the background sizes of the pass's earlier frames (prefix
+// table over cameras, cyclic in the frame index) and the tile adds its background offset.
+struct TileList {
+  uint64_t start;   // first entry in `sorted` (and first key of the robot list: rstart)
+  uint64_t rstart;  // first robot key in `keys`
+  int len;          // robot keys
+  int lb;           // background entries (merge)
+  uint64_t bo;      // first background entry in bg_keys / bg_rec (merge)
+};
+
+__device__ __forceinline__ TileList tile_list(const CompositeArgs& a, int fl, int t) {
+  TileList L;
+  const uint32_t* off = a.off + (size_t)fl * a.hist_stride;
+  const uint64_t fb = a.frame_base[fl] - a.key_base;
+  L.rstart = fb + off[t];
+  L.len = (int)(off[t + 1] - off[t]);
+  L.start = L.rstart;
+  L.lb = 0;
+  L.bo = 0;
+  if (a.bg_off) {
+    const int C = a.n_static_cams;
+    const int cam = (a.f0 + fl) % C;
+    const uint64_t* bof = a.bg_off + (size_t)cam * (a.n_tiles + 1);
+    L.bo = bof[t];
+    L.lb = (int)(bof[t + 1] - L.bo);
+    const int n = fl - a.fs, b0 = (a.f0 + a.fs) % C, r = n % C;
+    const uint64_t cyc = (b0 + r <= C) ? a.bg_cum[b0 + r] - a.bg_cum[b0]
+                                       : (a.bg_cum[C] - a.bg_cum[b0]) + a.bg_cum[b0 + r - C];
+    L.start = fb + (uint64_t)(n / C) * a.bg_cum[C] + cyc + off[t] + (L.bo - bof[0]);
+  }
+  return L;
+}
+
+constexpr uint32_t kBgTag = 0x80000000u;   // merged entry: background record index | tag
+
 template <int CAP>
 __global__ void __launch_bounds__(kSortThreadsA) k4a_sort(CompositeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -47,12 +85,56 @@ __global__ void __launch_bounds__(kSortThreadsA) k4a_sort(CompositeArgs a) {
   const int fl = a.fs + blockIdx.x / a.n_tiles;
   const int t = blockIdx.x % a.n_tiles;
   const int tid = threadIdx.x;
-  const uint32_t* off = a.off + (size_t)fl * a.hist_stride;
-  const uint64_t start = a.frame_base[fl] - a.key_base + off[t];
-  const int len = (int)(off[t + 1] - off[t]);
+  const TileList L = tile_list(a, fl, t);
+  const uint64_t start = L.rstart;
+  const int len = L.len;
+  const int base = a.slot_base;
+  if (a.bg_off) {   // static-camera merge (small variant only)
+    if (len + L.lb == 0) return;
+    uint32_t* dst = a.sorted + L.start;
+    const uint64_t* bk = a.bg_keys + L.bo;
+    const uint64_t* rk = nullptr;   // the robot keys in (zbits, id) order
+    if constexpr (!Sh::kPacked) {
+      if (len <= CAP) {
+        for (int e = tid; e < len; e += kSortThreadsA) sm.u.keys[0][e] = a.keys[start + e];
+        __syncthreads();
+        if (len > 1) count_sort(sm.u.keys[0], sm.u.keys[1], len, sm.s.count);
+        rk = sm.u.keys[0];
+      }
+    }
+    if (!rk) {
+      uint64_t* ga = const_cast<uint64_t*>(a.keys) + start;
+      uint64_t* gb = a.keys_alt + start;
+      const bool in_b = len > 1 && segment_sort(ga, gb, len, sm.s.sort);
+      __syncthreads();
+      rk = in_b ? gb : ga;
+    }
+    // keys are unique (R10): an entry's merged position is its own index plus the number of
+    // entries of the other list below it
+    for (int j = tid; j < len; j += kSortThreadsA) {
+      const uint64_t key = rk[j];
+      int lo = 0, hi = L.lb;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(bk + mid) < key) lo = mid + 1;
+        else hi = mid;
+      }
+      dst[j + lo] = (uint32_t)(__ldg(a.inv + (uint32_t)key) - base);
+    }
+    for (int i = tid; i < L.lb; i += kSortThreadsA) {
+      const uint64_t key = __ldg(bk + i);
+      int lo = 0, hi = len;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (rk[mid] < key) lo = mid + 1;
+        else hi = mid;
+      }
+      dst[i + lo] = kBgTag | (uint32_t)(L.bo + i);
+    }
+    return;
+  }
   if (len == 0) return;
   uint32_t* dst = a.sorted + start;
-  const int base = a.slot_base;
   if (len == 1) {
     if (tid == 0) dst[0] = (uint32_t)(__ldg(a.inv + (uint32_t)a.keys[start]) - base);
     return;
@@ -110,11 +192,10 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
     const int py0 = by0 + 2 * (lane >> 3);
     const bool in_x = px < a.width;
     const bool in0 = in_x && py0 < a.height, in1 = in_x && py0 + 1 < a.height;
-    const uint32_t* off = a.off + (size_t)fl * a.hist_stride;
-    const uint64_t start = a.frame_base[fl] - a.key_base + off[t];
-    const int len = (int)(off[t + 1] - off[t]);
+    const TileList L = tile_list(a, fl, t);
+    const int len = L.len + L.lb;   // merged length (lb = 0 unless static-camera merge)
     const float4* rec = a.rec + (size_t)fl * a.n * kRecQuads;
-    const uint32_t* slots = a.sorted + start;
+    const uint32_t* slots = a.sorted + L.start;
     const float pxc = (float)px + 0.5f;
     const float bcx = (float)bx0 + 4.0f, bcy = (float)by0 + 4.0f;  // block centre (pixel centres +-3.5)
 
@@ -129,7 +210,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
     // after the next is read one round ahead, so no cp.async waits on a slot load
     auto stage = [&](int b, uint32_t sl) {
       if (b * kWarpBatch + lane < len) {
-        const float4* r = rec + (size_t)sl * kRecQuads;
+        const float4* r = (sl & kBgTag) ? a.bg_rec + (size_t)(sl & ~kBgTag) * 3 : rec + (size_t)sl * kRecQuads;
         cp_async16(&S[b & 1][0][lane], r);
         cp_async16(&S[b & 1][1][lane], r + 1);
         cp_async16(&S[b & 1][2][lane], r + 2);

@@ -360,3 +360,19 @@ def test_rig_body_cameras_and_strided_poses_bit_identical_and_match_oracle():
     with pytest.raises(gsb.GsbError):
         g.render_rig(gu.to_dev(state), gu.to_dev(b.intrinsics), gu.to_dev(ext), gsb.RenderParams(W, H), rgb,
                      cam_body=cam_body, pose_env_stride=nb * 13, pose_body_stride=5)
+
+
+@pytest.mark.parametrize("name", ["C1", "T1", "T2", "T3", "T4", "T5", "T6"])
+def test_split_and_fused_compositing_bit_identical(name, monkeypatch):
+    """K4a + K4b (persistent warps) and the fused one-CTA-per-tile K4 compute the same
+    per-pixel sequence of operations over the same (z, id) order: forcing either path gives
+    bit-identical rgb, depth, alpha and n_eval (and so both inherit the oracle parity)."""
+    cfg = synth.CONFIGS[name]
+    sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
+    outs = {}
+    for path, thr in (("split", "0"), ("fused", "1000000000")):
+        monkeypatch.setenv("GSB_K4_SPLIT_MIN", thr)
+        outs[path] = gu.gpu_render(sc, b, cfg.width, cfg.height, stats=True)
+    for k in ("rgb", "depth", "alpha", "n_eval"):
+        assert np.array_equal(outs["split"][k], outs["fused"][k]), k
+    assert outs["split"]["stats"] == outs["fused"]["stats"]

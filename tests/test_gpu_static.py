@@ -118,3 +118,20 @@ def test_static_background_and_errors():
     # pre-binning from DEVICE tensors gives the same result
     g.prebin_static(gu.to_dev(Ks), gu.to_dev(Ws), gsb.RenderParams(W, H))
     _assert_identical(_render_static(g, cfg, b.poses, bg=bg), ref)
+
+
+@pytest.mark.parametrize("path", ["split", "fused"])
+@pytest.mark.parametrize("name", ["T2", "T6", "T7"])
+def test_static_merge_both_k4_paths_bit_identical(name, path, monkeypatch):
+    """The merge runs in the split path (K4a writes the merged list, K4b decodes background
+    entries) or in the fused kernel, chosen by list length; force each: bit-identical to
+    gsb_render on the broadcast cameras."""
+    monkeypatch.setenv("GSB_K4_SPLIT_MIN", "0" if path == "split" else "1000000000")
+    cfg = synth.CONFIGS[name]
+    sc = synth.make_scene(cfg)
+    Ks, Ws, b = _static_batch(cfg)
+    ref = gu.gpu_render(sc, b, cfg.width, cfg.height)
+    g = ref["scene"]
+    g.prebin_static(Ks, Ws, gsb.RenderParams(cfg.width, cfg.height))
+    g.reserve(cfg.n_envs, cfg.n_cams, cfg.width, cfg.height)
+    _assert_identical(_render_static(g, cfg, b.poses), ref)
