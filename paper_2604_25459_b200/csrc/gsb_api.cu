@@ -409,7 +409,7 @@ struct Pipeline {
     // `sorted` buffer q was last read by the K4b of pass pass_idx - 2
     if (sb != sc && pass_idx >= 2) CUDA_TRY(cudaStreamWaitEvent(sb, s->ev_k4b[q], 0));
     cudaStream_t cs = sb;   // stream of this pass's last compositing kernel
-    if (!c.score_sum && split) {
+    if (split) {
       tm.begin(KC_SORT, sb);
       launch_k4a_sort(c, long_lists && !merge, sb);   // K4a: tile sort (merge) -> ordered record slots
       s->launches++;

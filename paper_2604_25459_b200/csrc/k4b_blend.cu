@@ -171,6 +171,10 @@ __device__ __forceinline__ void cp_async_wait_group() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// SCORE (GSB_FLAG_SCORES, reading R30): every blended weight is also summed (6.26 fixed point,
+// __reduce_add_sync) and maxed (exact, float bits) over the warp per record, then added to the
+// scene's per-Gaussian accumulators with one global atomic pair per (warp, record).
+template <bool SCORE>
 __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a, int* __restrict__ counter,
                                                                   int n_items) {
   __shared__ __align__(16) float4 stg[kBlendWarps][2][3][kWarpBatch];   // 12 KB
@@ -221,13 +225,15 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
       const int k = b * kWarpBatch + lane;
       return k < len ? __ldg(slots + k) : 0u;
     };
-    uint32_t sl_next = 0;
+    uint32_t sl_next = 0, sl_cur = 0, sl_stg = 0;   // slots of rounds b + 2, b, b + 1 (this lane)
     if (rounds > 0) {
-      stage(0, slot_of(0));
+      sl_cur = slot_of(0);
+      stage(0, sl_cur);
       sl_next = slot_of(1);
     }
     for (int b = 0; b < rounds; ++b) {
       if (b + 1 < rounds) {
+        sl_stg = sl_next;
         stage(b + 1, sl_next);
         sl_next = slot_of(b + 2);
         cp_async_wait_group<1>();
@@ -272,14 +278,25 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
         const float arg1 = fmaf(-tb, tb, mm);
         const bool use0 = arg0 >= kLog2AlphaMin;   // alpha >= 1/255
         const bool use1 = arg1 >= kLog2AlphaMin;
+        float wb0 = 0.f, wb1 = 0.f;
         if (use0 || use1) {
           const float4 q2 = R2[j];                                 // r, g, b, z
-          blend(use0, arg0, q2, T0, r0c, g0c, b0c, d0, pyc0, ne0, base + j);
-          blend(use1, arg1, q2, T1, r1c, g1c, b1c, d1, pyc1, ne1, base + j);
+          wb0 = blend(use0, arg0, q2, T0, r0c, g0c, b0c, d0, pyc0, ne0, base + j);
+          wb1 = blend(use1, arg1, q2, T1, r1c, g1c, b1c, d1, pyc1, ne1, base + j);
+        }
+        if constexpr (SCORE) {
+          const uint32_t tot = __reduce_add_sync(FULL, __float2uint_rn((wb0 + wb1) * kScoreFix));
+          const uint32_t mx = __reduce_max_sync(FULL, __float_as_uint(fmaxf(wb0, wb1)));
+          const uint32_t g = __shfl_sync(FULL, sl_cur, j) + (uint32_t)a.slot_base;
+          if (lane == 0 && tot) {
+            atomicAdd(a.score_sum + g, (float)tot * (1.f / kScoreFix));
+            atomicMax(a.score_max + g, mx);
+          }
         }
         if ((++it & 15) == 0 && __all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) break;
       }
       __syncwarp();   // buffer b & 1 is free for round b + 2
+      sl_cur = sl_stg;
       if (__all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) break;
     }
     cp_async_wait_all();   // nothing may land in the buffers after this item
@@ -321,14 +338,15 @@ void launch_k4b_blend(const CompositeArgs& a, int* counter, cudaStream_t s) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4b_blend, kBlendWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4b_blend<false>, kBlendWarps * 32, 0);
     if (const char* e = getenv("GSB_K4B_PER_SM")) per_sm = std::min(per_sm, atoi(e));
     persistent = std::max(1, sms * std::max(1, per_sm));
   }
   const long long items = (long long)nf * a.n_tiles * 4;
   cudaMemsetAsync(counter, 0, sizeof(int), s);
   const unsigned g = (unsigned)std::min<long long>(persistent, (items + kBlendWarps - 1) / kBlendWarps);
-  k4b_blend<<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
+  if (a.score_sum) k4b_blend<true><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
+  else k4b_blend<false><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
 }
 
 }  // namespace gsb

@@ -30,8 +30,11 @@ def _render(g, b, W, H, scores=False, bg=(0.0, 0.0, 0.0)):
     return dict(rgb=rgb.cpu().numpy(), depth=dep.cpu().numpy(), alpha=alp.cpu().numpy(), n_eval=nev.cpu().numpy())
 
 
+@pytest.mark.parametrize("path", ["split", "fused"])
 @pytest.mark.parametrize("name", ["T1", "T2", "T6"])
-def test_scores_match_oracle(name):
+def test_scores_match_oracle(name, path, monkeypatch):
+    """Both compositing paths (K4b's per-warp atomics, the fused kernel's per-CTA shared sums)."""
+    monkeypatch.setenv("GSB_K4_SPLIT_MIN", "0" if path == "split" else "1000000000")
     cfg = synth.CONFIGS[name]
     sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
     W, H = cfg.width, cfg.height
