@@ -178,9 +178,11 @@ template <bool SCORE>
 __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a, int* __restrict__ counter,
                                                                   int n_items) {
   __shared__ __align__(16) float4 stg[kBlendWarps][2][3][kWarpBatch];   // 12 KB
+  __shared__ uint8_t wlist[kBlendWarps][kWarpBatch];   // a round's records that reach the block
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float4 (*S)[3][kWarpBatch] = stg[warp];
+  uint8_t* wl = wlist[warp];
   for (;;) {
     int item = 0;
     if (lane == 0) item = atomicAdd(counter, 1);
@@ -261,11 +263,15 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
         const float lbq = fmaf(px_, px_, lm * lm);
         ov = lbq <= fmaf(q1.y - kLog2AlphaMin, 1.02f, 0.02f);
       }
-      unsigned m = __ballot_sync(FULL, ov);
-      int it = 0;
-      while (m) {
-        const int j = __ffs(m) - 1;
-        m &= m - 1;
+      const unsigned hit = __ballot_sync(FULL, ov);
+      if (ov) wl[__popc(hit & lanemask_lt())] = (uint8_t)lane;
+      __syncwarp();
+      const int nsel = __popc(hit);
+      for (int i0 = 0; i0 < nsel; i0 += 16) {
+        const int i1 = min(nsel, i0 + 16);
+#pragma unroll 2
+        for (int i = i0; i < i1; ++i) {
+        const int j = wl[i];
         const float4 q0 = R0[j];                                   // u, v, p, q
         const float2 q1 = *reinterpret_cast<const float2*>(&R1[j]);  // r, log2 o
         const float dx = q0.x - pxc;
@@ -293,7 +299,8 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
             atomicMax(a.score_max + g, mx);
           }
         }
-        if ((++it & 15) == 0 && __all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) break;
+        }
+        if (__all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) break;
       }
       __syncwarp();   // buffer b & 1 is free for round b + 2
       sl_cur = sl_stg;
