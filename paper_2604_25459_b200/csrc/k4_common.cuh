@@ -47,6 +47,30 @@ __device__ __forceinline__ float blend(bool use, float arg, const float4& r2, fl
   return 0.f;
 }
 
+// blend() for a thread's two pixels at once.  The termination test's bookkeeping (n_eval,
+// moving the pixel centre away) runs in a warp-uniform branch taken only when some lane
+// terminates at this entry; otherwise the accumulators take unpredicated FMAs whose weight is 0
+// for unused pixels (fma(0, x, c) == c: the accumulators are >= +0), so the result equals
+// blend() bit for bit.  Returns the blended weights (reading R30 scores).
+__device__ __forceinline__ float2 blend2(bool use0, float arg0, bool use1, float arg1, const float4& r2, float& T0,
+                                         float& r0, float& g0, float& b0, float& d0, float& pyc0, int& ne0,
+                                         float& T1, float& r1, float& g1, float& b1, float& d1, float& pyc1,
+                                         int& ne1, int idx) {
+  float w0 = (use0 ? fminf(kAlphaMax, ex2_approx(arg0)) : 0.f) * T0;
+  float w1 = (use1 ? fminf(kAlphaMax, ex2_approx(arg1)) : 0.f) * T1;
+  float t0 = T0 - w0, t1 = T1 - w1;                    // T (1 - alpha)
+  const bool s0 = t0 < kTermT, s1 = t1 < kTermT;       // stop before blending (R13)
+  if (__any_sync(0xffffffffu, s0 || s1)) {
+    if (s0) { ne0 = idx + 1; pyc0 = kFar; w0 = 0.f; t0 = T0; }
+    if (s1) { ne1 = idx + 1; pyc1 = kFar; w1 = 0.f; t1 = T1; }
+  }
+  r0 = fmaf(w0, r2.x, r0); g0 = fmaf(w0, r2.y, g0); b0 = fmaf(w0, r2.z, b0); d0 = fmaf(w0, r2.w, d0);
+  r1 = fmaf(w1, r2.x, r1); g1 = fmaf(w1, r2.y, g1); b1 = fmaf(w1, r2.z, b1); d1 = fmaf(w1, r2.w, d1);
+  T0 = t0;
+  T1 = t1;
+  return make_float2(w0, w1);
+}
+
 // Reading R31 noise: counter-based Irwin-Hall(4) of 22-bit lowbias32-hashed uniforms (exact
 // integer arithmetic, so the oracle reproduces every draw); z * sqrt(3)/2^22 has unit variance.
 __device__ __forceinline__ uint32_t mix32(uint32_t x) {

@@ -285,10 +285,12 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
         const bool use0 = arg0 >= kLog2AlphaMin;   // alpha >= 1/255
         const bool use1 = arg1 >= kLog2AlphaMin;
         float wb0 = 0.f, wb1 = 0.f;
-        if (use0 || use1) {
+        if (__any_sync(FULL, use0 || use1)) {   // warp-uniform: blend2 votes inside
           const float4 q2 = R2[j];                                 // r, g, b, z
-          wb0 = blend(use0, arg0, q2, T0, r0c, g0c, b0c, d0, pyc0, ne0, base + j);
-          wb1 = blend(use1, arg1, q2, T1, r1c, g1c, b1c, d1, pyc1, ne1, base + j);
+          const float2 wb = blend2(use0, arg0, use1, arg1, q2, T0, r0c, g0c, b0c, d0, pyc0, ne0, T1, r1c, g1c, b1c,
+                                   d1, pyc1, ne1, base + j);
+          wb0 = wb.x;
+          wb1 = wb.y;
         }
         if constexpr (SCORE) {
           const uint32_t tot = __reduce_add_sync(FULL, __float2uint_rn((wb0 + wb1) * kScoreFix));
