@@ -10,6 +10,8 @@ Layout:
   mini.py       independent NumPy re-implementation (fp64) for small frames (pin 11).
   binning.py    integer-path oracle: fp32 tile rects (R9) and per-tile (zbits, id) lists (R10).
   obs.py        observation epilogue of reading R31 (image DR, uint8 / fp16 encoding), numpy fp32.
+  gsb_oracle.c also holds the reading-R32 ray-cast LiDAR (brute force per ray over all
+                Gaussians in (rho_f32 bits, id) order; `lidar_frame`).
 
 Each function cites the passage it follows; DESIGN.md §2 lists every reading (R1-R31).
 """
@@ -72,6 +74,16 @@ def lib():
         L.gsbo_compose_w2c.argtypes = [P, P, P]
         L.gsbo_fmaf.restype = ctypes.c_float
         L.gsbo_fmaf.argtypes = [ctypes.c_float, ctypes.c_float, ctypes.c_float]
+        L.gsbo_lidar_project.restype = ctypes.c_int
+        L.gsbo_lidar_project.argtypes = [P, P, P, P, P, ctypes.c_int64, P, ctypes.c_int, P, ctypes.c_float,
+                                         ctypes.c_float, P, P, P]
+        L.gsbo_lidar_cast.restype = ctypes.c_int
+        L.gsbo_lidar_cast.argtypes = [P, P, ctypes.c_int64, P, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_double, P, P, P, P, P, ctypes.c_int]
+        L.gsbo_range_key.restype = ctypes.c_float
+        L.gsbo_range_key.argtypes = [P, P, P]
+        L.gsbo_lidar_peak.restype = ctypes.c_double
+        L.gsbo_lidar_peak.argtypes = [P, P, P]
         L.gsbo_sh_basis.restype = None
         L.gsbo_sh_basis.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double, P]
         _lib = L
@@ -243,3 +255,83 @@ def sh_basis(deg: int, x: float, y: float, z: float) -> np.ndarray:
     Y = np.zeros(16)
     lib().gsbo_sh_basis(deg, x, y, z, _p(Y))
     return Y[: (deg + 1) ** 2]
+
+
+# ------------------------------------------------------------------------------------------
+# reading R32: batched ray-cast LiDAR against the Gaussians (§8(f) row 4; P:315, P:837-843,
+# tab:lidar P:320-329).  See the R32 block of gsb_oracle.c for the step-by-step definition.
+# ------------------------------------------------------------------------------------------
+LF = 12
+L_X, L_Y, L_Z, L_P00, L_P01, L_P02, L_P11, L_P12, L_P22, L_O, L_RHO32, L_RHO64 = range(LF)
+TOL_ALPHA = 2e-3
+
+
+@dataclass
+class LidarResult:
+    range: np.ndarray      # [R] sum_w w t^  (metres along the unit ray)
+    alpha: np.ndarray      # [R] 1 - T
+    masked: np.ndarray     # [R] reading-R28 threshold margin (range or alpha not compared)
+    n_blend: np.ndarray    # [R] entries blended
+    budget_range: np.ndarray
+    budget_alpha: np.ndarray
+    proj: np.ndarray       # [N, LF]
+    rhobits: np.ndarray    # [N] u32 binary32 range key
+    valid: np.ndarray      # [N] bool (R32 step 3)
+    order: np.ndarray      # valid ids by (rhobits, id)
+
+
+def lidar_project(scene, pose_env, w2s, near: float = 0.01, far: float = 1000.0):
+    """R32 steps 1-3 for one (env, sensor): (proj [N,LF] f64, rhobits [N] u32, valid [N] bool)."""
+    N = scene.n
+    out = np.zeros((N, LF), np.float64)
+    rb = np.zeros(N, np.uint32)
+    valid = np.zeros(N, np.uint8)
+    keep = [_c(scene.means, np.float32), _c(scene.scales, np.float32), _c(scene.quats, np.float32),
+            _c(scene.opacities, np.float32), _c(scene.body_id, np.int32),
+            _c(pose_env, np.float32).reshape(-1), _c(w2s, np.float32).reshape(-1)]
+    rc = lib().gsbo_lidar_project(_p(keep[0]), _p(keep[1]), _p(keep[2]), _p(keep[3]), _p(keep[4]), N,
+                                  _p(keep[5]), scene.n_bodies, _p(keep[6]), near, far, _p(out), _p(rb), _p(valid))
+    if rc != 0:
+        raise ValueError("oracle: body index out of range")
+    return out, rb, valid.astype(bool)
+
+
+def lidar_frame(scene, pose_env, w2s, dirs, near: float = 0.01, far: float = 1000.0,
+                nthreads: Optional[int] = None, delta_alpha: float = DELTA_ALPHA,
+                delta_T: float = DELTA_T) -> LidarResult:
+    """R32 steps 1-6 for one (env, sensor) and the rays `dirs` [R,3] (unit, sensor frame)."""
+    proj, rb, valid = lidar_project(scene, pose_env, w2s, near, far)
+    order = depth_order(rb, valid)     # (bits(rho), id): R10 with rho for z
+    dirs = _c(dirs, np.float32).reshape(-1, 3)
+    R = dirs.shape[0]
+    if order.size:
+        kap = 2.0 * np.log(255.0 * scene.opacities[order].astype(np.float64))
+        smax = np.abs(scene.scales[order].astype(np.float64)).max(axis=1)
+        tmax = float((proj[order, L_RHO64] + np.sqrt(np.maximum(kap, 0.0)) * smax).max())
+    else:
+        tmax = 0.0
+    rg = np.zeros(R); al = np.zeros(R); br = np.zeros(R); ba = np.zeros(R)
+    nb = np.zeros(R, np.int64)
+    if nthreads is None:
+        nthreads = os.cpu_count() or 1
+    lib().gsbo_lidar_cast(_p(proj), _p(order), order.size, _p(dirs), R, delta_alpha, delta_T, tmax,
+                          _p(rg), _p(al), _p(br), _p(ba), _p(nb), int(nthreads))
+    masked = (br > 0.5 * (TOL_DEPTH_REL * rg + TOL_DEPTH_ABS)) | (ba > 0.5 * TOL_ALPHA)
+    return LidarResult(rg, al, masked, nb, br, ba, proj, rb, valid, order)
+
+
+def range_key(w2s, pose_or_none, mu) -> np.float32:
+    """R32 binary32 range key of a single mean (C implementation)."""
+    w = _c(w2s, np.float32).reshape(-1)
+    m = _c(mu, np.float32).reshape(-1)
+    p = None if pose_or_none is None else _c(pose_or_none, np.float32).reshape(-1)
+    return np.float32(lib().gsbo_range_key(_p(w), _p(p), _p(m)))
+
+
+def lidar_peak(g_row, d):
+    """(D2, t^) of one projected Gaussian row (LF fields) on the half-ray along d."""
+    g = _c(g_row, np.float64).reshape(-1)
+    dv = _c(d, np.float64).reshape(-1)
+    th = np.zeros(1)
+    D2 = lib().gsbo_lidar_peak(_p(g), _p(dv), _p(th))
+    return float(D2), float(th[0])

@@ -458,3 +458,226 @@ int gsbo_composite(const double* proj, const uint32_t* order, int64_t n_order, c
 
 /* correctly rounded binary32 fma — exported to pin the numpy emulation */
 float gsbo_fmaf(float a, float b, float c) { return fmaf(a, b, c); }
+
+/* =================================================================================
+ * Batched ray-cast LiDAR against the Gaussians — SURVEY §8(f) row 4 ("batched ray-depth
+ * LiDAR", tab:lidar P:320-329; "Batch-LiDAR module utilizing ray-casting", P:315;
+ * "omnidirectional or bounded ray-casting"; height scan = downward rays).
+ * The paper gives no formula; reading R32 is what both sides compute:
+ *
+ *   sensor s of env e: world->sensor W = [R_s | t_s] (3x4 row-major, like a camera);
+ *   rays: unit directions d_j (sensor frame) from the sensor origin, j < R.
+ *   step 1  pose (as gsbo_project step 1): mu_w, Sigma_w by RLGK (R23)
+ *   step 2  range key: x_r = fma(M_r0,mu_x, fma(M_r1,mu_y, fma(M_r2,mu_z, m_r))) for r = 0..2,
+ *           M, m by the R11 chain applied to every row (static: M = W_R, m = t);
+ *           rho = sqrt_rn(fma(x0,x0, fma(x1,x1, x2*x2)))  — binary32, each op rounded
+ *   step 3  cull: near < rho <= far and o >= 1/255 (R4, R5 with rho for z)
+ *   step 4  order: (bits(rho), id) ascending (R10 with rho for z) — done by the caller
+ *   step 5  per ray, fp64: x = W mu_w + t, P = (W Sigma_w W^T)^-1,
+ *           t* = d^T P x / d^T P d, t^ = max(t*, 0)   (peak of the Gaussian on the half-ray),
+ *           D2 = (x - t^ d)^T P (x - t^ d),  alpha = min(0.99, o exp(-D2/2)),
+ *           then R12-R14 with t^ for z and no colour: skip alpha < 1/255, stop before
+ *           blending when T(1-alpha) < 1e-4, w = alpha T, range += w t^, T = T(1-alpha);
+ *           outputs range = sum w t^ and alpha = 1 - T  (R16 with t^ for z).
+ *   step 6  margin: flip budgets as R28 (alpha skip threshold and termination test).
+ * ================================================================================= */
+#define GSBO_LF 12
+enum { L_X = 0, L_Y, L_Z, L_P00, L_P01, L_P02, L_P11, L_P12, L_P22, L_O, L_RHO32, L_RHO64 };
+
+int gsbo_lidar_num_fields(void) { return GSBO_LF; }
+
+/* the rows of sensor<-local (M, m) in binary32 (R11 chain on every row; R32 step 2) */
+static void r32_rows(const float* w2s, const float* pose, float M[3][3], float m[3]) {
+  if (!pose) {
+    for (int r = 0; r < 3; ++r) {
+      for (int c = 0; c < 3; ++c) M[r][c] = w2s[r * 4 + c];
+      m[r] = w2s[r * 4 + 3];
+    }
+    return;
+  }
+  float R[3][3];
+  r11_rot_f32(pose + 3, R);
+  for (int r = 0; r < 3; ++r) {
+    const float W0 = w2s[r * 4 + 0], W1 = w2s[r * 4 + 1], W2 = w2s[r * 4 + 2], tr = w2s[r * 4 + 3];
+    for (int c = 0; c < 3; ++c) {
+      float p = W2 * R[2][c];
+      M[r][c] = fmaf(W0, R[0][c], fmaf(W1, R[1][c], p));
+    }
+    m[r] = fmaf(W0, pose[0], fmaf(W1, pose[1], fmaf(W2, pose[2], tr)));
+  }
+}
+
+/* binary32 range key of one mean (R32 step 2) — exported so tests can pin the chain */
+float gsbo_range_key(const float* w2s, const float* pose_or_null, const float* mu) {
+  float M[3][3], m[3], x[3];
+  r32_rows(w2s, pose_or_null, M, m);
+  for (int r = 0; r < 3; ++r) x[r] = fmaf(M[r][0], mu[0], fmaf(M[r][1], mu[1], fmaf(M[r][2], mu[2], m[r])));
+  float zz = x[2] * x[2];
+  return sqrtf(fmaf(x[0], x[0], fmaf(x[1], x[1], zz)));
+}
+
+/* Steps 1-3 for every Gaussian of one (env, sensor): out [n][GSBO_LF], rhobits [n], valid [n].
+ * Returns 0, or -1 on a body index out of range. */
+int gsbo_lidar_project(const float* means, const float* scales, const float* quats, const float* opac,
+                       const int32_t* body_id, int64_t n, const float* pose, int n_bodies, const float* w2s,
+                       float near_plane, float far_plane, double* out, uint32_t* rhobits, uint8_t* valid) {
+  double Wc[3][3], tc[3];
+  for (int r = 0; r < 3; ++r) {
+    for (int c = 0; c < 3; ++c) Wc[r][c] = w2s[r * 4 + c];
+    tc[r] = w2s[r * 4 + 3];
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    double* o = out + i * GSBO_LF;
+    memset(o, 0, sizeof(double) * GSBO_LF);
+    const int k = body_id[i];
+    if (k < -1 || k >= n_bodies) return -1;
+    double Rk[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}}, tk[3] = {0, 0, 0};
+    const float* pk = NULL;
+    if (k >= 0) {
+      pk = pose + (int64_t)k * 7;
+      double qk[4] = {pk[3], pk[4], pk[5], pk[6]};
+      rot_from_quat(qk, Rk);
+      tk[0] = pk[0]; tk[1] = pk[1]; tk[2] = pk[2];
+    }
+    const double mu[3] = {means[3 * i], means[3 * i + 1], means[3 * i + 2]};
+    double muw[3];
+    for (int r = 0; r < 3; ++r) muw[r] = Rk[r][0] * mu[0] + Rk[r][1] * mu[1] + Rk[r][2] * mu[2] + tk[r];
+    double qi[4] = {quats[4 * i], quats[4 * i + 1], quats[4 * i + 2], quats[4 * i + 3]};
+    double qn = sqrt(qi[0] * qi[0] + qi[1] * qi[1] + qi[2] * qi[2] + qi[3] * qi[3]);
+    for (int c = 0; c < 4; ++c) qi[c] /= qn;
+    double Ri[3][3], RiT[3][3], S2[3][3] = {{0}}, T1[3][3], Sl[3][3], RkT[3][3], Sw[3][3], WT[3][3], Ss[3][3];
+    rot_from_quat(qi, Ri);
+    for (int c = 0; c < 3; ++c) S2[c][c] = (double)scales[3 * i + c] * (double)scales[3 * i + c];
+    matmul3(Ri, S2, T1);
+    transpose3(Ri, RiT);
+    matmul3(T1, RiT, Sl);          /* Sigma_local (R23) */
+    matmul3(Rk, Sl, T1);
+    transpose3(Rk, RkT);
+    matmul3(T1, RkT, Sw);          /* Sigma_world */
+    matmul3(Wc, Sw, T1);
+    transpose3(Wc, WT);
+    matmul3(T1, WT, Ss);           /* Sigma_sensor = W Sigma_world W^T */
+    /* P = Sigma_sensor^-1 by the adjugate */
+    const double a = Ss[0][0], b = Ss[0][1], c = Ss[0][2], d = Ss[1][1], e = Ss[1][2], f = Ss[2][2];
+    const double A00 = d * f - e * e, A01 = c * e - b * f, A02 = b * e - c * d;
+    const double A11 = a * f - c * c, A12 = b * c - a * e, A22 = a * d - b * b;
+    const double det = a * A00 + b * A01 + c * A02;
+    o[L_P00] = A00 / det; o[L_P01] = A01 / det; o[L_P02] = A02 / det;
+    o[L_P11] = A11 / det; o[L_P12] = A12 / det; o[L_P22] = A22 / det;
+    for (int r = 0; r < 3; ++r) o[L_X + r] = Wc[r][0] * muw[0] + Wc[r][1] * muw[1] + Wc[r][2] * muw[2] + tc[r];
+    o[L_O] = opac[i];
+    const float rho = gsbo_range_key(w2s, pk, means + 3 * i);
+    uint32_t rb;
+    memcpy(&rb, &rho, 4);
+    rhobits[i] = rb;
+    o[L_RHO32] = rho;
+    o[L_RHO64] = sqrt(o[L_X] * o[L_X] + o[L_Y] * o[L_Y] + o[L_Z] * o[L_Z]);
+    valid[i] = (uint8_t)((rho > near_plane) && (rho <= far_plane) && ((double)opac[i] >= 1.0 / 255.0));
+  }
+  return 0;
+}
+
+/* the peak of Gaussian g on the half-ray t >= 0 along d: returns D2, writes t^ (R32 step 5) */
+static double r32_peak(const double* g, const double dv[3], double* that) {
+  const double P[3][3] = {{g[L_P00], g[L_P01], g[L_P02]}, {g[L_P01], g[L_P11], g[L_P12]},
+                          {g[L_P02], g[L_P12], g[L_P22]}};
+  double Pd[3], Px[3];
+  for (int r = 0; r < 3; ++r) {
+    Pd[r] = P[r][0] * dv[0] + P[r][1] * dv[1] + P[r][2] * dv[2];
+    Px[r] = P[r][0] * g[L_X] + P[r][1] * g[L_Y] + P[r][2] * g[L_Z];
+  }
+  const double dPd = dv[0] * Pd[0] + dv[1] * Pd[1] + dv[2] * Pd[2];
+  const double dPx = dv[0] * Px[0] + dv[1] * Px[1] + dv[2] * Px[2];
+  double t = dPx / dPd;
+  if (t < 0.0) t = 0.0;
+  const double e[3] = {g[L_X] - t * dv[0], g[L_Y] - t * dv[1], g[L_Z] - t * dv[2]};
+  double D2 = 0.0;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) D2 += e[r] * P[r][c] * e[c];
+  *that = t;
+  return D2;
+}
+
+double gsbo_lidar_peak(const double* g, const double* dv, double* that) { return r32_peak(g, dv, that); }
+
+typedef struct {
+  const double* proj;
+  const uint32_t* order;
+  int64_t n_order;
+  const float* dirs;
+  int64_t r0, r1;
+  double delta_alpha, delta_T, tmax;
+  double* out_range;
+  double* out_alpha;
+  double* out_budget_range;
+  double* out_budget_alpha;
+  int64_t* out_n_blend;
+} lidar_job;
+
+static void cast_ray(const lidar_job* jb, int64_t j) {
+  const double dv[3] = {jb->dirs[3 * j], jb->dirs[3 * j + 1], jb->dirs[3 * j + 2]};
+  double T = 1.0, Rg = 0.0, br = 0.0, ba = 0.0;
+  int64_t nb = 0;
+  const double thr = 1.0 / 255.0;
+  for (int64_t q = 0; q < jb->n_order; ++q) {
+    const double* g = jb->proj + (int64_t)jb->order[q] * GSBO_LF;
+    double th;
+    const double D2 = r32_peak(g, dv, &th);
+    const double araw = g[L_O] * exp(-0.5 * D2);
+    if (fabs(araw - thr) <= jb->delta_alpha * thr) { /* R28: skip-threshold flip */
+      br += 2.0 * T * thr * (1.0 + jb->delta_alpha) * jb->tmax;
+      ba += 2.0 * T * thr * (1.0 + jb->delta_alpha);
+    }
+    const double alpha = araw < 0.99 ? araw : 0.99;
+    if (alpha < thr) continue;
+    const double tT = T * (1.0 - alpha);
+    if (fabs(tT - 1e-4) <= jb->delta_T * 1e-4) { /* R28: termination flip */
+      br += T * jb->tmax;
+      ba += T;
+    }
+    if (tT < 1e-4) break;
+    const double w = alpha * T;
+    Rg += w * th;
+    T = tT;
+    nb++;
+  }
+  jb->out_range[j] = Rg;
+  jb->out_alpha[j] = 1.0 - T;
+  jb->out_budget_range[j] = br;
+  jb->out_budget_alpha[j] = ba;
+  jb->out_n_blend[j] = nb;
+}
+
+static void* lidar_worker(void* arg) {
+  const lidar_job* jb = (const lidar_job*)arg;
+  for (int64_t j = jb->r0; j < jb->r1; ++j) cast_ray(jb, j);
+  return NULL;
+}
+
+/* Step 5 (+6) for the listed rays over the range-ordered Gaussians (pure brute force). */
+int gsbo_lidar_cast(const double* proj, const uint32_t* order, int64_t n_order, const float* dirs, int64_t n_rays,
+                    double delta_alpha, double delta_T, double tmax, double* out_range, double* out_alpha,
+                    double* out_budget_range, double* out_budget_alpha, int64_t* out_n_blend, int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  if ((int64_t)nthreads > n_rays) nthreads = n_rays > 0 ? (int)n_rays : 1;
+  lidar_job jobs[256];
+  pthread_t th[256];
+  for (int t = 0; t < nthreads; ++t) {
+    lidar_job* jb = &jobs[t];
+    jb->proj = proj; jb->order = order; jb->n_order = n_order; jb->dirs = dirs;
+    jb->r0 = n_rays * t / nthreads;
+    jb->r1 = n_rays * (t + 1) / nthreads;
+    jb->delta_alpha = delta_alpha; jb->delta_T = delta_T; jb->tmax = tmax;
+    jb->out_range = out_range; jb->out_alpha = out_alpha;
+    jb->out_budget_range = out_budget_range; jb->out_budget_alpha = out_budget_alpha;
+    jb->out_n_blend = out_n_blend;
+  }
+  if (nthreads == 1) {
+    lidar_worker(&jobs[0]);
+  } else {
+    for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, lidar_worker, &jobs[t]);
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+  }
+  return 0;
+}

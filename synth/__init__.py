@@ -444,3 +444,74 @@ def env_slice(n_envs: int, rank: int, world: int) -> Tuple[int, int]:
     lo = (n_envs * rank) // world
     hi = (n_envs * (rank + 1)) // world
     return lo, hi
+
+
+# --------------------------------------------------------------------------------------
+# LiDAR inputs (§8(f) row 4, reading R32; tab:lidar P:320-329): ray patterns in the sensor
+# frame (x forward, y left, z up) and sensor extrinsics.  Inputs only: no method arithmetic.
+# --------------------------------------------------------------------------------------
+def lidar_pattern(kind: str, n_channels: int = 32, n_azimuth: int = 1024, step: int = 0,
+                  fov=(-25.0, 15.0), n_points: int = 0, seed: int = 0) -> np.ndarray:
+    """Unit ray directions [R,3] f32.
+    rotating:        n_channels elevations uniform in fov (deg) x n_azimuth azimuths over 360 deg
+    solid_state:     a bounded n_channels x n_azimuth grid, +-35 deg azimuth, elevation fov
+    non_repetitive:  a rose-curve (Livox-like) scan of n_points rays over a 70 deg cone whose
+                     phase advances with `step`, so successive scans cover different directions
+    height_scan:     a downward n_channels x n_azimuth grid (1.6 x 1.0 m at 1 m below the
+                     sensor), the Height Scan sensor of P:837
+    random:          n_points directions uniform on the sphere (seeded)"""
+    if kind == "rotating":
+        el = np.radians(np.linspace(fov[0], fov[1], n_channels))
+        az = np.linspace(-np.pi, np.pi, n_azimuth, endpoint=False) + np.pi / n_azimuth
+        E, A = np.meshgrid(el, az, indexing="ij")
+    elif kind == "solid_state":
+        el = np.radians(np.linspace(fov[0], fov[1], n_channels))
+        az = np.radians(np.linspace(-35.0, 35.0, n_azimuth))
+        E, A = np.meshgrid(el, az, indexing="ij")
+    elif kind == "non_repetitive":
+        n = n_points or n_channels * n_azimuth
+        t = np.arange(n) * (2 * np.pi / n) * 17.0 + 0.37 * step
+        r = np.radians(35.0) * np.abs(np.sin(2.5 * t + 0.11 * step))
+        ang = t * 0.5
+        y, z = r * np.cos(ang), r * np.sin(ang)
+        d = np.stack([np.ones(n), np.tan(y), np.tan(z)], 1)
+        return (d / np.linalg.norm(d, axis=1, keepdims=True)).astype(np.float32)
+    elif kind == "height_scan":
+        xs = np.linspace(-0.8, 0.8, n_azimuth)
+        ys = np.linspace(-0.5, 0.5, n_channels)
+        Y, X = np.meshgrid(ys, xs, indexing="ij")
+        d = np.stack([X.ravel(), Y.ravel(), -np.ones(X.size)], 1)
+        return (d / np.linalg.norm(d, axis=1, keepdims=True)).astype(np.float32)
+    elif kind == "random":
+        rng = np.random.default_rng(seed)
+        d = rng.normal(size=(n_points or n_channels * n_azimuth, 3))
+        return (d / np.linalg.norm(d, axis=1, keepdims=True)).astype(np.float32)
+    else:
+        raise ValueError(kind)
+    d = np.stack([np.cos(E) * np.cos(A), np.cos(E) * np.sin(A), np.sin(E)], -1).reshape(-1, 3)
+    return (d / np.linalg.norm(d, axis=1, keepdims=True)).astype(np.float32)
+
+
+def lidar_world_sensor(cfg: Config, env_ids) -> np.ndarray:
+    """World->sensor [B,3,4] f32 of a LiDAR fixed in the room near the robot (1.2 m above the
+    floor at (1.0, -0.8), facing the robot, yawed per env by U(+-10 deg))."""
+    env_ids = np.asarray(env_ids, np.int64).reshape(-1)
+    out = np.zeros((env_ids.size, 3, 4), np.float64)
+    for bi, e in enumerate(env_ids):
+        rng = np.random.default_rng(np.random.SeedSequence(4000 + cfg.cfg_id, spawn_key=(int(e),)))
+        yaw = math.atan2(0.8, -1.0) + math.radians(rng.uniform(-10.0, 10.0))
+        c, s = math.cos(yaw), math.sin(yaw)
+        Rs2w = np.array([[c, -s, 0.0], [s, c, 0.0], [0.0, 0.0, 1.0]])  # sensor x forward, z up
+        eye = np.array([1.0, -0.8, 1.2]) + rng.uniform(-0.02, 0.02, 3)
+        out[bi, :, :3] = Rs2w.T
+        out[bi, :, 3] = -Rs2w.T @ eye
+    return out.astype(np.float32)
+
+
+def lidar_body_mount() -> np.ndarray:
+    """Body->sensor [3,4] f32 of a LiDAR on body 0 (the robot base): 0.2 m above the body
+    origin, axes aligned with the body (reading R29 composes it per env on the device)."""
+    m = np.zeros((3, 4), np.float32)
+    m[:, :3] = np.eye(3)
+    m[:, 3] = [0.0, 0.0, -0.2]
+    return m
