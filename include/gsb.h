@@ -248,6 +248,50 @@ gsb_status gsb_filter_scene(gsb_scene scene, const uint8_t* keep, gsb_scene* out
 
 gsb_status gsb_destroy_scene(gsb_scene scene);
 
+/* ------------------------------------------------------------ batched ray-cast LiDAR (R32)
+ * §8(f) row 4: "Batch-LiDAR module utilizing ray-casting", rotating, solid-state and
+ * non-repetitive scans (tab:lidar P:320-329), omnidirectional/bounded LiDAR and the downward
+ * Height Scan.  The paper gives no formula; reading R32 (DESIGN.md,
+ * oracle/gsb_oracle.c) casts each ray against the same RLGK-posed Gaussians the cameras see:
+ *   x = sensor-frame mean, P = (sensor-frame Sigma)^-1, d = unit ray direction (sensor frame);
+ *   t^ = max(0, d^T P x / d^T P d)       peak of the Gaussian on the half-ray t >= 0
+ *   alpha = min(0.99, o exp(-(x - t^ d)^T P (x - t^ d) / 2))
+ * composited front-to-back in (bits(rho_f32), id) order, rho = |x| by the binary32 chain of
+ * R32 (R11 applied to all three rows), with the camera rules R12-R14 (skip alpha < 1/255,
+ * stop before blending when T(1-alpha) < 1e-4) and outputs
+ *   range = sum_w w t^   (metres; the ray's expected hit distance is range / alpha)
+ *   alpha = 1 - T.
+ * A point cloud is origin + (range / alpha) d for rays with alpha above the user's threshold. */
+typedef struct gsb_lidar_t* gsb_lidar; /* a ray pattern bound to one scene's device */
+
+/* Upload a ray pattern: dirs = HOST [n_rays, 3] fp32 unit vectors in the sensor frame
+ * (|norm - 1| <= 1e-5), any order (rotating, solid-state, non-repetitive, height scan ...).
+ * The pattern is bucketed into an azimuth x elevation grid of cells (n_az, n_el <= 256 each;
+ * 0 = automatic, ~32 rays per cell) covering the rays' angular window; Gaussians are binned
+ * into the same cells.  Synchronous.  Errors: INVALID_ARGUMENT, OUT_OF_MEMORY, CUDA. */
+gsb_status gsb_lidar_create(gsb_scene scene, const float* dirs, int32_t n_rays, int32_t n_az, int32_t n_el,
+                            gsb_lidar* out);
+
+/* Cast every ray of `lidar` for S sensors per env.  DEVICE pointers:
+ *   body_poses    [B, n_bodies, 7] fp32 (as gsb_render)
+ *   sensor_x      [B, S, 3, 4] fp32, or [S, 3, 4] when sensors_shared != 0: world->sensor
+ *                 [R | t] (sensor axes: the ray directions' frame), or, for a sensor with
+ *                 sensor_body[s] = k >= 0, the body->sensor mount composed per env by R29
+ *   sensor_body   [S] int32 HOST array, nullable (all world-fixed); S <= 16 when set
+ *   out_range     [B, S, n_rays] fp32, out_alpha [B, S, n_rays] fp32 (nullable)
+ * near < rho <= far culls by the range key (R4 with rho for z).  Allocates its workspace on
+ * first use and when a batch needs more (then synchronises); otherwise asynchronous on stream.
+ * Errors: INVALID_ARGUMENT, SHAPE_MISMATCH (n_bodies), UNKNOWN_BODY, OUT_OF_MEMORY, CUDA. */
+gsb_status gsb_render_lidar(gsb_scene scene, gsb_lidar lidar, const float* body_poses, int32_t n_envs,
+                            int32_t n_sensors, const float* sensor_x, int32_t sensors_shared,
+                            const int32_t* sensor_body, float near_plane, float far_plane, float* out_range,
+                            float* out_alpha, gsb_stream stream);
+
+/* Grid of the pattern: n_az, n_el, and the rays-per-cell work items (nullable outputs). */
+gsb_status gsb_lidar_info(gsb_lidar lidar, int32_t* n_az, int32_t* n_el, int32_t* n_items, int64_t* last_keys);
+
+gsb_status gsb_lidar_destroy(gsb_lidar lidar);
+
 /* Thread-local message for the last non-OK status (never NULL). */
 const char* gsb_last_error(void);
 

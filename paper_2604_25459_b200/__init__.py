@@ -32,7 +32,8 @@ EXPORTS = ["gsb_create_scene", "gsb_reserve", "gsb_render", "gsb_render_rig", "g
            "gsb_prebin_static", "gsb_render_static",
            "gsb_scores_reset", "gsb_get_scores", "gsb_filter_scene", "gsb_render_obs", "gsb_render_obs_host", "gsb_get_stats",
            "gsb_get_timings", "gsb_destroy_scene", "gsb_last_error", "gsb_version",
-           "gsb_debug_project", "gsb_debug_bin_sort"]
+           "gsb_debug_project", "gsb_debug_bin_sort",
+           "gsb_lidar_create", "gsb_render_lidar", "gsb_lidar_info", "gsb_lidar_destroy"]
 
 
 class GsbError(RuntimeError):
@@ -95,6 +96,11 @@ def lib() -> ctypes.CDLL:
     L.gsb_debug_project.argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P]
     L.gsb_debug_bin_sort.argtypes = [P, P, P, P, P, P, P, I32, I64, I32, I32, P, P, I64,
                                      ctypes.POINTER(I64), P]
+    L.gsb_lidar_create.argtypes = [P, P, I32, I32, I32, ctypes.POINTER(P)]
+    L.gsb_render_lidar.argtypes = [P, P, P, I32, I32, P, I32, P, ctypes.c_float, ctypes.c_float, P, P, P]
+    L.gsb_lidar_info.argtypes = [P, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32),
+                                 ctypes.POINTER(I64)]
+    L.gsb_lidar_destroy.argtypes = [P]
     for name in EXPORTS:
         if name not in ("gsb_last_error", "gsb_version"):
             getattr(L, name).restype = ctypes.c_int
@@ -349,6 +355,49 @@ class Scene:
         _check(lib().gsb_debug_project(self._h, _ptr(poses) if self.n_bodies else None, B, C, _ptr(intrinsics),
                                        _ptr(world_to_cam), ctypes.byref(p), _ptr(out_rec), _ptr(out_zbits),
                                        _ptr(out_valid), _stream(stream)))
+
+
+class Lidar:
+    """A LiDAR ray pattern bound to a scene (gsb_lidar_create; reading R32, §8(f) row 4).
+    dirs: [R,3] unit directions in the sensor frame (host array)."""
+
+    def __init__(self, scene: Scene, dirs, n_az: int = 0, n_el: int = 0):
+        d = np.ascontiguousarray(dirs, np.float32).reshape(-1, 3)
+        h = ctypes.c_void_p()
+        _check(lib().gsb_lidar_create(scene._h, d.ctypes.data, int(d.shape[0]), int(n_az), int(n_el), ctypes.byref(h)))
+        self._h, self.scene, self.n_rays = h, scene, int(d.shape[0])
+
+    def info(self):
+        a, e, it, k = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
+        _check(lib().gsb_lidar_info(self._h, ctypes.byref(a), ctypes.byref(e), ctypes.byref(it), ctypes.byref(k)))
+        return {"n_az": a.value, "n_el": e.value, "n_items": it.value, "keys": k.value}
+
+    def render(self, poses, sensor_x, out_range, out_alpha=None, sensor_body=None, near: float = 0.01,
+               far: float = 1000.0, stream=None):
+        """gsb_render_lidar on CUDA tensors: poses [B,nb,7]; sensor_x [B,S,3,4] (per env) or [S,3,4]
+        (shared) world->sensor, or body->sensor for sensors with sensor_body[s] >= 0;
+        out_range / out_alpha [B,S,R] float32."""
+        B, S = int(out_range.shape[0]), int(out_range.shape[1])
+        shared = 1 if sensor_x.dim() == 3 else 0
+        sb = None
+        if sensor_body is not None:
+            sb = np.ascontiguousarray(sensor_body, np.int32)
+            if sb.size != S:
+                raise ValueError("sensor_body needs one entry per sensor")
+        _check(lib().gsb_render_lidar(self.scene._h, self._h, _ptr(poses) if self.scene.n_bodies else None, B, S,
+                                      _ptr(sensor_x), shared, None if sb is None else sb.ctypes.data, near, far,
+                                      _ptr(out_range), _ptr(out_alpha), _stream(stream)))
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().gsb_lidar_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def debug_bin_sort(u, v, sxx, syy, kappa, zbits, valid, width: int, height: int, cap: int, stream=None):

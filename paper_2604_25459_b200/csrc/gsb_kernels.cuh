@@ -116,6 +116,46 @@ struct K0Rig {
   int cam_body[kMaxRigCams];
 };
 
+// ---------------------------------------------------------------- LiDAR (reading R32)
+struct LidarL1Args {
+  const float4 *g_mean, *g_L0, *g_L1, *g_L2;
+  const int2* g_ids;
+  int64_t n;            // Gaussians (record stride per frame)
+  int64_t np;           // n rounded up to 32: emission index of the seam part of Gaussian i = np + i
+  const float4* table;  // K0 per-(frame, body) transforms, frame = (env, sensor)
+  int nb1;
+  int f0, n_frames;
+  float near_plane, far_plane;
+  // cell grid: azimuth window [az0, az0 + az_span), elevation window [el0, el0 + n_el / el_inv)
+  float az0, az_span, az_inv, el0, el_inv;
+  int n_az, n_el;
+  float4* rec;          // [E][n][4]: A row 0 | m0, A row 1 | m1, A row 2 | m2, (log2 o, rho, -, -)
+  uint2* emit;          // [E][2 np] (bits(rho), cell rect)
+  uint32_t* vis_bits;   // [E][vis_words = 2 np / 32]
+  int64_t vis_words;
+  int* vcount;          // [E]
+  int* hist;            // [E][hist_stride] cell counts
+  int64_t hist_stride;
+};
+
+struct LidarL4Args {
+  const float4* rec;
+  int64_t n;
+  const uint32_t* off;          // [E][hist_stride] cell offsets within the frame
+  const uint64_t* frame_base;   // [E+1]
+  int64_t hist_stride;
+  const uint32_t* sorted;       // ids of every (frame, cell) list in (bits(rho), id) order (K3)
+  const int* inv;               // id -> internal index
+  const float4* rays;           // [R] (dx, dy, dz, bits(original ray index)), grouped by cell
+  const int4* items;            // (cell, first ray, ray count <= 32, 0)
+  int n_items, f0, n_frames, n_rays;
+  float* out_range;             // [F][R]
+  float* out_alpha;             // [F][R] or nullptr
+};
+
+void launch_kl1(const LidarL1Args& a, cudaStream_t s);
+void launch_kl4(const LidarL4Args& a, cudaStream_t s);
+
 void launch_k0(const K0Rig& rig, int n_frames, int n_cams, int n_bodies, int width, int height,
                float4* table, FrameCam* cams, cudaStream_t s);
 void launch_k1(const K1Args& a, int sh_degree, cudaStream_t s);

@@ -65,10 +65,12 @@ __global__ void k0_setup(K0Rig rig, int n_frames, int n_cams, int n_bodies, int 
     t[0] = p[0]; t[1] = p[1]; t[2] = p[2];
   }
   float M[3][3], m[3];
+  // rows 0, 1 by the same binary32 chain as the depth row (the LiDAR range key of reading R32
+  // uses all three rows; for the cameras only row 2 must be exact)
   for (int r = 0; r < 2; ++r) {
     for (int c = 0; c < 3; ++c)
-      M[r][c] = fmaf(W[r * 4 + 0], R[0][c], fmaf(W[r * 4 + 1], R[1][c], W[r * 4 + 2] * R[2][c]));
-    m[r] = fmaf(W[r * 4 + 0], t[0], fmaf(W[r * 4 + 1], t[1], fmaf(W[r * 4 + 2], t[2], W[r * 4 + 3])));
+      M[r][c] = __fmaf_rn(W[r * 4 + 0], R[0][c], __fmaf_rn(W[r * 4 + 1], R[1][c], __fmul_rn(W[r * 4 + 2], R[2][c])));
+    m[r] = __fmaf_rn(W[r * 4 + 0], t[0], __fmaf_rn(W[r * 4 + 1], t[1], __fmaf_rn(W[r * 4 + 2], t[2], W[r * 4 + 3])));
   }
   // depth row: exact chain, reading R11
   if (k < 0) {
@@ -88,7 +90,7 @@ __global__ void k0_setup(K0Rig rig, int n_frames, int n_cams, int n_bodies, int 
   o[1] = make_float4(M[1][0], M[1][1], M[1][2], m[1]);
   o[2] = make_float4(M[2][0], M[2][1], M[2][2], m[2]);
   o[3] = make_float4(cb[0], cb[1], cb[2], 0.f);
-  if (k < 0) {
+  if (k < 0 && cams) {   // cams == nullptr: LiDAR frames (no intrinsics)
     const float* K = rig.intr + (size_t)crow * 4;
     FrameCam fc;
     fc.fx = K[0]; fc.fy = K[1]; fc.cx = K[2]; fc.cy = K[3];

@@ -84,6 +84,12 @@ def test_host_side_validation_without_gpu():
     assert L.gsb_render(None, None, 1, 1, None, None, ctypes.byref(prm), None, None, None, None, None) == 1
     assert L.gsb_destroy_scene(None) == 0
     assert L.gsb_debug_bin_sort(None, None, None, None, None, None, None, 0, 0, 8, 8, None, None, 0, None, None) == 1
+    # LiDAR entry points validate before touching the device
+    d = np.float32([[1, 0, 0]])
+    assert L.gsb_lidar_create(None, d.ctypes.data, 1, 0, 0, ctypes.byref(ctypes.c_void_p())) == 1
+    assert L.gsb_render_lidar(None, None, None, 1, 1, None, 0, None, 0.01, 100.0, None, None, None) == 1
+    assert L.gsb_lidar_info(None, None, None, None, None) == 1
+    assert L.gsb_lidar_destroy(None) == 0
 
 
 def test_render_params_layout_matches_header(tmp_path):
