@@ -1384,9 +1384,9 @@ namespace {
 constexpr int kLidarMaxCells = 256;
 constexpr double kLidarPi = 3.14159265358979323846;
 
-// frames per LiDAR chunk: records (64 B) + emission (16 B) per (frame, Gaussian) within ~2 GB
+// frames per LiDAR chunk: records (80 B) + emission (16 B) per (frame, Gaussian) within ~2 GB
 int lidar_chunk(int64_t n, int F) {
-  const int64_t per = std::max<int64_t>(1, n) * 80 + 4096;
+  const int64_t per = std::max<int64_t>(1, n) * 96 + 4096;
   const int64_t e = std::max<int64_t>(1, ((int64_t)2 << 30) / per);
   return (int)std::min<int64_t>({e, (int64_t)F, 256});
 }
@@ -1547,7 +1547,7 @@ gsb_status gsb_render_lidar(gsb_scene s, gsb_lidar l, const float* poses, int32_
     l->np = (N + 31) / 32 * 32;
     const int64_t np = std::max<int64_t>(l->np, 32);
     l->hist_stride = ((int64_t)n_cells + 2 + 31) / 32 * 32;
-    CUDA_TRY(dalloc(&l->rec, (size_t)E * std::max<int64_t>(N, 1) * 4));
+    CUDA_TRY(dalloc(&l->rec, (size_t)E * std::max<int64_t>(N, 1) * kLidarRecQuads));
     CUDA_TRY(dalloc(&l->emit, (size_t)E * 2 * np));
     CUDA_TRY(dalloc(&l->vis_bits, (size_t)E * 2 * np / 32));
     CUDA_TRY(dalloc(&l->vcount, (size_t)E));
@@ -1604,10 +1604,14 @@ gsb_status gsb_render_lidar(gsb_scene s, gsb_lidar l, const float* poses, int32_
       c.fs = 0; c.fe = ne; c.key_base = 0; c.long_list = nullptr;
       c.keys = l->keys; c.keys_alt = l->keys_alt; c.sorted = l->sorted;
       launch_k2_emit(c, st);
-      launch_k3_sort(c, 0, st);
+      CompositeArgs k{};   // K4a: (bits(rho), id) order -> record slots (slot_base 0: internal index)
+      k.keys = l->keys; k.keys_alt = l->keys_alt; k.off = l->off; k.frame_base = l->frame_base;
+      k.hist_stride = l->hist_stride; k.key_base = 0; k.fs = 0; k.fe = ne; k.f0 = f0;
+      k.n_tiles = n_cells; k.tiles_x = l->n_az; k.inv = s->d_inv; k.slot_base = 0; k.sorted = l->sorted;
+      launch_k4a_sort(k, false, st);
       LidarL4Args b{};
       b.rec = l->rec; b.n = N; b.off = l->off; b.frame_base = l->frame_base; b.hist_stride = l->hist_stride;
-      b.sorted = l->sorted; b.inv = s->d_inv; b.rays = l->d_rays; b.items = l->d_items;
+      b.sorted = l->sorted; b.rays = l->d_rays; b.items = l->d_items;
       b.n_items = l->n_items; b.f0 = f0; b.n_frames = ne; b.n_rays = l->n_rays;
       b.out_range = out_range; b.out_alpha = out_alpha;
       launch_kl4(b, st);

@@ -117,6 +117,7 @@ struct K0Rig {
 };
 
 // ---------------------------------------------------------------- LiDAR (reading R32)
+constexpr int kLidarRecQuads = 5;   // float4s per LiDAR record
 struct LidarL1Args {
   const float4 *g_mean, *g_L0, *g_L1, *g_L2;
   const int2* g_ids;
@@ -129,7 +130,9 @@ struct LidarL1Args {
   // cell grid: azimuth window [az0, az0 + az_span), elevation window [el0, el0 + n_el / el_inv)
   float az0, az_span, az_inv, el0, el_inv;
   int n_az, n_el;
-  float4* rec;          // [E][n][4]: A row 0 | m0, A row 1 | m1, A row 2 | m2, (log2 o, rho, -, -)
+  float4* rec;          // [E][n][5]: A row 0 | m0, A row 1 | m1, A row 2 | m2, (x, c), (log2 o, rho, -, -)
+                        // A = whitening of the sensor-frame Sigma scaled by sqrt(log2(e)/2), m = A x,
+                        // c = cone-test threshold of the ray cull (d.x >= c)
   uint2* emit;          // [E][2 np] (bits(rho), cell rect)
   uint32_t* vis_bits;   // [E][vis_words = 2 np / 32]
   int64_t vis_words;
@@ -144,8 +147,8 @@ struct LidarL4Args {
   const uint32_t* off;          // [E][hist_stride] cell offsets within the frame
   const uint64_t* frame_base;   // [E+1]
   int64_t hist_stride;
-  const uint32_t* sorted;       // ids of every (frame, cell) list in (bits(rho), id) order (K3)
-  const int* inv;               // id -> internal index
+  const uint32_t* sorted;       // record slots (internal indices) of every (frame, cell) list in
+                                // (bits(rho), id) order (K4a)
   const float4* rays;           // [R] (dx, dy, dz, bits(original ray index)), grouped by cell
   const int4* items;            // (cell, first ray, ray count <= 32, 0)
   int n_items, f0, n_frames, n_rays;

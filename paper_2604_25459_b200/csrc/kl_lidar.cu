@@ -10,10 +10,11 @@
 //        when it crosses the azimuth seam of the grid window) + cell histogram
 //   K2   scan + key emission (the camera kernels; the seam rect is a second "virtual"
 //        Gaussian at index Np + i carrying the same id, so keys stay (bits(rho), id))
-//   K3   segmented radix sort of every (frame, cell) list (the camera kernel)
+//   K4a  per-(frame, cell) sort into record slots (the camera kernel: counting sort <= 1024
+//        keys, radix beyond)
 //   KL4  one warp per (frame, cell, <= 32 rays of the cell): records staged through shared
-//        memory 32 at a time, each lane casts its ray through the cell's sorted list with
-//        warp-vote early exit on transmittance.
+//        memory 32 at a time, a 4-op cone test per (ray, record) selects the pairs that get
+//        the exact evaluation, each lane composites its ray front to back, warp-vote exit.
 // The cell lists are conservative supersets (bounding ball of the alpha >= 1/255 ellipsoid,
 // widened by 1e-3 rad): an extra candidate evaluates alpha < 1/255 and is skipped exactly as
 // the brute-force oracle skips it, so the binning never changes an output.
@@ -149,11 +150,17 @@ __global__ void __launch_bounds__(128) kl1_project(LidarL1Args a) {
       const float m0 = A[0][0] * x0 + A[0][1] * x1 + A[0][2] * x2;
       const float m1 = A[1][0] * x0 + A[1][1] * x1 + A[1][2] * x2;
       const float m2 = A[2][0] * x0 + A[2][1] * x1 + A[2][2] * x2;
-      float4* o = a.rec + ((size_t)fl * a.n + i) * 4;
+      // cull quad: a ray whose peak lies in the ball has d.x >= sqrt(|x|^2 - rball^2); c is
+      // lowered by 1e-6 |x| (>> the fp32 error of d.x) and is -inf when the sensor is inside
+      const float xx = fmaf(x0, x0, fmaf(x1, x1, x2 * x2));
+      const float rr = rball * rball;
+      const float cth = xx > rr ? sqrtf(xx - rr) - 1e-6f * sqrtf(xx) : -1e30f;
+      float4* o = a.rec + ((size_t)fl * a.n + i) * kLidarRecQuads;
       o[0] = make_float4(A[0][0], A[0][1], A[0][2], m0);
       o[1] = make_float4(A[1][0], A[1][1], A[1][2], m1);
       o[2] = make_float4(A[2][0], A[2][1], A[2][2], m2);
-      o[3] = make_float4(log2o, rho, 0.f, 0.f);
+      o[3] = make_float4(x0, x1, x2, cth);
+      o[4] = make_float4(log2o, rho, 0.f, 0.f);
     }
     const uint32_t zb = __float_as_uint(rho);
     const uint32_t ra = pack_rect(ax0, ax1, ey0, ey1);
@@ -182,10 +189,16 @@ void launch_kl1(const LidarL1Args& a, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------------------ KL4
+// One warp per (frame, cell, <= 32 rays).  Per round, 32 records of the cell's sorted list are
+// staged in shared memory (one per lane, quad-major so the broadcast reads are conflict-free);
+// every lane tests its ray against the 32 cull quads (d.x >= c: 4 ops per pair) and a ballot
+// per record gives the lanes that must evaluate it; only records some lane accepts run the
+// exact R32 evaluation (~25 ops).  The lists are (bits(rho), id) ordered (K4a), so the lanes
+// composite front to back; the warp leaves when every lane has terminated.
 constexpr int kL4Warps = 4;
 
 __global__ void __launch_bounds__(32 * kL4Warps) kl4_cast(LidarL4Args a) {
-  __shared__ float4 st[kL4Warps][32][4];
+  __shared__ float4 st[kL4Warps][kLidarRecQuads][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * kL4Warps + warp;
   if (item >= a.n_items) return;   // warp-uniform
@@ -200,39 +213,51 @@ __global__ void __launch_bounds__(32 * kL4Warps) kl4_cast(LidarL4Args a) {
   const int n = (int)(off[it.x + 1] - off[it.x]);
   float T = 1.f, R = 0.f;
   bool done = !has;
-  const float4* rec = a.rec + (size_t)fl * a.n * 4;
+  const float4* rec = a.rec + (size_t)fl * a.n * kLidarRecQuads;
   for (int base = 0; base < n; base += 32) {
     if (__all_sync(FULL, done)) break;
     const int j = base + lane;
     if (j < n) {
-      const uint32_t id = __ldg(a.sorted + start + j);
-      const float4* r = rec + (size_t)__ldg(a.inv + id) * 4;
-      st[warp][lane][0] = __ldg(r + 0);
-      st[warp][lane][1] = __ldg(r + 1);
-      st[warp][lane][2] = __ldg(r + 2);
-      st[warp][lane][3] = __ldg(r + 3);
+      const float4* r = rec + (size_t)__ldg(a.sorted + start + j) * kLidarRecQuads;   // slot = internal index
+#pragma unroll
+      for (int q = 0; q < kLidarRecQuads; ++q) st[warp][q][lane] = __ldg(r + q);
+    } else {
+      st[warp][3][lane] = make_float4(0.f, 0.f, 0.f, 3e38f);   // never accepted
     }
     __syncwarp();
-    const int cnt = min(32, n - base);
-    for (int k = 0; k < cnt; ++k) {
-      const float4 q0 = st[warp][k][0], q1 = st[warp][k][1], q2 = st[warp][k][2];
-      const float log2o = st[warp][k][3].x;
-      const float w0 = fmaf(q0.x, ray.x, fmaf(q0.y, ray.y, q0.z * ray.z));
-      const float w1 = fmaf(q1.x, ray.x, fmaf(q1.y, ray.y, q1.z * ray.z));
-      const float w2 = fmaf(q2.x, ray.x, fmaf(q2.y, ray.y, q2.z * ray.z));
-      const float ww = fmaf(w0, w0, fmaf(w1, w1, w2 * w2));
-      const float wm = fmaf(w0, q0.w, fmaf(w1, q1.w, w2 * q2.w));
-      const float th = fmaxf(__fdividef(wm, ww), 0.f);     // t^ = max(t*, 0)
-      const float e0 = fmaf(-th, w0, q0.w), e1 = fmaf(-th, w1, q1.w), e2 = fmaf(-th, w2, q2.w);
-      const float arg = log2o - fmaf(e0, e0, fmaf(e1, e1, e2 * e2));
-      if (!done && arg >= kLog2AlphaMin) {   // alpha >= 1/255 (R12)
-        const float alpha = fminf(kAlphaMax, ex2_approx(arg));
-        const float tT = T * (1.f - alpha);
-        if (tT < kTermT) {
-          done = true;                        // stop before blending (R13)
-        } else {
-          R = fmaf(alpha * T, th, R);         // w t^ (R14 with t^ for z)
-          T = tT;
+    unsigned mine = 0;   // lanes (rays) that accept record `lane` of this round
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const float4 xc = st[warp][3][k];
+      const bool acc = !done && fmaf(ray.x, xc.x, fmaf(ray.y, xc.y, ray.z * xc.z)) >= xc.w;
+      const unsigned m = __ballot_sync(FULL, acc);
+      mine = lane == k ? m : mine;
+    }
+    unsigned work = __ballot_sync(FULL, mine != 0);
+    while (work) {
+      const int k = __ffs(work) - 1;
+      work &= work - 1;
+      const unsigned m = __shfl_sync(FULL, mine, k);
+      if (!done && ((m >> lane) & 1u)) {
+        const float4 q0 = st[warp][0][k], q1 = st[warp][1][k], q2 = st[warp][2][k];
+        const float log2o = st[warp][4][k].x;
+        const float w0 = fmaf(q0.x, ray.x, fmaf(q0.y, ray.y, q0.z * ray.z));
+        const float w1 = fmaf(q1.x, ray.x, fmaf(q1.y, ray.y, q1.z * ray.z));
+        const float w2 = fmaf(q2.x, ray.x, fmaf(q2.y, ray.y, q2.z * ray.z));
+        const float ww = fmaf(w0, w0, fmaf(w1, w1, w2 * w2));
+        const float wm = fmaf(w0, q0.w, fmaf(w1, q1.w, w2 * q2.w));
+        const float th = fmaxf(__fdividef(wm, ww), 0.f);     // t^ = max(t*, 0)
+        const float e0 = fmaf(-th, w0, q0.w), e1 = fmaf(-th, w1, q1.w), e2 = fmaf(-th, w2, q2.w);
+        const float arg = log2o - fmaf(e0, e0, fmaf(e1, e1, e2 * e2));
+        if (arg >= kLog2AlphaMin) {   // alpha >= 1/255 (R12)
+          const float alpha = fminf(kAlphaMax, ex2_approx(arg));
+          const float tT = T * (1.f - alpha);
+          if (tT < kTermT) {
+            done = true;                        // stop before blending (R13)
+          } else {
+            R = fmaf(alpha * T, th, R);         // w t^ (R14 with t^ for z)
+            T = tT;
+          }
         }
       }
     }

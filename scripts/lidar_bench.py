@@ -2,7 +2,7 @@
 gsb_render_lidar on the C3 scene (520 k Gaussians) for several ray patterns, CUDA events on the
 render stream, fresh poses per step.  One JSON line per pattern.
 
-   python scripts/lidar_bench.py [envs] [steps]
+   python scripts/lidar_bench.py [envs] [steps] [pattern ...]
 """
 import json
 import sys
@@ -28,7 +28,10 @@ patterns = {
     "non_repetitive_20000_body": (synth.lidar_pattern("non_repetitive", n_points=20000), mount, [0]),
     "height_scan_11x17_body": (synth.lidar_pattern("height_scan", 11, 17), mount, [0]),
 }
+only = sys.argv[3:]
 for name, (dirs, sx, sb) in patterns.items():
+    if only and name not in only:
+        continue
     lid = gsb.Lidar(g, dirs)
     R = lid.n_rays
     rng = torch.empty((B, 1, R), device="cuda")
