@@ -19,8 +19,15 @@ x ^= x>>16), the global frame index g = env_offset * C + f, and idx = ((g H + y)
     base = mix32(lo32(idx) ^ mix32(hi32(idx) ^ mix32(seed ^ mix32(step))))
     u_j  = mix32(base + j * 0x9E3779B9) >> 10      (j = 0..3, 22-bit uniforms)
     z    = float(u_0 + u_1 + u_2 + u_3) - 2^23     (exact in binary32).
-With noise_std = 0 the noise term is skipped (it would add +0).  Motion blur needs a pixel
-neighbourhood and is not part of this epilogue.
+With noise_std = 0 the noise term is skipped (it would add +0).
+
+Reading R33 — motion blur ("injection of image noise and motion blur"; no formula): a
+per-frame linear box blur of the composite c along an integer pixel motion (bx, by), applied
+BEFORE R31 (blur happens during the exposure, noise and encoding after it); depth is not
+blurred.  With L = max(|bx|, |by|) + 1 taps (L = 1: identity), tap k = 0..L-1 sits at
+    o_k(b) = floor((2 k b + (L-1)) / (2 (L-1))) - floor(b / 2)      (integer arithmetic)
+i.e. k b / (L-1) rounded half up, shifted to centre the segment; samples clamp to the image
+edge; in binary32 RN:  acc = ((c_0 + c_1) + c_2) + ...  in tap order, blurred = acc / L.
 """
 from __future__ import annotations
 
@@ -83,3 +90,30 @@ def epilogue(rgb, depth, dr, seed: int = 0, step: int = 0, frame_offset: int = 0
         with np.errstate(over="ignore"):   # beyond 65504 rounds to inf, as IEEE requires
             d16 = np.asarray(depth, np.float32).astype(np.float16)
     return q, d16
+
+
+def blur_taps(bx: int, by: int):
+    """Reading R33 tap offsets [(ox_k, oy_k)] of one frame (integer arithmetic)."""
+    L = max(abs(int(bx)), abs(int(by))) + 1
+    if L == 1:
+        return [(0, 0)]
+    d = 2 * (L - 1)
+    return [((2 * k * bx + (L - 1)) // d - bx // 2, (2 * k * by + (L - 1)) // d - by // 2) for k in range(L)]
+
+
+def motion_blur(rgb, blur):
+    """Reading R33 on frames rgb [F,3,H,W] (rounded to binary32) with blur [F,2] int (bx, by):
+    binary32 sequential tap sum over edge-clamped samples, then one division by L."""
+    c = np.asarray(rgb, np.float32)
+    F, _, H, W = c.shape
+    out = np.empty_like(c)
+    ys, xs = np.arange(H)[:, None], np.arange(W)[None, :]
+    for f in range(F):
+        taps = blur_taps(int(blur[f][0]), int(blur[f][1]))
+        acc = np.zeros((3, H, W), np.float32)
+        for ox, oy in taps:
+            yy = np.clip(ys + oy, 0, H - 1)
+            xx = np.clip(xs + ox, 0, W - 1)
+            acc = acc + c[f][:, yy, xx]
+        out[f] = acc / np.float32(len(taps))
+    return out
