@@ -157,8 +157,8 @@ gsb_status gsb_render_host(gsb_scene scene, const float* body_poses, int32_t n_e
  *   v = ((c*gain - 0.5)*contrast + 0.5) + brightness [+ (z*sqrt(3)/2^22)*noise_std]
  *   rgb8 = rint(clamp(v, 0, 1) * 255)            (NaN -> 0)
  * z = Irwin-Hall(4) counter-based noise keyed by (seed, step, global frame
- * (env_offset + e)*C + c, pixel, channel) — identical under any env slicing.  Motion blur is
- * not part of the epilogue. */
+ * (env_offset + e)*C + c, pixel, channel) — identical under any env slicing.  Motion blur
+ * (a neighbourhood operation) is not part of this fused epilogue: see gsb_obs_encode. */
 #define GSB_OBS_DEPTH_F16 1u  /* out_depth holds IEEE half bits (uint16), else fp32 */
 typedef struct {
   const float* image_dr;  /* [B, C, 4] fp32 (gain, contrast, brightness, noise_std) per frame, or
@@ -182,6 +182,22 @@ gsb_status gsb_render_obs_host(gsb_scene scene, const float* body_poses, int32_t
                                int32_t n_cams, const float* intrinsics, const float* world_to_cam,
                                const gsb_render_params* params, const gsb_obs_params* obs,
                                uint8_t* out_rgb8, void* out_depth, gsb_stream stream);
+
+/* The observation encoding as a standalone pass over rendered fp32 frames, with the motion blur
+ * of reading R33 ("image noise and motion blur", oracle/obs.py) in front of
+ * the R31 DR/encoding.  Per frame f with blur[f] = (bx, by) integer pixels (each clamped to
+ * [-64, 64]):
+ * L = max(|bx|, |by|) + 1 taps at o_k = floor((2 k b + L - 1) / (2 (L - 1))) - floor(b / 2) per
+ * axis, edge-clamped samples, acc = sum in tap order (binary32 RN), blurred = acc / L; then R31.
+ * Depth is not blurred.  DEVICE pointers:
+ *   rgb        [B, C, 3, H, W] fp32 (e.g. gsb_render's out_rgb), depth [B, C, H, W] fp32 (nullable)
+ *   blur       [B, C, 2] int32 (nullable = no blur; then the codes equal gsb_render_obs's)
+ *   obs        as gsb_render_obs (image_dr DEVICE); out_rgb8 [B, C, 3, H, W] uint8;
+ *   out_depth  [B, C, H, W] fp16 bits or fp32 per GSB_OBS_DEPTH_F16 (written when depth != NULL).
+ * Asynchronous on stream; no scene needed.  Errors: INVALID_ARGUMENT, CUDA. */
+gsb_status gsb_obs_encode(const float* rgb, const float* depth, int32_t n_envs, int32_t n_cams, int32_t width,
+                          int32_t height, const gsb_obs_params* obs, const int32_t* blur, uint8_t* out_rgb8,
+                          void* out_depth, gsb_stream stream);
 
 /* Static-camera background pre-binning (§8(f) row 2; exploits RLGK's static/dynamic split,
  * PAPER.md App. B.2: static Gaussians never move, so with cameras fixed in the world

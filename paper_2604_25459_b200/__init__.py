@@ -33,7 +33,7 @@ EXPORTS = ["gsb_create_scene", "gsb_reserve", "gsb_render", "gsb_render_rig", "g
            "gsb_scores_reset", "gsb_get_scores", "gsb_filter_scene", "gsb_render_obs", "gsb_render_obs_host", "gsb_get_stats",
            "gsb_get_timings", "gsb_destroy_scene", "gsb_last_error", "gsb_version",
            "gsb_debug_project", "gsb_debug_bin_sort",
-           "gsb_lidar_create", "gsb_render_lidar", "gsb_lidar_info", "gsb_lidar_destroy"]
+           "gsb_obs_encode", "gsb_lidar_create", "gsb_render_lidar", "gsb_lidar_info", "gsb_lidar_destroy"]
 
 
 class GsbError(RuntimeError):
@@ -96,6 +96,7 @@ def lib() -> ctypes.CDLL:
     L.gsb_debug_project.argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P]
     L.gsb_debug_bin_sort.argtypes = [P, P, P, P, P, P, P, I32, I64, I32, I32, P, P, I64,
                                      ctypes.POINTER(I64), P]
+    L.gsb_obs_encode.argtypes = [P, P, I32, I32, I32, I32, op, P, P, P, P]
     L.gsb_lidar_create.argtypes = [P, P, I32, I32, I32, ctypes.POINTER(P)]
     L.gsb_render_lidar.argtypes = [P, P, P, I32, I32, P, I32, P, ctypes.c_float, ctypes.c_float, P, P, P]
     L.gsb_lidar_info.argtypes = [P, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32),
@@ -398,6 +399,16 @@ class Lidar:
             self.close()
         except Exception:
             pass
+
+
+def obs_encode(rgb, out_rgb8, depth=None, out_depth=None, blur=None, image_dr=None, seed: int = 0, step: int = 0,
+               env_offset: int = 0, depth_f16: bool = True, stream=None):
+    """gsb_obs_encode on CUDA tensors: rgb [B,C,3,H,W] float32 -> out_rgb8 uint8, with the reading-R33
+    motion blur (blur [B,C,2] int32 pixel extents, or None) before the reading-R31 image DR."""
+    B, C, _, H, W = (int(v) for v in rgb.shape)
+    o = Scene._obs(image_dr, seed, step, env_offset, depth_f16, False)
+    _check(lib().gsb_obs_encode(_ptr(rgb), _ptr(depth), B, C, W, H, ctypes.byref(o), _ptr(blur), _ptr(out_rgb8),
+                                _ptr(out_depth), _stream(stream)))
 
 
 def debug_bin_sort(u, v, sxx, syy, kappa, zbits, valid, width: int, height: int, cap: int, stream=None):

@@ -1071,6 +1071,29 @@ gsb_status gsb_render_obs(gsb_scene s, const float* poses, int32_t n_envs, int32
                      f16 ? nullptr : (float*)out_depth, nullptr, nullptr, (cudaStream_t)stream);
 }
 
+gsb_status gsb_obs_encode(const float* rgb, const float* depth, int32_t n_envs, int32_t n_cams, int32_t width,
+                          int32_t height, const gsb_obs_params* obs, const int32_t* blur, uint8_t* out_rgb8,
+                          void* out_depth, gsb_stream stream) {
+  gsb_status r = validate_obs(obs, out_rgb8);
+  if (r != GSB_OK) return r;
+  if (n_envs < 0 || n_cams < 1 || width < 1 || height < 1 || width > kMaxDim || height > kMaxDim)
+    return fail(GSB_ERR_INVALID_ARGUMENT, "bad frame shape (%d envs, %d cams, %dx%d)", n_envs, n_cams, width, height);
+  const int64_t F = (int64_t)n_envs * n_cams;
+  if (F == 0) return GSB_OK;
+  if (F > 65535) return fail(GSB_ERR_CAPACITY, "%lld frames > 65535 per call", (long long)F);
+  if (!rgb) return fail(GSB_ERR_INVALID_ARGUMENT, "rgb is NULL");
+  EncodeArgs a{};
+  a.rgb = rgb; a.depth = depth; a.blur = blur; a.dr = obs->image_dr; a.seed = obs->seed; a.step = obs->step;
+  a.frame_offset = obs->env_offset * n_cams; a.n_frames = (int)F; a.width = width; a.height = height;
+  a.out_rgb8 = out_rgb8;
+  const bool f16 = (obs->flags & GSB_OBS_DEPTH_F16) != 0;
+  a.out_depth16 = (depth && f16) ? (uint16_t*)out_depth : nullptr;
+  a.out_depth32 = (depth && !f16) ? (float*)out_depth : nullptr;
+  launch_k6_encode(a, (cudaStream_t)stream);
+  LAUNCH_CHECK();
+  return GSB_OK;
+}
+
 gsb_status gsb_render_obs_host(gsb_scene s, const float* poses, int32_t n_envs, int32_t n_cams, const float* intr,
                                const float* w2c, const gsb_render_params* p, const gsb_obs_params* obs,
                                uint8_t* out_rgb8, void* out_depth, gsb_stream stream) {

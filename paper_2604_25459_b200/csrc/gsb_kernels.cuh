@@ -157,6 +157,21 @@ struct LidarL4Args {
 };
 
 void launch_kl1(const LidarL1Args& a, cudaStream_t s);
+
+// K6: reading R33 motion blur + reading R31 encoding over rendered fp32 frames (gsb_obs_encode)
+struct EncodeArgs {
+  const float* rgb;       // [F][3][H][W]
+  const float* depth;     // [F][H][W] or nullptr
+  const int32_t* blur;    // [F][2] (bx, by) or nullptr
+  const float* dr;        // [F][4] or nullptr
+  uint32_t seed, step;
+  int64_t frame_offset;   // global frame index of frame 0 (noise counters)
+  int n_frames, width, height;
+  uint8_t* out_rgb8;      // [F][3][H][W]
+  uint16_t* out_depth16;  // fp16 bits, or nullptr
+  float* out_depth32;     // or fp32 copy, or nullptr
+};
+void launch_k6_encode(const EncodeArgs& a, cudaStream_t s);
 void launch_kl4(const LidarL4Args& a, cudaStream_t s);
 
 void launch_k0(const K0Rig& rig, int n_frames, int n_cams, int n_bodies, int width, int height,

@@ -90,6 +90,15 @@ __device__ __forceinline__ float irwin_hall4(uint64_t idx, uint32_t kseed) {
 }
 constexpr float kNoiseS3 = 1.7320508075688772f / 4194304.f;   // sqrt(3) / 2^22 (power-of-2 divisor: exact)
 
+// Reading R31 on one value: image DR (gain, contrast, brightness, noise_std) = dr, then the
+// 8-bit code; binary32 RN ops in the order of oracle/obs.py.  idx = the value's noise counter.
+__device__ __forceinline__ uint8_t r31_encode(float c, float4 dr, uint64_t idx, uint32_t kseed) {
+  float v = __fadd_rn(__fmul_rn(__fsub_rn(__fmul_rn(c, dr.x), 0.5f), dr.y), 0.5f);
+  v = __fadd_rn(v, dr.z);
+  if (dr.w != 0.f) v = __fadd_rn(v, __fmul_rn(__fmul_rn(irwin_hall4(idx, kseed), kNoiseS3), dr.w));
+  return (uint8_t)__float2uint_rn(__fmul_rn(__saturatef(v), 255.f));
+}
+
 // first index in sorted k[0..n) whose value is >= x
 template <typename T, typename P>
 __device__ __forceinline__ int lower_bound(P k, int n, T x) {
@@ -126,13 +135,8 @@ __device__ __forceinline__ void store_pixels(const CompositeArgs& a, size_t f, i
       const float cc[3] = {fmaf(T, a.bg0, h ? r1c : r0c), fmaf(T, a.bg1, h ? g1c : g0c), fmaf(T, a.bg2, h ? b1c : b0c)};
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) {
-        float v = __fadd_rn(__fmul_rn(__fsub_rn(__fmul_rn(cc[ch], dr.x), 0.5f), dr.y), 0.5f);
-        v = __fadd_rn(v, dr.z);
-        if (dr.w != 0.f) {
-          const uint64_t idx = ((gf * (uint64_t)a.height + (uint64_t)y) * (uint64_t)a.width + (uint64_t)px) * 3u + ch;
-          v = __fadd_rn(v, __fmul_rn(__fmul_rn(irwin_hall4(idx, kseed), kNoiseS3), dr.w));
-        }
-        o8[ch * plane + p] = (uint8_t)__float2uint_rn(__fmul_rn(__saturatef(v), 255.f));
+        const uint64_t idx = ((gf * (uint64_t)a.height + (uint64_t)y) * (uint64_t)a.width + (uint64_t)px) * 3u + ch;
+        o8[ch * plane + p] = r31_encode(cc[ch], dr, idx, kseed);
       }
       const float d = h ? d1 : d0;
       if (a.obs_depth16) a.obs_depth16[f * plane + p] = __half_as_ushort(__float2half_rn(d));
