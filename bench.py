@@ -169,12 +169,25 @@ def run_reference(args, cfg):
     v = float(np.median([r["value"] for r in vals]))
     out = {"metric": "env-camera frames/s at 640x480", "value": v, "unit": "env-camera frames/s",
            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-           "dtype": "f64", "data": "synthetic", "config": {"workload": cfg.name},
+           "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic",
+           "config": config_dict(cfg, cfg.n_envs if args.scaling == "weak" else synth.env_slice(cfg.n_envs, 0, world)[1],
+                                 world, args),
            "cpu_baseline": {"value": v, "unit": "env-camera frames/s", "cores": vals[0]["cores"], "kind": "oracle",
                             "sample": vals[0]["sample"].replace("4096", "1024")},
            "e2e": {"value": v, "unit": "env-camera frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
+
+
+def config_dict(cfg, B, world, args):
+    """The workload named in both arms' JSON lines."""
+    C, W, H = cfg.n_cams, cfg.width, cfg.height
+    total = B * world if args.scaling == "weak" else cfg.n_envs
+    return {"workload": f"{cfg.name}: {B} envs x {C} cam per GPU, {W}x{H}, "
+                        f"{cfg.n_bg} static + {cfg.n_rb} robot Gaussians on {cfg.n_bodies} bodies, SH {cfg.sh_degree}",
+            "envs_per_gpu": B, "frames_per_step": total * C,
+            "l2": "256 MB buffer written between timed steps (outside the events); "
+                  "per-step working set (5 GB outputs) >> L2", "parallelism": f"env-slices x{world}"}
 
 
 # ------------------------------------------------------------------------------ GPU arm
@@ -189,6 +202,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: cfg.n_envs envs per rank (C3, the headline); strong: cfg.n_envs envs in total, "
+                         "contiguous slices per rank (SURVEY §8(e): C5 8192 envs over G GPUs)")
     args = ap.parse_args()
     cfg = synth.CONFIGS[args.config]
     if args.impl == "reference":
@@ -201,9 +217,16 @@ def main():
     dev = torch.device("cuda", local % torch.cuda.device_count() if world > 1 else 0)
     peaks, peaks_kind = load_peaks()
 
-    # weak scaling: every rank renders its own cfg.n_envs envs (global ids rank*B + [0, B))
-    B, C, W, H = cfg.n_envs, cfg.n_cams, cfg.width, cfg.height
-    env_ids = np.arange(rank * B, (rank + 1) * B)
+    # weak scaling: every rank renders its own cfg.n_envs envs (global ids rank*B + [0, B));
+    # strong scaling: the cfg.n_envs envs are split into contiguous slices (synth.env_slice)
+    C, W, H = cfg.n_cams, cfg.width, cfg.height
+    if args.scaling == "weak":
+        B = cfg.n_envs
+        env_ids = np.arange(rank * B, (rank + 1) * B)
+    else:
+        lo, hi = synth.env_slice(cfg.n_envs, rank, world)
+        env_ids = np.arange(lo, hi)
+        B = hi - lo
     scene = synth.make_scene(cfg)
     g = gsb.Scene.from_synth(scene, device=dev.index)
     g.reserve(B, C, W, H, chunk_frames=args.chunk, host_io=not args.no_e2e)
@@ -249,7 +272,7 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
     t_dev = sum(step_ms) / 1e3
     t_max = max_over_ranks(t_dev, world)
-    frames_total = B * C * args.steps * world
+    frames_total = (B * world if args.scaling == "weak" else cfg.n_envs) * C * args.steps
     value = frames_total / t_max
 
     # roofline of the dominant kernel (K4b persistent compositing; the fused K4 when
@@ -285,7 +308,7 @@ def main():
         t_e2e = max_over_ranks(e0.elapsed_time(e1) / 1e3, world)
         h2d = h_poses[0].numel() * 4 + h_intr.numel() * 4 + h_w2c.numel() * 4
         d2h = h_rgb.numel() * 4 + h_dep.numel() * 4
-        e2e = {"value": B * C * args.e2e_steps * world / t_e2e, "unit": "env-camera frames/s",
+        e2e = {"value": (B * world if args.scaling == "weak" else cfg.n_envs) * C * args.e2e_steps / t_e2e, "unit": "env-camera frames/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps}
 
     cpu = None
@@ -305,15 +328,13 @@ def main():
             "warmup": args.warmup,
             "ms_per_step": t_max / args.steps * 1e3,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": args.scaling,
+            "step_ms": {"median": float(np.median(step_ms)), "min": float(np.min(step_ms)),
+                        "max": float(np.max(step_ms))},
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: {B} envs x {C} cam per GPU, {W}x{H}, "
-                                   f"{cfg.n_bg} static + {cfg.n_rb} robot Gaussians on {cfg.n_bodies} bodies, "
-                                   f"SH {cfg.sh_degree}", "envs_per_gpu": B, "frames_per_step": B * C * world,
-                       "l2": "256 MB buffer written between timed steps (outside the events); "
-                             "per-step working set (5 GB outputs) >> L2", "parallelism": f"env-slices x{world}"},
+            "config": config_dict(cfg, B, world, args),
             "gpu_launches": int(np.mean(launches)),
             "roofline": {"bound": "alu", "kernel": "K4b blend" if os.environ.get("GSB_K4") != "fused" else "K4 composite", "achieved": achieved, "peak": peak,
                          "unit": "Top/s (fp32 thread-ops)", "frac": achieved / peak, "traffic": traffic,
