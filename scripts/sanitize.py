@@ -22,3 +22,27 @@ for name in ("T1", "T6", "T3"):
              gsb.RenderParams(W, H, stats=True), rgb, dep, alp, nev)
     torch.cuda.synchronize()
     print(name, "ok", g.stats(), float(rgb.mean()))
+
+# LiDAR (reading R32) and the standalone encoder with motion blur (reading R33)
+cfg = synth.CONFIGS["T1"]
+sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
+g = gsb.Scene.from_synth(sc)
+for pat in (synth.lidar_pattern("rotating", 8, 64), synth.lidar_pattern("solid_state", 8, 32)):
+    lid = gsb.Lidar(g, pat)
+    B = cfg.n_envs
+    rr = torch.zeros((B, 2, lid.n_rays), device="cuda")
+    ra = torch.zeros((B, 2, lid.n_rays), device="cuda")
+    sx = np.stack([synth.lidar_world_sensor(cfg, np.arange(B)),
+                   np.broadcast_to(synth.lidar_body_mount(), (B, 3, 4))], 1).astype(np.float32).copy()
+    lid.render(torch.from_numpy(b.poses).cuda(), torch.from_numpy(sx).cuda(), rr, ra, sensor_body=[-1, 0])
+    torch.cuda.synchronize()
+    print("lidar ok", lid.info(), float(ra.mean()))
+    lid.close()
+rgb = torch.rand((2, 2, 3, 33, 47), device="cuda")
+dep = torch.rand((2, 2, 33, 47), device="cuda")
+out8 = torch.zeros((2, 2, 3, 33, 47), dtype=torch.uint8, device="cuda")
+od = torch.zeros((2, 2, 33, 47), dtype=torch.float16, device="cuda")
+blur = torch.tensor([[[5, -3], [0, 0]], [[-9, 2], [70, 1]]], dtype=torch.int32, device="cuda")
+gsb.obs_encode(rgb, out8, depth=dep, out_depth=od, blur=blur)
+torch.cuda.synchronize()
+print("encode ok", int(out8.float().mean()))
