@@ -191,9 +191,9 @@ void launch_kl1(const LidarL1Args& a, cudaStream_t s) {
 // ------------------------------------------------------------------------------ KL4
 // One warp per (frame, cell, <= 32 rays).  Per round, 32 records of the cell's sorted list are
 // staged in shared memory (one per lane, quad-major so the broadcast reads are conflict-free);
-// every lane tests its ray against the 32 cull quads (d.x >= c: 4 ops per pair) and a ballot
-// per record gives the lanes that must evaluate it; only records some lane accepts run the
-// exact R32 evaluation (~25 ops).  The lists are (bits(rho), id) ordered (K4a), so the lanes
+// every lane tests its ray against the 32 cull quads (d.x >= c: 4 ops per pair) into its own
+// bit mask, then walks its accepted records in list order with the exact R32 evaluation
+// (~25 ops) — lanes diverge, but every executed evaluation is a useful one.  The lists are (bits(rho), id) ordered (K4a), so the lanes
 // composite front to back; the warp leaves when every lane has terminated.
 constexpr int kL4Warps = 4;
 
@@ -225,39 +225,37 @@ __global__ void __launch_bounds__(32 * kL4Warps) kl4_cast(LidarL4Args a) {
       st[warp][3][lane] = make_float4(0.f, 0.f, 0.f, 3e38f);   // never accepted
     }
     __syncwarp();
-    unsigned mine = 0;   // lanes (rays) that accept record `lane` of this round
+    unsigned mine = 0;   // records of this round whose cone test this lane's ray passes
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
       const float4 xc = st[warp][3][k];
-      const bool acc = !done && fmaf(ray.x, xc.x, fmaf(ray.y, xc.y, ray.z * xc.z)) >= xc.w;
-      const unsigned m = __ballot_sync(FULL, acc);
-      mine = lane == k ? m : mine;
+      const bool acc = fmaf(ray.x, xc.x, fmaf(ray.y, xc.y, ray.z * xc.z)) >= xc.w;
+      mine |= acc ? (1u << k) : 0u;
     }
-    unsigned work = __ballot_sync(FULL, mine != 0);
-    while (work) {
-      const int k = __ffs(work) - 1;
-      work &= work - 1;
-      const unsigned m = __shfl_sync(FULL, mine, k);
-      if (!done && ((m >> lane) & 1u)) {
-        const float4 q0 = st[warp][0][k], q1 = st[warp][1][k], q2 = st[warp][2][k];
-        const float log2o = st[warp][4][k].x;
-        const float w0 = fmaf(q0.x, ray.x, fmaf(q0.y, ray.y, q0.z * ray.z));
-        const float w1 = fmaf(q1.x, ray.x, fmaf(q1.y, ray.y, q1.z * ray.z));
-        const float w2 = fmaf(q2.x, ray.x, fmaf(q2.y, ray.y, q2.z * ray.z));
-        const float ww = fmaf(w0, w0, fmaf(w1, w1, w2 * w2));
-        const float wm = fmaf(w0, q0.w, fmaf(w1, q1.w, w2 * q2.w));
-        const float th = fmaxf(__fdividef(wm, ww), 0.f);     // t^ = max(t*, 0)
-        const float e0 = fmaf(-th, w0, q0.w), e1 = fmaf(-th, w1, q1.w), e2 = fmaf(-th, w2, q2.w);
-        const float arg = log2o - fmaf(e0, e0, fmaf(e1, e1, e2 * e2));
-        if (arg >= kLog2AlphaMin) {   // alpha >= 1/255 (R12)
-          const float alpha = fminf(kAlphaMax, ex2_approx(arg));
-          const float tT = T * (1.f - alpha);
-          if (tT < kTermT) {
-            done = true;                        // stop before blending (R13)
-          } else {
-            R = fmaf(alpha * T, th, R);         // w t^ (R14 with t^ for z)
-            T = tT;
-          }
+    if (done) mine = 0u;
+    // each lane walks its own accepted records in list order (front to back for its ray)
+    while (mine) {
+      const int k = __ffs(mine) - 1;
+      mine &= mine - 1;
+      const float4 q0 = st[warp][0][k], q1 = st[warp][1][k], q2 = st[warp][2][k];
+      const float log2o = st[warp][4][k].x;
+      const float w0 = fmaf(q0.x, ray.x, fmaf(q0.y, ray.y, q0.z * ray.z));
+      const float w1 = fmaf(q1.x, ray.x, fmaf(q1.y, ray.y, q1.z * ray.z));
+      const float w2 = fmaf(q2.x, ray.x, fmaf(q2.y, ray.y, q2.z * ray.z));
+      const float ww = fmaf(w0, w0, fmaf(w1, w1, w2 * w2));
+      const float wm = fmaf(w0, q0.w, fmaf(w1, q1.w, w2 * q2.w));
+      const float th = fmaxf(__fdividef(wm, ww), 0.f);     // t^ = max(t*, 0)
+      const float e0 = fmaf(-th, w0, q0.w), e1 = fmaf(-th, w1, q1.w), e2 = fmaf(-th, w2, q2.w);
+      const float arg = log2o - fmaf(e0, e0, fmaf(e1, e1, e2 * e2));
+      if (arg >= kLog2AlphaMin) {   // alpha >= 1/255 (R12)
+        const float alpha = fminf(kAlphaMax, ex2_approx(arg));
+        const float tT = T * (1.f - alpha);
+        if (tT < kTermT) {
+          done = true;                        // stop before blending (R13)
+          mine = 0u;
+        } else {
+          R = fmaf(alpha * T, th, R);         // w t^ (R14 with t^ for z)
+          T = tT;
         }
       }
     }
