@@ -90,6 +90,11 @@ def test_host_side_validation_without_gpu():
     assert L.gsb_render_lidar(None, None, None, 1, 1, None, 0, None, 0.01, 100.0, None, None, None) == 1
     assert L.gsb_lidar_info(None, None, None, None, None) == 1
     assert L.gsb_lidar_destroy(None) == 0
+    # the standalone encoder rejects missing parameters before any device work
+    assert L.gsb_obs_encode(None, None, 1, 1, 8, 8, None, None, None, None, None) == 1
+    o = gsb.gsb_obs_params()
+    assert L.gsb_obs_encode(None, None, 1, 1, 8, 8, ctypes.byref(o), None, None, None, None) == 1
+    assert L.gsb_obs_encode(None, None, 1, 0, 8, 8, ctypes.byref(o), None, 1, None, None) == 1
 
 
 def test_render_params_layout_matches_header(tmp_path):

@@ -193,6 +193,42 @@ def test_render_full_size_sampled_pixels(name):
     assert st["P"] == int(gout["n_eval"].astype(np.int64).sum())
 
 
+@pytest.mark.slow
+def test_render_c5_full_size_sampled_pixels():
+    """C5 (1 M Gaussians, 8192 envs) in the bench's strong-scaling launch at N = 1 (all 8192
+    envs in one call, 40 GB of outputs kept on the device): sampled pixels of frames
+    {0, B/2, B-1} are pulled from the device and compared with the oracle."""
+    cfg = synth.CONFIGS["C5"]
+    sc = synth.make_scene(cfg)
+    B, W, H = cfg.n_envs, cfg.width, cfg.height
+    b = synth.make_batch(cfg)
+    g = gsb.Scene.from_synth(sc)
+    g.reserve(B, 1, W, H)
+    rgb = torch.full((B, 1, 3, H, W), float("nan"), device="cuda")
+    dep = torch.full((B, 1, H, W), float("nan"), device="cuda")
+    alp = torch.full((B, 1, H, W), float("nan"), device="cuda")
+    nev = torch.full((B, 1, H, W), -7, dtype=torch.int32, device="cuda")
+    g.render(gu.to_dev(b.poses), gu.to_dev(b.intrinsics), gu.to_dev(b.w2c), gsb.RenderParams(W, H), rgb, dep, alp, nev)
+    torch.cuda.synchronize()
+    assert not bool(torch.isnan(rgb).any()) and int((nev < 0).sum()) == 0
+    kap = gu.kappa_f32(sc)
+    rng = np.random.default_rng(55)
+    for e in (0, B // 2, B - 1):
+        px = rng.integers(0, W, 256)
+        py = rng.integers(0, H, 256)
+        gout = {"rgb": rgb[e:e + 1].cpu().numpy(), "depth": dep[e:e + 1].cpu().numpy(),
+                "alpha": alp[e:e + 1].cpu().numpy(), "n_eval": nev[e:e + 1].cpu().numpy()}
+        ref = _oracle_frame(sc, b, e, 0, W, H, pixels=(px, py))
+        sub = synth.Batch(b.poses[e:e + 1], b.intrinsics[e:e + 1], b.w2c[e:e + 1])
+        rec, zb, va = gu.gpu_project(g, sub, W, H)
+        r = gu.compare_frame(gout, 0, 0, ref, W, H, pix=(px, py), gpu_rec=rec[0], gpu_zb=zb[0], gpu_valid=va[0],
+                             kap=kap)
+        print("C5", e, r)
+        assert r["rgb_fail"] == 0 and r["dep_fail"] == 0 and r["alp_fail"] == 0, r
+        assert r["n_eval_fail"] == 0, r
+        assert r["masked_frac"] <= MASK_CAP, r
+
+
 # --------------------------------------------------------------------------- invariants
 def test_batch_slicing_and_chunking_bit_identical():
     """Per-env frames are bit-identical whether rendered in one call, as env slices (the
