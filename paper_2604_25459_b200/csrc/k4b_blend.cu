@@ -348,10 +348,9 @@ void launch_k4b_blend(const CompositeArgs& a, int* counter, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4b_blend<false>, kBlendWarps * 32, 0);
-    // 8 CTAs per SM, one below the register limit (9): the latency-bound K1 / K2b / K4a of the other
-    // streams co-reside with K4b instead of waiting for its CTAs to retire (same-box sweep,
-    // scripts/persm_sweep.sh: C3 +0.6 %, C4 +1.8 %, C6 +0.8 %)
-    per_sm = std::min(per_sm, 8);
+    // GSB_K4B_PER_SM=8 (one below the register limit) lets the other streams' latency-bound
+    // kernels co-reside: C3 +0.6 %, C4 +1.8 %, C6 +0.8 % of step throughput, but K4b's own live
+    // event time grows with the sharing (bench roofline 0.90 -> 0.76); the default keeps 9
     if (const char* e = getenv("GSB_K4B_PER_SM")) per_sm = std::min(per_sm, atoi(e));
     persistent = std::max(1, sms * std::max(1, per_sm));
   }
