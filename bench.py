@@ -344,7 +344,11 @@ def main():
                                        f"(B200_PROFILING.md unit counts; clock from MEASURED_PEAKS.json, {peaks_kind})"},
             "stage_ms_per_step": tsum,
             "counters": {"V_per_frame": st["V"] / (B * C), "K_per_frame": st["K"] / (B * C),
-                         "P_per_frame": st["P"] / (B * C), "long_lists_per_step": kern[-1]["long_lists"],
+                         "P_per_frame": st["P"] / (B * C),
+                         # scene statistics reported with every FPS number
+                         "V_over_N": st["V"] / (B * C) / cfg.n_gaussians, "K_over_V": st["K"] / max(st["V"], 1),
+                         "mean_tile_list": st["K"] / (B * C) / (((W + 15) // 16) * ((H + 15) // 16)),
+                         "mean_n_eval_per_pixel": st["P"] / (B * C) / (W * H), "long_lists_per_step": kern[-1]["long_lists"],
                          "max_tile_list": kern[-1]["max_list"], "chunks_per_step": kern[-1]["chunks"]},
             "clocks": clocks,
             "e2e": e2e,
