@@ -1407,11 +1407,13 @@ namespace {
 constexpr int kLidarMaxCells = 256;
 constexpr double kLidarPi = 3.14159265358979323846;
 
-// frames per LiDAR chunk: records (80 B) + emission (16 B) per (frame, Gaussian) within ~2 GB
+// frames per LiDAR chunk: records (80 B) + emission (16 B) per (frame, Gaussian) within ~8 GB
+// (KL4's parallelism is frames x ray groups: sparse patterns such as a height scan need many
+// frames per launch to fill the GPU)
 int lidar_chunk(int64_t n, int F) {
   const int64_t per = std::max<int64_t>(1, n) * 96 + 4096;
-  const int64_t e = std::max<int64_t>(1, ((int64_t)2 << 30) / per);
-  return (int)std::min<int64_t>({e, (int64_t)F, 256});
+  const int64_t e = std::max<int64_t>(1, ((int64_t)8 << 30) / per);
+  return (int)std::min<int64_t>({e, (int64_t)F, 1024});
 }
 
 }  // namespace

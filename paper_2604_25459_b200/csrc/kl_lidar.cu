@@ -214,17 +214,25 @@ __global__ void __launch_bounds__(32 * kL4Warps) kl4_cast(LidarL4Args a) {
   float T = 1.f, R = 0.f;
   bool done = !has;
   const float4* rec = a.rec + (size_t)fl * a.n * kLidarRecQuads;
-  for (int base = 0; base < n; base += 32) {
-    if (__all_sync(FULL, done)) break;
+  // the next round's records are loaded into registers while this round is composited
+  float4 pf[kLidarRecQuads];
+  auto prefetch = [&](int base) {
     const int j = base + lane;
     if (j < n) {
       const float4* r = rec + (size_t)__ldg(a.sorted + start + j) * kLidarRecQuads;   // slot = internal index
 #pragma unroll
-      for (int q = 0; q < kLidarRecQuads; ++q) st[warp][q][lane] = __ldg(r + q);
+      for (int q = 0; q < kLidarRecQuads; ++q) pf[q] = __ldg(r + q);
     } else {
-      st[warp][3][lane] = make_float4(0.f, 0.f, 0.f, 3e38f);   // never accepted
+      pf[3] = make_float4(0.f, 0.f, 0.f, 3e38f);   // never accepted
     }
+  };
+  if (n > 0) prefetch(0);
+  for (int base = 0; base < n; base += 32) {
+    if (__all_sync(FULL, done)) break;
+#pragma unroll
+    for (int q = 0; q < kLidarRecQuads; ++q) st[warp][q][lane] = pf[q];
     __syncwarp();
+    if (base + 32 < n) prefetch(base + 32);
     unsigned mine = 0;   // records of this round whose cone test this lane's ray passes
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
