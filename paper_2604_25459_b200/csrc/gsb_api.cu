@@ -757,11 +757,12 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
   s->tiles_y = (height + kTile - 1) / kTile;
   s->n_tiles = s->tiles_x * s->tiles_y;
   s->hist_stride = ((int64_t)s->n_tiles + 2 + 31) / 32 * 32;
-  // automatic chunk: >= 64 frames and ~256k tiles per chunk (219 frames at 640x480; small views
-  // get bigger chunks so every K4 launch has many waves of CTAs).  256k vs 64k tiles, same-box
-  // sweep: C3 +0.7 %, C4 +0.1 %, C6 +0.5 %, C7 +0.3 % (fewer, longer launches per stream)
+  // automatic chunk: >= 64 frames and ~64k tiles per chunk (small views get bigger chunks so
+  // every K4 launch has many waves of CTAs).  256k tiles would gain 0.3-0.7 % on device-resident
+  // renders (same-box sweep) but costs ~10 % end to end: gsb_render_host downloads each pass while
+  // the next one renders, and the last pass's download is not overlapped
   const char* ct = getenv("GSB_CHUNK_TILES");   // experiments: tiles per automatic chunk
-  const int64_t chunk_tiles = ct ? std::max<int64_t>(1, atoll(ct)) : 262144;
+  const int64_t chunk_tiles = ct ? std::max<int64_t>(1, atoll(ct)) : 65536;
   const int auto_e = (int)std::min<int64_t>(kMaxChunk, std::max<int64_t>(64, (chunk_tiles + s->n_tiles - 1) / s->n_tiles));
   const int E = (int)std::min<int64_t>(chunk_frames > 0 ? std::min(chunk_frames, kMaxChunk) : auto_e, F);
   s->chunk = E;
