@@ -166,3 +166,32 @@ def test_lidar_c3_full_size_sampled_rays():
         ref = oracle.lidar_frame(scene, poses[e], w2s, dirs[rays])
         res = _compare(rng_t[e, 0].cpu().numpy(), alp_t[e, 0].cpu().numpy(), ref, rays)
         _check(res, f"C3 lidar env {e} {lid.info()}")
+
+
+def test_lidar_many_sensors_max_grid_single_ray():
+    """Sixteen sensors per env (alternating world-fixed and body-mounted on different bodies),
+    the largest cell grid (256 x 256), and a one-ray pattern: every ray against the oracle."""
+    cfg = synth.CONFIGS["T4"]
+    scene = synth.make_scene(cfg)
+    B, S = cfg.n_envs, 16
+    poses = synth.make_poses(cfg, np.arange(B), 3)
+    Wsens = synth.lidar_world_sensor(cfg, np.arange(B))
+    mount = synth.lidar_body_mount()
+    sx = np.zeros((B, S, 3, 4), np.float32)
+    sb = np.full(S, -1, np.int32)
+    for s in range(S):
+        if s % 2:
+            sb[s] = s % cfg.n_bodies
+            sx[:, s] = mount
+        else:
+            sx[:, s] = Wsens
+    g = gsb.Scene.from_synth(scene)
+    for dirs, grid in ((synth.lidar_pattern("random", n_points=3000, seed=11), (256, 256)),
+                       (np.float32([[0.6, 0.0, -0.8]]), (0, 0))):
+        lid = gsb.Lidar(g, dirs, *grid)
+        g_rng, g_alp = _gpu_lidar(g, lid, poses, sx, sb)
+        for e in range(B):
+            for s in range(S):
+                ref = oracle.lidar_frame(scene, poses[e], _w2s(sx, sb, poses, e, s), dirs)
+                _check(_compare(g_rng[e, s], g_alp[e, s], ref), f"sensors env {e} sensor {s} {lid.info()}")
+        lid.close()
