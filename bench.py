@@ -281,6 +281,22 @@ def main():
     pairs_per_launch = st["P"] / max(comp_launches[0], 1)
     achieved = FP32_OPS_PER_PAIR * pairs_per_launch / (k4_avg_ms / 1e3) / 1e12
     peak = SM_COUNT * LANES_PER_SM * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    # whole-path roofline: T_roof = max(B_alg / BW, Ops_alg / R_fp32) per
+    # step, from the oracle's work counts (V, K, P of the STATS render), not from our SASS
+    F_step = B * C
+    n_g = cfg.n_gaussians
+    chunk_e = 64
+    b_alg = F_step * ((240 if cfg.sh_degree == 3 else 60) * n_g / chunk_e + 8 * n_g) \
+        + 108 * st["V"] + 32 * st["K"] + 16 * W * H * F_step
+    ops_alg = FP32_OPS_PER_PAIR * st["P"] + 15 * n_g * F_step + (190 if cfg.sh_degree == 3 else 105) * st["V"]
+    bw = peaks.get("hbm_gbs", 6546.6) * 1e9
+    t_hbm, t_alu = b_alg / bw, ops_alg / (peak * 1e12)
+    t_roof = max(t_hbm, t_alu)
+    path_roof = {"t_roof_ms_per_step": t_roof * 1e3, "bound": "alu" if t_alu >= t_hbm else "hbm",
+                 "t_alu_ms": t_alu * 1e3, "t_hbm_ms": t_hbm * 1e3,
+                 "frac": t_roof / (t_max / args.steps) if args.scaling == "weak" or world == 1 else None,
+                 "basis": "B_alg = (240|60)N/64 + 8N + 108V + 32K + 16Npx bytes and Ops_alg = 18P + 15N + "
+                          "(190|105)V fp32 ops per frame (SURVEY §8(d) d.4); BW = MEASURED_PEAKS hbm_gbs"}
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "k4_ncu_summary.json")) as f:
@@ -342,6 +358,7 @@ def main():
                          "avg_launch_ms": k4_avg_ms,
                          "peak_basis": f"148 SM x 128 lanes x {peaks.get('sm_max_mhz', 1965.0)} MHz "
                                        f"(B200_PROFILING.md unit counts; clock from MEASURED_PEAKS.json, {peaks_kind})"},
+            "path_roofline": path_roof,
             "stage_ms_per_step": tsum,
             "counters": {"V_per_frame": st["V"] / (B * C), "K_per_frame": st["K"] / (B * C),
                          "P_per_frame": st["P"] / (B * C),
