@@ -5,6 +5,7 @@ render stream, fresh poses per step.  One JSON line per pattern.
    python scripts/lidar_bench.py [envs] [steps] [pattern ...]
 """
 import json
+import os
 import sys
 
 import numpy as np
@@ -32,7 +33,8 @@ only = sys.argv[3:]
 for name, (dirs, sx, sb) in patterns.items():
     if only and name not in only:
         continue
-    lid = gsb.Lidar(g, dirs)
+    grid = os.environ.get("GSB_LIDAR_GRID")   # "n_az,n_el" override (sweeps)
+    lid = gsb.Lidar(g, dirs, *(int(v) for v in grid.split(","))) if grid else gsb.Lidar(g, dirs)
     R = lid.n_rays
     rng = torch.empty((B, 1, R), device="cuda")
     alp = torch.empty((B, 1, R), device="cuda")
