@@ -1381,6 +1381,7 @@ struct gsb_lidar_t {
   int4* d_items = nullptr;
   // workspace
   int ws_frames = 0;          // chunk capacity (frames)
+  int ws_req = 0;             // chunk size requested when the workspace was sized (>= ws_frames)
   int table_frames = 0;
   int64_t np = 0;
   int64_t hist_stride = 0;
@@ -1402,7 +1403,7 @@ struct gsb_lidar_t {
     cudaFree(off); cudaFree(frame_base); cudaFree(ids2); cudaFree(keys); cudaFree(keys_alt); cudaFree(sorted);
     rec = nullptr; emit = nullptr; vis_bits = nullptr; vcount = nullptr; hist = nullptr;
     off = nullptr; frame_base = nullptr; ids2 = nullptr; keys = keys_alt = nullptr; sorted = nullptr;
-    ws_frames = 0; key_cap = 0;
+    ws_frames = 0; ws_req = 0; key_cap = 0;
   }
 };
 
@@ -1560,7 +1561,7 @@ gsb_status gsb_render_lidar(gsb_scene s, gsb_lidar l, const float* poses, int32_
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t N = s->n;
   const int n_cells = l->n_az * l->n_el;
-  const int E = lidar_chunk(N, F);
+  int E = lidar_chunk(N, F);
   // workspace (grows on demand; synchronises then)
   if (l->table_frames < F) {
     CUDA_TRY(cudaStreamSynchronize(st));
@@ -1570,13 +1571,21 @@ gsb_status gsb_render_lidar(gsb_scene s, gsb_lidar l, const float* poses, int32_
     CUDA_TRY(dalloc(&l->table, (size_t)F * (s->n_bodies + 1) * 4));
     l->table_frames = F;
   }
-  if (l->ws_frames < E || l->np != (N + 31) / 32 * 32) {
+  if (l->ws_req < E || l->np != (N + 31) / 32 * 32) {
+    const int req = E;
     CUDA_TRY(cudaStreamSynchronize(st));
     l->free_ws();
     l->np = (N + 31) / 32 * 32;
     const int64_t np = std::max<int64_t>(l->np, 32);
     l->hist_stride = ((int64_t)n_cells + 2 + 31) / 32 * 32;
-    CUDA_TRY(dalloc(&l->rec, (size_t)E * std::max<int64_t>(N, 1) * kLidarRecQuads));
+    // the records dominate the workspace: on an allocation failure retry with half the frames
+    for (;;) {
+      const cudaError_t e = dalloc(&l->rec, (size_t)E * std::max<int64_t>(N, 1) * kLidarRecQuads);
+      if (e == cudaSuccess) break;
+      if (e != cudaErrorMemoryAllocation || E == 1) CUDA_TRY(e);
+      cudaGetLastError();   // clear the sticky-free allocation error
+      E = std::max(1, E / 2);
+    }
     CUDA_TRY(dalloc(&l->emit, (size_t)E * 2 * np));
     CUDA_TRY(dalloc(&l->vis_bits, (size_t)E * 2 * np / 32));
     CUDA_TRY(dalloc(&l->vcount, (size_t)E));
@@ -1590,7 +1599,9 @@ gsb_status gsb_render_lidar(gsb_scene s, gsb_lidar l, const float* poses, int32_
       CUDA_TRY(cudaMemcpy(l->ids2 + l->np, s->d_ids, sizeof(int2) * N, cudaMemcpyDeviceToDevice));
     }
     l->ws_frames = E;
+    l->ws_req = req;
   }
+  E = std::min(E, l->ws_frames);
   launch_k0(rig, F, n_sensors, s->n_bodies, 1, 1, l->table, nullptr, st);
   LAUNCH_CHECK();
   l->last_keys = 0;
