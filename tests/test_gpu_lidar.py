@@ -195,3 +195,25 @@ def test_lidar_many_sensors_max_grid_single_ray():
                 ref = oracle.lidar_frame(scene, poses[e], _w2s(sx, sb, poses, e, s), dirs)
                 _check(_compare(g_rng[e, s], g_alp[e, s], ref), f"sensors env {e} sensor {s} {lid.info()}")
         lid.close()
+
+
+def test_lidar_empty_scene_and_culled_ranges():
+    """N = 0: every ray returns range 0, alpha 0.  A near/far window excluding every Gaussian
+    gives the same; a window keeping some matches the oracle with the same near/far."""
+    sc = scene_from(np.zeros((0, 3)), np.zeros((0, 3)))
+    g = gsb.Scene.from_synth(sc)
+    dirs = synth.lidar_pattern("rotating", 4, 32)
+    lid = gsb.Lidar(g, dirs)
+    sx = np.hstack([np.eye(3), np.zeros((3, 1))]).astype(np.float32)[None, None].copy()
+    r, a = _gpu_lidar(g, lid, np.zeros((1, 0, 7), np.float32), sx, None)
+    assert (r == 0).all() and (a == 0).all()
+    cfg = synth.CONFIGS["T3"]
+    scene = synth.make_scene(cfg)
+    g2 = gsb.Scene.from_synth(scene)
+    lid2 = gsb.Lidar(g2, dirs)
+    sx2 = synth.lidar_world_sensor(cfg, [0])[:, None].copy()
+    r, a = _gpu_lidar(g2, lid2, np.zeros((1, 0, 7), np.float32), sx2, None, near=900.0, far=1000.0)
+    assert (r == 0).all() and (a == 0).all()
+    r, a = _gpu_lidar(g2, lid2, np.zeros((1, 0, 7), np.float32), sx2, None, near=2.0, far=4.0)
+    ref = oracle.lidar_frame(scene, np.zeros((0, 7), np.float32), sx2[0, 0], dirs, near=2.0, far=4.0)
+    _check(_compare(r[0, 0], a[0, 0], ref), "near/far window")
