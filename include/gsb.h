@@ -65,6 +65,9 @@ typedef enum {
                                stream for gsb_get_timings */
 #define GSB_FLAG_SCORES 4u  /* also accumulate the pruning scores of reading R30 into the
                                scene (gsb_get_scores); not with gsb_render_static */
+#define GSB_FLAG_STATIC_PER_ENV 8u /* gsb_render_static only: one camera per env, env e uses
+                               pre-binned camera e (per-env domain-randomised cameras that stay
+                               fixed over an episode); needs n_envs <= the pre-binned count */
 
 /* reserve flags */
 #define GSB_RESERVE_HOST_IO 1u /* also reserve device staging for gsb_render_host */
@@ -207,7 +210,8 @@ gsb_status gsb_obs_encode(const float* rgb, const float* depth, int32_t n_envs, 
  * the sorted per-(camera, tile) lists and their records in the scene (replacing any previous
  * pre-binning; synchronous).  Call gsb_reserve (again) afterwards if the scene was reserved
  * before, so the merge workspace exists.
- * gsb_render_static then renders B envs x those C cameras (frame f = e*C + c): per frame only
+ * gsb_render_static then renders B envs x those C cameras (frame f = e*C + c; with
+ * GSB_FLAG_STATIC_PER_ENV: B <= C envs x 1 camera, env e seen by camera e): per frame only
  * the robot Gaussians are projected, binned and sorted, and K4 merges each tile's robot list
  * with the camera's background list in (zbits, id) order (keys are unique, reading R10).
  * Outputs, layout and determinism as gsb_render with intrinsics/world_to_cam broadcast over

@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("GSB_LIB_PATH") or os.path.join(_HERE, "libgsb.so")  #
 GSB_FLAG_STATS = 1
 GSB_FLAG_TIMING = 2
 GSB_FLAG_SCORES = 4
+GSB_FLAG_STATIC_PER_ENV = 8
 GSB_OBS_DEPTH_F16 = 1
 GSB_RESERVE_HOST_IO = 1
 
@@ -161,6 +162,7 @@ class RenderParams:
     stats: bool = False
     timing: bool = False
     scores: bool = False   # accumulate the reading-R30 pruning scores into the scene
+    static_per_env: bool = False   # gsb_render_static: env e uses pre-binned camera e
 
     def to_c(self) -> gsb_render_params:
         p = gsb_render_params()
@@ -169,7 +171,8 @@ class RenderParams:
             p.background[k] = float(self.background[k])
         p.sh_degree = self.sh_degree
         p.flags = ((GSB_FLAG_STATS if self.stats else 0) | (GSB_FLAG_TIMING if self.timing else 0)
-                   | (GSB_FLAG_SCORES if self.scores else 0))
+                   | (GSB_FLAG_SCORES if self.scores else 0)
+                   | (GSB_FLAG_STATIC_PER_ENV if self.static_per_env else 0))
         return p
 
 

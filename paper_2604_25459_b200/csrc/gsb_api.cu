@@ -1023,7 +1023,11 @@ gsb_status gsb_render_static(gsb_scene s, const float* poses, int32_t n_envs, co
                              gsb_stream stream) {
   if (!s) return fail(GSB_ERR_INVALID_ARGUMENT, "scene is NULL");
   if (s->sb_cams < 1) return fail(GSB_ERR_INVALID_ARGUMENT, "gsb_prebin_static was not called");
-  gsb_status r = validate_render(s, poses, n_envs, s->sb_cams, s->sb_intr, s->sb_w2c, p, out_rgb);
+  const bool per_env = p && (p->flags & GSB_FLAG_STATIC_PER_ENV);
+  if (per_env && n_envs > s->sb_cams)
+    return fail(GSB_ERR_SHAPE_MISMATCH, "GSB_FLAG_STATIC_PER_ENV: %d envs > %d pre-binned cameras", n_envs, s->sb_cams);
+  const int C = per_env ? 1 : s->sb_cams;
+  gsb_status r = validate_render(s, poses, n_envs, C, s->sb_intr, s->sb_w2c, p, out_rgb);
   if (r != GSB_OK) return r;
   const int D = p->sh_degree < 0 ? s->sh_degree : p->sh_degree;
   if (p->width != s->sb_w || p->height != s->sb_h || p->near_plane != s->sb_near || p->far_plane != s->sb_far ||
@@ -1034,9 +1038,10 @@ gsb_status gsb_render_static(gsb_scene s, const float* poses, int32_t n_envs, co
   DeviceGuard g(s->device);
   s->dl_rgb = nullptr; s->dl_depth = nullptr; s->dl_alpha = nullptr; s->dl_neval = nullptr;
   K0Rig rig = default_rig(s, poses, s->sb_intr, s->sb_w2c);
-  rig.cams_shared = 1;
-  return render_impl(s, rig, n_envs, s->sb_cams, p, out_rgb, out_depth, out_alpha, out_neval, (cudaStream_t)stream,
-                     true);
+  // frame f uses pre-binned camera f mod C in K4's merge; K0 reads the same camera: shared
+  // camera rows (cam = f mod C) or, per env, row f (= env e, one camera per env)
+  rig.cams_shared = per_env ? 0 : 1;
+  return render_impl(s, rig, n_envs, C, p, out_rgb, out_depth, out_alpha, out_neval, (cudaStream_t)stream, true);
 }
 
 namespace {

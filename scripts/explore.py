@@ -30,7 +30,7 @@ torch.cuda.empty_cache()
 print(json.dumps(res), flush=True)
 
 envs = {"C2": 64, "C3": 1024, "C4": 4096, "C5": 1024, "C6": 4096, "C7": 256, "T1": 3}
-MODES = ("rig", "static", "scores", "obs")
+MODES = ("rig", "static", "scores", "obs", "static_env")
 _named = [n for n in sys.argv[1:] if n in synth.CONFIGS]
 _modes_only = bool(sys.argv[1:]) and all(a in MODES for a in sys.argv[1:])
 for name in ([] if _modes_only or ("static" in sys.argv[1:]) else (_named or ["C2", "C4", "C5", "C3"])):
@@ -149,6 +149,48 @@ if "static" in sys.argv[1:] or not sys.argv[1:]:
                           "prebin_s": round(t_prebin, 3), **res}), flush=True)
         del g, rgb, dep
         torch.cuda.empty_cache()
+
+# §8(f) row 2 with per-env cameras (GSB_FLAG_STATIC_PER_ENV): the bench's C3 workload exactly
+# (each env's domain-randomised camera, fixed over the episode), background pre-binned per env
+if "static_env" in sys.argv[1:]:
+    cfg = synth.CONFIGS["C3"]
+    B = 1024
+    sc = synth.make_scene(cfg)
+    g = gsb.Scene.from_synth(sc)
+    K, W = synth.make_cameras(cfg, np.arange(B))
+    torch.cuda.synchronize()
+    t0 = time.time()
+    g.prebin_static(K[:, 0].copy(), W[:, 0].copy(), gsb.RenderParams(cfg.width, cfg.height))
+    t_prebin = time.time() - t0
+    g.reserve(B, 1, cfg.width, cfg.height)
+    Kd, Wd = torch.from_numpy(K).cuda(), torch.from_numpy(W).cuda()
+    poses = [torch.from_numpy(synth.make_poses(cfg, np.arange(B), s)).cuda() for s in range(4)]
+    rgb = torch.empty((B, 1, 3, cfg.height, cfg.width), device="cuda")
+    dep = torch.empty((B, 1, cfg.height, cfg.width), device="cuda")
+    res = {}
+    for mode in ("render", "render_static_per_env"):
+        prm = gsb.RenderParams(cfg.width, cfg.height, static_per_env=(mode != "render"))
+
+        def call(s):
+            if mode == "render":
+                g.render(poses[s], Kd, Wd, prm, rgb, dep)
+            else:
+                g.render_static(poses[s], prm, rgb, dep)
+        for s in range(2):
+            call(s)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        for s in range(5):
+            call((s + 1) % 4)
+        e1.record()
+        torch.cuda.synchronize()
+        res[mode] = {"fps": 5 * B / (e0.elapsed_time(e1) / 1e3)}
+    print(json.dumps({"config": "C3 per-env static cameras (GSB_FLAG_STATIC_PER_ENV)", "frames": B,
+                      "prebin_s": round(t_prebin, 3), "prebin_GB": round(torch.cuda.memory_allocated() / 1e9, 1),
+                      **res}), flush=True)
+    del g, rgb, dep
+    torch.cuda.empty_cache()
 
 # §8(f) row 3 measurement: C3 render with GSB_FLAG_SCORES (pruning-score accumulation) vs plain
 if "scores" in sys.argv[1:] or not sys.argv[1:]:

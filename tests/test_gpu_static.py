@@ -135,3 +135,39 @@ def test_static_merge_both_k4_paths_bit_identical(name, path, monkeypatch):
     g.prebin_static(Ks, Ws, gsb.RenderParams(cfg.width, cfg.height))
     g.reserve(cfg.n_envs, cfg.n_cams, cfg.width, cfg.height)
     _assert_identical(_render_static(g, cfg, b.poses), ref)
+
+
+@pytest.mark.parametrize("name", ["T2", "T5", "T7"])
+def test_static_per_env_cameras_bit_identical(name):
+    """GSB_FLAG_STATIC_PER_ENV: every env has its own domain-randomised camera, fixed over the
+    episode, pre-binned once; rendering env e with pre-binned camera e is bit-identical to
+    gsb_render with the same per-env cameras, at two physics steps and for an env prefix."""
+    cfg = synth.CONFIGS[name]
+    sc = synth.make_scene(cfg)
+    B = cfg.n_envs + 2
+    ids = np.arange(B)
+    K, Wc = synth.make_cameras(cfg, ids)
+    K, Wc = K[:, :1].copy(), Wc[:, :1].copy()          # one camera per env
+    g = gsb.Scene.from_synth(sc)
+    g.prebin_static(K[:, 0].copy(), Wc[:, 0].copy(), gsb.RenderParams(cfg.width, cfg.height))
+    g.reserve(B, 1, cfg.width, cfg.height)
+    H, W = cfg.height, cfg.width
+    for step in (0, 4):
+        b = synth.Batch(synth.make_poses(cfg, ids, step), K, Wc)
+        ref = gu.gpu_render(sc, b, W, H, gscene=g, stats=True)
+        for n in (B, B - 1):
+            rgb = torch.full((n, 1, 3, H, W), float("nan"), device="cuda")
+            dep = torch.full((n, 1, H, W), float("nan"), device="cuda")
+            alp = torch.full((n, 1, H, W), float("nan"), device="cuda")
+            nev = torch.full((n, 1, H, W), -7, dtype=torch.int32, device="cuda")
+            g.render_static(gu.to_dev(b.poses[:n]), gsb.RenderParams(W, H, static_per_env=True, stats=True), rgb, dep,
+                            alp, nev)
+            torch.cuda.synchronize()
+            out = dict(rgb=rgb.cpu().numpy(), depth=dep.cpu().numpy(), alpha=alp.cpu().numpy(), n_eval=nev.cpu().numpy())
+            _assert_identical(out, {k: v[:n] for k, v in ref.items() if k in ("rgb", "depth", "alpha", "n_eval")})
+            if n == B:
+                assert g.stats() == ref["stats"]
+    with pytest.raises(gsb.GsbError):   # more envs than pre-binned cameras
+        g.reserve(B + 1, 1, W, H)
+        g.render_static(gu.to_dev(synth.make_poses(cfg, np.arange(B + 1), 0)),
+                        gsb.RenderParams(W, H, static_per_env=True), torch.zeros((B + 1, 1, 3, H, W), device="cuda"))
