@@ -957,6 +957,7 @@ gsb_status gsb_prebin_static(gsb_scene s, int32_t n_cams, const float* intr, con
   PB_TRY(dalloc(&fbase, (size_t)C + 2));
   PB_TRY(cudaMemsetAsync(vcount, 0, sizeof(int) * C, st));
   PB_TRY(cudaMemsetAsync(hist, 0, sizeof(int) * C * stride, st));
+  PB_TRY(cudaMemsetAsync(off, 0, sizeof(uint32_t) * C * stride, st));   // padding rows are read back below
   K1Args a{};
   a.g_mean = s->d_mean; a.g_L0 = s->d_L0; a.g_L1 = s->d_L1; a.g_L2 = s->d_L2; a.g_sh = s->d_sh;
   a.g_ids = s->d_ids;
@@ -1332,6 +1333,7 @@ gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, 
   DBG_TRY(dalloc(&fbase, (size_t)F + 2));
   DBG_TRY(cudaMemsetAsync(vcount, 0, sizeof(int) * F, st));
   DBG_TRY(cudaMemsetAsync(hist, 0, sizeof(int) * F * stride, st));
+  DBG_TRY(cudaMemsetAsync(off, 0, sizeof(uint32_t) * F * stride, st));   // padding rows are read back below
   launch_k1_external(u, v, sxx, syy, kappa, zbits, valid, n, 0, F, width, height, tiles_x, emit, vbits, vwords,
                      vcount, hist, stride, st);
   launch_k2_scan(hist, off, stride, F, n_tiles, fbase, nullptr, nullptr, 0, nullptr, nullptr, st);

@@ -46,3 +46,17 @@ blur = torch.tensor([[[5, -3], [0, 0]], [[-9, 2], [70, 1]]], dtype=torch.int32, 
 gsb.obs_encode(rgb, out8, depth=dep, out_depth=od, blur=blur)
 torch.cuda.synchronize()
 print("encode ok", int(out8.float().mean()))
+
+# static-camera merge with per-env pre-binned cameras (GSB_FLAG_STATIC_PER_ENV)
+cfg = synth.CONFIGS["T2"]
+sc = synth.make_scene(cfg)
+B = cfg.n_envs
+K, Wc = synth.make_cameras(cfg, np.arange(B))
+g = gsb.Scene.from_synth(sc)
+g.prebin_static(K[:, 0].copy(), Wc[:, 0].copy(), gsb.RenderParams(cfg.width, cfg.height))
+g.reserve(B, 1, cfg.width, cfg.height)
+rgb = torch.zeros((B, 1, 3, cfg.height, cfg.width), device="cuda")
+g.render_static(torch.from_numpy(synth.make_poses(cfg, np.arange(B), 1)).cuda(),
+                gsb.RenderParams(cfg.width, cfg.height, static_per_env=True), rgb)
+torch.cuda.synchronize()
+print("static per-env ok", float(rgb.mean()))
