@@ -94,6 +94,11 @@ uint64_t split_min_avg() {
   return e ? (uint64_t)strtoull(e, nullptr, 10) : 200u;
 }
 
+bool slot_keys_on() {   // GSB_SLOT_KEYS=0: keys carry the creation id on every path
+  const char* e = getenv("GSB_SLOT_KEYS");
+  return !(e && e[0] == '0');
+}
+
 bool two_streams() {   // GSB_STREAMS=1: everything on the caller's stream (A/B comparisons)
   static const bool v = [] {
     const char* e = getenv("GSB_STREAMS");
@@ -368,6 +373,19 @@ struct Pipeline {
     uint32_t* sorted = (q && sb != sc) ? s->sorted2 : s->sorted;
     a.keys = s->keys; a.keys_alt = s->keys_alt; a.sorted = sorted;
     a.long_list = s->long_list[sl];
+    // the compositing path of this pass (decided before emission: the split path's small K4a
+    // variant takes keys that carry the record slot instead of the creation id)
+    uint64_t n_entries = n_keys;   // sorted entries of the pass (merge: + background lists)
+    if (merge)
+      for (int f = fs; f < fe; ++f) n_entries += (uint64_t)s->sb_K[(f0 + f) % s->sb_cams];
+    // many lists beyond the small fused-sort capacity (e.g. 128x128 views): larger variant
+    const bool long_lists = (uint64_t)n_long * 4 > (uint64_t)(fe - fs) * n_tiles;
+    // split K4a + K4b unless the lists are short on average (then the one-CTA-per-tile kernel's
+    // shared staging beats per-warp record reads; measured crossover ~200-330 keys per tile)
+    const bool split = split_k4() && n_entries >= split_min_avg() * (uint64_t)(fe - fs) * n_tiles &&
+                       n_entries <= (uint64_t)s->cap;
+    const bool slot_keys = split && !merge && !long_lists && slot_keys_on();
+    if (slot_keys) a.ids = nullptr;   // key low word = index in the launch range = record slot
     tm.begin(KC_EMIT, sb);
     launch_k2_emit(a, sb);
     if (count > 0) s->launches++;
@@ -380,13 +398,12 @@ struct Pipeline {
     c.key_base = key_base;
     c.inv = s->d_inv;
     c.slot_base = (int)first;
-    uint64_t n_entries = n_keys;   // sorted entries of the pass (merge: + background lists)
     if (merge) {
       c.bg_off = s->bg_off; c.bg_keys = s->bg_keys; c.bg_rec = s->bg_rec; c.n_static_cams = s->sb_cams;
       c.qpos_g = s->qpos;
       c.bg_cum = s->d_bgcum;
-      for (int f = fs; f < fe; ++f) n_entries += (uint64_t)s->sb_K[(f0 + f) % s->sb_cams];
     }
+    if (slot_keys) c.keys_internal_ids = s->d_ids + first;
     c.fs = fs; c.fe = fe; c.f0 = f0; c.width = W; c.height = H; c.tiles_x = tiles_x; c.n_tiles = n_tiles;
     c.bg0 = p->background[0]; c.bg1 = p->background[1]; c.bg2 = p->background[2];
     c.out_rgb = out_rgb; c.out_depth = out_depth; c.out_alpha = out_alpha; c.out_n_eval = out_neval;
@@ -400,12 +417,6 @@ struct Pipeline {
       c.obs_seed = s->obs->seed; c.obs_step = s->obs->step;
       c.obs_frame_offset = s->obs->env_offset * (int64_t)n_cams;
     }
-    // many lists beyond the small fused-sort capacity (e.g. 128x128 views): larger variant
-    const bool long_lists = (uint64_t)n_long * 4 > (uint64_t)(fe - fs) * n_tiles;
-    // split K4a + K4b unless the lists are short on average (then the one-CTA-per-tile kernel's
-    // shared staging beats per-warp record reads; measured crossover ~200-330 keys per tile)
-    const bool split = split_k4() && n_entries >= split_min_avg() * (uint64_t)(fe - fs) * n_tiles &&
-                       n_entries <= (uint64_t)s->cap;
     // `sorted` buffer q was last read by the K4b of pass pass_idx - 2
     if (sb != sc && pass_idx >= 2) CUDA_TRY(cudaStreamWaitEvent(sb, s->ev_k4b[q], 0));
     cudaStream_t cs = sb;   // stream of this pass's last compositing kernel

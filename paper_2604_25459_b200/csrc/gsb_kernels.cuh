@@ -101,6 +101,10 @@ struct CompositeArgs {
   const float* obs_dr;      // [F][4] (gain, contrast, brightness, noise_std) per frame, or nullptr
   uint32_t obs_seed, obs_step;
   int64_t obs_frame_offset; // global index of this call's frame 0 (noise streams)
+  // K4a: keys carry the record slot (internal index - slot_base) instead of the creation id
+  // (K2b with ids = nullptr); equal-depth runs are then re-ordered by the creation id ids[slot].x
+  // so the order is still (bits(z), id) of reading R10, and no id -> slot gather is needed
+  const int2* keys_internal_ids;   // template (id, body) of the launch's range, or nullptr
 };
 
 constexpr int kMaxRigCams = 16;  // cameras per env that can be body-attached (gsb_render_rig)
