@@ -305,10 +305,12 @@ __device__ __forceinline__ void radix_pass32(const uint32_t* src, uint32_t* dst,
   }
 }
 
-// n <= 65536.  Returns true if the sorted words ended in `b` (else `a`).
+// n <= 65536.  Returns true if the sorted words ended in `b` (else `a`).  With `ids` the keys'
+// low words are record slots and equal-field runs are finished by (bits(z), ids[slot].x) — the
+// (bits(z), id) order of reading R10 without a creation id in the key.
 template <int NT>
 __device__ __forceinline__ bool packed_sort(const uint64_t* __restrict__ gkeys, int n, uint32_t* a, uint32_t* b,
-                                            SortShared<NT>& sm) {
+                                            SortShared<NT>& sm, const int2* __restrict__ ids = nullptr) {
   constexpr int kWarps = SortShared<NT>::kWarps;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t zmin = 0xffffffffu;
@@ -346,9 +348,17 @@ __device__ __forceinline__ bool packed_sort(const uint64_t* __restrict__ gkeys, 
   uint32_t* r = in_b ? b : a;
   int dup = 0;
   for (int e = tid + 1; e < n; e += NT) dup |= (r[e] >> 16) == (r[e - 1] >> 16);
-  if (__syncthreads_or(dup))
-    fix_runs<NT>(r, n, [](uint32_t w) { return w >> 16; },
-                 [gkeys](uint32_t x, uint32_t y) { return __ldg(gkeys + (x & 0xffffu)) < __ldg(gkeys + (y & 0xffffu)); });
+  if (__syncthreads_or(dup)) {
+    if (ids)
+      fix_runs<NT>(r, n, [](uint32_t w) { return w >> 16; }, [gkeys, ids](uint32_t x, uint32_t y) {
+        const uint64_t kx = __ldg(gkeys + (x & 0xffffu)), ky = __ldg(gkeys + (y & 0xffffu));
+        const uint32_t zx = hi32(kx), zy = hi32(ky);
+        return zx != zy ? zx < zy : __ldg(&ids[(uint32_t)kx].x) < __ldg(&ids[(uint32_t)ky].x);
+      });
+    else
+      fix_runs<NT>(r, n, [](uint32_t w) { return w >> 16; },
+                   [gkeys](uint32_t x, uint32_t y) { return __ldg(gkeys + (x & 0xffffu)) < __ldg(gkeys + (y & 0xffffu)); });
+  }
   return in_b;
 }
 

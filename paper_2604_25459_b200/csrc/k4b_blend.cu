@@ -196,18 +196,25 @@ __global__ void __launch_bounds__(kSortThreadsA) k4a_sort(CompositeArgs a) {
     if (tid == 0) dst[0] = kid ? (uint32_t)a.keys[start] : (uint32_t)(__ldg(a.inv + (uint32_t)a.keys[start]) - base);
     return;
   }
-  if (kid && !Sh::kPacked) {   // keys carry the slot: sort, fix equal-depth runs, write slots
+  if (kid) {   // keys carry the slot: sort, restore the (z, id) order of equal depths, write slots
     if (len <= CAP) {
-      uint64_t* k0 = sm.u.keys[0];
-      for (int e = tid; e < len; e += kSortThreadsA) k0[e] = a.keys[start + e];
-      __syncthreads();
-      count_sort(k0, sm.u.keys[1], len, sm.s.count);
-      if (fix_equal_depth_runs(k0, len, kid)) {
-        for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)k0[e];
-      } else {   // long equal-depth runs: re-sort by (z, id) keys and gather the slots
-        slot_keys_to_id_keys(k0, len, kid);
+      if constexpr (Sh::kPacked) {
+        const uint64_t* gk = a.keys + start;
+        const bool in_b = packed_sort(gk, len, sm.u.buf[0], sm.u.buf[1], sm.s.sort, kid);
+        const uint32_t* res = sm.u.buf[in_b ? 1 : 0];
+        for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)__ldg(gk + (res[e] & 0xffffu));
+      } else {
+        uint64_t* k0 = sm.u.keys[0];
+        for (int e = tid; e < len; e += kSortThreadsA) k0[e] = a.keys[start + e];
+        __syncthreads();
         count_sort(k0, sm.u.keys[1], len, sm.s.count);
-        for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)k0[e]) - base);
+        if (fix_equal_depth_runs(k0, len, kid)) {
+          for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)k0[e];
+        } else {   // long equal-depth runs: re-sort by (z, id) keys and gather the slots
+          slot_keys_to_id_keys(k0, len, kid);
+          count_sort(k0, sm.u.keys[1], len, sm.s.count);
+          for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)k0[e]) - base);
+        }
       }
     } else {
       uint64_t* ga = const_cast<uint64_t*>(a.keys) + start;

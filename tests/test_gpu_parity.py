@@ -414,13 +414,16 @@ def test_split_and_fused_compositing_bit_identical(name, monkeypatch):
     assert outs["split"]["stats"] == outs["fused"]["stats"]
 
 
-@pytest.mark.parametrize("n,spread,layers", [(600, 0.25, 1), (400, 0.3, 40), (2500, 0.05, 1)])
-def test_equal_depth_ties_resolved_by_id(n, spread, layers, monkeypatch):
+@pytest.mark.parametrize("n,spread,layers,size", [(600, 0.25, 1, 128), (400, 0.3, 40, 128), (2500, 0.05, 1, 128),
+                                                  (3000, 0.3, 1, 32), (3000, 0.3, 25, 32)])
+def test_equal_depth_ties_resolved_by_id(n, spread, layers, size, monkeypatch):
     """Reading R10 on the split path whose keys carry record slots: Gaussians at exactly equal
     camera depth (identical fp32 keys) in tile lists, creation order shuffled against the internal
     (Morton) order.  One fronto-parallel plane (every key of a tile ties: the long-run fallback),
-    `layers` planes (short runs fixed in place), and > 1024 keys in one tile (the HBM sort).
-    Full frames against the oracle and bit-identical to keys carrying the creation id."""
+    `layers` planes (short runs fixed in place), > 1024 keys in one tile (the HBM sort), and a
+    32 x 32 image whose every tile holds > 1024 keys (the packed K4a variant, runs finished by
+    (z, id) through the slot).  Full frames against the oracle and bit-identical to keys
+    carrying the creation id."""
     rng = np.random.default_rng(n + layers)
     z = 2.0 + 0.05 * rng.integers(0, layers, n)
     means = np.stack([rng.uniform(-spread, spread, n), rng.uniform(-spread, spread, n), z], 1)
@@ -428,15 +431,16 @@ def test_equal_depth_ties_resolved_by_id(n, spread, layers, monkeypatch):
     q /= np.linalg.norm(q, axis=1, keepdims=True)
     sc = scene_from(means, np.exp(rng.uniform(np.log(0.01), np.log(0.04), (n, 3))), q, rng.uniform(0.05, 0.6, n),
                     rng.uniform(0, 1, (n, 3)))
-    K, W = identity_cam(fx=100.0, fy=100.0, cx=64.5, cy=48.5)
+    Wd, Hd = size, size * 3 // 4 if size > 32 else size
+    K, W = identity_cam(fx=100.0, fy=100.0, cx=Wd / 2 + 0.5, cy=Hd / 2 + 0.5)
     b = synth.Batch(np.zeros((1, 0, 7), np.float32), K[None, None].copy(), W[None, None].copy())
     monkeypatch.setenv("GSB_K4_SPLIT_MIN", "0")   # force the split (K4a + K4b) path
-    out = gu.gpu_render(sc, b, 128, 96, stats=True)
+    out = gu.gpu_render(sc, b, Wd, Hd, stats=True)
     monkeypatch.setenv("GSB_SLOT_KEYS", "0")
-    ref_ids = gu.gpu_render(sc, b, 128, 96)
+    ref_ids = gu.gpu_render(sc, b, Wd, Hd)
     for k in ("rgb", "depth", "alpha", "n_eval"):
         assert np.array_equal(out[k], ref_ids[k]), k
-    ref = oracle.render_frame(sc, b.poses[0], K, W, oracle.RenderParams(128, 96))
+    ref = oracle.render_frame(sc, b.poses[0], K, W, oracle.RenderParams(Wd, Hd))
     rgb = out["rgb"][0, 0].transpose(1, 2, 0)
     ok = ~ref.masked
     assert np.abs(rgb - ref.rgb).max(-1)[ok].max() <= oracle.TOL_RGB
