@@ -384,7 +384,7 @@ struct Pipeline {
     // shared staging beats per-warp record reads; measured crossover ~200-330 keys per tile)
     const bool split = split_k4() && n_entries >= split_min_avg() * (uint64_t)(fe - fs) * n_tiles &&
                        n_entries <= (uint64_t)s->cap;
-    const bool slot_keys = split && !merge && slot_keys_on();
+    const bool slot_keys = !merge && slot_keys_on();
     if (slot_keys) a.ids = nullptr;   // key low word = index in the launch range = record slot
     tm.begin(KC_EMIT, sb);
     launch_k2_emit(a, sb);

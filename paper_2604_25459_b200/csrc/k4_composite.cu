@@ -110,15 +110,21 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
   const bool fused = len <= CAP;
   const uint32_t* slots = nullptr;
   float4* stg = nullptr;
+  // keys carrying the record slot (K4a's scheme, gsb_sort.cuh): no id -> slot gather; equal
+  // depths re-sorted by creation id (or, for long runs, the list re-keyed by id and re-sorted)
+  const int2* kid = MERGE ? nullptr : a.keys_internal_ids;
+  bool kid_fallback = false;
   if constexpr (Sh::kPacked) {
     stg = reinterpret_cast<float4*>(sm.u.buf[0]);
     if (fused && len > 0) {
       const uint64_t* gk = a.keys + start;
-      const bool in_b = packed_sort(gk, len, sm.u.buf[0], sm.u.buf[1], sm.s.sort);
+      const bool in_b = packed_sort(gk, len, sm.u.buf[0], sm.u.buf[1], sm.s.sort, kid);
       const uint32_t* res = sm.u.buf[in_b ? 1 : 0];
       uint32_t* sl = sm.u.buf[in_b ? 0 : 1];
-      for (int e = tid; e < len; e += kCompThreads)
-        sl[e] = (uint32_t)(__ldg(a.inv + (uint32_t)__ldg(gk + (res[e] & 0xffffu))) - a.slot_base);
+      for (int e = tid; e < len; e += kCompThreads) {
+        const uint64_t key = __ldg(gk + (res[e] & 0xffffu));
+        sl[e] = kid ? (uint32_t)key : (uint32_t)(__ldg(a.inv + (uint32_t)key) - a.slot_base);
+      }
       slots = sl;
       stg = reinterpret_cast<float4*>(sm.u.buf[in_b ? 1 : 0]);
     }
@@ -133,14 +139,20 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
         in_b = len > 1 && segment_sort(sm.u.keys[0], sm.u.keys[1], len, sm.s.sort);
       } else if (len > 1) {
         count_sort(sm.u.keys[0], sm.u.keys[1], len, sm.s.count);   // result in keys[0]
+        if (kid && !fix_equal_depth_runs<kCompThreads>(sm.u.keys[0], len, kid)) {
+          slot_keys_to_id_keys<kCompThreads>(sm.u.keys[0], len, kid);
+          count_sort(sm.u.keys[0], sm.u.keys[1], len, sm.s.count);
+          kid_fallback = true;
+        }
       }
+      const bool direct = kid && !kid_fallback;   // key low word = slot
       uint32_t sl[CAP / kCompThreads];
 #pragma unroll
       for (int k = 0; k < CAP / kCompThreads; ++k) {
         const int e = tid + k * kCompThreads;
         if (e < len) {
           const uint64_t key = sm.u.keys[in_b ? 1 : 0][e];
-          sl[k] = (uint32_t)(__ldg(a.inv + (uint32_t)key) - a.slot_base);
+          sl[k] = direct ? (uint32_t)key : (uint32_t)(__ldg(a.inv + (uint32_t)key) - a.slot_base);
           if constexpr (MERGE) sm.qpos[e] = (uint32_t)(e + lower_bound(bkeys, lb, key));
         }
       }
@@ -158,8 +170,20 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
     uint64_t* gb = a.keys_alt + start;
     const bool in_b = segment_sort(ga, gb, len, sm.s.sort);
     uint32_t* dst = a.sorted + start;
-    const uint64_t* r = in_b ? gb : ga;
-    for (int e = tid; e < len; e += kCompThreads) dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)r[e]) - a.slot_base);
+    uint64_t* r = in_b ? gb : ga;
+    bool direct = false;
+    if (kid) {
+      __syncthreads();
+      direct = fix_equal_depth_runs<kCompThreads>(r, len, kid);
+      if (!direct) {
+        uint64_t* o = in_b ? ga : gb;
+        slot_keys_to_id_keys<kCompThreads>(r, len, kid);
+        if (segment_sort(r, o, len, sm.s.sort)) r = o;
+        __syncthreads();
+      }
+    }
+    for (int e = tid; e < len; e += kCompThreads)
+      dst[e] = direct ? (uint32_t)r[e] : (uint32_t)(__ldg(a.inv + (uint32_t)r[e]) - a.slot_base);
     slots = dst;
     if constexpr (MERGE) {
       uint32_t* qg = a.qpos_g + start;

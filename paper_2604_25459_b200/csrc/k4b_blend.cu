@@ -77,62 +77,6 @@ __device__ __forceinline__ TileList tile_list(const CompositeArgs& a, int fl, in
 
 constexpr uint32_t kBgTag = 0x80000000u;   // merged entry: background record index | tag
 
-// Keys (bits(z) << 32 | slot) sorted by the full key are in (z, slot) order; reading R10 wants
-// (z, creation id).  Runs of equal z (rare) are re-sorted by ids[slot].x: run starts are found
-// read-only first (up to kRunSlots per thread), then each run is insertion-sorted by its starting
-// thread after a barrier.  Returns false — nothing changed — when a run is longer than
-// kShortRun or a thread found too many runs (e.g. a fronto-parallel plane: every key ties); the
-// caller then re-sorts the list by (z, id) keys.
-constexpr int kRunSlots = 4;
-constexpr int kShortRun = 32;
-
-template <typename P>
-__device__ __forceinline__ bool fix_equal_depth_runs(P r, int n, const int2* __restrict__ ids) {
-  const int tid = threadIdx.x;
-  int starts[kRunSlots];
-  int ns = 0;
-  bool bad = false;
-  for (int e = tid; e + 1 < n; e += kSortThreadsA) {
-    const uint32_t z = hi32(r[e]);
-    if (hi32(r[e + 1]) == z && (e == 0 || hi32(r[e - 1]) != z)) {
-      int s1 = e + 2;
-      while (s1 < n && s1 - e <= kShortRun && hi32(r[s1]) == z) ++s1;
-      if (s1 - e > kShortRun || ns == kRunSlots) bad = true;
-      else starts[ns++] = e;
-    }
-  }
-  if (__syncthreads_or(bad)) return false;
-  if (!__syncthreads_or(ns > 0)) return true;
-  for (int k = 0; k < ns; ++k) {
-    const int s0 = starts[k];
-    const uint32_t z = hi32(r[s0]);
-    int s1 = s0 + 1;
-    while (s1 < n && hi32(r[s1]) == z) ++s1;
-    for (int i = s0 + 1; i < s1; ++i) {   // insertion sort by creation id (runs are short)
-      const uint64_t key = r[i];
-      const int id = __ldg(&ids[(uint32_t)key].x);
-      int j = i - 1;
-      while (j >= s0 && __ldg(&ids[(uint32_t)r[j]].x) > id) {
-        r[j + 1] = r[j];
-        --j;
-      }
-      r[j + 1] = key;
-    }
-  }
-  __syncthreads();
-  return true;
-}
-
-// the fallback: key low words slot -> creation id (the high word, bits(z), is kept)
-template <typename P>
-__device__ __forceinline__ void slot_keys_to_id_keys(P r, int n, const int2* __restrict__ ids) {
-  for (int e = threadIdx.x; e < n; e += kSortThreadsA) {
-    const uint64_t k = r[e];
-    r[e] = (k & 0xffffffff00000000ull) | (uint32_t)__ldg(&ids[(uint32_t)k].x);
-  }
-  __syncthreads();
-}
-
 template <int CAP>
 __global__ void __launch_bounds__(kSortThreadsA) k4a_sort(CompositeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -208,10 +152,10 @@ __global__ void __launch_bounds__(kSortThreadsA) k4a_sort(CompositeArgs a) {
         for (int e = tid; e < len; e += kSortThreadsA) k0[e] = a.keys[start + e];
         __syncthreads();
         count_sort(k0, sm.u.keys[1], len, sm.s.count);
-        if (fix_equal_depth_runs(k0, len, kid)) {
+        if (fix_equal_depth_runs<kSortThreadsA>(k0, len, kid)) {
           for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)k0[e];
         } else {   // long equal-depth runs: re-sort by (z, id) keys and gather the slots
-          slot_keys_to_id_keys(k0, len, kid);
+          slot_keys_to_id_keys<kSortThreadsA>(k0, len, kid);
           count_sort(k0, sm.u.keys[1], len, sm.s.count);
           for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)k0[e]) - base);
         }
@@ -222,11 +166,11 @@ __global__ void __launch_bounds__(kSortThreadsA) k4a_sort(CompositeArgs a) {
       const bool in_b = segment_sort(ga, gb, len, sm.s.sort);
       __syncthreads();
       uint64_t* r = in_b ? gb : ga;
-      if (fix_equal_depth_runs(r, len, kid)) {
+      if (fix_equal_depth_runs<kSortThreadsA>(r, len, kid)) {
         for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)r[e];
       } else {
         uint64_t* o = in_b ? ga : gb;
-        slot_keys_to_id_keys(r, len, kid);
+        slot_keys_to_id_keys<kSortThreadsA>(r, len, kid);
         const bool in_o = segment_sort(r, o, len, sm.s.sort);
         __syncthreads();
         const uint64_t* rr = in_o ? o : r;

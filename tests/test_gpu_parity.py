@@ -416,8 +416,9 @@ def test_split_and_fused_compositing_bit_identical(name, monkeypatch):
 
 @pytest.mark.parametrize("n,spread,layers,size", [(600, 0.25, 1, 128), (400, 0.3, 40, 128), (2500, 0.05, 1, 128),
                                                   (3000, 0.3, 1, 32), (3000, 0.3, 25, 32)])
-def test_equal_depth_ties_resolved_by_id(n, spread, layers, size, monkeypatch):
-    """Reading R10 on the split path whose keys carry record slots: Gaussians at exactly equal
+@pytest.mark.parametrize("path", ["split", "fused"])
+def test_equal_depth_ties_resolved_by_id(n, spread, layers, size, path, monkeypatch):
+    """Reading R10 with keys that carry record slots (split and fused paths): Gaussians at exactly equal
     camera depth (identical fp32 keys) in tile lists, creation order shuffled against the internal
     (Morton) order.  One fronto-parallel plane (every key of a tile ties: the long-run fallback),
     `layers` planes (short runs fixed in place), > 1024 keys in one tile (the HBM sort), and a
@@ -434,7 +435,8 @@ def test_equal_depth_ties_resolved_by_id(n, spread, layers, size, monkeypatch):
     Wd, Hd = size, size * 3 // 4 if size > 32 else size
     K, W = identity_cam(fx=100.0, fy=100.0, cx=Wd / 2 + 0.5, cy=Hd / 2 + 0.5)
     b = synth.Batch(np.zeros((1, 0, 7), np.float32), K[None, None].copy(), W[None, None].copy())
-    monkeypatch.setenv("GSB_K4_SPLIT_MIN", "0")   # force the split (K4a + K4b) path
+    # force the split (K4a + K4b) or the fused (one CTA per tile) compositing path
+    monkeypatch.setenv("GSB_K4_SPLIT_MIN", "0" if path == "split" else "1000000000")
     out = gu.gpu_render(sc, b, Wd, Hd, stats=True)
     monkeypatch.setenv("GSB_SLOT_KEYS", "0")
     ref_ids = gu.gpu_render(sc, b, Wd, Hd)
