@@ -1656,7 +1656,9 @@ gsb_status gsb_render_lidar(gsb_scene s, gsb_lidar l, const float* poses, int32_
     }
     if (K > 0) {
       ChunkArgs c{};
-      c.rec = nullptr; c.emit = l->emit; c.ids = l->ids2; c.n = 2 * l->np;
+      // keys carry the (virtual) index: the seam copy np + i of Gaussian i keeps its own key, K4a
+      // restores the (bits(rho), id) order of equal ranges through ids2 and KL4 folds np + i to i
+      c.rec = nullptr; c.emit = l->emit; c.ids = nullptr; c.n = 2 * l->np;
       c.vis_bits = l->vis_bits; c.vis_words = 2 * l->np / 32; c.hist = l->hist; c.hist_stride = l->hist_stride;
       c.off = l->off; c.frame_base = l->frame_base; c.n_tiles = n_cells; c.tiles_x = l->n_az;
       c.fs = 0; c.fe = ne; c.key_base = 0; c.long_list = nullptr;
@@ -1666,10 +1668,11 @@ gsb_status gsb_render_lidar(gsb_scene s, gsb_lidar l, const float* poses, int32_
       k.keys = l->keys; k.keys_alt = l->keys_alt; k.off = l->off; k.frame_base = l->frame_base;
       k.hist_stride = l->hist_stride; k.key_base = 0; k.fs = 0; k.fe = ne; k.f0 = f0;
       k.n_tiles = n_cells; k.tiles_x = l->n_az; k.inv = s->d_inv; k.slot_base = 0; k.sorted = l->sorted;
+      k.keys_internal_ids = l->ids2;
       launch_k4a_sort(k, false, st);
       LidarL4Args b{};
       b.rec = l->rec; b.n = N; b.off = l->off; b.frame_base = l->frame_base; b.hist_stride = l->hist_stride;
-      b.sorted = l->sorted; b.rays = l->d_rays; b.items = l->d_items;
+      b.sorted = l->sorted; b.rays = l->d_rays; b.items = l->d_items; b.np = l->np;
       b.n_items = l->n_items; b.f0 = f0; b.n_frames = ne; b.n_rays = l->n_rays;
       b.out_range = out_range; b.out_alpha = out_alpha;
       launch_kl4(b, st);

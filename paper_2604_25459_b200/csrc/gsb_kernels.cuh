@@ -151,8 +151,9 @@ struct LidarL4Args {
   const uint32_t* off;          // [E][hist_stride] cell offsets within the frame
   const uint64_t* frame_base;   // [E+1]
   int64_t hist_stride;
-  const uint32_t* sorted;       // record slots (internal indices) of every (frame, cell) list in
-                                // (bits(rho), id) order (K4a)
+  const uint32_t* sorted;       // record slots of every (frame, cell) list in (bits(rho), id) order
+                                // (K4a): internal index i, or np + i for a seam copy
+  int64_t np;
   const float4* rays;           // [R] (dx, dy, dz, bits(original ray index)), grouped by cell
   const int4* items;            // (cell, first ray, ray count <= 32, 0)
   int n_items, f0, n_frames, n_rays;

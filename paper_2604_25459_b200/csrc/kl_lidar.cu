@@ -219,7 +219,9 @@ __global__ void __launch_bounds__(32 * kL4Warps) kl4_cast(LidarL4Args a) {
   auto prefetch = [&](int base) {
     const int j = base + lane;
     if (j < n) {
-      const float4* r = rec + (size_t)__ldg(a.sorted + start + j) * kLidarRecQuads;   // slot = internal index
+      uint32_t slot = __ldg(a.sorted + start + j);
+      if (slot >= (uint32_t)a.np) slot -= (uint32_t)a.np;   // seam copy -> its Gaussian
+      const float4* r = rec + (size_t)slot * kLidarRecQuads;
 #pragma unroll
       for (int q = 0; q < kLidarRecQuads; ++q) pf[q] = __ldg(r + q);
     } else {
