@@ -284,12 +284,11 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
           const float arg1 = fmaf(-tb, tb, mm);
           const bool use0 = arg0 >= kLog2AlphaMin;   // alpha >= 1/255
           const bool use1 = arg1 >= kLog2AlphaMin;
-          float wb0 = 0.f, wb1 = 0.f;
-          if (use0 || use1) {
-            const float4 q2 = R2[j];                                 // r, g, b, z
-            wb0 = blend(use0, arg0, q2, T0, r0c, g0c, b0c, d0, pyc0, ne0, base + j);
-            wb1 = blend(use1, arg1, q2, T1, r1c, g1c, b1c, d1, pyc1, ne1, base + j);
-          }
+          // unconditional two-pixel blend (as K4b): for an unused entry it is an exact no-op
+          const float4 q2 = R2[j];                                 // r, g, b, z
+          const float2 wb = blend2(use0, arg0, use1, arg1, q2, T0, r0c, g0c, b0c, d0, pyc0, ne0, T1, r1c, g1c,
+                                   b1c, d1, pyc1, ne1, base + j);
+          const float wb0 = wb.x, wb1 = wb.y;
           if constexpr (SCORE) {
             // warp sum in 6.26 fixed point (|error| <= 2^-27 per pixel weight; 64 pixels x 0.99
             // < 2^6) and exact max of the float bits (w >= 0): two REDUX instructions
