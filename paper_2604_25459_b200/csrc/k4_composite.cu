@@ -267,8 +267,8 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
         nsel += __popc(hit);
       }
       __syncwarp();
-      for (int i0 = 0; i0 < nsel; i0 += 16) {
-        const int i1 = min(nsel, i0 + 16);
+      for (int i0 = 0; i0 < nsel; i0 += 32) {
+        const int i1 = min(nsel, i0 + 32);
 #pragma unroll 2
         for (int i = i0; i < i1; ++i) {
           const uint32_t j = wl[i];

@@ -307,8 +307,8 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
       if (ov) wl[__popc(hit & lanemask_lt())] = (uint8_t)lane;
       __syncwarp();
       const int nsel = __popc(hit);
-      for (int i0 = 0; i0 < nsel; i0 += 16) {
-        const int i1 = min(nsel, i0 + 16);
+      for (int i0 = 0; i0 < nsel; i0 += 32) {
+        const int i1 = min(nsel, i0 + 32);
 #pragma unroll 2
         for (int i = i0; i < i1; ++i) {
         const int j = wl[i];
