@@ -374,7 +374,7 @@ constexpr int kShortRun = 32;
 template <int NT, typename P>
 __device__ __forceinline__ bool fix_equal_depth_runs(P r, int n, const int2* __restrict__ ids) {
   const int tid = threadIdx.x;
-  int starts[kRunSlots];
+  int starts[kRunSlots], ends[kRunSlots];   // runs [start, end) found in the read-only pass
   int ns = 0;
   bool bad = false;
   for (int e = tid; e + 1 < n; e += NT) {
@@ -382,17 +382,18 @@ __device__ __forceinline__ bool fix_equal_depth_runs(P r, int n, const int2* __r
     if (hi32(r[e + 1]) == z && (e == 0 || hi32(r[e - 1]) != z)) {
       int s1 = e + 2;
       while (s1 < n && s1 - e <= kShortRun && hi32(r[s1]) == z) ++s1;
-      if (s1 - e > kShortRun || ns == kRunSlots) bad = true;
-      else starts[ns++] = e;
+      if (s1 - e > kShortRun || ns == kRunSlots) {
+        bad = true;
+      } else {
+        starts[ns] = e;
+        ends[ns++] = s1;
+      }
     }
   }
   if (__syncthreads_or(bad)) return false;
   if (!__syncthreads_or(ns > 0)) return true;
-  for (int k = 0; k < ns; ++k) {
-    const int s0 = starts[k];
-    const uint32_t z = hi32(r[s0]);
-    int s1 = s0 + 1;
-    while (s1 < n && hi32(r[s1]) == z) ++s1;
+  for (int k = 0; k < ns; ++k) {   // each run is touched by its finder only
+    const int s0 = starts[k], s1 = ends[k];
     for (int i = s0 + 1; i < s1; ++i) {   // insertion sort by creation id (runs are short)
       const uint64_t key = r[i];
       const int id = __ldg(&ids[(uint32_t)key].x);

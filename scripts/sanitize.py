@@ -60,3 +60,29 @@ g.render_static(torch.from_numpy(synth.make_poses(cfg, np.arange(B), 1)).cuda(),
                 gsb.RenderParams(cfg.width, cfg.height, static_per_env=True), rgb)
 torch.cuda.synchronize()
 print("static per-env ok", float(rgb.mean()))
+
+# keys carrying record slots with equal-depth runs (in-place run sort and the re-keyed fallback),
+# on the split (K4a) and the fused (K4) path, incl. > 1024 tied keys in a tile (HBM sort)
+import os  # noqa: E402
+sys.path.insert(0, "tests")
+from helpers import identity_cam, scene_from  # noqa: E402
+for n, spread, layers, size in ((600, 0.25, 1, 128), (400, 0.3, 40, 128), (2500, 0.05, 1, 128), (3000, 0.3, 25, 32)):
+    rng = np.random.default_rng(n + layers)
+    z = 2.0 + 0.05 * rng.integers(0, layers, n)
+    means = np.stack([rng.uniform(-spread, spread, n), rng.uniform(-spread, spread, n), z], 1)
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    sc = scene_from(means, np.exp(rng.uniform(np.log(0.01), np.log(0.04), (n, 3))), q, rng.uniform(0.05, 0.6, n),
+                    rng.uniform(0, 1, (n, 3)))
+    Wd, Hd = size, (size * 3 // 4 if size > 32 else size)
+    K, W = identity_cam(fx=100.0, fy=100.0, cx=Wd / 2 + 0.5, cy=Hd / 2 + 0.5)
+    g = gsb.Scene.from_synth(sc)
+    g.reserve(1, 1, Wd, Hd)
+    for split_min in ("0", "1000000000"):
+        os.environ["GSB_K4_SPLIT_MIN"] = split_min
+        rgb = torch.zeros((1, 1, 3, Hd, Wd), device="cuda")
+        g.render(None, torch.from_numpy(K[None, None].copy()).cuda(), torch.from_numpy(W[None, None].copy()).cuda(),
+                 gsb.RenderParams(Wd, Hd), rgb)
+        torch.cuda.synchronize()
+    os.environ.pop("GSB_K4_SPLIT_MIN")
+    print("ties ok", n, layers, float(rgb.mean()))
