@@ -321,7 +321,9 @@ const char* gsb_version(void);
 /* ------------------------------------------------------------------ test-only entry points */
 
 /* K1 projection only, dense per (frame, Gaussian) (DEVICE pointers, same inputs as gsb_render):
- *   out_rec   [F, N, 12] fp32: u, v, conic a, b, c, opacity, r, g, b, z, Sigma2D_xx, Sigma2D_yy
+ *   out_rec   [F, N, 16] fp32: u, v, conic a, b, c, opacity, r, g, b, z, Sigma2D_xx, Sigma2D_yy,
+ *             then the values K4 composites with: the whitening factor (p, q, r) of Sigma2D^-1
+ *             scaled by sqrt(log2(e)/2) (arg = log2 o - (p dx)^2 - (q dx + r dy)^2) and log2 o
  *   out_zbits [F, N] uint32  bits of the fp32 depth key (reading R11)
  *   out_valid [F, N] uint8   near < z <= far and o >= 1/255 (R4, R5)
  * Requires the same reservation as gsb_render for B*C frames. */
@@ -341,6 +343,30 @@ gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, 
                               int32_t n_frames, int64_t n_gaussians, int32_t width, int32_t height,
                               int64_t* out_tile_offsets, uint32_t* out_ids, int64_t cap,
                               int64_t* out_K, gsb_stream stream);
+
+/* The PRODUCTION binning and tile sort — K2b emission and the sort that feeds compositing in
+ * gsb_render (K4a of the split path, or the fused K4's in-CTA sort) — on external projections
+ * (the ORACLE's values rounded to fp32), so the integer path the render really runs is
+ * compared list for list with the binning oracle (readings R9, R10).
+ *   u .. valid   [F, N] DEVICE arrays indexed by record SLOT j (the internal order)
+ *   slot_ids     [N] DEVICE int32: creation id of slot j (a permutation of [0, N)); keys break
+ *                depth ties by this id, so a non-identity permutation exercises the slot-key
+ *                path's re-ordering of equal-depth runs
+ *   variant      0 = what gsb_render picks for this batch (split if >= 200 keys per tile on
+ *                average, packed sort if > 1/4 of the lists exceed 1024 keys), 1 = K4a with the
+ *                counting sort (<= 1024 keys in smem, HBM radix beyond), 2 = K4a packed (<= 4096,
+ *                HBM beyond), 3 = fused K4 small, 4 = fused K4 packed
+ *   key_mode     0 = keys carry the record slot (gsb_render's default), 1 = keys carry the id
+ *   out_tile_offsets [F, T_t + 1] DEVICE int64 (absolute positions in out_ids),
+ *   out_ids      [cap] DEVICE uint32: creation ids of every (frame, tile) list in sorted order
+ *   out_K, out_variant (HOST): total keys and the variant that ran (1..4).
+ * Allocates its own scratch and synchronises (test-only).  CAPACITY if K > cap. */
+gsb_status gsb_debug_tile_lists(const float* u, const float* v, const float* sxx, const float* syy,
+                                const float* kappa, const uint32_t* zbits, const uint8_t* valid,
+                                const int32_t* slot_ids, int32_t n_frames, int64_t n_gaussians,
+                                int32_t width, int32_t height, int32_t variant, int32_t key_mode,
+                                int64_t* out_tile_offsets, uint32_t* out_ids, int64_t cap,
+                                int64_t* out_K, int32_t* out_variant, gsb_stream stream);
 
 #ifdef __cplusplus
 }

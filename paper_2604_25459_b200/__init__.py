@@ -33,7 +33,7 @@ EXPORTS = ["gsb_create_scene", "gsb_reserve", "gsb_render", "gsb_render_rig", "g
            "gsb_prebin_static", "gsb_render_static",
            "gsb_scores_reset", "gsb_get_scores", "gsb_filter_scene", "gsb_render_obs", "gsb_render_obs_host", "gsb_get_stats",
            "gsb_get_timings", "gsb_destroy_scene", "gsb_last_error", "gsb_version",
-           "gsb_debug_project", "gsb_debug_bin_sort",
+           "gsb_debug_project", "gsb_debug_bin_sort", "gsb_debug_tile_lists",
            "gsb_obs_encode", "gsb_lidar_create", "gsb_render_lidar", "gsb_lidar_info", "gsb_lidar_destroy"]
 
 
@@ -97,6 +97,8 @@ def lib() -> ctypes.CDLL:
     L.gsb_debug_project.argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P]
     L.gsb_debug_bin_sort.argtypes = [P, P, P, P, P, P, P, I32, I64, I32, I32, P, P, I64,
                                      ctypes.POINTER(I64), P]
+    L.gsb_debug_tile_lists.argtypes = [P, P, P, P, P, P, P, P, I32, I64, I32, I32, I32, I32, P, P, I64,
+                                       ctypes.POINTER(I64), ctypes.POINTER(I32), P]
     L.gsb_obs_encode.argtypes = [P, P, I32, I32, I32, I32, op, P, P, P, P]
     L.gsb_lidar_create.argtypes = [P, P, I32, I32, I32, ctypes.POINTER(P)]
     L.gsb_render_lidar.argtypes = [P, P, P, I32, I32, P, I32, P, ctypes.c_float, ctypes.c_float, P, P, P]
@@ -426,6 +428,24 @@ def debug_bin_sort(u, v, sxx, syy, kappa, zbits, valid, width: int, height: int,
     _check(lib().gsb_debug_bin_sort(_ptr(u), _ptr(v), _ptr(sxx), _ptr(syy), _ptr(kappa), _ptr(zbits), _ptr(valid),
                                     F, N, width, height, _ptr(offs), _ptr(ids), cap, ctypes.byref(K), _stream(stream)))
     return offs, ids[:K.value]
+
+
+def debug_tile_lists(u, v, sxx, syy, kappa, zbits, valid, slot_ids, width: int, height: int, cap: int,
+                     variant: int = 0, key_mode: int = 0, stream=None):
+    """gsb_debug_tile_lists on CUDA tensors [F,N] indexed by record slot (slot_ids [N] int32: creation
+    id of each slot).  Returns (offsets [F,T+1] int64, ids[:K] (int32 view of uint32), variant run)."""
+    import torch
+    F, N = int(u.shape[0]), int(u.shape[1])
+    T = ((width + 15) // 16) * ((height + 15) // 16)
+    dev = u.device
+    offs = torch.empty((F, T + 1), dtype=torch.int64, device=dev)
+    ids = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    K = ctypes.c_int64()
+    var = ctypes.c_int32()
+    _check(lib().gsb_debug_tile_lists(_ptr(u), _ptr(v), _ptr(sxx), _ptr(syy), _ptr(kappa), _ptr(zbits), _ptr(valid),
+                                      _ptr(slot_ids), F, N, width, height, int(variant), int(key_mode), _ptr(offs),
+                                      _ptr(ids), cap, ctypes.byref(K), ctypes.byref(var), _stream(stream)))
+    return offs, ids[:K.value], var.value
 
 
 def version() -> str:

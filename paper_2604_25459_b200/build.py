@@ -34,11 +34,25 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Each translation unit compiled separately (in parallel) into build/*.o, then linked."""
     if not force and up_to_date():
         return OUT
-    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", OUT, *sources(), *LINK]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, "-c", "-o", obj, src]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd), file=sys.stderr)
+        subprocess.check_call(cmd)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(sources()), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(compile_one, sources()))
+    cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, *LINK]
     print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
     return OUT

@@ -10,6 +10,8 @@ namespace gsb {
 constexpr int kFusedSortCap = 1024;  // tile lists up to this length are sorted in K4 smem (8 CTAs/SM);
                                      // chunks with many longer lists use a 4x variant
 
+constexpr int kDbgRecFloats = 16;   // gsb_debug_project record (include/gsb.h)
+
 struct K1Args {
   // template (K5: shared read-only buffer, one copy for every env)
   const float4* g_mean;
@@ -105,6 +107,9 @@ struct CompositeArgs {
   // (K2b with ids = nullptr); equal-depth runs are then re-ordered by the creation id ids[slot].x
   // so the order is still (bits(z), id) of reading R10, and no id -> slot gather is needed
   const int2* keys_internal_ids;   // template (id, body) of the launch's range, or nullptr
+  // gsb_debug_tile_lists only: the fused K4 writes each tile's sorted slot list here (at the
+  // list's key offset) and returns before compositing; nullptr in every render
+  uint32_t* dbg_lists;
 };
 
 constexpr int kMaxRigCams = 16;  // cameras per env that can be body-attached (gsb_render_rig)

@@ -258,11 +258,12 @@ __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
         }
         if (debug && in) {
           const size_t o = (size_t)f * a.n + id;
-          float* d = a.dbg_rec + o * 12;
+          float* d = a.dbg_rec + o * kDbgRecFloats;
           const float idet = 1.0f / det;
           d[0] = u; d[1] = v; d[2] = syy * idet; d[3] = -sxy * idet; d[4] = sxx * idet;
           d[5] = opac; d[6] = rgb.x; d[7] = rgb.y; d[8] = rgb.z; d[9] = z; d[10] = sxx; d[11] = syy;
           if (offscreen && rect_ok) d[11] = __int_as_float(0x7fc0dead);  // bound violated: flag loudly
+          d[12] = pw; d[13] = qw; d[14] = rw; d[15] = log2o;   // what K4 composites with
         }
       }
     }

@@ -196,6 +196,10 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
     sm.smax[0][tid] = 0u; sm.smax[1][tid] = 0u;
   }
   __syncthreads();  // the slot list is complete (and the sort buffers are free)
+  if (a.dbg_lists) {   // gsb_debug_tile_lists: export the sorted list, no compositing
+    for (int e = tid; e < len; e += kCompThreads) a.dbg_lists[start + e] = slots[e];
+    return;
+  }
 
   // stage round b's records into buffer (b & 1): one record (3 x 16 B cp.async) per thread
   const int total = len + lb;   // merged list length (lb = 0 unless MERGE)

@@ -446,6 +446,33 @@ def env_slice(n_envs: int, rank: int, world: int) -> Tuple[int, int]:
     return lo, hi
 
 
+def sample_pixels(width: int, height: int, seed: int, grid: int = 64, full_tiles: int = 2):
+    """Pixel sample of one frame for the full-size parity checks and the oracle timing
+    (SURVEY §8(d) d.6): one uniformly drawn pixel in each cell of a grid x grid partition of
+    the image (4096 stratified pixels at grid = 64), plus every pixel of `full_tiles` distinct
+    16x16 tiles drawn uniformly (ragged edge tiles included).  Returns (px, py, n_strat) int64;
+    the first n_strat entries are the stratified ones."""
+    rng = np.random.default_rng(seed)
+    gx = min(grid, width)
+    gy = min(grid, height)
+    cx, cy = np.meshgrid(np.arange(gx), np.arange(gy))
+    cx, cy = cx.reshape(-1), cy.reshape(-1)
+    x0, x1 = (cx * width) // gx, ((cx + 1) * width) // gx
+    y0, y1 = (cy * height) // gy, ((cy + 1) * height) // gy
+    px = x0 + (rng.random(cx.size) * (x1 - x0)).astype(np.int64)
+    py = y0 + (rng.random(cy.size) * (y1 - y0)).astype(np.int64)
+    tw, th = (width + 15) // 16, (height + 15) // 16
+    tiles = rng.choice(tw * th, size=min(full_tiles, tw * th), replace=False)
+    tx, ty = [px], [py]
+    for t in tiles:
+        x_lo, y_lo = (t % tw) * 16, (t // tw) * 16
+        yy, xx = np.meshgrid(np.arange(y_lo, min(y_lo + 16, height)), np.arange(x_lo, min(x_lo + 16, width)),
+                             indexing="ij")
+        tx.append(xx.reshape(-1))
+        ty.append(yy.reshape(-1))
+    return np.concatenate(tx).astype(np.int64), np.concatenate(ty).astype(np.int64), int(px.size)
+
+
 # --------------------------------------------------------------------------------------
 # LiDAR inputs (§8(f) row 4, reading R32; tab:lidar P:320-329): ray patterns in the sensor
 # frame (x forward, y left, z up) and sensor extrinsics.  Inputs only: no method arithmetic.

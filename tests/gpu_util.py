@@ -42,7 +42,7 @@ def gpu_render(scene: synth.Scene, batch: synth.Batch, W: int, H: int, bg=(0.0, 
 def gpu_project(g: gsb.Scene, batch: synth.Batch, W: int, H: int, sh_degree=-1):
     B, C = batch.intrinsics.shape[:2]
     N = g.n
-    rec = torch.zeros((B * C, N, 12), device="cuda")
+    rec = torch.zeros((B * C, N, 16), device="cuda")
     zb = torch.zeros((B * C, N), dtype=torch.int32, device="cuda")
     va = torch.zeros((B * C, N), dtype=torch.uint8, device="cuda")
     g.debug_project(to_dev(batch.poses), to_dev(batch.intrinsics), to_dev(batch.w2c),

@@ -161,33 +161,40 @@ def test_render_oversize_tile_list_matches_oracle():
                          kap=gu.kappa_f32(sc))
     print(r)
     assert gout["n_eval"].max() > 0
-    assert gout["stats"] if False else True
     assert r["rgb_fail"] == 0 and r["dep_fail"] == 0 and r["n_eval_fail"] == 0, r
 
 
+def _check_sampled(name, gout_frame, sc, b, e, W, H, g, kap, seed):
+    """SURVEY d.6 sample of frame (e, camera 0): 4096 stratified pixels + 2 full tiles, element by
+    element against the oracle; n_eval located in the GPU's own tile list."""
+    px, py, _ = synth.sample_pixels(W, H, seed=seed)
+    ref = _oracle_frame(sc, b, e, 0, W, H, pixels=(px, py))
+    sub = synth.Batch(b.poses[e:e + 1], b.intrinsics[e:e + 1], b.w2c[e:e + 1])
+    rec, zb, va = gu.gpu_project(g, sub, W, H)
+    r = gu.compare_frame(gout_frame, 0, 0, ref, W, H, pix=(px, py), gpu_rec=rec[0], gpu_zb=zb[0], gpu_valid=va[0],
+                         kap=kap)
+    print(name, e, r)
+    assert r["n_pix"] == px.size
+    assert r["rgb_fail"] == 0 and r["dep_fail"] == 0 and r["alp_fail"] == 0, r
+    assert r["n_eval_fail"] == 0, r
+    assert r["masked_frac"] <= MASK_CAP, r
+    return r
+
+
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["C3", "C4", "C6", "C7"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C6", "C7"])
 def test_render_full_size_sampled_pixels(name):
     """BASELINE configs at full size, in the bench's launch configuration (all envs in one call;
-    C3 is the headline, C4 the 128x128 two-camera case, C6/C7 the 224x224 and 1280x720 §8(f)
-    row-4 workloads): sampled pixels of frames {0, B/2, B-1} against the oracle."""
+    C2 the 64-env robot scene, C3 the headline, C4 the 128x128 two-camera case, C6/C7 the
+    224x224 and 1280x720 §8(f) row-4 workloads): frames {0, B/2, B-1}, each on the d.6 sample
+    (4096 stratified pixels + 2 full tiles), against the oracle."""
     cfg = synth.CONFIGS[name]
     sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
     gout = gu.gpu_render(sc, b, cfg.width, cfg.height, stats=True)
     kap = gu.kappa_f32(sc)
-    rng = np.random.default_rng(33)
-    for e in (0, cfg.n_envs // 2, cfg.n_envs - 1):
-        px = rng.integers(0, cfg.width, 384)
-        py = rng.integers(0, cfg.height, 384)
-        ref = _oracle_frame(sc, b, e, 0, cfg.width, cfg.height, pixels=(px, py))
-        sub = synth.Batch(b.poses[e:e + 1], b.intrinsics[e:e + 1], b.w2c[e:e + 1])
-        rec, zb, va = gu.gpu_project(gout["scene"], sub, cfg.width, cfg.height)
-        r = gu.compare_frame(gout, e, 0, ref, cfg.width, cfg.height, pix=(px, py), gpu_rec=rec[0], gpu_zb=zb[0],
-                             gpu_valid=va[0], kap=kap)
-        print(name, e, r)
-        assert r["rgb_fail"] == 0 and r["dep_fail"] == 0 and r["alp_fail"] == 0, r
-        assert r["n_eval_fail"] == 0, r
-        assert r["masked_frac"] <= MASK_CAP, r
+    for k, e in enumerate((0, cfg.n_envs // 2, cfg.n_envs - 1)):
+        fr = {key: gout[key][e:e + 1] for key in ("rgb", "depth", "alpha", "n_eval")}
+        _check_sampled(name, fr, sc, b, e, cfg.width, cfg.height, gout["scene"], kap, seed=33 + k)
     st = gout["stats"]
     assert st["V"] > 0 and st["K"] >= st["V"] and st["P"] > 0
     assert st["P"] == int(gout["n_eval"].astype(np.int64).sum())
@@ -196,8 +203,8 @@ def test_render_full_size_sampled_pixels(name):
 @pytest.mark.slow
 def test_render_c5_full_size_sampled_pixels():
     """C5 (1 M Gaussians, 8192 envs) in the bench's strong-scaling launch at N = 1 (all 8192
-    envs in one call, 40 GB of outputs kept on the device): sampled pixels of frames
-    {0, B/2, B-1} are pulled from the device and compared with the oracle."""
+    envs in one call, 40 GB of outputs kept on the device): frames {0, B/2, B-1} are pulled
+    from the device and compared with the oracle on the d.6 sample."""
     cfg = synth.CONFIGS["C5"]
     sc = synth.make_scene(cfg)
     B, W, H = cfg.n_envs, cfg.width, cfg.height
@@ -212,21 +219,41 @@ def test_render_c5_full_size_sampled_pixels():
     torch.cuda.synchronize()
     assert not bool(torch.isnan(rgb).any()) and int((nev < 0).sum()) == 0
     kap = gu.kappa_f32(sc)
-    rng = np.random.default_rng(55)
-    for e in (0, B // 2, B - 1):
-        px = rng.integers(0, W, 256)
-        py = rng.integers(0, H, 256)
-        gout = {"rgb": rgb[e:e + 1].cpu().numpy(), "depth": dep[e:e + 1].cpu().numpy(),
-                "alpha": alp[e:e + 1].cpu().numpy(), "n_eval": nev[e:e + 1].cpu().numpy()}
-        ref = _oracle_frame(sc, b, e, 0, W, H, pixels=(px, py))
-        sub = synth.Batch(b.poses[e:e + 1], b.intrinsics[e:e + 1], b.w2c[e:e + 1])
-        rec, zb, va = gu.gpu_project(g, sub, W, H)
-        r = gu.compare_frame(gout, 0, 0, ref, W, H, pix=(px, py), gpu_rec=rec[0], gpu_zb=zb[0], gpu_valid=va[0],
-                             kap=kap)
-        print("C5", e, r)
-        assert r["rgb_fail"] == 0 and r["dep_fail"] == 0 and r["alp_fail"] == 0, r
-        assert r["n_eval_fail"] == 0, r
-        assert r["masked_frac"] <= MASK_CAP, r
+    for k, e in enumerate((0, B // 2, B - 1)):
+        fr = {"rgb": rgb[e:e + 1].cpu().numpy(), "depth": dep[e:e + 1].cpu().numpy(),
+              "alpha": alp[e:e + 1].cpu().numpy(), "n_eval": nev[e:e + 1].cpu().numpy()}
+        _check_sampled("C5", fr, sc, b, e, W, H, g, kap, seed=55 + k)
+
+
+def test_near_far_boundary_matches_oracle():
+    """Reading R4 at its boundary: keep iff near < z <= far on the fp32 key.  Gaussians exactly
+    at near and at far, and one ulp inside/outside each: the GPU's cull flags equal the
+    oracle's, and the frame (only the kept ones visible) matches the oracle."""
+    near, far = np.float32(1.0), np.float32(5.0)
+    zs = np.float32([near, np.nextafter(near, np.float32(9)), far, np.nextafter(far, np.float32(9)),
+                     np.nextafter(far, np.float32(0))])
+    xs = np.float32([-0.3, -0.15, 0.0, 0.15, 0.3]) * zs
+    sc = scene_from(np.stack([xs, np.zeros(5, np.float32), zs], 1), np.repeat(0.05 * zs[:, None] / 3, 3, 1), opac=0.9,
+                    colours=[[0.9, 0.1, 0.1], [0.1, 0.9, 0.1], [0.1, 0.1, 0.9], [0.9, 0.9, 0.1], [0.5, 0.5, 0.5]])
+    K, Wc = identity_cam(fx=100, fy=100, cx=32, cy=24)
+    b = synth.Batch(np.zeros((1, 0, 7), np.float32), K[None, None], Wc[None, None])
+    prm = oracle.RenderParams(64, 48, near=float(near), far=float(far))
+    _, ozb, ovalid = oracle.project(sc, b.poses[0], K, Wc, prm)
+    assert ovalid.tolist() == [False, True, True, False, True]
+    gout = gu.gpu_render(sc, b, 64, 48, near=float(near), far=float(far))
+    g = gout["scene"]
+    rec = torch.zeros((1, 5, 16), device="cuda")
+    zb = torch.zeros((1, 5), dtype=torch.int32, device="cuda")
+    va = torch.zeros((1, 5), dtype=torch.uint8, device="cuda")
+    g.debug_project(gu.to_dev(b.poses), gu.to_dev(b.intrinsics), gu.to_dev(b.w2c),
+                    gsb.RenderParams(64, 48, near=float(near), far=float(far)), rec, zb, va)
+    torch.cuda.synchronize()
+    assert np.array_equal(zb.cpu().numpy()[0].view(np.uint32), ozb)
+    assert va.cpu().numpy()[0].astype(bool).tolist() == ovalid.tolist()
+    ref = oracle.render_frame(sc, b.poses[0], K, Wc, prm)
+    r = gu.compare_frame(gout, 0, 0, ref, 64, 48)
+    assert r["rgb_fail"] == 0 and r["dep_fail"] == 0 and r["alp_fail"] == 0, r
+    assert gout["alpha"].max() > 0.5
 
 
 # --------------------------------------------------------------------------- invariants

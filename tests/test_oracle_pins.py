@@ -645,3 +645,62 @@ def test_obs_noise_is_unit_variance_irwin_hall_and_counter_based():
     other, _ = obs.epilogue(rgb, None, dr, seed=5, step=10)
     assert (other != full).mean() > 0.3
     assert float(obs.S3) == pytest.approx(np.sqrt(3) / 2 ** 22, rel=1e-7)
+
+
+# ---------------------------------------------------------------- pin 2b (closed form, rotated)
+@pytest.mark.parametrize("theta_deg", [30.0, -65.0, 120.0])
+def test_pin2b_rotated_anisotropic_footprint_via_inverse(theta_deg):
+    """An anisotropic Gaussian (sa, sb, sc) on the optical axis, rotated by theta about the
+    camera z axis through its OWN quaternion: Sigma2D = (f/z)^2 R2 diag(sa^2, sb^2) R2^T + 0.3 I
+    with R2 the 2D rotation by theta (J = diag(f/z) there); the conic is np.linalg.inv(Sigma2D),
+    so (a, b, c) = inv[0,0], inv[0,1], inv[1,1] including the sign of the off-diagonal b; and
+    at off-axis pixels alpha = o exp(-1/2 d^T inv(Sigma2D) d) with d = (u - px, v - py)
+    (3DGS EWA [P:212]; readings R7, R12).  A dropped or sign-flipped b term fails here."""
+    z, f, sa, sb, sz, o = 3.0, 100.0, 0.08, 0.02, 0.01, 0.9
+    h = math.radians(theta_deg) / 2
+    q = np.float32([math.cos(h), 0.0, 0.0, math.sin(h)])
+    sc = scene_from([0, 0, z], [sa, sb, sz], quats=q, opac=o)
+    K, W = identity_cam(fx=f, fy=f, cx=32.5, cy=24.5)
+    r = _frame(sc, K, W)
+    p = r.proj[0]
+    th = 2.0 * math.atan2(float(q[3]), float(q[0]))          # the angle of the fp32 quaternion
+    c_, s_ = math.cos(th), math.sin(th)
+    R2 = np.array([[c_, -s_], [s_, c_]])
+    sa32, sb32 = float(np.float32(sa)), float(np.float32(sb))
+    S2 = (f / z) ** 2 * R2 @ np.diag([sa32 ** 2, sb32 ** 2]) @ R2.T + 0.3 * np.eye(2)
+    inv = np.linalg.inv(S2)
+    assert p[oracle.F_SXX] == pytest.approx(S2[0, 0], rel=1e-10)
+    assert p[oracle.F_SYY] == pytest.approx(S2[1, 1], rel=1e-10)
+    assert p[oracle.F_SXY] == pytest.approx(S2[0, 1], rel=1e-9, abs=1e-12)
+    assert p[oracle.F_A] == pytest.approx(inv[0, 0], rel=1e-9)
+    assert p[oracle.F_B] == pytest.approx(inv[0, 1], rel=1e-9)
+    assert p[oracle.F_C] == pytest.approx(inv[1, 1], rel=1e-9)
+    o32 = float(np.float32(o))
+    for dpx, dpy in ((2, 1), (-2, 1), (1, -2), (3, 3), (-3, 2)):
+        px, py = 32 + dpx, 24 + dpy
+        d = np.array([p[oracle.F_U] - (px + 0.5), p[oracle.F_V] - (py + 0.5)])
+        a_exp = min(0.99, o32 * math.exp(-0.5 * d @ inv @ d))
+        if a_exp >= 1 / 255:
+            assert r.alpha[py, px] == pytest.approx(a_exp, rel=1e-9)
+        else:
+            assert r.alpha[py, px] == 0.0
+
+
+# ---------------------------------------------------------------- pin 8b (special case, R4)
+def test_pin8b_near_far_cull_boundary():
+    """Reading R4 on the fp32 key: keep iff near < z <= far.  Gaussians exactly at near and far
+    and one ulp on either side (identity camera: the R11 key is z exactly): at near culled,
+    one ulp beyond near kept, at far kept, one ulp beyond far culled; the image shows only the
+    kept ones (a culled Gaussian's pixels stay background)."""
+    near, far = np.float32(1.0), np.float32(5.0)
+    zs = np.float32([near, np.nextafter(near, np.float32(9)), far, np.nextafter(far, np.float32(9))])
+    xs = np.float32([-0.3, -0.1, 0.1, 0.3]) * zs
+    sc = scene_from(np.stack([xs, np.zeros(4, np.float32), zs], 1), np.repeat(0.02 * zs[:, None], 3, 1), opac=0.9)
+    K, W = identity_cam(fx=100, fy=100, cx=32, cy=24)
+    prm = oracle.RenderParams(64, 48, near=float(near), far=float(far))
+    r = _frame(sc, K, W, prm)
+    assert r.zbits.view(np.float32).tolist() == zs.tolist()
+    assert r.valid.tolist() == [False, True, True, False]
+    for i, kept in enumerate([False, True, True, False]):
+        u = int(np.floor(r.proj[i, oracle.F_U])); v = int(np.floor(r.proj[i, oracle.F_V]))
+        assert (r.alpha[v, u] > 0.5) == kept, i

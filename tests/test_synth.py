@@ -56,3 +56,24 @@ def test_pose_quaternions_unit_and_chain_links():
     assert np.allclose(np.linalg.norm(p[..., 3:], axis=-1), 1, atol=1e-6)
     d = np.linalg.norm(np.diff(p[..., :3].astype(np.float64), axis=1), axis=-1)
     assert np.allclose(d, 0.3, atol=1e-5)
+
+
+def test_sample_pixels_stratified_and_full_tiles():
+    """SURVEY d.6 sample: one pixel per cell of a 64x64 grid + every pixel of 2 tiles."""
+    for W, H in ((640, 480), (128, 128), (1280, 720), (224, 224), (17, 9)):
+        px, py, n = synth.sample_pixels(W, H, seed=3)
+        g = (min(64, W), min(64, H))
+        assert n == g[0] * g[1]
+        assert px.min() >= 0 and px.max() < W and py.min() >= 0 and py.max() < H
+        bx = (np.arange(g[0] + 1) * W) // g[0]        # cell boundaries
+        by = (np.arange(g[1] + 1) * H) // g[1]
+        cx, cy = np.searchsorted(bx, px[:n], side="right") - 1, np.searchsorted(by, py[:n], side="right") - 1
+        assert len(set(zip(cx.tolist(), cy.tolist()))) == n     # one pixel in every cell
+        tiles = set(((py[n:] // 16) * ((W + 15) // 16) + px[n:] // 16).tolist())
+        assert len(tiles) == min(2, ((W + 15) // 16) * ((H + 15) // 16))
+        for t in tiles:   # each drawn tile complete (ragged edges included)
+            x0, y0 = (t % ((W + 15) // 16)) * 16, (t // ((W + 15) // 16)) * 16
+            size = (min(x0 + 16, W) - x0) * (min(y0 + 16, H) - y0)
+            assert np.sum(((py[n:] // 16) * ((W + 15) // 16) + px[n:] // 16) == t) == size
+    a, b = synth.sample_pixels(640, 480, 5), synth.sample_pixels(640, 480, 5)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
