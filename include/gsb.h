@@ -230,6 +230,14 @@ gsb_status gsb_render_static(gsb_scene scene, const float* body_poses, int32_t n
 /* Counters of the last render made with GSB_FLAG_STATS (synchronises with it). */
 gsb_status gsb_get_stats(gsb_scene scene, int64_t* visible_V, int64_t* keys_K, int64_t* pairs_P);
 
+/* The same counters plus the SURVEY §8(d) d.4 (iv) workload statistic: pixels whose
+ * compositing stopped at the termination test (reading R13), out of all pixels rendered. */
+typedef struct {
+  int64_t visible_V, keys_K, pairs_P;
+  int64_t terminated_pixels, pixels;
+} gsb_stats;
+gsb_status gsb_get_stats_ext(gsb_scene scene, gsb_stats* out);
+
 /* Per-kernel-class device time of the last render made with GSB_FLAG_TIMING, in ms
  * (synchronises with it), and the number of kernels libgsb launched in that render. */
 typedef struct {
@@ -353,13 +361,15 @@ gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, 
  *                depth ties by this id, so a non-identity permutation exercises the slot-key
  *                path's re-ordering of equal-depth runs
  *   variant      0 = what gsb_render picks for this batch (split if >= 200 keys per tile on
- *                average, packed sort if > 1/4 of the lists exceed 1024 keys), 1 = K4a with the
- *                counting sort (<= 1024 keys in smem, HBM radix beyond), 2 = K4a packed (<= 4096,
- *                HBM beyond), 3 = fused K4 small, 4 = fused K4 packed
+ *                average, packed sort if > 1/4 of the lists exceed 1024 keys), 1 = K4a as the
+ *                render runs it for short lists (one warp per list <= 1024 keys, one CTA with the
+ *                HBM radix per longer list), 2 = K4a packed (<= 4096, HBM beyond), 3 = fused K4
+ *                small, 4 = fused K4 packed, 5 = K4a one CTA per list (counting sort <= 1024 keys
+ *                in smem, HBM radix beyond; the LiDAR path's sort)
  *   key_mode     0 = keys carry the record slot (gsb_render's default), 1 = keys carry the id
  *   out_tile_offsets [F, T_t + 1] DEVICE int64 (absolute positions in out_ids),
  *   out_ids      [cap] DEVICE uint32: creation ids of every (frame, tile) list in sorted order
- *   out_K, out_variant (HOST): total keys and the variant that ran (1..4).
+ *   out_K, out_variant (HOST): total keys and the variant that ran (1..5).
  * Allocates its own scratch and synchronises (test-only).  CAPACITY if K > cap. */
 gsb_status gsb_debug_tile_lists(const float* u, const float* v, const float* sxx, const float* syy,
                                 const float* kappa, const uint32_t* zbits, const uint8_t* valid,

@@ -35,11 +35,35 @@
 #include <stdlib.h>
 #include <string.h>
 
-#define GSBO_NF 17
+#define GSBO_NF 20
 enum {
   F_U = 0, F_V, F_SXX, F_SXY, F_SYY, F_A, F_B, F_C, F_R, F_G, F_BL, F_O, F_KAPPA,
-  F_Z32, F_Z64, F_XC, F_YC
+  F_Z32, F_Z64, F_XC, F_YC,
+  F_EU, F_EV, /* reading R28: bounds on |u_gpu - u|, |v_gpu - v| (px), see R28_K_POS */
+  F_EQ        /* reading R28: relative bound of K4's quadratic form, see R28_K_CONIC */
 };
+
+/* ---------------------------------------------------------------------------------
+ * Reading R28: the threshold-margin mask uses a forward error bound of the GPU's
+ * binary32 evaluation, not a flat margin.  EPS = binary32 unit roundoff 2^-24.
+ * ------------------------------------------------------------------------------- */
+#define R28_EPS (1.0 / 16777216.0)
+/* position: the GPU computes x = M mu + m from fp32 M = W R(q_k), m = W t_k + t_f (each a
+ * chain of fp32 ops), then u = f (x / z32) + c with z32 the R11 key.  First-order bound:
+ *   |du| <= f/|z| (K_POS EPS S_x + |x/z| (|z32 - z| + K_POS EPS S_z)) + 2 EPS |u|
+ * with S_r = sum_k |W_rk| (sum_c |R_kc mu_c| + |t_k|) + |t_fr| (the magnitudes summed by the
+ * chain).  K_POS = 4: measured max |du| is 1.12 x the unit-count bound (scripts/alpha_error.py,
+ * T1-T6 + C2-C4 on B200), so the bound holds with 3.5x to spare. */
+#define R28_K_POS 4.0
+/* K4's quadratic form from K1's whitening factor (Sigma2D in binary32, rsqrt/div approximations):
+ * measured error <= 17.7 EPS |power| for Gaussians whose centre is inside the R6 frustum clamp
+ * and <= 45.7 EPS |power| for clamped ones (off-screen giants) -> K_CONIC = 32 / 96 */
+#define R28_K_CONIC 32.0
+#define R28_K_CONIC_CLAMPED 96.0
+/* K4's own binary32 evaluation: dx = u - px (one rounding of dx), then 5 fused ops; measured
+ * <= 2.6 x EPS (|w_x| |u| + |w_y| |v| + |power| + |ln o|) -> bound K_EVAL EPS (|w.d| + |power|
+ * + |ln o|) with w.d = 2 |power| the exact form of the dx/dy rounding, K_EVAL = 8 */
+#define R28_K_EVAL 8.0
 
 int gsbo_num_fields(void) { return GSBO_NF; }
 
@@ -247,7 +271,18 @@ int gsbo_project(const float* means, const float* scales, const float* quats, co
     o[F_Z64] = z; o[F_XC] = xc[0]; o[F_YC] = xc[1];
     o[F_U] = fx * xc[0] / z + cx;
     o[F_V] = fy * xc[1] / z + cy;
+    { /* reading R28: bound on the GPU's binary32 u, v (see R28_K_POS) */
+      double mag[3], S[3];
+      for (int r = 0; r < 3; ++r)
+        mag[r] = fabs(Rk[r][0] * mu[0]) + fabs(Rk[r][1] * mu[1]) + fabs(Rk[r][2] * mu[2]) + fabs(tk[r]);
+      for (int r = 0; r < 3; ++r)
+        S[r] = fabs(Wc[r][0]) * mag[0] + fabs(Wc[r][1]) * mag[1] + fabs(Wc[r][2]) * mag[2] + fabs(tc[r]);
+      const double dz = fabs((double)z32 - z) + R28_K_POS * R28_EPS * S[2];
+      o[F_EU] = fabs(fx / z) * (R28_K_POS * R28_EPS * S[0] + fabs(xc[0] / z) * dz) + 2.0 * R28_EPS * fabs(o[F_U]);
+      o[F_EV] = fabs(fy / z) * (R28_K_POS * R28_EPS * S[1] + fabs(xc[1] / z) * dz) + 2.0 * R28_EPS * fabs(o[F_V]);
+    }
     double txz = xc[0] / z, tyz = xc[1] / z;
+    o[F_EQ] = R28_EPS * ((fabs(txz) > limx || fabs(tyz) > limy) ? R28_K_CONIC_CLAMPED : R28_K_CONIC);
     if (txz < -limx) txz = -limx;
     if (txz > limx) txz = limx;
     if (tyz < -limy) tyz = -limy;
@@ -309,7 +344,8 @@ typedef struct {
   int64_t p0, p1;
   double bg[3];
   int mode; /* 0 = pure brute force, 1 = box accelerated (R8) */
-  double delta_alpha, delta_T, cmax, zmax;
+  double margin_scale, cmax, zmax; /* R28 bound multiplier (1 = the model; 0 = no mask) */
+  double bg_sign;                   /* 1 if every background channel is >= 0, else 2 */
   double* out_rgb;
   double* out_depth;
   double* out_alpha;
@@ -318,7 +354,7 @@ typedef struct {
   double* out_budget_rgb;
   double* out_budget_depth;
   uint8_t* out_term_near;
-  double delta_T_int;
+  double* out_eT;           /* R28: relative error bound of the GPU's final T */
   /* pruning scores (§8(f) row 3, reading R30), all NULL unless requested; per-thread arrays
    * indexed by Gaussian id, merged after the join */
   double* w_sum;            /* sum of blend weights w = alpha T over the pixels */
@@ -327,13 +363,36 @@ typedef struct {
   uint8_t* touched;         /* Gaussians whose R8 box holds a masked pixel */
 } comp_job;
 
+/* Reading R28: bound on |power_gpu - power| for one (pixel, Gaussian) pair, in natural-log
+ * units (= the relative error of alpha): position (w = Sigma2D^-1 d = -grad_u power), K1's
+ * quadratic form, K4's binary32 evaluation.  dx = u - px_c, dy = v - py_c. */
+static double r28_delta(const double* g, double dx, double dy, double power) {
+  const double wx = g[F_A] * dx + g[F_B] * dy, wy = g[F_B] * dx + g[F_C] * dy;
+  return fabs(wx) * g[F_EU] + fabs(wy) * g[F_EV] + g[F_EQ] * fabs(power) +
+         R28_K_EVAL * R28_EPS * (fabs(wx * dx) + fabs(wy * dy) + fabs(power) - log(g[F_O]));
+}
+
+/* r28_delta of n pairs (Gaussian row gid[k] of proj, pixel (px[k], py[k])) — exported so the
+ * GPU tests can check the measured alpha error of every near-threshold pair against it */
+void gsbo_r28_delta(const double* proj, const int64_t* gid, const int32_t* px, const int32_t* py, int64_t n,
+                    double* out) {
+  for (int64_t k = 0; k < n; ++k) {
+    const double* g = proj + gid[k] * GSBO_NF;
+    const double dx = g[F_U] - ((double)px[k] + 0.5), dy = g[F_V] - ((double)py[k] + 0.5);
+    const double power = -0.5 * (g[F_A] * dx * dx + g[F_C] * dy * dy) - g[F_B] * dx * dy;
+    out[k] = r28_delta(g, dx, dy, power);
+  }
+}
+
 static void composite_pixel(const comp_job* jb, int64_t p) {
   const double pxc = (double)jb->px[p] + 0.5, pyc = (double)jb->py[p] + 0.5; /* R3 */
   double T = 1.0, C[3] = {0, 0, 0}, D = 0.0;
   double brgb = 0.0, bdep = 0.0;
+  double eT = 0.0; /* R28: relative bound of |T_gpu - T| / T before the current entry */
   int64_t term = -1, n_eval = 0;
   uint8_t term_near = 0;
   const double thr = 1.0 / 255.0;
+  const double ks = jb->margin_scale;
   for (int64_t j = 0; j < jb->n_order; ++j) {
     const uint32_t i = jb->order[j];
     const double* g = jb->proj + (int64_t)i * GSBO_NF;
@@ -345,22 +404,38 @@ static void composite_pixel(const comp_job* jb, int64_t p) {
     const double dx = g[F_U] - pxc, dy = g[F_V] - pyc;
     const double power = -0.5 * (g[F_A] * dx * dx + g[F_C] * dy * dy) - g[F_B] * dx * dy; /* R12 */
     if (power > 0.0) continue;
+    const double delta = ks * r28_delta(g, dx, dy, power);
     const double araw = g[F_O] * exp(power);
-    /* R28: skip-threshold flip budget (effect of blending vs skipping this entry) */
-    if (fabs(araw - thr) <= jb->delta_alpha * thr) {
-      brgb += T * thr * (1.0 + jb->delta_alpha) * jb->cmax;
-      bdep += T * thr * (1.0 + jb->delta_alpha) * jb->zmax;
+    /* R28: skip-threshold flip (blend vs skip this entry): this entry's contribution and the
+     * (1 - alpha) scaling of everything behind it; later T values then carry the factor too */
+    if (fabs(power - log(thr / g[F_O])) <= delta) {
+      /* |blend - skip| = |a T c_i - a (everything behind, background included)|: a difference
+       * of two non-negative terms (colours >= 0 by the SH clamp; a background >= 0), each at
+       * most a T cmax; twice that when the background has a negative channel */
+      const double am = thr * exp(delta);
+      brgb += jb->bg_sign * T * am * jb->cmax;
+      bdep += T * am * jb->zmax;
+      eT += am / (1.0 - am);
     }
     const double alpha = araw < 0.99 ? araw : 0.99;
     if (alpha < thr) continue;
     const double tT = T * (1.0 - alpha); /* R13 */
-    /* R28: termination flip budget (stop vs continue at this entry) */
-    if (fabs(tT - 1e-4) <= jb->delta_T * 1e-4) {
-      brgb += T * 2.0 * jb->cmax;
-      bdep += T * jb->zmax;
+    /* R28: relative error of the GPU's tT = T - alpha T: the error of alpha scaled by
+     * alpha / (1 - alpha) (clamped alphas: 0.99f - 0.99 = 9.5e-9), ex2.approx (2 EPS), and the
+     * two roundings of w = alpha T and T - w relative to T (1 - alpha) */
+    const double ea = (araw > 0.99 * exp(delta)) ? ks * 1e-8 / (1.0 - alpha)
+                                                 : alpha / (1.0 - alpha) * (delta + ks * 2.0 * R28_EPS);
+    const double eTn = eT + ea + ks * 2.0 * R28_EPS / (1.0 - alpha);
+    /* R28: termination flip (stop vs continue): everything from here on; n_eval (an integer
+     * decided by this test) is then not compared either */
+    if (fabs(tT - 1e-4) <= eTn * tT) {
+      /* stop: C + T bg; continue: C + alpha T c_i + (entries behind: <= tT cmax) + T_end bg */
+      double dc = 0.0;
+      for (int c = 0; c < 3; ++c) dc = fmax(dc, fabs(g[F_R + c] - jb->bg[c]));
+      brgb += alpha * T * dc + 2.0 * tT * (1.0 + eTn) * jb->cmax;
+      bdep += alpha * T * g[F_Z32] + tT * (1.0 + eTn) * jb->zmax;
+      term_near = 1;
     }
-    /* R28: the integer n_eval is decided by this test; flag it when within fp32 reach */
-    if (fabs(tT - 1e-4) <= jb->delta_T_int * 1e-4) term_near = 1;
     if (tT < 1e-4) {
       term = (int64_t)i;
       break;
@@ -375,6 +450,7 @@ static void composite_pixel(const comp_job* jb, int64_t p) {
     C[2] += w * g[F_BL];
     D += w * g[F_Z32];
     T = tT;
+    eT = eTn;
   }
   for (int c = 0; c < 3; ++c) jb->out_rgb[p * 3 + c] = C[c] + T * jb->bg[c];
   jb->out_depth[p] = D;          /* R16 */
@@ -384,6 +460,7 @@ static void composite_pixel(const comp_job* jb, int64_t p) {
   jb->out_budget_rgb[p] = brgb;
   jb->out_budget_depth[p] = bdep;
   jb->out_term_near[p] = term_near;
+  if (jb->out_eT) jb->out_eT[p] = eT;
   if (jb->touched && jb->mask_in && jb->mask_in[p]) {
     /* a masked pixel may blend any Gaussian whose exact box holds it on either side of a flip */
     for (int64_t j = 0; j < jb->n_order; ++j) {
@@ -402,11 +479,11 @@ static void* composite_worker(void* arg) {
 }
 
 int gsbo_composite(const double* proj, const uint32_t* order, int64_t n_order, const int32_t* px,
-                   const int32_t* py, int64_t npix, const float* bg, int mode, double delta_alpha,
-                   double delta_T, double cmax, double zmax, double* out_rgb, double* out_depth,
+                   const int32_t* py, int64_t npix, const float* bg, int mode, double margin_scale,
+                   double cmax, double zmax, double* out_rgb, double* out_depth,
                    double* out_alpha, int64_t* out_term_id, int64_t* out_n_eval,
                    double* out_budget_rgb, double* out_budget_depth, uint8_t* out_term_near,
-                   double delta_T_int, int nthreads, int64_t n_gauss, double* out_w_sum, double* out_w_max,
+                   double* out_eT, int nthreads, int64_t n_gauss, double* out_w_sum, double* out_w_max,
                    const uint8_t* mask_in, uint8_t* out_touched) {
   if (nthreads < 1) nthreads = 1;
   if (nthreads > 256) nthreads = 256;
@@ -421,11 +498,12 @@ int gsbo_composite(const double* proj, const uint32_t* order, int64_t n_order, c
     jb->p1 = npix * (t + 1) / nthreads;
     for (int c = 0; c < 3; ++c) jb->bg[c] = bg[c];
     jb->mode = mode;
-    jb->delta_alpha = delta_alpha; jb->delta_T = delta_T; jb->cmax = cmax; jb->zmax = zmax;
+    jb->margin_scale = margin_scale; jb->cmax = cmax; jb->zmax = zmax;
+    jb->bg_sign = (bg[0] >= 0.f && bg[1] >= 0.f && bg[2] >= 0.f) ? 1.0 : 2.0;
     jb->out_rgb = out_rgb; jb->out_depth = out_depth; jb->out_alpha = out_alpha;
     jb->out_term_id = out_term_id; jb->out_n_eval = out_n_eval;
     jb->out_budget_rgb = out_budget_rgb; jb->out_budget_depth = out_budget_depth;
-    jb->out_term_near = out_term_near; jb->delta_T_int = delta_T_int;
+    jb->out_term_near = out_term_near; jb->out_eT = out_eT;
     jb->w_sum = jb->w_max = NULL; jb->mask_in = mask_in; jb->touched = NULL;
     if (out_w_sum && out_w_max) {
       jb->w_sum = (double*)calloc((size_t)n_gauss + 1, sizeof(double));

@@ -32,6 +32,7 @@ STATUS = {0: "GSB_OK", 1: "GSB_ERR_INVALID_ARGUMENT", 2: "GSB_ERR_SHAPE_MISMATCH
 EXPORTS = ["gsb_create_scene", "gsb_reserve", "gsb_render", "gsb_render_rig", "gsb_render_host",
            "gsb_prebin_static", "gsb_render_static",
            "gsb_scores_reset", "gsb_get_scores", "gsb_filter_scene", "gsb_render_obs", "gsb_render_obs_host", "gsb_get_stats",
+           "gsb_get_stats_ext",
            "gsb_get_timings", "gsb_destroy_scene", "gsb_last_error", "gsb_version",
            "gsb_debug_project", "gsb_debug_bin_sort", "gsb_debug_tile_lists",
            "gsb_obs_encode", "gsb_lidar_create", "gsb_render_lidar", "gsb_lidar_info", "gsb_lidar_destroy"]
@@ -61,6 +62,11 @@ class gsb_timings(ctypes.Structure):
                 ("long_lists", ctypes.c_int64), ("max_list", ctypes.c_int64)]
 
 
+class gsb_stats(ctypes.Structure):
+    _fields_ = [("visible_V", ctypes.c_int64), ("keys_K", ctypes.c_int64), ("pairs_P", ctypes.c_int64),
+                ("terminated_pixels", ctypes.c_int64), ("pixels", ctypes.c_int64)]
+
+
 _lib = None
 
 
@@ -88,6 +94,7 @@ def lib() -> ctypes.CDLL:
     L.gsb_get_scores.argtypes = [P, P, P, P]
     L.gsb_filter_scene.argtypes = [P, P, ctypes.POINTER(P)]
     L.gsb_get_stats.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]
+    L.gsb_get_stats_ext.argtypes = [P, ctypes.POINTER(gsb_stats)]
     L.gsb_get_timings.argtypes = [P, ctypes.POINTER(gsb_timings)]
     L.gsb_destroy_scene.argtypes = [P]
     L.gsb_last_error.argtypes = []
@@ -348,6 +355,13 @@ class Scene:
         V, K, P = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _check(lib().gsb_get_stats(self._h, ctypes.byref(V), ctypes.byref(K), ctypes.byref(P)))
         return {"V": V.value, "K": K.value, "P": P.value}
+
+    def stats_ext(self):
+        """gsb_get_stats_ext: V, K, P plus terminated pixels (reading R13) out of all pixels."""
+        st = gsb_stats()
+        _check(lib().gsb_get_stats_ext(self._h, ctypes.byref(st)))
+        return {"V": st.visible_V, "K": st.keys_K, "P": st.pairs_P, "terminated": st.terminated_pixels,
+                "pixels": st.pixels}
 
     def timings(self):
         t = gsb_timings()

@@ -225,7 +225,7 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
   CUDA_TRY(dalloc(&s->keys, (size_t)cap));
   CUDA_TRY(dalloc(&s->keys_alt, (size_t)cap));
   CUDA_TRY(dalloc(&s->sorted, (size_t)cap));
-  CUDA_TRY(dalloc(&s->d_pairs, 1));
+  CUDA_TRY(dalloc(&s->d_pairs, 2));
   CUDA_TRY(dalloc(&s->d_counter, 1));
   CUDA_TRY(cudaStreamCreateWithFlags(&s->sp, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&s->sc, cudaStreamNonBlocking));
@@ -266,6 +266,21 @@ gsb_status gsb_get_stats(gsb_scene s, int64_t* V, int64_t* K, int64_t* P) {
   if (V) *V = s->stat_V;
   if (K) *K = s->stat_K;
   if (P) *P = (int64_t)pairs;
+  return GSB_OK;
+}
+
+gsb_status gsb_get_stats_ext(gsb_scene s, gsb_stats* out) {
+  if (!s || !out) return fail(GSB_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!s->stats_valid) return fail(GSB_ERR_INVALID_ARGUMENT, "last render had no GSB_FLAG_STATS");
+  DeviceGuard g(s->device);
+  CUDA_TRY(cudaStreamSynchronize(s->last_stream));
+  unsigned long long c[2] = {0, 0};
+  CUDA_TRY(cudaMemcpy(c, s->d_pairs, sizeof(c), cudaMemcpyDeviceToHost));
+  out->visible_V = s->stat_V;
+  out->keys_K = s->stat_K;
+  out->pairs_P = (int64_t)c[0];
+  out->terminated_pixels = (int64_t)c[1];
+  out->pixels = s->stat_pixels;
   return GSB_OK;
 }
 

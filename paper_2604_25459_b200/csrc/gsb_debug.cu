@@ -115,7 +115,7 @@ gsb_status gsb_debug_tile_lists(const float* u, const float* v, const float* sxx
                                 int32_t variant, int32_t key_mode, int64_t* out_offsets, uint32_t* out_ids,
                                 int64_t cap, int64_t* out_K, int32_t* out_variant, gsb_stream stream) {
   if (F < 1 || n < 0 || width < 1 || height < 1 || width > kMaxDim || height > kMaxDim || cap < 0 || !out_K ||
-      !out_offsets || variant < 0 || variant > 4 || key_mode < 0 || key_mode > 1 ||
+      !out_offsets || variant < 0 || variant > 5 || key_mode < 0 || key_mode > 1 ||
       (n > 0 && (!u || !v || !sxx || !syy || !kappa || !zbits || !valid || !slot_ids)))
     return fail(GSB_ERR_INVALID_ARGUMENT, "bad debug_tile_lists arguments");
   if (n >= (int64_t)1 << 31) return fail(GSB_ERR_CAPACITY, "n >= 2^31");
@@ -139,9 +139,11 @@ gsb_status gsb_debug_tile_lists(const float* u, const float* v, const float* sxx
   uint2* emit = nullptr; int* vcount = nullptr; int* hist = nullptr; uint32_t* off = nullptr;
   uint32_t* vbits = nullptr; uint64_t* fbase = nullptr; uint64_t* keys = nullptr; uint64_t* keys_alt = nullptr;
   uint32_t* sorted = nullptr; uint32_t* lists = nullptr; int2* d_ids = nullptr; int* d_inv = nullptr;
+  uint32_t* d_long = nullptr;
   auto cleanup = [&]() {
     cudaFree(emit); cudaFree(vcount); cudaFree(hist); cudaFree(off); cudaFree(fbase); cudaFree(vbits);
     cudaFree(keys); cudaFree(keys_alt); cudaFree(sorted); cudaFree(lists); cudaFree(d_ids); cudaFree(d_inv);
+    cudaFree(d_long);
   };
 #define DBG_TRY(expr)                                                              \
   do {                                                                             \
@@ -182,10 +184,12 @@ gsb_status gsb_debug_tile_lists(const float* u, const float* v, const float* sxx
     return fail(GSB_ERR_CAPACITY, "K = %llu exceeds cap %lld", (unsigned long long)K, (long long)cap);
   }
   // the render's choices (gsb_render.cu, Pipeline::pass): long-list variant, split vs fused
-  uint64_t n_long = 0;
+  std::vector<uint32_t> hlong;   // K2a's long-list entries (frame << 16 | tile)
   for (int f = 0; f < F; ++f)
     for (int t = 0; t < n_tiles; ++t)
-      n_long += hoff[(size_t)f * stride + t + 1] - hoff[(size_t)f * stride + t] > (uint32_t)kFusedSortCap;
+      if (hoff[(size_t)f * stride + t + 1] - hoff[(size_t)f * stride + t] > (uint32_t)kWarpSortCap)
+        hlong.push_back(((uint32_t)f << 16) | (uint32_t)t);
+  const uint64_t n_long = hlong.size();
   int var = variant;
   if (var == 0) {
     const bool long_lists = n_long * 4 > (uint64_t)F * n_tiles;
@@ -209,7 +213,15 @@ gsb_status gsb_debug_tile_lists(const float* u, const float* v, const float* sxx
   c.keys = keys; c.keys_alt = keys_alt; c.key_base = 0; c.inv = d_inv; c.slot_base = 0;
   c.keys_internal_ids = slot_keys ? d_ids : nullptr;
   c.fs = 0; c.fe = F; c.f0 = 0; c.width = width; c.height = height; c.tiles_x = tiles_x; c.n_tiles = n_tiles;
-  if (var <= 2) {
+  if (var == 1 && n_long > 0) {       // the render's K4a: warp per short list + CTA per long list
+    DBG_TRY(dalloc(&d_long, (size_t)n_long));
+    DBG_TRY(cudaMemcpy(d_long, hlong.data(), sizeof(uint32_t) * n_long, cudaMemcpyHostToDevice));
+  }
+  if (var == 1) {
+    c.long_list = d_long ? d_long : sorted;   // (non-null: selects the warp path)
+    c.n_long = (uint32_t)n_long;
+  }
+  if (var <= 2 || var == 5) {
     launch_k4a_sort(c, var == 2, st);   // K4a: slots in (bits(z), id) order -> sorted
   } else {
     c.dbg_lists = sorted;               // fused K4: its in-CTA sort exports the slot lists

@@ -7,7 +7,8 @@
 
 namespace gsb {
 
-constexpr int kFusedSortCap = 1024;  // tile lists up to this length are sorted in K4 smem (8 CTAs/SM);
+constexpr int kFusedSortCap = 1024;
+constexpr int kWarpSortCap = kFusedSortCap;  // K4a: lists up to this length are sorted by one warp  // tile lists up to this length are sorted in K4 smem (8 CTAs/SM);
                                      // chunks with many longer lists use a 4x variant
 
 constexpr int kDbgRecFloats = 16;   // gsb_debug_project record (include/gsb.h)
@@ -94,7 +95,7 @@ struct CompositeArgs {
   float* out_depth;       // [F][H][W] or nullptr
   float* out_alpha;
   int32_t* out_n_eval;
-  unsigned long long* stat_pairs;  // nullptr unless STATS
+  unsigned long long* stat_pairs;  // nullptr unless STATS: [0] evaluated pairs P, [1] terminated pixels
   float* score_sum;         // [N] by internal index, nullptr unless GSB_FLAG_SCORES (reading R30)
   uint32_t* score_max;      // [N] float bits of the max weight
   // observation epilogue (gsb_render_obs, §8(f) row 4, reading R31); obs_rgb8 == nullptr: fp32 outputs
@@ -107,6 +108,10 @@ struct CompositeArgs {
   // (K2b with ids = nullptr); equal-depth runs are then re-ordered by the creation id ids[slot].x
   // so the order is still (bits(z), id) of reading R10, and no id -> slot gather is needed
   const int2* keys_internal_ids;   // template (id, body) of the launch's range, or nullptr
+  // lists longer than kWarpSortCap of this chunk ((frame << 16 | tile), from K2a): the split path's
+  // K4a sorts short lists one warp per tile and these with a CTA each; nullptr = CTA per tile
+  const uint32_t* long_list;
+  uint32_t n_long;
   // gsb_debug_tile_lists only: the fused K4 writes each tile's sorted slot list here (at the
   // list's key offset) and returns before compositing; nullptr in every render
   uint32_t* dbg_lists;

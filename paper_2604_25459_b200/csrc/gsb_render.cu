@@ -124,6 +124,8 @@ struct Pipeline {
       c.bg_cum = s->d_bgcum;
     }
     if (slot_keys) c.keys_internal_ids = s->d_ids + first;
+    c.long_list = s->long_list[sl];   // K4a: lists > kWarpSortCap get a CTA each
+    c.n_long = n_long;
     c.fs = fs; c.fe = fe; c.f0 = f0; c.width = W; c.height = H; c.tiles_x = tiles_x; c.n_tiles = n_tiles;
     c.bg0 = p->background[0]; c.bg1 = p->background[1]; c.bg2 = p->background[2];
     c.out_rgb = out_rgb; c.out_depth = out_depth; c.out_alpha = out_alpha; c.out_n_eval = out_neval;
@@ -307,7 +309,8 @@ gsb_status render_impl(gsb_scene s, const K0Rig& rig, int n_envs, int n_cams, co
     s->ev_pool.resize(8192);
     for (auto& e : s->ev_pool) CUDA_TRY(cudaEventCreate(&e));
   }
-  if (p->flags & GSB_FLAG_STATS) CUDA_TRY(cudaMemsetAsync(s->d_pairs, 0, sizeof(unsigned long long), st));
+  if (p->flags & GSB_FLAG_STATS) CUDA_TRY(cudaMemsetAsync(s->d_pairs, 0, 2 * sizeof(unsigned long long), st));
+  s->stat_pixels = (int64_t)F * p->width * p->height;
   Pipeline pl{};
   pl.s = s; pl.st = st; pl.p = p;
   pl.sp = pl.sc = pl.sb = st;

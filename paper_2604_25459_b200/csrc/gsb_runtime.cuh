@@ -165,7 +165,7 @@ struct gsb_scene_t {
   // last-render bookkeeping
   cudaStream_t last_stream = nullptr;
   bool stats_valid = false;
-  int64_t stat_V = 0, stat_K = 0, stat_long = 0, stat_maxseg = 0;
+  int64_t stat_V = 0, stat_K = 0, stat_long = 0, stat_maxseg = 0, stat_pixels = 0;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<std::pair<int, size_t>> ev_marks;  // (class, index of begin event)

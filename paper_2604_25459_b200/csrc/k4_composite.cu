@@ -332,6 +332,9 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
     if (lane == 0) sm.red[warp] = v;
+    // terminated pixels (R13 stop reached: the centre was moved to kFar)
+    const unsigned nt = __reduce_add_sync(FULL, (unsigned)(in0 && pyc0 == kFar) + (unsigned)(in1 && pyc1 == kFar));
+    if (lane == 0 && nt) atomicAdd(a.stat_pairs + 1, (unsigned long long)nt);
     __syncthreads();
     if (tid == 0) {
       unsigned long long s = 0;

@@ -77,13 +77,23 @@ __device__ __forceinline__ TileList tile_list(const CompositeArgs& a, int fl, in
 
 constexpr uint32_t kBgTag = 0x80000000u;   // merged entry: background record index | tag
 
-template <int CAP>
+// LONG: one CTA per entry of a.long_list (the chunk's lists longer than kWarpSortCap; entries of
+// frames outside this pass return), the short lists being sorted by k4a_warp_sort
+template <int CAP, bool LONG = false>
 __global__ void __launch_bounds__(kSortThreadsA) k4a_sort(CompositeArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using Sh = K4aShared<CAP>;
   Sh& sm = *reinterpret_cast<Sh*>(smem_raw);
-  const int fl = a.fs + blockIdx.x / a.n_tiles;
-  const int t = blockIdx.x % a.n_tiles;
+  int fl, t;
+  if constexpr (LONG) {
+    const uint32_t e = a.long_list[blockIdx.x];
+    fl = (int)(e >> 16);
+    t = (int)(e & 0xffffu);
+    if (fl < a.fs || fl >= a.fe) return;
+  } else {
+    fl = a.fs + blockIdx.x / a.n_tiles;
+    t = blockIdx.x % a.n_tiles;
+  }
   const int tid = threadIdx.x;
   const TileList L = tile_list(a, fl, t);
   const uint64_t start = L.rstart;
@@ -199,6 +209,134 @@ __global__ void __launch_bounds__(kSortThreadsA) k4a_sort(CompositeArgs a) {
     const bool in_b = segment_sort(ga, gb, len, sm.s.sort);
     const uint64_t* r = in_b ? gb : ga;
     for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)r[e]) - base);
+  }
+}
+
+
+// ------------------------------------------------------------------------------ K4a, one warp per list
+// Lists of up to kWarpSortCap keys (98.5 % of C3's) are sorted by ONE warp each, with no CTA
+// barrier (the CTA-per-tile sort above spent most of its time in per-CTA fixed costs — 2048-bin
+// scans, barriers — for lists averaging 340 keys).  Counting sort on the top kWarpBits varying
+// bits of (zbits - zmin) (range from the list's zmin and zmax: the highest varying bit of
+// z - zmin is the highest bit of zmax - zmin); scatter into the bucket with shared atomics; then
+// every key takes its rank among the keys of its bucket by (bits(z), id) and is written straight
+// to its final position as a record slot.  With slot keys an equal-depth pair is ordered by the
+// creation ids ids[slot] (gathered only for ties); a list with a run of more than kShortRun equal
+// depths (e.g. a fronto-parallel plane) is re-keyed by id and re-ranked (reading R10).
+constexpr int kWarpBits = 9;
+constexpr int kWarpBins = 1 << kWarpBits;
+constexpr int kK4aWarps = 4;   // lists (warps) per CTA
+
+struct K4aWarpShared {
+  uint64_t buf[kWarpSortCap];   // the list, bucketed
+  uint32_t bins[kWarpBins];
+};
+
+__global__ void __launch_bounds__(kK4aWarps * 32) k4a_warp_sort(CompositeArgs a, int n_lists) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  K4aWarpShared& sm = reinterpret_cast<K4aWarpShared*>(smem_raw)[warp];
+  const int ft = blockIdx.x * kK4aWarps + warp;
+  if (ft >= n_lists) return;   // warp-uniform
+  const int fl = a.fs + ft / a.n_tiles;
+  const int t = ft % a.n_tiles;
+  const TileList L = tile_list(a, fl, t);
+  const int n = L.len;
+  if (n == 0 || n > kWarpSortCap) return;   // long lists: k4a_sort<.., true>
+  const uint64_t* gk = a.keys + L.rstart;
+  uint32_t* dst = a.sorted + L.start;
+  const int2* kid = a.keys_internal_ids;   // slot keys: key low word = slot
+  const int base = a.slot_base;
+  auto slot_of = [&](uint64_t key) -> uint32_t {
+    return kid ? (uint32_t)key : (uint32_t)(__ldg(a.inv + (uint32_t)key) - base);
+  };
+  if (n == 1) {
+    if (lane == 0) dst[0] = slot_of(__ldg(gk));
+    return;
+  }
+  // depth range -> bucket shift
+  uint32_t zmin = 0xffffffffu, zmax = 0u;
+  for (int e = lane; e < n; e += 32) {
+    const uint32_t z = hi32(__ldg(gk + e));
+    zmin = min(zmin, z);
+    zmax = max(zmax, z);
+  }
+  zmin = __reduce_min_sync(FULL, zmin);
+  zmax = __reduce_max_sync(FULL, zmax);
+  const uint32_t span = zmax - zmin;
+  const int hb = span ? 31 - __clz(span) : -1;
+  const int lo = hb >= kWarpBits ? hb - kWarpBits + 1 : 0;
+  // histogram
+  constexpr int PER = kWarpBins / 32;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) sm.bins[lane * PER + k] = 0u;
+  __syncwarp();
+  for (int e = lane; e < n; e += 32) atomicAdd(&sm.bins[(hi32(__ldg(gk + e)) - zmin) >> lo], 1u);
+  __syncwarp();
+  // exclusive scan (PER consecutive buckets per lane)
+  uint32_t v[PER], sum = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) { v[k] = sm.bins[lane * PER + k]; sum += v[k]; }
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += y;
+  }
+  uint32_t run = inc - sum;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) { sm.bins[lane * PER + k] = run; run += v[k]; }
+  __syncwarp();
+  // scatter into the buckets (cursors advance: afterwards bins[b] = end of bucket b)
+  for (int e = lane; e < n; e += 32) {
+    const uint64_t key = __ldg(gk + e);
+    sm.buf[atomicAdd(&sm.bins[(hi32(key) - zmin) >> lo], 1u)] = key;
+  }
+  __syncwarp();
+  // rank inside the bucket: (bits(z), id); ids gathered for equal depths only
+  bool long_run = false;
+  for (int p = lane; p < n; p += 32) {
+    const uint64_t key = sm.buf[p];
+    const uint32_t z = hi32(key);
+    const uint32_t b = (z - zmin) >> lo;
+    const int s0 = b ? (int)sm.bins[b - 1] : 0, s1 = (int)sm.bins[b];
+    int rank = 0, eq = 0;
+    for (int q = s0; q < s1; ++q) {
+      const uint64_t kq = sm.buf[q];
+      rank += kq < key;
+      eq += hi32(kq) == z;
+    }
+    if (kid && eq > 1) {   // equal depths: order by creation id instead of slot
+      if (eq > kShortRun + 1) {
+        long_run = true;
+      } else {
+        const int idp = __ldg(&kid[(uint32_t)key].x);
+        rank = 0;
+        for (int q = s0; q < s1; ++q) {
+          const uint64_t kq = sm.buf[q];
+          const uint32_t zq = hi32(kq);
+          rank += zq < z || (zq == z && q != p && __ldg(&kid[(uint32_t)kq].x) < idp);
+        }
+      }
+    }
+    dst[s0 + rank] = slot_of(key);
+  }
+  if (__any_sync(FULL, long_run)) {   // long equal-depth runs: re-key by id, re-rank by (z, id)
+    __syncwarp();
+    for (int p = lane; p < n; p += 32) {
+      const uint64_t k = sm.buf[p];
+      sm.buf[p] = (k & 0xffffffff00000000ull) | (uint32_t)__ldg(&kid[(uint32_t)k].x);
+    }
+    __syncwarp();
+    for (int p = lane; p < n; p += 32) {
+      const uint64_t key = sm.buf[p];
+      const uint32_t b = (hi32(key) - zmin) >> lo;
+      const int s0 = b ? (int)sm.bins[b - 1] : 0, s1 = (int)sm.bins[b];
+      int rank = 0;
+      for (int q = s0; q < s1; ++q) rank += sm.buf[q] < key;
+      dst[s0 + rank] = (uint32_t)(__ldg(a.inv + (uint32_t)key) - base);
+    }
   }
 }
 
@@ -356,26 +494,49 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
       if (lane == 0 && v) atomicAdd(a.stat_pairs, v);
+      // terminated pixels (R13 stop reached: the centre was moved to kFar)
+      const unsigned nt = __reduce_add_sync(FULL, (unsigned)(in0 && pyc0 == kFar) + (unsigned)(in1 && pyc1 == kFar));
+      if (lane == 0 && nt) atomicAdd(a.stat_pairs + 1, (unsigned long long)nt);
     }
   }
 }
 
-template <int CAP>
+template <int CAP, bool LONG = false>
 static void launch_k4a_variant(const CompositeArgs& a, unsigned grid, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k4a_sort<CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K4aShared<CAP>));
+    cudaFuncSetAttribute(k4a_sort<CAP, LONG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K4aShared<CAP>));
     attr = true;
   }
-  k4a_sort<CAP><<<grid, kSortThreadsA, sizeof(K4aShared<CAP>), s>>>(a);
+  k4a_sort<CAP, LONG><<<grid, kSortThreadsA, sizeof(K4aShared<CAP>), s>>>(a);
+}
+
+static bool warp_k4a_on() {   // GSB_K4A=cta: one CTA per list for every list (A/B comparisons)
+  const char* e = getenv("GSB_K4A");
+  return !(e && e[0] == 'c');
 }
 
 void launch_k4a_sort(const CompositeArgs& a, bool long_lists, cudaStream_t s) {
   const int nf = a.fe - a.fs;
   if (nf <= 0) return;
   const unsigned grid = (unsigned)nf * a.n_tiles;
-  if (long_lists) launch_k4a_variant<4 * kFusedSortCap>(a, grid, s);
-  else launch_k4a_variant<kFusedSortCap>(a, grid, s);
+  if (long_lists) {
+    launch_k4a_variant<4 * kFusedSortCap>(a, grid, s);
+  } else if (a.long_list && !a.bg_off && warp_k4a_on()) {
+    // short lists one warp each; the chunk's long lists (K2a's list) one CTA each
+    const int n_lists = (int)grid;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k4a_warp_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(kK4aWarps * sizeof(K4aWarpShared)));
+      attr = true;
+    }
+    k4a_warp_sort<<<(n_lists + kK4aWarps - 1) / kK4aWarps, kK4aWarps * 32, kK4aWarps * sizeof(K4aWarpShared), s>>>(
+        a, n_lists);
+    if (a.n_long > 0) launch_k4a_variant<kFusedSortCap, true>(a, a.n_long, s);
+  } else {
+    launch_k4a_variant<kFusedSortCap>(a, grid, s);
+  }
 }
 
 void launch_k4b_blend(const CompositeArgs& a, int* counter, cudaStream_t s) {

@@ -27,38 +27,7 @@ THR = np.log2(1.0 / 255.0)
 f32 = np.float32
 
 
-def fma32(a, b, c):
-    return (a.astype(np.float64) * b.astype(np.float64) + c.astype(np.float64)).astype(np.float32)
-
-
-def pairs_near_threshold(proj, ids, W, H, win):
-    """(gaussian index, px, py) of pixel centres inside the R8 box of each id (vectorised)."""
-    u, v = proj[ids, oracle.F_U], proj[ids, oracle.F_V]
-    rx = np.sqrt(proj[ids, oracle.F_KAPPA] * proj[ids, oracle.F_SXX])
-    ry = np.sqrt(proj[ids, oracle.F_KAPPA] * proj[ids, oracle.F_SYY])
-    x0 = np.clip(np.ceil(u - rx - 0.5), 0, W - 1).astype(np.int64)
-    x1 = np.clip(np.floor(u + rx - 0.5), 0, W - 1).astype(np.int64)
-    y0 = np.clip(np.ceil(v - ry - 0.5), 0, H - 1).astype(np.int64)
-    y1 = np.clip(np.floor(v + ry - 0.5), 0, H - 1).astype(np.int64)
-    nx, ny = np.maximum(x1 - x0 + 1, 0), np.maximum(y1 - y0 + 1, 0)
-    out_g, out_x, out_y = [], [], []
-    cnt = nx * ny
-    sel = cnt > 0
-    ids, x0, y0, nx, cnt = ids[sel], x0[sel], y0[sel], nx[sel], cnt[sel]
-    for lo in range(0, ids.size, 20000):
-        sl = slice(lo, lo + 20000)
-        c = cnt[sl]
-        g = np.repeat(ids[sl], c)
-        k = np.arange(c.sum()) - np.repeat(np.cumsum(c) - c, c)
-        px = np.repeat(x0[sl], c) + k % np.repeat(nx[sl], c)
-        py = np.repeat(y0[sl], c) + k // np.repeat(nx[sl], c)
-        dx = proj[g, oracle.F_U] - (px + 0.5)
-        dy = proj[g, oracle.F_V] - (py + 0.5)
-        power = -0.5 * (proj[g, oracle.F_A] * dx * dx + proj[g, oracle.F_C] * dy * dy) - proj[g, oracle.F_B] * dx * dy
-        arg = np.log2(proj[g, oracle.F_O]) + power * LOG2E
-        keep = np.abs(arg - THR) < win
-        out_g.append(g[keep]); out_x.append(px[keep]); out_y.append(py[keep])
-    return np.concatenate(out_g), np.concatenate(out_x), np.concatenate(out_y)
+pairs_near_threshold = gu.pairs_near_threshold
 
 
 def measure(name, max_frames=4, win=0.05):
@@ -88,13 +57,7 @@ def measure(name, max_frames=4, win=0.05):
             arg_o = np.log2(proj[gi, oracle.F_O]) + power * LOG2E
             # GPU arithmetic in binary32 on the GPU's record
             u, v, p, q, rr, l2o = (r[:, k].astype(f32) for k in (0, 1, 12, 13, 14, 15))
-            pxc, pyc = (px + 0.5).astype(f32), (py + 0.5).astype(f32)
-            dx = (u - pxc).astype(f32)
-            t1 = (p * dx).astype(f32)
-            mm = fma32(-t1, t1, l2o)
-            qdx = (q * dx).astype(f32)
-            ta = fma32(rr, (v - pyc).astype(f32), qdx)
-            arg_g = fma32(-ta, ta, mm)
+            arg_g = gu.k4_arg_f32(r, px, py)
             # the same on the record in fp64 (record error only)
             dxr = u.astype(np.float64) - (px + 0.5)
             dyr = v.astype(np.float64) - (py + 0.5)

@@ -101,7 +101,7 @@ def test_render_params_layout_matches_header(tmp_path):
     """ctypes structs == the C compiler's layout of include/gsb.h (sizes and every offset)."""
     import subprocess
     structs = {"gsb_render_params": gsb.gsb_render_params, "gsb_timings": gsb.gsb_timings,
-               "gsb_obs_params": gsb.gsb_obs_params}
+               "gsb_obs_params": gsb.gsb_obs_params, "gsb_stats": gsb.gsb_stats}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "gsb.h"', "int main(void) {"]
     for name, cls in structs.items():
         lines.append(f'printf("{name} %zu\\n", sizeof({name}));')

@@ -17,7 +17,7 @@ from tests.helpers import scene_from
 
 pytestmark = pytest.mark.gpu
 
-MASK_CAP = 0.02
+MASK_CAP = oracle.MASK_CAP
 
 
 def _sensors(cfg, env_ids, with_body=True):

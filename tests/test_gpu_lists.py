@@ -2,8 +2,8 @@
 offsets and id lists given the oracle's fp32 projected values"; readings R9, R10).
 
 gsb_debug_tile_lists runs K2b emission and the sort that really feeds compositing in gsb_render
-— K4a's one-pass counting sort (<= 1024 keys in shared memory), its packed radix variant
-(<= 4096), the HBM radix beyond either, and the fused K4's in-CTA sorts — with keys carrying the
+— K4a's warp-per-list counting sort (<= 1024 keys), its CTA-per-list counting sort and packed
+radix variant (<= 4096), the HBM radix beyond either, and the fused K4's in-CTA sorts — with keys carrying the
 record slot (the render's default: equal-depth runs re-ordered by creation id) or the id.  The
 inputs are the oracle's projections rounded to fp32, laid out in a random internal (slot)
 order, so every depth tie must be broken through the slot -> id map.  Every (frame, tile) list
@@ -21,7 +21,8 @@ from tests import gpu_util as gu
 
 pytestmark = pytest.mark.gpu
 
-VARIANTS = {1: "K4a count", 2: "K4a packed", 3: "fused K4 small", 4: "fused K4 packed"}
+VARIANTS = {1: "K4a warp + long CTA", 2: "K4a packed", 3: "fused K4 small", 4: "fused K4 packed",
+            5: "K4a CTA count"}
 
 
 def _oracle_fp32(sc, b, cfg, frames):
@@ -73,40 +74,44 @@ def test_production_tile_lists_small_configs(name):
     sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
     frames = [(e, c) for e in range(cfg.n_envs) for c in range(cfg.n_cams)]
     arr, zb, va = _oracle_fp32(sc, b, cfg, frames)
-    _check(arr, zb, va, cfg.width, cfg.height, variants=(0, 1, 2, 3, 4), seed=len(name))
+    _check(arr, zb, va, cfg.width, cfg.height, variants=(0, 1, 2, 3, 4, 5), seed=len(name))
 
 
-def test_production_tile_lists_ties_and_oversize_lists():
-    """> 4096 keys in one tile (the HBM radix of every variant) and many exactly equal depths
-    (equal-depth runs longer than 32, the re-keyed fallback, and short runs fixed in place)."""
+@pytest.mark.parametrize("size", [32, 160])
+def test_production_tile_lists_ties_and_oversize_lists(size):
+    """32x32: > 4096 keys in one tile (the HBM radix of every variant); 160x160: ~100-300-key lists
+    (K4a's warp path) — both with many exactly equal depths (equal-depth runs longer than 32, the
+    re-keyed fallback, and short runs fixed in place)."""
     rng = np.random.default_rng(3)
-    F, N, W, H = 2, 9000, 32, 32
-    arr = {"u": rng.uniform(2, 30, (F, N)), "v": rng.uniform(2, 30, (F, N)), "sxx": rng.uniform(0.5, 3, (F, N)),
+    F, N, W, H = 2, 9000, size, size
+    arr = {"u": rng.uniform(2, W - 2, (F, N)), "v": rng.uniform(2, H - 2, (F, N)), "sxx": rng.uniform(0.5, 3, (F, N)),
            "syy": rng.uniform(0.5, 3, (F, N)), "kappa": rng.uniform(0.5, 8, (F, N))}
     arr = {k: x.astype(np.float32) for k, x in arr.items()}
-    arr["u"][:, ::4] = rng.uniform(4, 12, (F, (N + 3) // 4))   # one tile with > 4096 keys
-    arr["v"][:, ::4] = rng.uniform(4, 12, (F, (N + 3) // 4))
+    if size == 32:   # one tile with > 4096 keys
+        arr["u"][:, ::4] = rng.uniform(4, 12, (F, (N + 3) // 4))
+        arr["v"][:, ::4] = rng.uniform(4, 12, (F, (N + 3) // 4))
     z = rng.choice(np.float32([1.0, 1.5, 2.0, 2.25]), (F, N)).astype(np.float32)
     z[:, ::3] = rng.uniform(0.5, 5, (F, (N + 2) // 3)).astype(np.float32)
     z[:, 1::7] = np.float32(3.0) + np.float32(2 ** -20) * rng.integers(0, 3, (F, len(range(1, N, 7))))
     zb = z.view(np.uint32)
     va = (rng.random((F, N)) < 0.95).astype(np.uint8)
-    offs = _check(arr, zb, va, W, H, variants=(1, 2, 3, 4), seed=5)
-    assert np.diff(offs[0]).max() > 4096
+    offs = _check(arr, zb, va, W, H, variants=(1, 2, 3, 4, 5), seed=5)
+    L = np.diff(offs, axis=1)
+    assert (L.max() > 4096) if size == 32 else (L.max() <= 1024 and L.mean() > 100)
 
 
 @pytest.mark.slow
 @pytest.mark.parametrize("name,auto", [("C3", 1), ("C4", 2)])
 def test_production_tile_lists_full_size(name, auto):
     """Every tile of frames {0, B/2, B-1} (all cameras) at full size: the variant gsb_render picks
-    for the config (C3: K4a counting sort with HBM radix for the > 1024-key lists; C4: K4a packed)
-    and the other K4a variant, with slot keys and id keys."""
+    for the config (C3: K4a warp sort, a CTA with the HBM radix for each > 1024-key list; C4: K4a
+    packed) and the other K4a variants, with slot keys and id keys."""
     cfg = synth.CONFIGS[name]
     sc = synth.make_scene(cfg)
     envs = [0, cfg.n_envs // 2, cfg.n_envs - 1]
     b = synth.make_batch(cfg, envs)
     frames = [(k, c) for k in range(len(envs)) for c in range(cfg.n_cams)]
     arr, zb, va = _oracle_fp32(sc, b, cfg, frames)
-    offs = _check(arr, zb, va, cfg.width, cfg.height, variants=(0, 1, 2), seed=11, expect_auto=auto)
+    offs = _check(arr, zb, va, cfg.width, cfg.height, variants=(0, 1, 2, 5), seed=11, expect_auto=auto)
     L = np.diff(offs, axis=1)
     print(name, "keys", int(L.sum()), "longest list", int(L.max()), "lists > 1024:", int((L > 1024).sum()))

@@ -704,3 +704,55 @@ def test_pin8b_near_far_cull_boundary():
     for i, kept in enumerate([False, True, True, False]):
         u = int(np.floor(r.proj[i, oracle.F_U])); v = int(np.floor(r.proj[i, oracle.F_V]))
         assert (r.alpha[v, u] > 0.5) == kept, i
+
+
+# ---------------------------------------------------------------- reading R28 (error bound)
+def test_r28_position_bound_covers_a_binary32_projection():
+    """Reading R28's position term: F_EU / F_EV bound |u_f32 - u| and |v_f32 - v| for a binary32
+    evaluation of the projection chain (x, y, z by the R11-style fma chain of the pose and
+    camera rows — mini.depth_key_f32 applied to each camera row — then u = fma(f, x * rn(1/z), c)),
+    over random bodies, poses, DR cameras and means spanning a room-sized scene; and the bound
+    is not vacuous (within 8x of the worst observed error)."""
+    rng = np.random.default_rng(28)
+    worst = 0.0
+    for trial in range(60):
+        W = np.zeros((3, 4), np.float32)
+        q = rng.normal(size=4)
+        q /= np.linalg.norm(q)
+        W[:, :3] = synth._quat_to_mat(q)
+        W[:, 3] = rng.normal(0, 2, 3)
+        n = 400
+        body = rng.integers(-1, 3, n)
+        sc = scene_from(rng.uniform(-3, 3, (n, 3)), 0.02, body=body, n_bodies=3)
+        pose = random_pose(rng, 3)
+        pose[:, :3] *= 10
+        K = np.float32([rng.uniform(50, 600), rng.uniform(50, 600), 320, 240])
+        proj, zb, valid = oracle.project(sc, pose, K, W, oracle.RenderParams(640, 480, near=0.05))
+        for i in np.nonzero(valid)[0]:
+            p = None if body[i] < 0 else pose[body[i]]
+            rows = [mini.depth_key_f32(W[[1, 2, r]], p, sc.means[i][None])[0] for r in (0, 1)]
+            z32 = zb[i:i + 1].view(np.float32)[0]
+            iz = np.float32(1.0 / np.float64(z32))
+            u32 = mini.fma32(K[0], np.float32(rows[0] * iz), K[2])
+            v32 = mini.fma32(K[1], np.float32(rows[1] * iz), K[3])
+            for val, f, fe in ((u32, oracle.F_U, oracle.F_EU), (v32, oracle.F_V, oracle.F_EV)):
+                err = abs(float(val) - proj[i, f])
+                assert err <= proj[i, fe], (trial, i, err, proj[i, fe])
+                worst = max(worst, err / proj[i, fe])
+    assert worst >= 1.0 / 8.0, worst
+
+
+def test_r28_mask_monotone_in_the_bound_and_empty_without_it():
+    """margin_scale = 0 disables the mask (no pixel masked, no termination test flagged); the
+    masked set only grows with the bound; unmasked pixels are identical (the bound never
+    changes what is composited)."""
+    cfg = synth.CONFIGS["T1"]
+    sc, b = synth.make_scene(cfg), synth.make_batch(cfg, [0])
+    prm = oracle.RenderParams(cfg.width, cfg.height)
+    fr = [oracle.render_frame(sc, b.poses[0], b.intrinsics[0, 0], b.w2c[0, 0], prm, margin_scale=k)
+          for k in (0.0, 1.0, 30.0)]
+    assert not fr[0].masked.any() and not fr[0].term_near.any() and not fr[0].eT.any()
+    assert np.all(fr[1].masked <= fr[2].masked) and np.all(fr[1].term_near <= fr[2].term_near)
+    assert fr[2].masked.sum() > fr[1].masked.sum() > 0
+    for f in fr[1:]:
+        assert np.array_equal(f.rgb, fr[0].rgb) and np.array_equal(f.alpha, fr[0].alpha)
