@@ -48,7 +48,10 @@ MASK_CAP = 1e-2
 
 
 def build_oracle(force: bool = False) -> str:
-    """Compile liboracle.so: plain C, -O2, no fast-math, no FMA contraction (R11)."""
+    """Compile liboracle.so: plain C, -O2, no fast-math, no FMA contraction (R11).
+    GSB_ORACLE_LIB names a prebuilt variant instead (scripts/host_sanitize.py: ASan/UBSan)."""
+    if os.environ.get("GSB_ORACLE_LIB"):
+        return os.environ["GSB_ORACLE_LIB"]
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
         cmd = ["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
                "-pthread", "-o", _SO, _SRC, "-lm"]
@@ -62,8 +65,7 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        build_oracle()
-        L = ctypes.CDLL(_SO)
+        L = ctypes.CDLL(build_oracle())
         P = ctypes.c_void_p
         L.gsbo_project.restype = ctypes.c_int
         L.gsbo_project.argtypes = [P, P, P, P, P, ctypes.c_int, ctypes.c_int, P, ctypes.c_int64, P,

@@ -153,6 +153,34 @@ def _hptr(a) -> Optional[int]:
     return a.data_ptr()
 
 
+_DT = {"f32": ("float32", np.float32), "i32": ("int32", np.int32), "u8": ("uint8", np.uint8),
+       "f16": ("float16", np.float16)}
+
+
+def _buf(t, kind: str, n: int, name: str, device: Optional[int]):
+    """Validate a buffer before its pointer crosses the C ABI (which cannot check it): dtype,
+    contiguity, at least n elements, and on the scene's CUDA device (device = index) or on the host
+    (device = None).  Raises ValueError; None passes (nullable arguments)."""
+    if t is None:
+        return
+    tname, npt = _DT[kind]
+    if isinstance(t, np.ndarray):
+        if device is not None:
+            raise ValueError(f"{name}: expected a CUDA tensor on device {device}, got a numpy array")
+        ok_dt, numel = t.dtype == npt, t.size
+    else:
+        import torch
+        if device is not None and (not t.is_cuda or (t.device.index or 0) != device):
+            raise ValueError(f"{name}: expected a tensor on cuda:{device}, got {t.device}")
+        if device is None and t.is_cuda:
+            raise ValueError(f"{name}: expected a host tensor, got {t.device}")
+        ok_dt, numel = t.dtype == getattr(torch, tname), t.numel()
+    if not ok_dt:
+        raise ValueError(f"{name}: expected {tname}, got {t.dtype}")
+    if numel < n:
+        raise ValueError(f"{name}: {numel} elements < the {n} required")
+
+
 def _stream(stream) -> Optional[int]:
     if stream is None:
         import torch
@@ -245,11 +273,39 @@ class Scene:
         _check(lib().gsb_reserve(self._h, max_envs, n_cams, width, height, chunk_frames, key_capacity,
                                  GSB_RESERVE_HOST_IO if host_io else 0))
 
+    def _check_io(self, B, C, params, poses, intrinsics, w2c, out_rgb, out_depth, out_alpha, out_n_eval, dev):
+        """Shapes the C ABI assumes, checked here (it cannot): inputs and outputs of B x C frames."""
+        F, px = B * C, params.width * params.height
+        if self.n_bodies and poses is not None:
+            _buf(poses, "f32", B * self.n_bodies * 7, "poses", dev)
+        _buf(intrinsics, "f32", F * 4, "intrinsics", dev)
+        _buf(w2c, "f32", F * 12, "world_to_cam", dev)
+        if out_rgb is None:
+            raise ValueError("out_rgb is required")
+        _buf(out_rgb, "f32", F * 3 * px, "out_rgb", dev)
+        _buf(out_depth, "f32", F * px, "out_depth", dev)
+        _buf(out_alpha, "f32", F * px, "out_alpha", dev)
+        _buf(out_n_eval, "i32", F * px, "out_n_eval", dev)
+
+    def _check_obs(self, B, C, params, poses, intrinsics, w2c, out_rgb8, out_depth, image_dr, depth_f16, dev):
+        F, px = B * C, params.width * params.height
+        if self.n_bodies and poses is not None:
+            _buf(poses, "f32", B * self.n_bodies * 7, "poses", dev)
+        _buf(intrinsics, "f32", F * 4, "intrinsics", dev)
+        _buf(w2c, "f32", F * 12, "world_to_cam", dev)
+        if out_rgb8 is None:
+            raise ValueError("out_rgb8 is required")
+        _buf(out_rgb8, "u8", F * 3 * px, "out_rgb8", dev)
+        _buf(out_depth, "f16" if depth_f16 else "f32", F * px, "out_depth", dev)
+        _buf(image_dr, "f32", F * 4, "image_dr", dev)
+
     def render(self, poses, intrinsics, world_to_cam, params: RenderParams, out_rgb, out_depth=None,
                out_alpha=None, out_n_eval=None, stream=None):
         """gsb_render on CUDA tensors: poses [B,nb,7], intrinsics [B,C,4], world_to_cam [B,C,3,4],
         out_rgb [B,C,3,H,W] (float32), out_depth/out_alpha [B,C,H,W] float32, out_n_eval int32."""
         B, C = int(intrinsics.shape[0]), int(intrinsics.shape[1])
+        self._check_io(B, C, params, poses, intrinsics, world_to_cam, out_rgb, out_depth, out_alpha, out_n_eval,
+                       self.device)
         p = params.to_c()
         _check(lib().gsb_render(self._h, _ptr(poses) if self.n_bodies else None, B, C, _ptr(intrinsics),
                                 _ptr(world_to_cam), ctypes.byref(p), _ptr(out_rgb), _ptr(out_depth),
@@ -261,6 +317,12 @@ class Scene:
         """gsb_render_rig: strided poses (element strides, in floats) and body-attached cameras:
         cam_body[c] = k >= 0 makes cam_extrinsics[:, c] the body->camera mount on body k."""
         B, C = int(intrinsics.shape[0]), int(intrinsics.shape[1])
+        body = max(int(pose_body_stride), 7)
+        env = int(pose_env_stride) or self.n_bodies * body
+        need = (B - 1) * env + (self.n_bodies - 1) * body + 7 if (B and self.n_bodies) else 0
+        self._check_io(B, C, params, None, intrinsics, cam_extrinsics, out_rgb, out_depth, out_alpha, out_n_eval,
+                       self.device)
+        _buf(poses, "f32", need, "poses", self.device)
         p = params.to_c()
         cb = None
         if cam_body is not None:
@@ -276,6 +338,8 @@ class Scene:
                     out_alpha=None, out_n_eval=None, stream=None):
         """gsb_render_host on host (pinned) buffers; synchronous."""
         B, C = int(intrinsics.shape[0]), int(intrinsics.shape[1])
+        self._check_io(B, C, params, poses, intrinsics, world_to_cam, out_rgb, out_depth, out_alpha, out_n_eval,
+                       None)
         p = params.to_c()
         _check(lib().gsb_render_host(self._h, _hptr(poses) if self.n_bodies else None, B, C,
                                      _hptr(intrinsics), _hptr(world_to_cam), ctypes.byref(p), _hptr(out_rgb),
@@ -293,6 +357,8 @@ class Scene:
                       out_n_eval=None, stream=None):
         """gsb_render_static: B envs x the pre-binned cameras; out_rgb [B,C,3,H,W]."""
         B = int(out_rgb.shape[0])
+        C = int(out_rgb.shape[1]) if out_rgb.dim() == 5 else 1
+        self._check_io(B, C, params, poses, None, None, out_rgb, out_depth, out_alpha, out_n_eval, self.device)
         p = params.to_c()
         _check(lib().gsb_render_static(self._h, _ptr(poses) if self.n_bodies else None, B, ctypes.byref(p),
                                        _ptr(out_rgb), _ptr(out_depth), _ptr(out_alpha), _ptr(out_n_eval),
@@ -312,6 +378,8 @@ class Scene:
         """gsb_render_obs: uint8 RGB [B,C,3,H,W] (+ depth [B,C,H,W] as float16 or float32) with the
         reading-R31 image DR (image_dr [B,C,4] CUDA float32: gain, contrast, brightness, noise_std)."""
         B, C = int(intrinsics.shape[0]), int(intrinsics.shape[1])
+        self._check_obs(B, C, params, poses, intrinsics, world_to_cam, out_rgb8, out_depth, image_dr, depth_f16,
+                        self.device)
         p = params.to_c()
         o = self._obs(image_dr, seed, step, env_offset, depth_f16, False)
         _check(lib().gsb_render_obs(self._h, _ptr(poses) if self.n_bodies else None, B, C, _ptr(intrinsics),
@@ -323,6 +391,8 @@ class Scene:
                         stream=None):
         """gsb_render_obs_host on host (pinned) buffers; synchronous."""
         B, C = int(intrinsics.shape[0]), int(intrinsics.shape[1])
+        self._check_obs(B, C, params, poses, intrinsics, world_to_cam, out_rgb8, out_depth, image_dr, depth_f16,
+                        None)
         p = params.to_c()
         o = self._obs(image_dr, seed, step, env_offset, depth_f16, True)
         _check(lib().gsb_render_obs_host(self._h, _hptr(poses) if self.n_bodies else None, B, C,

@@ -105,25 +105,64 @@ __device__ __forceinline__ int warp_compact_slot(bool take, int* counter) {
 }
 
 // Add 1 to counter[t] for every tile t of this lane's rect (when `has`), aggregated over the
-// warp: lanes whose r-th tile coincides share one atomic (__match_any_sync).  Rects with more
-// than kBigRect tiles are walked by the whole warp cooperatively afterwards.  All 32 lanes of
-// the warp must call this.
+// warp.  The warp's rects are Morton-coherent, so their union box is usually small: when it holds
+// at most 32 tiles, each lane counts its tiles into the warp's 32-entry shared scratch (shared
+// atomics) and lane j then adds the count of box tile j with one global RED — all of the warp's
+// distinct tiles in one instruction.  Otherwise lanes whose r-th tile coincides share one atomic
+// per round (__match_any_sync).  Rects with more than kBigRect tiles are walked by the whole warp
+// cooperatively afterwards.  All 32 lanes of the warp must call this; `scratch` = 32 words of
+// shared memory private to the warp (or nullptr: rounds only).
 constexpr int kBigRect = 8;
+#ifndef GSB_UNION_BOX
+#define GSB_UNION_BOX 1   // 0: match_any rounds only (A/B comparisons)
+#endif
 
-__device__ __forceinline__ void warp_tile_count(bool has, uint32_t rect, int tiles_x, int* counter) {
+struct UnionBox {
+  int x0, y0, w, n;   // origin, width and tile count of the warp's union box (n = 0: empty)
+};
+
+__device__ __forceinline__ UnionBox warp_union_box(bool part, int tx0, int tx1, int ty0, int ty1) {
+  const unsigned FULL = 0xffffffffu;
+  UnionBox b;
+  const unsigned x0 = __reduce_min_sync(FULL, part ? (unsigned)tx0 : 0xffffu);
+  const unsigned y0 = __reduce_min_sync(FULL, part ? (unsigned)ty0 : 0xffffu);
+  const unsigned x1 = __reduce_max_sync(FULL, part ? (unsigned)tx1 : 0u);
+  const unsigned y1 = __reduce_max_sync(FULL, part ? (unsigned)ty1 : 0u);
+  b.x0 = (int)x0; b.y0 = (int)y0;
+  b.w = (int)x1 - (int)x0 + 1;
+  b.n = x0 == 0xffffu ? 0 : b.w * ((int)y1 - (int)y0 + 1);
+  return b;
+}
+
+__device__ __forceinline__ void warp_tile_count(bool has, uint32_t rect, int tiles_x, int* counter,
+                                                uint32_t* scratch = nullptr) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int tx0 = rect & 0xff, tx1 = (rect >> 8) & 0xff, ty0 = (rect >> 16) & 0xff, ty1 = rect >> 24;
   const int nt = has ? (tx1 - tx0 + 1) * (ty1 - ty0 + 1) : 0;
   const bool big = nt > kBigRect;
-  const int rounds = __reduce_max_sync(FULL, big ? 0 : nt);
-  int tx = tx0, ty = ty0;  // this lane's r-th tile, stepped row-major (no division)
-  for (int r = 0; r < rounds; ++r) {
-    const bool act = !big && r < nt;
-    const int t = act ? ty * tiles_x + tx : -1 - lane;
-    const unsigned peers = __match_any_sync(FULL, t);
-    if (act && lane == __ffs(peers) - 1) atomicAdd(counter + t, __popc(peers));
-    if (++tx > tx1) { tx = tx0; ++ty; }
+  const bool part = nt > 0 && !big;
+  const UnionBox ub = (GSB_UNION_BOX && scratch) ? warp_union_box(part, tx0, tx1, ty0, ty1) : UnionBox{0, 0, 0, 64};
+  if (ub.n > 0 && ub.n <= 32) {
+    scratch[lane] = 0u;
+    __syncwarp();
+    if (part)
+      for (int y = ty0; y <= ty1; ++y)
+        for (int x = tx0; x <= tx1; ++x) atomicAdd(&scratch[(y - ub.y0) * ub.w + (x - ub.x0)], 1u);
+    __syncwarp();
+    const uint32_t c = scratch[lane];
+    if (lane < ub.n && c) atomicAdd(counter + (ub.y0 + lane / ub.w) * tiles_x + ub.x0 + lane % ub.w, (int)c);
+    __syncwarp();   // scratch free for the caller's next use
+  } else if (ub.n > 0) {
+    const int rounds = __reduce_max_sync(FULL, part ? nt : 0);
+    int tx = tx0, ty = ty0;  // this lane's r-th tile, stepped row-major (no division)
+    for (int r = 0; r < rounds; ++r) {
+      const bool act = part && r < nt;
+      const int t = act ? ty * tiles_x + tx : -1 - lane;
+      const unsigned peers = __match_any_sync(FULL, t);
+      if (act && lane == __ffs(peers) - 1) atomicAdd(counter + t, __popc(peers));
+      if (++tx > tx1) { tx = tx0; ++ty; }
+    }
   }
   unsigned bm = __ballot_sync(FULL, big);
   while (bm) {
@@ -131,10 +170,8 @@ __device__ __forceinline__ void warp_tile_count(bool has, uint32_t rect, int til
     bm &= bm - 1;
     const uint32_t rj = __shfl_sync(FULL, rect, j);
     const int jx0 = rj & 0xff, jx1 = (rj >> 8) & 0xff, jy0 = (rj >> 16) & 0xff, jy1 = rj >> 24;
-    const int jw = jx1 - jx0 + 1;
     for (int y = jy0; y <= jy1; ++y)
       for (int x = jx0 + lane; x <= jx1; x += 32) atomicAdd(counter + y * tiles_x + x, 1);
-    (void)jw;
   }
 }
 

@@ -7,11 +7,34 @@
 
 namespace gsb {
 
-constexpr int kFusedSortCap = 1024;
-constexpr int kWarpSortCap = kFusedSortCap;  // K4a: lists up to this length are sorted by one warp  // tile lists up to this length are sorted in K4 smem (8 CTAs/SM);
+constexpr int kFusedSortCap = 1024;  // tile lists up to this length are sorted in K4 smem (8 CTAs/SM);
                                      // chunks with many longer lists use a 4x variant
+#ifndef GSB_WARP_SORT_CAP
+#define GSB_WARP_SORT_CAP 512
+#endif
+constexpr int kWarpSortCap = GSB_WARP_SORT_CAP;  // K4a: lists up to this length are sorted by one warp
+                                                 // each; K2a lists the longer ones (long_list) for a CTA each
 
 constexpr int kDbgRecFloats = 16;   // gsb_debug_project record (include/gsb.h)
+
+// Kernel attributes and launch geometry are per DEVICE: caches keyed by the current device.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+// cudaFuncSetAttribute(max dynamic smem) once per (kernel, device); `done` is the caller's
+// static [kMaxDevices] table.  Returns the CUDA error (also left for cudaGetLastError, so the
+// caller's launch check reports it); the caller skips its launch on failure.
+template <typename Kernel>
+inline cudaError_t ensure_smem_attr(Kernel* fn, int bytes, int* done) {
+  const int dev = current_device();
+  if (dev >= 0 && dev < kMaxDevices && done[dev] == bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && dev >= 0 && dev < kMaxDevices) done[dev] = bytes;
+  return e;
+}
 
 struct K1Args {
   // template (K5: shared read-only buffer, one copy for every env)

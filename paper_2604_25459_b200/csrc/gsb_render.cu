@@ -76,7 +76,7 @@ struct Pipeline {
     tm.end();
     tm.begin(KC_SCAN, sp);
     launch_k2_scan(s->hist[sl], s->off[sl], s->hist_stride, nf, n_tiles, s->frame_base[sl], s->long_list[sl],
-                   s->long_cnt[sl], kFusedSortCap, s->vcount[sl], s->d_rb[sl], sp);
+                   s->long_cnt[sl], kWarpSortCap, s->vcount[sl], s->d_rb[sl], sp);
     s->launches += 2;
     LAUNCH_CHECK();
     tm.end();

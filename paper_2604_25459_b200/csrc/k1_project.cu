@@ -165,6 +165,7 @@ __device__ __forceinline__ float sqrt_approx(float x) { return x * rsqrtf(x); }
 
 template <int D, bool DEBUG>
 __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
+  __shared__ uint32_t tile_scratch[4][32];   // warp_tile_count's per-warp union-box counts
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool in = i < a.n;
   float4 mean = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
       r[2] = make_float4(rgb.x, rgb.y, rgb.z, z);
       a.emit[(size_t)fl * a.n + i] = make_uint2(__float_as_uint(z), rect);
     }
-    warp_tile_count(vis, rect, a.tiles_x, a.hist + (size_t)fl * a.hist_stride);
+    warp_tile_count(vis, rect, a.tiles_x, a.hist + (size_t)fl * a.hist_stride, tile_scratch[threadIdx.x >> 5]);
   }
 }
 

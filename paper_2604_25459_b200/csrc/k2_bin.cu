@@ -112,6 +112,7 @@ void launch_k2_scan(int* hist, uint32_t* off, int64_t hist_stride, int n_frames,
 // template is Morton-ordered, so a warp's Gaussians overlap the same tiles); rects with more
 // than kBigRect tiles are emitted by the whole warp cooperatively.
 __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
+  __shared__ uint32_t tile_scratch[8][32];   // per-warp union-box counts
   const unsigned FULL = 0xffffffffu;
   const int fl = a.fs + blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -134,10 +135,43 @@ __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
   const int tx0 = rect & 0xff, tx1 = (rect >> 8) & 0xff, ty0 = (rect >> 16) & 0xff, ty1 = rect >> 24;
   const int nt = has ? (tx1 - tx0 + 1) * (ty1 - ty0 + 1) : 0;
   const bool big = nt > kBigRect;
-  const int rounds = __reduce_max_sync(FULL, big ? 0 : nt);
+  const bool part = nt > 0 && !big;
+  // union box of the warp's rects <= 32 tiles (the usual case): every key's rank inside its
+  // (warp, tile) group from a shared atomic, then ONE returning global atomic per distinct tile,
+  // all issued by one instruction (lane j: box tile j) — no serial rounds of atomic latency
+  const UnionBox ub = GSB_UNION_BOX ? warp_union_box(part, tx0, tx1, ty0, ty1) : UnionBox{0, 0, 0, 64};
+  const int rounds = __reduce_max_sync(FULL, part ? nt : 0);
+  if (ub.n > 0 && ub.n <= 32) {
+    uint32_t* sc = tile_scratch[threadIdx.x >> 5];
+    sc[lane] = 0u;
+    __syncwarp();
+    uint32_t rk[kBigRect];
+    int tx = tx0, ty = ty0;
+#pragma unroll
+    for (int r = 0; r < kBigRect; ++r) {
+      if (r < nt && part) {
+        rk[r] = atomicAdd(&sc[(ty - ub.y0) * ub.w + (tx - ub.x0)], 1u);
+        if (++tx > tx1) { tx = tx0; ++ty; }
+      }
+    }
+    __syncwarp();
+    const uint32_t c = sc[lane];
+    uint32_t base = 0u;
+    if (lane < ub.n && c) base = (uint32_t)atomicAdd(cur + (ub.y0 + lane / ub.w) * a.tiles_x + ub.x0 + lane % ub.w, (int)c);
+    tx = tx0; ty = ty0;
+#pragma unroll
+    for (int r = 0; r < kBigRect; ++r) {
+      if (r < rounds) {
+        const int j = (ty - ub.y0) * ub.w + (tx - ub.x0);
+        const uint32_t b = __shfl_sync(FULL, base, part && r < nt ? j : 0);
+        if (part && r < nt) keys[off[ty * a.tiles_x + tx] + b + rk[r]] = key;
+        if (++tx > tx1) { tx = tx0; ++ty; }
+      }
+    }
+  }
   int tx = tx0, ty = ty0;  // this lane's r-th tile, stepped row-major (no division)
-  for (int r = 0; r < rounds; ++r) {
-    const bool act = !big && r < nt;
+  for (int r = 0; r < (ub.n > 32 ? rounds : 0); ++r) {
+    const bool act = part && r < nt;
     const int t = act ? ty * a.tiles_x + tx : -1 - lane;
     const unsigned peers = __match_any_sync(FULL, t);
     const int leader = __ffs(peers) - 1;
@@ -179,6 +213,7 @@ __global__ void __launch_bounds__(128) k1_external(const float* __restrict__ u, 
                                                    uint2* __restrict__ emit, uint32_t* __restrict__ vis_bits,
                                                    int64_t vis_words, int* __restrict__ vcount,
                                                    int* __restrict__ hist, int64_t hist_stride) {
+  __shared__ uint32_t tile_scratch[4][32];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool in = i < n;
   for (int fl = 0; fl < n_frames; ++fl) {
@@ -194,7 +229,7 @@ __global__ void __launch_bounds__(128) k1_external(const float* __restrict__ u, 
     }
     const uint32_t rect = pack_rect(tx0, tx1, ty0, ty1);
     if (vis) emit[(size_t)fl * n + i] = make_uint2(zbits[o], rect);
-    warp_tile_count(vis, rect, tiles_x, hist + (size_t)fl * hist_stride);
+    warp_tile_count(vis, rect, tiles_x, hist + (size_t)fl * hist_stride, tile_scratch[threadIdx.x >> 5]);
   }
 }
 

@@ -89,11 +89,8 @@ void launch_k3_sort(const ChunkArgs& a, uint32_t n_long, cudaStream_t s) {
   const unsigned grid = a.long_list ? n_long : (unsigned)nf * a.n_tiles;
   if (grid == 0) return;
   const size_t smem = sizeof(SortShared<kSortThreads>) + 2 * kSmemCap * sizeof(uint64_t);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k3_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  static int attr[kMaxDevices];
+  if (ensure_smem_attr(k3_sort, (int)smem, attr) != cudaSuccess) return;
   k3_sort<<<grid, kSortThreads, smem, s>>>(a);
 }
 

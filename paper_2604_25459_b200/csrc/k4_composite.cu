@@ -346,12 +346,10 @@ __global__ void __launch_bounds__(kCompThreads, MINB) k4_composite(CompositeArgs
 
 template <int CAP, int MINB, bool MERGE, bool SCORE>
 static void launch_k4_variant(const CompositeArgs& a, unsigned grid, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k4_composite<CAP, MINB, MERGE, SCORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(K4Shared<CAP, MERGE, SCORE>));
-    attr = true;
-  }
+  static int attr[kMaxDevices];
+  if (ensure_smem_attr(k4_composite<CAP, MINB, MERGE, SCORE>, (int)sizeof(K4Shared<CAP, MERGE, SCORE>), attr) !=
+      cudaSuccess)
+    return;
   k4_composite<CAP, MINB, MERGE, SCORE><<<grid, kCompThreads, sizeof(K4Shared<CAP, MERGE, SCORE>), s>>>(a);
 }
 

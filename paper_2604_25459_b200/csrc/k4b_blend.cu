@@ -223,9 +223,15 @@ __global__ void __launch_bounds__(kSortThreadsA) k4a_sort(CompositeArgs a) {
 // to its final position as a record slot.  With slot keys an equal-depth pair is ordered by the
 // creation ids ids[slot] (gathered only for ties); a list with a run of more than kShortRun equal
 // depths (e.g. a fronto-parallel plane) is re-keyed by id and re-ranked (reading R10).
-constexpr int kWarpBits = 9;
+#ifndef GSB_WARP_BITS
+#define GSB_WARP_BITS 9
+#endif
+constexpr int kWarpBits = GSB_WARP_BITS;
 constexpr int kWarpBins = 1 << kWarpBits;
-constexpr int kK4aWarps = 4;   // lists (warps) per CTA
+#ifndef GSB_K4A_WARPS
+#define GSB_K4A_WARPS 4
+#endif
+constexpr int kK4aWarps = GSB_K4A_WARPS;   // lists (warps) per CTA
 
 struct K4aWarpShared {
   uint64_t buf[kWarpSortCap];   // the list, bucketed
@@ -503,11 +509,8 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
 
 template <int CAP, bool LONG = false>
 static void launch_k4a_variant(const CompositeArgs& a, unsigned grid, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k4a_sort<CAP, LONG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(K4aShared<CAP>));
-    attr = true;
-  }
+  static int attr[kMaxDevices];
+  if (ensure_smem_attr(k4a_sort<CAP, LONG>, (int)sizeof(K4aShared<CAP>), attr) != cudaSuccess) return;
   k4a_sort<CAP, LONG><<<grid, kSortThreadsA, sizeof(K4aShared<CAP>), s>>>(a);
 }
 
@@ -525,12 +528,8 @@ void launch_k4a_sort(const CompositeArgs& a, bool long_lists, cudaStream_t s) {
   } else if (a.long_list && !a.bg_off && warp_k4a_on()) {
     // short lists one warp each; the chunk's long lists (K2a's list) one CTA each
     const int n_lists = (int)grid;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k4a_warp_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(kK4aWarps * sizeof(K4aWarpShared)));
-      attr = true;
-    }
+    static int attr[kMaxDevices];
+    if (ensure_smem_attr(k4a_warp_sort, (int)(kK4aWarps * sizeof(K4aWarpShared)), attr) != cudaSuccess) return;
     k4a_warp_sort<<<(n_lists + kK4aWarps - 1) / kK4aWarps, kK4aWarps * 32, kK4aWarps * sizeof(K4aWarpShared), s>>>(
         a, n_lists);
     if (a.n_long > 0) launch_k4a_variant<kFusedSortCap, true>(a, a.n_long, s);
@@ -542,10 +541,12 @@ void launch_k4a_sort(const CompositeArgs& a, bool long_lists, cudaStream_t s) {
 void launch_k4b_blend(const CompositeArgs& a, int* counter, cudaStream_t s) {
   const int nf = a.fe - a.fs;
   if (nf <= 0) return;
-  static int persistent = 0;
+  static int persistent_dev[kMaxDevices];   // persistent grid of the device (SM count x CTAs per SM)
+  const int dev = current_device();
+  int tmp = 0;
+  int& persistent = (dev >= 0 && dev < kMaxDevices) ? persistent_dev[dev] : tmp;
   if (!persistent) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
+    int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4b_blend<false>, kBlendWarps * 32, 0);
     // GSB_K4B_PER_SM=8 (one below the register limit) lets the other streams' latency-bound

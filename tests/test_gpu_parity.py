@@ -513,3 +513,50 @@ def test_equal_depth_ties_resolved_by_id(n, spread, layers, size, path, monkeypa
     ok = ~ref.masked
     assert np.abs(rgb - ref.rgb).max(-1)[ok].max() <= oracle.TOL_RGB
     assert (np.abs(out["depth"][0, 0] - ref.depth) <= oracle.TOL_DEPTH_REL * ref.depth + oracle.TOL_DEPTH_ABS)[ok].all()
+
+
+def test_binding_rejects_bad_buffers_before_the_abi():
+    """The C ABI takes raw pointers and cannot check dtype, device or size: the binding does, so
+    a wrong buffer raises ValueError instead of an out-of-bounds device write."""
+    cfg = synth.CONFIGS["T3"]
+    sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
+    g = gsb.Scene.from_synth(sc)
+    B, C, H, W = cfg.n_envs, cfg.n_cams, cfg.height, cfg.width
+    g.reserve(B, C, W, H)
+    prm = gsb.RenderParams(W, H)
+    args = (gu.to_dev(b.poses), gu.to_dev(b.intrinsics), gu.to_dev(b.w2c), prm)
+    good = torch.zeros((B, C, 3, H, W), device="cuda")
+    bad = [torch.zeros((B, C, 3, H, W), device="cuda", dtype=torch.float16),     # dtype
+           torch.zeros((B, C, 3, H, W)),                                         # host tensor
+           torch.zeros((B, C, 3, H, W - 1), device="cuda")]                      # too small
+    for t in bad:
+        with pytest.raises(ValueError):
+            g.render(*args, t)
+    with pytest.raises(ValueError):   # n_eval must be int32
+        g.render(*args, good, None, None, torch.zeros((B, C, H, W), device="cuda"))
+    with pytest.raises(ValueError):   # undersized cameras
+        g.render(gu.to_dev(b.poses), gu.to_dev(b.intrinsics[:1]).repeat(1, 1, 1)[:, :, :3].contiguous(),
+                 gu.to_dev(b.w2c), prm, good)
+    g.render(*args, good)             # the well-formed call still works
+    torch.cuda.synchronize()
+    assert torch.isfinite(good).all()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two CUDA devices in one process")
+def test_two_devices_in_one_process_bit_identical():
+    """Launch caches (kernel smem attributes, the persistent K4b grid) are per device: one process
+    driving scenes on cuda:0 and cuda:1 renders the same frames bit for bit on both."""
+    cfg = synth.CONFIGS["T2"]
+    sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
+    outs = []
+    for dev in (0, 1):
+        with torch.cuda.device(dev):
+            g = gsb.Scene.from_synth(sc, device=dev)
+            B, C, H, W = cfg.n_envs, cfg.n_cams, cfg.height, cfg.width
+            g.reserve(B, C, W, H)
+            rgb = torch.zeros((B, C, 3, H, W), device=f"cuda:{dev}")
+            g.render(torch.from_numpy(b.poses).to(f"cuda:{dev}"), torch.from_numpy(b.intrinsics).to(f"cuda:{dev}"),
+                     torch.from_numpy(b.w2c).to(f"cuda:{dev}"), gsb.RenderParams(W, H), rgb)
+            torch.cuda.synchronize(dev)
+            outs.append(rgb.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
