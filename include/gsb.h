@@ -68,6 +68,14 @@ typedef enum {
 #define GSB_FLAG_STATIC_PER_ENV 8u /* gsb_render_static only: one camera per env, env e uses
                                pre-binned camera e (per-env domain-randomised cameras that stay
                                fixed over an episode); needs n_envs <= the pre-binned count */
+#define GSB_FLAG_FIXED_PLAN 16u /* gsb_render / gsb_render_rig / gsb_render_obs: a launch sequence
+                                  that depends only on the call's shapes — no host synchronisation and
+                                  no data-dependent launch choice (split K4a + K4b compositing for
+                                  every chunk, one pass per chunk) — so the whole render can be
+                                  captured in a CUDA graph on the caller's stream.  A chunk whose tile
+                                  keys exceed the reserved key capacity sets the scene's overflow flag
+                                  (gsb_get_overflow) and its frames are left unwritten.  Not with
+                                  GSB_FLAG_STATS / GSB_FLAG_TIMING, host-buffer or static renders. */
 
 /* reserve flags */
 #define GSB_RESERVE_HOST_IO 1u /* also reserve device staging for gsb_render_host */
@@ -227,6 +235,11 @@ gsb_status gsb_render_static(gsb_scene scene, const float* body_poses, int32_t n
                              const gsb_render_params* params, float* out_rgb, float* out_depth,
                              float* out_alpha, int32_t* out_n_eval, gsb_stream stream);
 
+/* GSB_FLAG_FIXED_PLAN renders: *out = 1 if any chunk since the last call overflowed the reserved key
+ * capacity (its frames were not written; reserve a larger key_capacity), else 0; resets the flag.
+ * Synchronises with the scene's last render. */
+gsb_status gsb_get_overflow(gsb_scene scene, int32_t* out);
+
 /* Counters of the last render made with GSB_FLAG_STATS (synchronises with it). */
 gsb_status gsb_get_stats(gsb_scene scene, int64_t* visible_V, int64_t* keys_K, int64_t* pairs_P);
 
@@ -362,8 +375,10 @@ gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, 
  *                path's re-ordering of equal-depth runs
  *   variant      0 = what gsb_render picks for this batch (split if >= 200 keys per tile on
  *                average, packed sort if > 1/4 of the lists exceed 1024 keys), 1 = K4a as the
- *                render runs it for short lists (one warp per list <= 1024 keys, one CTA with the
- *                HBM radix per longer list), 2 = K4a packed (<= 4096, HBM beyond), 3 = fused K4
+ *                render runs it for short lists (one warp per list <= 512 keys, one CTA with the
+ *                index counting sort per longer list <= 4096, HBM radix beyond), 2 = K4a for views
+ *                whose lists are mostly long (one CTA per list: index counting sort <= 4096, HBM
+ *                radix beyond), 3 = fused K4
  *                small, 4 = fused K4 packed, 5 = K4a one CTA per list (counting sort <= 1024 keys
  *                in smem, HBM radix beyond; the LiDAR path's sort)
  *   key_mode     0 = keys carry the record slot (gsb_render's default), 1 = keys carry the id

@@ -21,6 +21,7 @@ GSB_FLAG_STATS = 1
 GSB_FLAG_TIMING = 2
 GSB_FLAG_SCORES = 4
 GSB_FLAG_STATIC_PER_ENV = 8
+GSB_FLAG_FIXED_PLAN = 16
 GSB_OBS_DEPTH_F16 = 1
 GSB_RESERVE_HOST_IO = 1
 
@@ -32,7 +33,7 @@ STATUS = {0: "GSB_OK", 1: "GSB_ERR_INVALID_ARGUMENT", 2: "GSB_ERR_SHAPE_MISMATCH
 EXPORTS = ["gsb_create_scene", "gsb_reserve", "gsb_render", "gsb_render_rig", "gsb_render_host",
            "gsb_prebin_static", "gsb_render_static",
            "gsb_scores_reset", "gsb_get_scores", "gsb_filter_scene", "gsb_render_obs", "gsb_render_obs_host", "gsb_get_stats",
-           "gsb_get_stats_ext",
+           "gsb_get_stats_ext", "gsb_get_overflow",
            "gsb_get_timings", "gsb_destroy_scene", "gsb_last_error", "gsb_version",
            "gsb_debug_project", "gsb_debug_bin_sort", "gsb_debug_tile_lists",
            "gsb_obs_encode", "gsb_lidar_create", "gsb_render_lidar", "gsb_lidar_info", "gsb_lidar_destroy"]
@@ -70,6 +71,17 @@ class gsb_stats(ctypes.Structure):
 _lib = None
 
 
+class _Absent:
+    """Stands in for a symbol an older libgsb build lacks (A/B runs of old builds); every export
+    of include/gsb.h is required of the current build by tests/test_abi.py."""
+    argtypes = None
+    restype = None
+
+
+def _sig(L, name):
+    return getattr(L, name) if hasattr(L, name) else _Absent()
+
+
 def lib() -> ctypes.CDLL:
     """Load libgsb.so (built by paper_2604_25459_b200/build.py).  Fails loudly if absent."""
     global _lib
@@ -79,42 +91,43 @@ def lib() -> ctypes.CDLL:
         raise ImportError(f"libgsb.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'`")
     L = ctypes.CDLL(LIB_PATH)
     P, I32, I64, U32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32
-    L.gsb_create_scene.argtypes = [P, P, P, P, P, I32, P, I64, I32, I32, ctypes.POINTER(P)]
-    L.gsb_reserve.argtypes = [P, I32, I32, I32, I32, I32, I64, U32]
+    _sig(L, 'gsb_create_scene').argtypes = [P, P, P, P, P, I32, P, I64, I32, I32, ctypes.POINTER(P)]
+    _sig(L, 'gsb_reserve').argtypes = [P, I32, I32, I32, I32, I32, I64, U32]
     rp = ctypes.POINTER(gsb_render_params)
-    L.gsb_render.argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P, P]
-    L.gsb_render_host.argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P, P]
-    L.gsb_render_rig.argtypes = [P, P, I64, I64, I32, I32, P, P, P, rp, P, P, P, P, P]
-    L.gsb_prebin_static.argtypes = [P, I32, P, P, rp, P]
-    L.gsb_render_static.argtypes = [P, P, I32, rp, P, P, P, P, P]
-    L.gsb_scores_reset.argtypes = [P, P]
+    _sig(L, 'gsb_render').argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P, P]
+    _sig(L, 'gsb_render_host').argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P, P]
+    _sig(L, 'gsb_render_rig').argtypes = [P, P, I64, I64, I32, I32, P, P, P, rp, P, P, P, P, P]
+    _sig(L, 'gsb_prebin_static').argtypes = [P, I32, P, P, rp, P]
+    _sig(L, 'gsb_render_static').argtypes = [P, P, I32, rp, P, P, P, P, P]
+    _sig(L, 'gsb_scores_reset').argtypes = [P, P]
     op = ctypes.POINTER(gsb_obs_params)
-    L.gsb_render_obs.argtypes = [P, P, I32, I32, P, P, rp, op, P, P, P]
-    L.gsb_render_obs_host.argtypes = [P, P, I32, I32, P, P, rp, op, P, P, P]
-    L.gsb_get_scores.argtypes = [P, P, P, P]
-    L.gsb_filter_scene.argtypes = [P, P, ctypes.POINTER(P)]
-    L.gsb_get_stats.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]
-    L.gsb_get_stats_ext.argtypes = [P, ctypes.POINTER(gsb_stats)]
-    L.gsb_get_timings.argtypes = [P, ctypes.POINTER(gsb_timings)]
-    L.gsb_destroy_scene.argtypes = [P]
-    L.gsb_last_error.argtypes = []
-    L.gsb_version.argtypes = []
+    _sig(L, 'gsb_render_obs').argtypes = [P, P, I32, I32, P, P, rp, op, P, P, P]
+    _sig(L, 'gsb_render_obs_host').argtypes = [P, P, I32, I32, P, P, rp, op, P, P, P]
+    _sig(L, 'gsb_get_scores').argtypes = [P, P, P, P]
+    _sig(L, 'gsb_filter_scene').argtypes = [P, P, ctypes.POINTER(P)]
+    _sig(L, 'gsb_get_stats').argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]
+    _sig(L, 'gsb_get_stats_ext').argtypes = [P, ctypes.POINTER(gsb_stats)]
+    _sig(L, 'gsb_get_overflow').argtypes = [P, ctypes.POINTER(I32)]
+    _sig(L, 'gsb_get_timings').argtypes = [P, ctypes.POINTER(gsb_timings)]
+    _sig(L, 'gsb_destroy_scene').argtypes = [P]
+    _sig(L, 'gsb_last_error').argtypes = []
+    _sig(L, 'gsb_version').argtypes = []
     L.gsb_last_error.restype = ctypes.c_char_p
     L.gsb_version.restype = ctypes.c_char_p
-    L.gsb_debug_project.argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P]
-    L.gsb_debug_bin_sort.argtypes = [P, P, P, P, P, P, P, I32, I64, I32, I32, P, P, I64,
+    _sig(L, 'gsb_debug_project').argtypes = [P, P, I32, I32, P, P, rp, P, P, P, P]
+    _sig(L, 'gsb_debug_bin_sort').argtypes = [P, P, P, P, P, P, P, I32, I64, I32, I32, P, P, I64,
                                      ctypes.POINTER(I64), P]
-    L.gsb_debug_tile_lists.argtypes = [P, P, P, P, P, P, P, P, I32, I64, I32, I32, I32, I32, P, P, I64,
+    _sig(L, 'gsb_debug_tile_lists').argtypes = [P, P, P, P, P, P, P, P, I32, I64, I32, I32, I32, I32, P, P, I64,
                                        ctypes.POINTER(I64), ctypes.POINTER(I32), P]
-    L.gsb_obs_encode.argtypes = [P, P, I32, I32, I32, I32, op, P, P, P, P]
-    L.gsb_lidar_create.argtypes = [P, P, I32, I32, I32, ctypes.POINTER(P)]
-    L.gsb_render_lidar.argtypes = [P, P, P, I32, I32, P, I32, P, ctypes.c_float, ctypes.c_float, P, P, P]
-    L.gsb_lidar_info.argtypes = [P, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32),
+    _sig(L, 'gsb_obs_encode').argtypes = [P, P, I32, I32, I32, I32, op, P, P, P, P]
+    _sig(L, 'gsb_lidar_create').argtypes = [P, P, I32, I32, I32, ctypes.POINTER(P)]
+    _sig(L, 'gsb_render_lidar').argtypes = [P, P, P, I32, I32, P, I32, P, ctypes.c_float, ctypes.c_float, P, P, P]
+    _sig(L, 'gsb_lidar_info').argtypes = [P, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32),
                                  ctypes.POINTER(I64)]
-    L.gsb_lidar_destroy.argtypes = [P]
+    _sig(L, 'gsb_lidar_destroy').argtypes = [P]
     for name in EXPORTS:
         if name not in ("gsb_last_error", "gsb_version"):
-            getattr(L, name).restype = ctypes.c_int
+            _sig(L, name).restype = ctypes.c_int
     _lib = L
     return L
 
@@ -200,6 +213,7 @@ class RenderParams:
     timing: bool = False
     scores: bool = False   # accumulate the reading-R30 pruning scores into the scene
     static_per_env: bool = False   # gsb_render_static: env e uses pre-binned camera e
+    fixed_plan: bool = False   # no host sync / data-dependent launches: capturable in a CUDA graph
 
     def to_c(self) -> gsb_render_params:
         p = gsb_render_params()
@@ -209,7 +223,8 @@ class RenderParams:
         p.sh_degree = self.sh_degree
         p.flags = ((GSB_FLAG_STATS if self.stats else 0) | (GSB_FLAG_TIMING if self.timing else 0)
                    | (GSB_FLAG_SCORES if self.scores else 0)
-                   | (GSB_FLAG_STATIC_PER_ENV if self.static_per_env else 0))
+                   | (GSB_FLAG_STATIC_PER_ENV if self.static_per_env else 0)
+                   | (GSB_FLAG_FIXED_PLAN if self.fixed_plan else 0))
         return p
 
 
@@ -432,6 +447,13 @@ class Scene:
         _check(lib().gsb_get_stats_ext(self._h, ctypes.byref(st)))
         return {"V": st.visible_V, "K": st.keys_K, "P": st.pairs_P, "terminated": st.terminated_pixels,
                 "pixels": st.pixels}
+
+    def overflow(self) -> bool:
+        """gsb_get_overflow: did a GSB_FLAG_FIXED_PLAN render since the last call exceed the key
+        capacity (its frames unwritten)?  Resets the flag; synchronises the device."""
+        v = ctypes.c_int32()
+        _check(lib().gsb_get_overflow(self._h, ctypes.byref(v)))
+        return bool(v.value)
 
     def timings(self):
         t = gsb_timings()

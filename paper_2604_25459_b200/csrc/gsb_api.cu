@@ -214,11 +214,11 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
     CUDA_TRY(dalloc(&s->vcount[sl], (size_t)E));
     CUDA_TRY(dalloc(&s->vis_bits[sl], (size_t)E * std::max<int64_t>(s->vis_words, 1)));
     CUDA_TRY(dalloc(&s->long_list[sl], (size_t)E * s->n_tiles));
-    CUDA_TRY(dalloc(&s->long_cnt[sl], 1));
+    CUDA_TRY(dalloc(&s->long_cnt[sl], 2));
     CUDA_TRY(dalloc(&s->hist[sl], (size_t)E * s->hist_stride));
     CUDA_TRY(dalloc(&s->off[sl], (size_t)E * s->hist_stride));
     CUDA_TRY(dalloc(&s->frame_base[sl], (size_t)E + 2));
-    CUDA_TRY(cudaHostAlloc((void**)&s->h_rb[sl], sizeof(uint64_t) * (2 * E + 3), cudaHostAllocMapped));
+    CUDA_TRY(cudaHostAlloc((void**)&s->h_rb[sl], sizeof(uint64_t) * (2 * E + 4), cudaHostAllocMapped));
     CUDA_TRY(cudaHostGetDevicePointer((void**)&s->d_rb[sl], s->h_rb[sl], 0));
     CUDA_TRY(cudaEventCreateWithFlags(&s->ev_counts[sl], cudaEventDisableTiming));
   }
@@ -226,6 +226,8 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
   CUDA_TRY(dalloc(&s->keys_alt, (size_t)cap));
   CUDA_TRY(dalloc(&s->sorted, (size_t)cap));
   CUDA_TRY(dalloc(&s->d_pairs, 2));
+  CUDA_TRY(dalloc(&s->d_overflow, 4));
+  CUDA_TRY(cudaMemset(s->d_overflow, 0, 4 * sizeof(int)));
   CUDA_TRY(dalloc(&s->d_counter, 1));
   CUDA_TRY(cudaStreamCreateWithFlags(&s->sp, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&s->sc, cudaStreamNonBlocking));
@@ -281,6 +283,18 @@ gsb_status gsb_get_stats_ext(gsb_scene s, gsb_stats* out) {
   out->pairs_P = (int64_t)c[0];
   out->terminated_pixels = (int64_t)c[1];
   out->pixels = s->stat_pixels;
+  return GSB_OK;
+}
+
+gsb_status gsb_get_overflow(gsb_scene s, int32_t* out) {
+  if (!s || !out) return fail(GSB_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!s->reserved) return fail(GSB_ERR_INVALID_ARGUMENT, "gsb_reserve was not called");
+  DeviceGuard g(s->device);
+  CUDA_TRY(cudaDeviceSynchronize());   // the render may have been replayed from a graph on any stream
+  int v = 0;
+  CUDA_TRY(cudaMemcpy(&v, s->d_overflow, sizeof(int), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemset(s->d_overflow, 0, sizeof(int)));
+  *out = v;
   return GSB_OK;
 }
 

@@ -113,12 +113,26 @@ __device__ __forceinline__ int warp_compact_slot(bool take, int* counter) {
 // cooperatively afterwards.  All 32 lanes of the warp must call this; `scratch` = 32 words of
 // shared memory private to the warp (or nullptr: rounds only).
 constexpr int kBigRect = 8;
+#ifndef GSB_TILE_DIV
+#define GSB_TILE_DIV 0
+#endif
 #ifndef GSB_UNION_BOX
 #define GSB_UNION_BOX 1   // 0: match_any rounds only (A/B comparisons)
 #endif
 
 struct UnionBox {
   int x0, y0, w, n;   // origin, width and tile count of the warp's union box (n = 0: empty)
+  // tile index of box entry j < n (row-major in the box), without an integer division:
+  // (j + 0.5) / w is at least 1 / (2w) >= 1/64 from an integer, far above the fp32 error of a
+  // fast division (j, w <= 32)
+  __device__ __forceinline__ int tile_of(int j, int tiles_x) const {
+#if GSB_TILE_DIV
+    return (y0 + j / w) * tiles_x + x0 + j % w;
+#else
+    const int yy = (int)__fdividef((float)j + 0.5f, (float)w);   // 2-ulp division, far inside the margin
+    return (y0 + yy) * tiles_x + x0 + (j - yy * w);
+#endif
+  }
 };
 
 __device__ __forceinline__ UnionBox warp_union_box(bool part, int tx0, int tx1, int ty0, int ty1) {
@@ -151,7 +165,7 @@ __device__ __forceinline__ void warp_tile_count(bool has, uint32_t rect, int til
         for (int x = tx0; x <= tx1; ++x) atomicAdd(&scratch[(y - ub.y0) * ub.w + (x - ub.x0)], 1u);
     __syncwarp();
     const uint32_t c = scratch[lane];
-    if (lane < ub.n && c) atomicAdd(counter + (ub.y0 + lane / ub.w) * tiles_x + ub.x0 + lane % ub.w, (int)c);
+    if (lane < ub.n && c) atomicAdd(counter + ub.tile_of(lane, tiles_x), (int)c);
     __syncwarp();   // scratch free for the caller's next use
   } else if (ub.n > 0) {
     const int rounds = __reduce_max_sync(FULL, part ? nt : 0);

@@ -190,9 +190,13 @@ gsb_status gsb_debug_tile_lists(const float* u, const float* v, const float* sxx
       if (hoff[(size_t)f * stride + t + 1] - hoff[(size_t)f * stride + t] > (uint32_t)kWarpSortCap)
         hlong.push_back(((uint32_t)f << 16) | (uint32_t)t);
   const uint64_t n_long = hlong.size();
+  uint64_t n_vlong = 0;   // lists > kFusedSortCap: the render's packed-variant rule
+  for (int f = 0; f < F; ++f)
+    for (int t = 0; t < n_tiles; ++t)
+      n_vlong += hoff[(size_t)f * stride + t + 1] - hoff[(size_t)f * stride + t] > (uint32_t)kFusedSortCap;
   int var = variant;
   if (var == 0) {
-    const bool long_lists = n_long * 4 > (uint64_t)F * n_tiles;
+    const bool long_lists = n_vlong * 4 > (uint64_t)F * n_tiles;
     const bool split = split_k4() && K >= split_min_avg() * (uint64_t)F * n_tiles;
     var = split ? (long_lists ? 2 : 1) : (long_lists ? 4 : 3);
   }

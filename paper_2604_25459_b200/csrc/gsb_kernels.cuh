@@ -88,6 +88,7 @@ struct ChunkArgs {
   uint64_t* keys;         // [cap]   (zbits << 32) | id
   uint64_t* keys_alt;     // [cap]   scratch for oversize segments
   uint32_t* sorted;       // [cap]   sorted ids of the lists K3 sorted
+  const int* overflow;    // GSB_FLAG_FIXED_PLAN: the chunk's flag (keys beyond capacity: skip), or nullptr
 };
 
 struct CompositeArgs {
@@ -135,6 +136,8 @@ struct CompositeArgs {
   // K4a sorts short lists one warp per tile and these with a CTA each; nullptr = CTA per tile
   const uint32_t* long_list;
   uint32_t n_long;
+  const uint32_t* n_long_dev;   // GSB_FLAG_FIXED_PLAN: long-list count read on the device (K2a's)
+  const int* overflow;          // GSB_FLAG_FIXED_PLAN: skip the chunk (keys beyond capacity), or nullptr
   // gsb_debug_tile_lists only: the fused K4 writes each tile's sorted slot list here (at the
   // list's key offset) and returns before compositing; nullptr in every render
   uint32_t* dbg_lists;
@@ -226,12 +229,15 @@ void launch_k1_external(const float* u, const float* v, const float* sxx, const 
 // off[f][T] = K_f, off[f][T+1] = longest tile list of frame f; frame_base[E] = total keys,
 // frame_base[E+1] = longest tile list of the chunk
 // Lists longer than long_thresh are appended to long_list (frame << 16 | tile), counted in
-// *long_count (both may be null).
+// long_count[0]; long_count[1] counts those longer than kFusedSortCap (both may be null).
 // host_mapped (device view of mapped pinned memory, may be null) receives
 // [frame_base[0..E+1], vcount[0..E), long_count] as u64.
+// overflow (nullable, GSB_FLAG_FIXED_PLAN): the chunk's flag, set to (total keys > key_cap); a
+// set flag also sets *sticky
 void launch_k2_scan(int* hist, uint32_t* off, int64_t hist_stride, int n_frames, int n_tiles,
                     uint64_t* frame_base, uint32_t* long_list, uint32_t* long_count, int long_thresh,
-                    const int* vcount, uint64_t* host_mapped, cudaStream_t s);
+                    const int* vcount, uint64_t* host_mapped, cudaStream_t s, int* overflow = nullptr,
+                    int* sticky = nullptr, uint64_t key_cap = 0);
 void launch_k2_emit(const ChunkArgs& a, cudaStream_t s);
 void launch_k3_sort(const ChunkArgs& a, uint32_t n_long, cudaStream_t s);
 // gather K3-sorted background lists (ids in `sorted`) into list-ordered keys + 3-quad records

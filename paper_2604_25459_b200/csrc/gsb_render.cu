@@ -52,12 +52,14 @@ struct Pipeline {
   int32_t* out_neval;
   int64_t first = 0, count = 0;   // Gaussian range [first, first + count) of the internal order
   bool merge = false;             // static cameras: merge with the pre-binned background lists
+  bool fixed = false;             // GSB_FLAG_FIXED_PLAN: no host sync, no data-dependent launch choice
+  uint32_t n_vlong = 0;           // the chunk's lists longer than kFusedSortCap
 
   gsb_status project_chunk(int c, int f0, int nf) {
     const int sl = c & 1;
     if (c >= 2) CUDA_TRY(cudaStreamWaitEvent(sp, s->ev_done[sl], 0));   // chunk c-2 left this slot
     CUDA_TRY(cudaMemsetAsync(s->vcount[sl], 0, sizeof(int) * nf, sp));
-    CUDA_TRY(cudaMemsetAsync(s->long_cnt[sl], 0, sizeof(uint32_t), sp));
+    CUDA_TRY(cudaMemsetAsync(s->long_cnt[sl], 0, 2 * sizeof(uint32_t), sp));
     CUDA_TRY(cudaMemsetAsync(s->hist[sl], 0, sizeof(int) * s->hist_stride * nf, sp));
     K1Args a{};
     a.g_mean = s->d_mean + first; a.g_L0 = s->d_L0 + first; a.g_L1 = s->d_L1 + first;
@@ -76,7 +78,8 @@ struct Pipeline {
     tm.end();
     tm.begin(KC_SCAN, sp);
     launch_k2_scan(s->hist[sl], s->off[sl], s->hist_stride, nf, n_tiles, s->frame_base[sl], s->long_list[sl],
-                   s->long_cnt[sl], kWarpSortCap, s->vcount[sl], s->d_rb[sl], sp);
+                   s->long_cnt[sl], kWarpSortCap, s->vcount[sl], fixed ? nullptr : s->d_rb[sl], sp,
+                   fixed ? s->d_overflow + 1 + sl : nullptr, s->d_overflow, (uint64_t)s->cap);
     s->launches += 2;
     LAUNCH_CHECK();
     tm.end();
@@ -99,11 +102,14 @@ struct Pipeline {
     if (merge)
       for (int f = fs; f < fe; ++f) n_entries += (uint64_t)s->sb_K[(f0 + f) % s->sb_cams];
     // many lists beyond the small fused-sort capacity (e.g. 128x128 views): larger variant
-    const bool long_lists = (uint64_t)n_long * 4 > (uint64_t)(fe - fs) * n_tiles;
+    // (fixed plan: the small variant, whose long-list CTAs handle any length)
+    const bool long_lists = !fixed && (uint64_t)n_vlong * 4 > (uint64_t)(fe - fs) * n_tiles;
     // split K4a + K4b unless the lists are short on average (then the one-CTA-per-tile kernel's
-    // shared staging beats per-warp record reads; measured crossover ~200-330 keys per tile)
-    const bool split = split_k4() && n_entries >= split_min_avg() * (uint64_t)(fe - fs) * n_tiles &&
-                       n_entries <= (uint64_t)s->cap;
+    // shared staging beats per-warp record reads; measured crossover ~200-330 keys per tile);
+    // always split under the fixed plan
+    const bool split = fixed || (split_k4() && n_entries >= split_min_avg() * (uint64_t)(fe - fs) * n_tiles &&
+                                 n_entries <= (uint64_t)s->cap);
+    if (fixed) a.overflow = s->d_overflow + 1 + sl;
     const bool slot_keys = !merge && slot_keys_on();
     if (slot_keys) a.ids = nullptr;   // key low word = index in the launch range = record slot
     tm.begin(KC_EMIT, sb);
@@ -126,6 +132,10 @@ struct Pipeline {
     if (slot_keys) c.keys_internal_ids = s->d_ids + first;
     c.long_list = s->long_list[sl];   // K4a: lists > kWarpSortCap get a CTA each
     c.n_long = n_long;
+    if (fixed) {   // the long-list count and the chunk's overflow flag stay on the device
+      c.n_long_dev = s->long_cnt[sl];
+      c.overflow = s->d_overflow + 1 + sl;
+    }
     c.fs = fs; c.fe = fe; c.f0 = f0; c.width = W; c.height = H; c.tiles_x = tiles_x; c.n_tiles = n_tiles;
     c.bg0 = p->background[0]; c.bg1 = p->background[1]; c.bg2 = p->background[2];
     c.out_rgb = out_rgb; c.out_depth = out_depth; c.out_alpha = out_alpha; c.out_n_eval = out_neval;
@@ -200,8 +210,15 @@ struct Pipeline {
 
   gsb_status finish_chunk(int c, int f0, int nf) {
     const int sl = c & 1;
-    CUDA_TRY(cudaEventSynchronize(s->ev_counts[sl]));
-    gsb_status r = finish_passes(c, f0, nf);
+    gsb_status r;
+    if (fixed) {   // one pass over the chunk, enqueued without reading its counts: binning waits
+      s->chunks++;  // for the chunk's scan on the device (which also joins the projection stream)
+      CUDA_TRY(cudaStreamWaitEvent(sb, s->ev_counts[sl], 0));
+      r = pass(sl, f0, 0, nf, 0, 0, 0);
+    } else {
+      CUDA_TRY(cudaEventSynchronize(s->ev_counts[sl]));
+      r = finish_passes(c, f0, nf);
+    }
     if (r != GSB_OK) return r;
     if (sb != sc) {   // the chunk is done when both its binning and its compositing are
       CUDA_TRY(cudaEventRecord(s->ev_bin, sb));
@@ -225,7 +242,8 @@ struct Pipeline {
         s->stat_K += s->sb_K[cam];
       }
     s->chunks++;
-    const uint32_t n_long = (uint32_t)rb[2 * nf + 2];
+    const uint32_t n_long = (uint32_t)rb[2 * nf + 2];    // lists > kWarpSortCap (K4a's long-list table)
+    n_vlong = (uint32_t)rb[2 * nf + 3];                 // lists > kFusedSortCap (packed-variant rule)
     s->stat_long += n_long;
     s->stat_maxseg = std::max<int64_t>(s->stat_maxseg, (int64_t)fb[nf + 1]);
     if (fb[nf] <= (uint64_t)s->cap) return pass(sl, f0, 0, nf, 0, fb[nf], n_long);
@@ -305,6 +323,9 @@ gsb_status render_impl(gsb_scene s, const K0Rig& rig, int n_envs, int n_cams, co
   s->ev_used = 0;
   s->ev_marks.clear();
   const bool timing = (p->flags & GSB_FLAG_TIMING) != 0;
+  const bool fixed = (p->flags & GSB_FLAG_FIXED_PLAN) != 0;
+  if (fixed && (merge || s->dl_rgb || s->dl_rgb8 || (p->flags & (GSB_FLAG_STATS | GSB_FLAG_TIMING))))
+    return fail(GSB_ERR_INVALID_ARGUMENT, "GSB_FLAG_FIXED_PLAN: not with STATS/TIMING, host-buffer or static renders");
   if (timing && s->ev_pool.empty()) {
     s->ev_pool.resize(8192);
     for (auto& e : s->ev_pool) CUDA_TRY(cudaEventCreate(&e));
@@ -325,6 +346,7 @@ gsb_status render_impl(gsb_scene s, const K0Rig& rig, int n_envs, int n_cams, co
   pl.tm = Timer{s, st, timing};
   pl.out_rgb = out_rgb; pl.out_depth = out_depth; pl.out_alpha = out_alpha; pl.out_neval = out_neval;
   pl.merge = merge;
+  pl.fixed = fixed;
   pl.n_cams = n_cams;
   pl.first = merge ? s->n_bg : 0;      // static cameras: only the robot Gaussians per frame
   pl.count = s->n - pl.first;

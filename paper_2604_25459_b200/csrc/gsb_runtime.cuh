@@ -153,6 +153,7 @@ struct gsb_scene_t {
   uint64_t *keys = nullptr, *keys_alt = nullptr;
   uint32_t* sorted = nullptr;
   unsigned long long* d_pairs = nullptr;
+  int* d_overflow = nullptr;   // GSB_FLAG_FIXED_PLAN: [0] sticky flag, [1..2] per chunk slot
   int* d_counter = nullptr;   // K4b work-item counter
   // host-io staging
   bool host_io = false;
@@ -211,6 +212,8 @@ struct gsb_scene_t {
       frame_base[s] = nullptr; h_rb[s] = nullptr; d_rb[s] = nullptr; ev_counts[s] = nullptr;
     }
     cudaFree(keys); cudaFree(keys_alt); cudaFree(sorted); cudaFree(d_pairs); cudaFree(qpos); cudaFree(d_counter);
+    cudaFree(d_overflow);
+    d_overflow = nullptr;
     d_counter = nullptr;
     qpos = nullptr;
     cudaFree(st_poses); cudaFree(st_intr); cudaFree(st_w2c);

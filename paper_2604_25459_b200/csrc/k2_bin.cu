@@ -56,7 +56,10 @@ __global__ void __launch_bounds__(kScanThreads) k2_scan_tiles(int* __restrict__ 
     if (t < n_tiles) {
       o[t] = carry + wsum[warp] + inc - x;
       h[t] = 0;
-      if (long_list && x > (uint32_t)long_thresh) long_list[atomicAdd(long_count, 1u)] = ((uint32_t)f << 16) | (uint32_t)t;
+      if (long_list && x > (uint32_t)long_thresh) {
+        long_list[atomicAdd(long_count, 1u)] = ((uint32_t)f << 16) | (uint32_t)t;
+        if (x > (uint32_t)kFusedSortCap) atomicAdd(long_count + 1, 1u);   // the packed-variant rule
+      }
     }
     __syncthreads();
     if (tid == kScanThreads - 1) carry_s = carry + wsum[warp] + inc;
@@ -77,7 +80,8 @@ __global__ void __launch_bounds__(kScanThreads) k2_scan_tiles(int* __restrict__ 
 // readback never queues behind output copies on the copy engine.
 __global__ void k2_scan_frames(const uint32_t* __restrict__ off, int64_t stride, int n_tiles,
                                int n_frames, uint64_t* __restrict__ frame_base, const int* __restrict__ vcount,
-                               const uint32_t* __restrict__ long_count, volatile uint64_t* __restrict__ host) {
+                               const uint32_t* __restrict__ long_count, volatile uint64_t* __restrict__ host,
+                               int* __restrict__ overflow, int* __restrict__ sticky, uint64_t key_cap) {
   if (threadIdx.x != 0) return;
   uint64_t acc = 0, mx = 0;
   for (int f = 0; f < n_frames; ++f) {
@@ -88,22 +92,28 @@ __global__ void k2_scan_frames(const uint32_t* __restrict__ off, int64_t stride,
   }
   frame_base[n_frames] = acc;
   frame_base[n_frames + 1] = mx;
+  if (overflow) {   // fixed plan: one pass per chunk; the chunk is skipped when it does not fit
+    *overflow = acc > key_cap ? 1 : 0;            // this chunk (its slot's flag)
+    if (acc > key_cap) *sticky = 1;               // read and reset by gsb_get_overflow
+  }
   if (host) {
     host[n_frames] = acc;
     host[n_frames + 1] = mx;
     for (int f = 0; f < n_frames; ++f) host[n_frames + 2 + f] = vcount ? (uint64_t)vcount[f] : 0ull;
-    host[2 * n_frames + 2] = long_count ? (uint64_t)*long_count : 0ull;
+    host[2 * n_frames + 2] = long_count ? (uint64_t)long_count[0] : 0ull;
+    host[2 * n_frames + 3] = long_count ? (uint64_t)long_count[1] : 0ull;
     __threadfence_system();
   }
 }
 
 void launch_k2_scan(int* hist, uint32_t* off, int64_t hist_stride, int n_frames, int n_tiles,
                     uint64_t* frame_base, uint32_t* long_list, uint32_t* long_count, int long_thresh,
-                    const int* vcount, uint64_t* host_mapped, cudaStream_t s) {
+                    const int* vcount, uint64_t* host_mapped, cudaStream_t s, int* overflow, int* sticky,
+                    uint64_t key_cap) {
   k2_scan_tiles<<<n_frames, kScanThreads, 0, s>>>(hist, off, hist_stride, n_tiles, long_list, long_count,
                                                   long_thresh);
   k2_scan_frames<<<1, 32, 0, s>>>(off, hist_stride, n_tiles, n_frames, frame_base, vcount, long_count,
-                                  host_mapped);
+                                  host_mapped, overflow, sticky, key_cap);
 }
 
 // ------------------------------------------------------------------------------ emission
@@ -111,9 +121,13 @@ void launch_k2_scan(int* hist, uint32_t* off, int64_t hist_stride, int n_frames,
 // at once.  Keys of a warp's Gaussians that land in the same tile share one cursor atomic (the
 // template is Morton-ordered, so a warp's Gaussians overlap the same tiles); rects with more
 // than kBigRect tiles are emitted by the whole warp cooperatively.
+#ifndef GSB_K2B_BREAK
+#define GSB_K2B_BREAK 0   // 1: warp-uniform early exit from the unrolled rounds (A/B)
+#endif
 __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
   __shared__ uint32_t tile_scratch[8][32];   // per-warp union-box counts
   const unsigned FULL = 0xffffffffu;
+  if (a.overflow && *a.overflow) return;   // fixed plan: chunk beyond the key capacity
   const int fl = a.fs + blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) >= a.n) return;  // whole warp past N
@@ -147,6 +161,16 @@ __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
     __syncwarp();
     uint32_t rk[kBigRect];
     int tx = tx0, ty = ty0;
+#if GSB_K2B_BREAK
+#pragma unroll
+    for (int r = 0; r < kBigRect; ++r) {
+      if (r >= rounds) break;   // warp-uniform
+      if (part && r < nt) {
+        rk[r] = atomicAdd(&sc[(ty - ub.y0) * ub.w + (tx - ub.x0)], 1u);
+        if (++tx > tx1) { tx = tx0; ++ty; }
+      }
+    }
+#else
 #pragma unroll
     for (int r = 0; r < kBigRect; ++r) {
       if (r < nt && part) {
@@ -154,11 +178,24 @@ __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
         if (++tx > tx1) { tx = tx0; ++ty; }
       }
     }
+#endif
     __syncwarp();
     const uint32_t c = sc[lane];
     uint32_t base = 0u;
-    if (lane < ub.n && c) base = (uint32_t)atomicAdd(cur + (ub.y0 + lane / ub.w) * a.tiles_x + ub.x0 + lane % ub.w, (int)c);
+    if (lane < ub.n && c) base = (uint32_t)atomicAdd(cur + ub.tile_of(lane, a.tiles_x), (int)c);
     tx = tx0; ty = ty0;
+#if GSB_K2B_BREAK
+#pragma unroll
+    for (int r = 0; r < kBigRect; ++r) {
+      if (r >= rounds) break;   // warp-uniform
+      const bool act = part && r < nt;
+      const uint32_t b = __shfl_sync(FULL, base, act ? (ty - ub.y0) * ub.w + (tx - ub.x0) : 0);
+      if (act) {
+        keys[off[ty * a.tiles_x + tx] + b + rk[r]] = key;
+        if (++tx > tx1) { tx = tx0; ++ty; }
+      }
+    }
+#else
 #pragma unroll
     for (int r = 0; r < kBigRect; ++r) {
       if (r < rounds) {
@@ -168,6 +205,7 @@ __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
         if (++tx > tx1) { tx = tx0; ++ty; }
       }
     }
+#endif
   }
   int tx = tx0, ty = ty0;  // this lane's r-th tile, stepped row-major (no division)
   for (int r = 0; r < (ub.n > 32 ? rounds : 0); ++r) {

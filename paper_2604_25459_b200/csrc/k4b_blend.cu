@@ -77,23 +77,10 @@ __device__ __forceinline__ TileList tile_list(const CompositeArgs& a, int fl, in
 
 constexpr uint32_t kBgTag = 0x80000000u;   // merged entry: background record index | tag
 
-// LONG: one CTA per entry of a.long_list (the chunk's lists longer than kWarpSortCap; entries of
-// frames outside this pass return), the short lists being sorted by k4a_warp_sort
-template <int CAP, bool LONG = false>
-__global__ void __launch_bounds__(kSortThreadsA) k4a_sort(CompositeArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+// one (frame, tile) list of K4a: sort, then record slots into `sorted`
+template <int CAP>
+__device__ __forceinline__ void k4a_sort_list(const CompositeArgs& a, int fl, int t, K4aShared<CAP>& sm) {
   using Sh = K4aShared<CAP>;
-  Sh& sm = *reinterpret_cast<Sh*>(smem_raw);
-  int fl, t;
-  if constexpr (LONG) {
-    const uint32_t e = a.long_list[blockIdx.x];
-    fl = (int)(e >> 16);
-    t = (int)(e & 0xffffu);
-    if (fl < a.fs || fl >= a.fe) return;
-  } else {
-    fl = a.fs + blockIdx.x / a.n_tiles;
-    t = blockIdx.x % a.n_tiles;
-  }
   const int tid = threadIdx.x;
   const TileList L = tile_list(a, fl, t);
   const uint64_t start = L.rstart;
@@ -213,6 +200,193 @@ __global__ void __launch_bounds__(kSortThreadsA) k4a_sort(CompositeArgs a) {
 }
 
 
+
+// K4a, one CTA per list: every (frame, tile) list of the pass (grid = lists), or — LONG — the
+// entries of a.long_list (the chunk's lists longer than kWarpSortCap, the short ones being sorted
+// by k4a_warp_sort), grid-stride so that the count may live on the device (fixed plan); entries
+// of frames outside this pass are skipped
+template <int CAP, bool LONG = false>
+__global__ void __launch_bounds__(kSortThreadsA) k4a_sort(CompositeArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  using Sh = K4aShared<CAP>;
+  Sh& sm = *reinterpret_cast<Sh*>(smem_raw);
+  if (a.overflow && *a.overflow) return;   // fixed plan: chunk beyond the key capacity
+  if constexpr (LONG) {   // grid-stride over the long-list table (count on the host or the device)
+    const uint32_t n = a.n_long_dev ? *a.n_long_dev : a.n_long;
+    for (uint32_t k = blockIdx.x; k < n; k += gridDim.x) {
+      const uint32_t e = a.long_list[k];
+      const int fl = (int)(e >> 16), t = (int)(e & 0xffffu);
+      if (fl >= a.fs && fl < a.fe) k4a_sort_list<CAP>(a, fl, t, sm);
+      __syncthreads();   // the shared buffers are reused by the next list
+    }
+  } else {
+    k4a_sort_list<CAP>(a, a.fs + blockIdx.x / a.n_tiles, blockIdx.x % a.n_tiles, sm);
+  }
+}
+
+
+// ------------------------------------------------------------------------------ K4a, one CTA per long list
+// Lists of kWarpSortCap < n <= kIdxCap keys (and, for views whose lists are mostly long, every
+// list) are sorted by one 256-thread CTA with a counting sort that never moves the 64-bit keys:
+// buckets = the top kIdxBits varying bits of (zbits - zmin); the keys' 16-bit local indices are
+// scattered into their buckets (shared atomics), then each key takes its rank among its bucket's
+// keys by (bits(z), id) — read through L1 from the list in HBM/L2 — and its slot is written at
+// bucket start + rank.  Six barriers per list, whatever n.  Equal depths with slot keys are
+// ordered by ids[slot]; a run of more than kShortRun equal depths sends the list to the HBM radix
+// with (z, id) keys (reading R10).  Longer lists: the HBM radix (segment_sort).
+constexpr int kIdxCap = 4096;
+constexpr int kIdxBits = 12;
+struct K4aIdxShared {
+  union {
+    SortShared<kSortThreadsA> sort;   // the HBM radix (lists > kIdxCap, long equal-depth runs)
+    struct {
+      uint32_t bins[1 << kIdxBits];
+      uint32_t wmin[kSortThreadsA / 32], wmax[kSortThreadsA / 32], wsum[kSortThreadsA / 32];
+    } c;
+  } s;
+  uint16_t buf[kIdxCap];
+};
+
+// the HBM path of one list: LSD radix of 64-bit keys in keys / keys_alt (gsb_sort.cuh)
+__device__ __forceinline__ void k4a_hbm_list(const CompositeArgs& a, uint64_t start, int len, uint32_t* dst,
+                                             SortShared<kSortThreadsA>& ss) {
+  const int tid = threadIdx.x;
+  const int2* kid = a.keys_internal_ids;
+  const int base = a.slot_base;
+  uint64_t* ga = const_cast<uint64_t*>(a.keys) + start;
+  uint64_t* gb = a.keys_alt + start;
+  const bool in_b = segment_sort(ga, gb, len, ss);
+  __syncthreads();
+  uint64_t* r = in_b ? gb : ga;
+  if (!kid) {
+    for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)r[e]) - base);
+  } else if (fix_equal_depth_runs<kSortThreadsA>(r, len, kid)) {
+    for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)r[e];
+  } else {
+    uint64_t* o = in_b ? ga : gb;
+    slot_keys_to_id_keys<kSortThreadsA>(r, len, kid);
+    const bool in_o = segment_sort(r, o, len, ss);
+    __syncthreads();
+    const uint64_t* rr = in_o ? o : r;
+    for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)rr[e]) - base);
+  }
+}
+
+// one list by the index counting sort (n <= kIdxCap); false = a long equal-depth run (nothing
+// usable written: the caller re-sorts)
+__device__ __forceinline__ bool k4a_idx_list(const CompositeArgs& a, const uint64_t* __restrict__ gk, int n,
+                                             uint32_t* dst, K4aIdxShared& sm) {
+  constexpr int NT = kSortThreadsA, BINS = 1 << kIdxBits, PER = BINS / NT;
+  const unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int2* kid = a.keys_internal_ids;
+  const int base = a.slot_base;
+  uint32_t zmin = 0xffffffffu, zmax = 0u;
+  for (int e = tid; e < n; e += NT) {
+    const uint32_t z = hi32(__ldg(gk + e));
+    zmin = min(zmin, z);
+    zmax = max(zmax, z);
+  }
+  zmin = __reduce_min_sync(FULL, zmin);
+  zmax = __reduce_max_sync(FULL, zmax);
+  if (lane == 0) { sm.s.c.wmin[warp] = zmin; sm.s.c.wmax[warp] = zmax; }
+#pragma unroll
+  for (int k = 0; k < PER; ++k) sm.s.c.bins[tid * PER + k] = 0u;
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) { zmin = min(zmin, sm.s.c.wmin[w]); zmax = max(zmax, sm.s.c.wmax[w]); }
+  const uint32_t span = zmax - zmin;
+  const int hb = span ? 31 - __clz(span) : -1;
+  const int lo = hb >= kIdxBits ? hb - kIdxBits + 1 : 0;
+  for (int e = tid; e < n; e += NT) atomicAdd(&sm.s.c.bins[(hi32(__ldg(gk + e)) - zmin) >> lo], 1u);
+  __syncthreads();
+  uint32_t v[PER], sum = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) { v[k] = sm.s.c.bins[tid * PER + k]; sum += v[k]; }
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) sm.s.c.wsum[warp] = inc;
+  __syncthreads();
+  uint32_t run = inc - sum;
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) run += (w < warp) ? sm.s.c.wsum[w] : 0u;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) { sm.s.c.bins[tid * PER + k] = run; run += v[k]; }
+  __syncthreads();
+  for (int e = tid; e < n; e += NT)
+    sm.buf[atomicAdd(&sm.s.c.bins[(hi32(__ldg(gk + e)) - zmin) >> lo], 1u)] = (uint16_t)e;
+  __syncthreads();
+  bool long_run = false;
+  for (int p = tid; p < n; p += NT) {
+    const uint64_t key = __ldg(gk + sm.buf[p]);
+    const uint32_t z = hi32(key);
+    const uint32_t b = (z - zmin) >> lo;
+    const int s0 = b ? (int)sm.s.c.bins[b - 1] : 0, s1 = (int)sm.s.c.bins[b];
+    int rank = 0, eq = 0;
+    for (int q = s0; q < s1; ++q) {
+      const uint64_t kq = __ldg(gk + sm.buf[q]);
+      rank += kq < key;
+      eq += hi32(kq) == z;
+    }
+    if (kid && eq > 1) {   // equal depths: order by creation id instead of slot
+      if (eq > kShortRun + 1) {
+        long_run = true;
+      } else {
+        const int idp = __ldg(&kid[(uint32_t)key].x);
+        rank = 0;
+        for (int q = s0; q < s1; ++q) {
+          const uint64_t kq = __ldg(gk + sm.buf[q]);
+          const uint32_t zq = hi32(kq);
+          rank += zq < z || (zq == z && kq != key && __ldg(&kid[(uint32_t)kq].x) < idp);
+        }
+      }
+    }
+    dst[s0 + rank] = kid ? (uint32_t)key : (uint32_t)(__ldg(a.inv + (uint32_t)key) - base);
+  }
+  return !__syncthreads_or(long_run);
+}
+
+// ALL: every list of the pass, one CTA each (views whose lists are mostly long); else the
+// chunk's long-list table (lists > kWarpSortCap), grid-stride (the count may be on the device)
+template <bool ALL>
+__global__ void __launch_bounds__(kSortThreadsA) k4a_idx_sort(CompositeArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K4aIdxShared& sm = *reinterpret_cast<K4aIdxShared*>(smem_raw);
+  if (a.overflow && *a.overflow) return;   // fixed plan: chunk beyond the key capacity
+  const uint32_t n_items = ALL ? (uint32_t)((a.fe - a.fs) * a.n_tiles) : (a.n_long_dev ? *a.n_long_dev : a.n_long);
+  for (uint32_t k = blockIdx.x; k < n_items; k += gridDim.x) {
+    int fl, t;
+    if constexpr (ALL) {
+      fl = a.fs + (int)(k / (uint32_t)a.n_tiles);
+      t = (int)(k % (uint32_t)a.n_tiles);
+    } else {
+      const uint32_t e = a.long_list[k];
+      fl = (int)(e >> 16);
+      t = (int)(e & 0xffffu);
+      if (fl < a.fs || fl >= a.fe) continue;   // CTA-uniform
+    }
+    const TileList L = tile_list(a, fl, t);
+    const int len = L.len;
+    uint32_t* dst = a.sorted + L.start;
+    if (len <= 1) {
+      if (len == 1 && threadIdx.x == 0) {
+        const uint64_t key = a.keys[L.rstart];
+        dst[0] = a.keys_internal_ids ? (uint32_t)key : (uint32_t)(__ldg(a.inv + (uint32_t)key) - a.slot_base);
+      }
+      continue;
+    }
+    if (len > kIdxCap || !k4a_idx_list(a, a.keys + L.rstart, len, dst, sm)) {
+      __syncthreads();   // the index sort's shared state is dead; the radix reuses the union
+      k4a_hbm_list(a, L.rstart, len, dst, sm.s.sort);
+    }
+    __syncthreads();     // shared buffers reused by the next list
+  }
+}
+
 // ------------------------------------------------------------------------------ K4a, one warp per list
 // Lists of up to kWarpSortCap keys (98.5 % of C3's) are sorted by ONE warp each, with no CTA
 // barrier (the CTA-per-tile sort above spent most of its time in per-CTA fixed costs — 2048-bin
@@ -228,6 +402,9 @@ __global__ void __launch_bounds__(kSortThreadsA) k4a_sort(CompositeArgs a) {
 #endif
 constexpr int kWarpBits = GSB_WARP_BITS;
 constexpr int kWarpBins = 1 << kWarpBits;
+#ifndef GSB_K4A_IDX
+#define GSB_K4A_IDX 1   // 0: the long lists by count_sort<1024> / packed_sort<4096> (A/B comparisons)
+#endif
 #ifndef GSB_K4A_WARPS
 #define GSB_K4A_WARPS 4
 #endif
@@ -245,6 +422,7 @@ __global__ void __launch_bounds__(kK4aWarps * 32) k4a_warp_sort(CompositeArgs a,
   K4aWarpShared& sm = reinterpret_cast<K4aWarpShared*>(smem_raw)[warp];
   const int ft = blockIdx.x * kK4aWarps + warp;
   if (ft >= n_lists) return;   // warp-uniform
+  if (a.overflow && *a.overflow) return;   // fixed plan: chunk beyond the key capacity
   const int fl = a.fs + ft / a.n_tiles;
   const int t = ft % a.n_tiles;
   const TileList L = tile_list(a, fl, t);
@@ -367,7 +545,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float4 (*S)[3][kWarpBatch] = stg[warp];
   uint8_t* wl = wlist[warp];
-  for (;;) {
+  for (;;) {   // (fixed plan: an overflowed chunk's counter starts at n_items, see launch_k4b_blend)
     int item = 0;
     if (lane == 0) item = atomicAdd(counter, 1);
     item = __shfl_sync(FULL, item, 0);
@@ -523,7 +701,11 @@ void launch_k4a_sort(const CompositeArgs& a, bool long_lists, cudaStream_t s) {
   const int nf = a.fe - a.fs;
   if (nf <= 0) return;
   const unsigned grid = (unsigned)nf * a.n_tiles;
-  if (long_lists) {
+  if (long_lists && GSB_K4A_IDX && !a.bg_off) {   // every list one CTA, by the index counting sort
+    static int attr[kMaxDevices];
+    if (ensure_smem_attr(k4a_idx_sort<true>, (int)sizeof(K4aIdxShared), attr) != cudaSuccess) return;
+    k4a_idx_sort<true><<<grid, kSortThreadsA, sizeof(K4aIdxShared), s>>>(a);
+  } else if (long_lists) {
     launch_k4a_variant<4 * kFusedSortCap>(a, grid, s);
   } else if (a.long_list && !a.bg_off && warp_k4a_on()) {
     // short lists one warp each; the chunk's long lists (K2a's list) one CTA each
@@ -532,10 +714,29 @@ void launch_k4a_sort(const CompositeArgs& a, bool long_lists, cudaStream_t s) {
     if (ensure_smem_attr(k4a_warp_sort, (int)(kK4aWarps * sizeof(K4aWarpShared)), attr) != cudaSuccess) return;
     k4a_warp_sort<<<(n_lists + kK4aWarps - 1) / kK4aWarps, kK4aWarps * 32, kK4aWarps * sizeof(K4aWarpShared), s>>>(
         a, n_lists);
-    if (a.n_long > 0) launch_k4a_variant<kFusedSortCap, true>(a, a.n_long, s);
+    unsigned lg = a.n_long;
+    if (a.n_long_dev) {   // fixed plan: the count is on the device: a persistent grid-stride launch
+      int sms = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device());
+      lg = (unsigned)std::max(1, std::min(n_lists, 4 * sms));
+    }
+    if (lg > 0) {
+      if (GSB_K4A_IDX) {
+        static int attr_i[kMaxDevices];
+        if (ensure_smem_attr(k4a_idx_sort<false>, (int)sizeof(K4aIdxShared), attr_i) != cudaSuccess) return;
+        k4a_idx_sort<false><<<lg, kSortThreadsA, sizeof(K4aIdxShared), s>>>(a);
+      } else {
+        launch_k4a_variant<kFusedSortCap, true>(a, lg, s);
+      }
+    }
   } else {
     launch_k4a_variant<kFusedSortCap>(a, grid, s);
   }
+}
+
+// fixed plan: K4b's work counter starts at 0, or past the last item when the chunk overflowed
+__global__ void k4b_counter_init(int* counter, const int* overflow, int n_items) {
+  *counter = *overflow ? n_items : 0;
 }
 
 void launch_k4b_blend(const CompositeArgs& a, int* counter, cudaStream_t s) {
@@ -556,7 +757,8 @@ void launch_k4b_blend(const CompositeArgs& a, int* counter, cudaStream_t s) {
     persistent = std::max(1, sms * std::max(1, per_sm));
   }
   const long long items = (long long)nf * a.n_tiles * 4;
-  cudaMemsetAsync(counter, 0, sizeof(int), s);
+  if (a.overflow) k4b_counter_init<<<1, 1, 0, s>>>(counter, a.overflow, (int)items);
+  else cudaMemsetAsync(counter, 0, sizeof(int), s);
   const unsigned g = (unsigned)std::min<long long>(persistent, (items + kBlendWarps - 1) / kBlendWarps);
   if (a.score_sum) k4b_blend<true><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
   else k4b_blend<false><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);

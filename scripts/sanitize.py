@@ -86,3 +86,38 @@ for n, spread, layers, size in ((600, 0.25, 1, 128), (400, 0.3, 40, 128), (2500,
         torch.cuda.synchronize()
     os.environ.pop("GSB_K4_SPLIT_MIN")
     print("ties ok", n, layers, float(rgb.mean()))
+
+# round 2: fixed-plan render (device-side long-list count, overflow flag) and the K4a index sort
+# on 513..4096-key lists with equal-depth runs (64x64 view of a 3000-Gaussian layered plane)
+cfg = synth.CONFIGS["T2"]
+sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
+g = gsb.Scene.from_synth(sc)
+g.reserve(cfg.n_envs, 1, cfg.width, cfg.height)
+rgb = torch.zeros((cfg.n_envs, 1, 3, cfg.height, cfg.width), device="cuda")
+g.render(torch.from_numpy(b.poses).cuda(), torch.from_numpy(b.intrinsics).cuda(), torch.from_numpy(b.w2c).cuda(),
+         gsb.RenderParams(cfg.width, cfg.height, fixed_plan=True), rgb)
+torch.cuda.synchronize()
+print("fixed plan ok", g.overflow(), float(rgb.mean()))
+g.reserve(cfg.n_envs, 1, cfg.width, cfg.height, 0, 1000)
+g.render(torch.from_numpy(b.poses).cuda(), torch.from_numpy(b.intrinsics).cuda(), torch.from_numpy(b.w2c).cuda(),
+         gsb.RenderParams(cfg.width, cfg.height, fixed_plan=True), rgb)
+torch.cuda.synchronize()
+print("fixed plan overflow ok", g.overflow())
+n, layers = 3000, 25
+rng = np.random.default_rng(64)
+z = 2.0 + 0.05 * rng.integers(0, layers, n)
+means = np.stack([rng.uniform(-0.3, 0.3, n), rng.uniform(-0.3, 0.3, n), z], 1)
+q = rng.normal(size=(n, 4))
+q /= np.linalg.norm(q, axis=1, keepdims=True)
+sc = scene_from(means, np.exp(rng.uniform(np.log(0.01), np.log(0.04), (n, 3))), q, rng.uniform(0.05, 0.6, n),
+                rng.uniform(0, 1, (n, 3)))
+K, W = identity_cam(fx=100.0, fy=100.0, cx=32.5, cy=32.5)
+g = gsb.Scene.from_synth(sc)
+g.reserve(1, 1, 64, 64)
+os.environ["GSB_K4_SPLIT_MIN"] = "0"
+rgb = torch.zeros((1, 1, 3, 64, 64), device="cuda")
+g.render(None, torch.from_numpy(K[None, None].copy()).cuda(), torch.from_numpy(W[None, None].copy()).cuda(),
+         gsb.RenderParams(64, 64, stats=True), rgb)
+torch.cuda.synchronize()
+os.environ.pop("GSB_K4_SPLIT_MIN")
+print("index sort ties ok", g.stats(), float(rgb.mean()))

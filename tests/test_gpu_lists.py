@@ -2,8 +2,9 @@
 offsets and id lists given the oracle's fp32 projected values"; readings R9, R10).
 
 gsb_debug_tile_lists runs K2b emission and the sort that really feeds compositing in gsb_render
-— K4a's warp-per-list counting sort (<= 1024 keys), its CTA-per-list counting sort and packed
-radix variant (<= 4096), the HBM radix beyond either, and the fused K4's in-CTA sorts — with keys carrying the
+— K4a's warp-per-list counting sort (<= 512 keys), its CTA-per-list index counting sort (<= 4096;
+also the legacy CTA counting sort of the LiDAR path), the HBM radix beyond, and the fused K4's
+in-CTA sorts (count and packed radix) — with keys carrying the
 record slot (the render's default: equal-depth runs re-ordered by creation id) or the id.  The
 inputs are the oracle's projections rounded to fp32, laid out in a random internal (slot)
 order, so every depth tie must be broken through the slot -> id map.  Every (frame, tile) list
@@ -77,11 +78,12 @@ def test_production_tile_lists_small_configs(name):
     _check(arr, zb, va, cfg.width, cfg.height, variants=(0, 1, 2, 3, 4, 5), seed=len(name))
 
 
-@pytest.mark.parametrize("size", [32, 160])
+@pytest.mark.parametrize("size", [32, 64, 160])
 def test_production_tile_lists_ties_and_oversize_lists(size):
-    """32x32: > 4096 keys in one tile (the HBM radix of every variant); 160x160: ~100-300-key lists
-    (K4a's warp path) — both with many exactly equal depths (equal-depth runs longer than 32, the
-    re-keyed fallback, and short runs fixed in place)."""
+    """32x32: > 4096 keys in one tile (the HBM radix of every variant); 64x64: ~500-1000-key lists
+    (K4a's index counting sort); 160x160: ~100-300-key lists (K4a's warp path) — all with many
+    exactly equal depths (equal-depth runs longer than 32, the re-keyed fallback, and short runs
+    fixed in place)."""
     rng = np.random.default_rng(3)
     F, N, W, H = 2, 9000, size, size
     arr = {"u": rng.uniform(2, W - 2, (F, N)), "v": rng.uniform(2, H - 2, (F, N)), "sxx": rng.uniform(0.5, 3, (F, N)),
@@ -97,7 +99,12 @@ def test_production_tile_lists_ties_and_oversize_lists(size):
     va = (rng.random((F, N)) < 0.95).astype(np.uint8)
     offs = _check(arr, zb, va, W, H, variants=(1, 2, 3, 4, 5), seed=5)
     L = np.diff(offs, axis=1)
-    assert (L.max() > 4096) if size == 32 else (L.max() <= 1024 and L.mean() > 100)
+    if size == 32:
+        assert L.max() > 4096
+    elif size == 64:
+        assert L.min() > 512 and L.max() <= 4096
+    else:
+        assert L.max() <= 1024 and L.mean() > 100
 
 
 @pytest.mark.slow
