@@ -289,14 +289,13 @@ class Scene:
                                  GSB_RESERVE_HOST_IO if host_io else 0))
 
     def _check_io(self, B, C, params, poses, intrinsics, w2c, out_rgb, out_depth, out_alpha, out_n_eval, dev):
-        """Shapes the C ABI assumes, checked here (it cannot): inputs and outputs of B x C frames."""
+        """Shapes the C ABI assumes, checked here (it cannot): inputs and outputs of B x C frames.
+        Missing (None) buffers are left to the C ABI, which rejects a NULL required pointer."""
         F, px = B * C, params.width * params.height
         if self.n_bodies and poses is not None:
             _buf(poses, "f32", B * self.n_bodies * 7, "poses", dev)
         _buf(intrinsics, "f32", F * 4, "intrinsics", dev)
         _buf(w2c, "f32", F * 12, "world_to_cam", dev)
-        if out_rgb is None:
-            raise ValueError("out_rgb is required")
         _buf(out_rgb, "f32", F * 3 * px, "out_rgb", dev)
         _buf(out_depth, "f32", F * px, "out_depth", dev)
         _buf(out_alpha, "f32", F * px, "out_alpha", dev)
@@ -308,8 +307,6 @@ class Scene:
             _buf(poses, "f32", B * self.n_bodies * 7, "poses", dev)
         _buf(intrinsics, "f32", F * 4, "intrinsics", dev)
         _buf(w2c, "f32", F * 12, "world_to_cam", dev)
-        if out_rgb8 is None:
-            raise ValueError("out_rgb8 is required")
         _buf(out_rgb8, "u8", F * 3 * px, "out_rgb8", dev)
         _buf(out_depth, "f16" if depth_f16 else "f32", F * px, "out_depth", dev)
         _buf(image_dr, "f32", F * 4, "image_dr", dev)
