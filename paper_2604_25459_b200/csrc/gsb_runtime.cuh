@@ -76,10 +76,12 @@ inline bool split_k4() {
   return v != 0;
 }
 // pass-average list length (keys per tile) from which the split path is used; GSB_K4_SPLIT_MIN
-// overrides it (read per pass: tests force either path)
+// overrides it (read per pass: tests force either path).  Since round 2's K4a and K2b the split
+// path wins at every measured list length (C2 +15 %, C7 +18 %), so the default is 0: the fused
+// one-CTA-per-tile K4 runs only when forced (tests, A/B)
 inline uint64_t split_min_avg() {
   const char* e = getenv("GSB_K4_SPLIT_MIN");
-  return e ? (uint64_t)strtoull(e, nullptr, 10) : 200u;
+  return e ? (uint64_t)strtoull(e, nullptr, 10) : 0u;
 }
 
 inline bool slot_keys_on() {   // GSB_SLOT_KEYS=0: keys carry the creation id on every path
