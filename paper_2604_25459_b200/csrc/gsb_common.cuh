@@ -34,7 +34,7 @@ constexpr float kLog2AlphaMin = -7.99435343685885793f;
 struct FrameCam {
   float fx, fy, cx, cy;
   float limx, limy;  // reading R6: 1.3 * W / (2 fx), 1.3 * H / (2 fy)
-  float pad0, pad1;
+  float kx, ky;      // 1 + limx^2, 1 + limy^2 (K1's conservative screen-cull bound)
 };
 
 // ---------------------------------------------------------------- reading R11 (exact chain)

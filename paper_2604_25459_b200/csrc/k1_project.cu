@@ -96,7 +96,8 @@ __global__ void k0_setup(K0Rig rig, int n_frames, int n_cams, int n_bodies, int 
     fc.fx = K[0]; fc.fy = K[1]; fc.cx = K[2]; fc.cy = K[3];
     fc.limx = 1.3f * (float)width / (2.0f * K[0]);
     fc.limy = 1.3f * (float)height / (2.0f * K[1]);
-    fc.pad0 = fc.pad1 = 0.f;
+    fc.kx = 1.f + fc.limx * fc.limx;   // (1 + lim^2): the screen-cull bound's clamp factor
+    fc.ky = 1.f + fc.limy * fc.limy;
     cams[f] = fc;
   }
 }
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
       const FrameCam cam = a.cams[f];
       const float x = fmaf(r0.x, mean.x, fmaf(r0.y, mean.y, fmaf(r0.z, mean.z, r0.w)));
       const float y = fmaf(r1.x, mean.x, fmaf(r1.y, mean.y, fmaf(r1.z, mean.z, r1.w)));
-      const float iz = __frcp_rn(z);
+      const float iz = __fdividef(1.f, z);   // ~1 ulp: inside reading R28's position bound (K_POS eps S_z)
       const float xz = x * iz, yz = y * iz;
       u = fmaf(cam.fx, xz, cam.cx);
       v = fmaf(cam.fy, yz, cam.cy);
@@ -216,8 +217,8 @@ __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
       // Conservative screen cull: Sigma2D_xx <= jx^2 (1 + limx^2) smax^2 + 0.3 (rows of M are
       // orthonormal, |t/z| <= lim after the clamp), so the exact R9 extents are inside
       // bx, by; a Gaussian whose bound box misses the image has an empty R9 rect as well.
-      const float bx = 1.02f * sqrt_approx(kappa * fmaf(jx * jx * (1.f + cam.limx * cam.limx), smax2, 0.3f)) + 1.f;
-      const float by = 1.02f * sqrt_approx(kappa * fmaf(jy * jy * (1.f + cam.limy * cam.limy), smax2, 0.3f)) + 1.f;
+      const float bx = 1.02f * sqrt_approx(kappa * fmaf(jx * jx * cam.kx, smax2, 0.3f)) + 1.f;
+      const float by = 1.02f * sqrt_approx(kappa * fmaf(jy * jy * cam.ky, smax2, 0.3f)) + 1.f;
       const bool offscreen = (u + bx < 0.f) || (u - bx > fw) || (v + by < 0.f) || (v - by > fh);
       if (!offscreen || debug) {
         // EWA Jacobian with the 1.3 frustum clamp (reading R6), applied to M: rows of J M
@@ -295,7 +296,7 @@ __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
       r[2] = make_float4(rgb.x, rgb.y, rgb.z, z);
       a.emit[(size_t)fl * a.n + i] = make_uint2(__float_as_uint(z), rect);
     }
-    warp_tile_count(vis, rect, a.tiles_x, a.hist + (size_t)fl * a.hist_stride, tile_scratch[threadIdx.x >> 5]);
+    if (bal) warp_tile_count(vis, rect, a.tiles_x, a.hist + (size_t)fl * a.hist_stride, tile_scratch[threadIdx.x >> 5]);
   }
 }
 
