@@ -50,6 +50,11 @@ constexpr double kLidarPi = 3.14159265358979323846;
 // frames per LiDAR chunk: records (80 B) + emission (16 B) per (frame, Gaussian) within ~8 GB
 // (KL4's parallelism is frames x ray groups: sparse patterns such as a height scan need many
 // frames per launch to fill the GPU)
+bool lidar_idx_sort() {
+  const char* e = getenv("GSB_LIDAR_K4A");
+  return !(e && e[0] == 'c');
+}
+
 int lidar_chunk(int64_t n, int F) {
   const int64_t per = std::max<int64_t>(1, n) * 96 + 4096;
   const int64_t e = std::max<int64_t>(1, ((int64_t)8 << 30) / per);
@@ -286,7 +291,9 @@ gsb_status gsb_render_lidar(gsb_scene s, gsb_lidar l, const float* poses, int32_
       k.hist_stride = l->hist_stride; k.key_base = 0; k.fs = 0; k.fe = ne; k.f0 = f0;
       k.n_tiles = n_cells; k.tiles_x = l->n_az; k.inv = s->d_inv; k.slot_base = 0; k.sorted = l->sorted;
       k.keys_internal_ids = l->ids2;
-      launch_k4a_sort(k, false, st);
+      // the cell lists: one CTA each with the index counting sort (<= 4096 keys, HBM radix beyond);
+      // GSB_LIDAR_K4A=cta: the round-1 CTA counting sort (A/B)
+      launch_k4a_sort(k, lidar_idx_sort(), st);
       LidarL4Args b{};
       b.rec = l->rec; b.n = N; b.off = l->off; b.frame_base = l->frame_base; b.hist_stride = l->hist_stride;
       b.sorted = l->sorted; b.rays = l->d_rays; b.items = l->d_items; b.np = l->np;

@@ -14,6 +14,7 @@
 // registers) and loops over the E frames of a chunk, so the shared read-only template (K5)
 // is read from HBM once per chunk, not once per frame.
 #include <algorithm>
+#include <cstdlib>
 
 #include "gsb_common.cuh"
 #include "gsb_kernels.cuh"
@@ -311,7 +312,8 @@ void launch_k1(const K1Args& a, int sh_degree, cudaStream_t s) {
   if (a.n == 0) return;
   // >= ~4 waves of 8 CTAs x 148 SMs: split the frame loop over gridDim.y when N is small
   const unsigned gx = (unsigned)((a.n + 127) / 128);
-  const unsigned gy = (unsigned)std::max(1, std::min(a.n_frames, (int)((4736 + gx - 1) / gx)));
+  unsigned gy = (unsigned)std::max(1, std::min(a.n_frames, (int)((4736 + gx - 1) / gx)));
+  if (const char* e = getenv("GSB_K1_GY")) gy = (unsigned)std::max(1, std::min(a.n_frames, atoi(e)));   // A/B
   const dim3 grid(gx, gy);
   const bool dbg = a.dbg_rec != nullptr;
 #define K1_CASE(D)                                            \
