@@ -310,9 +310,10 @@ void launch_k0(const K0Rig& rig, int n_frames, int n_cams, int n_bodies, int wid
 
 void launch_k1(const K1Args& a, int sh_degree, cudaStream_t s) {
   if (a.n == 0) return;
-  // >= ~4 waves of 8 CTAs x 148 SMs: split the frame loop over gridDim.y when N is small
   const unsigned gx = (unsigned)((a.n + 127) / 128);
-  unsigned gy = (unsigned)std::max(1, std::min(a.n_frames, (int)((4736 + gx - 1) / gx)));
+  // >= ~8 waves of 8 CTAs x 148 SMs: each CTA loops over E / gy frames, so a CTA is short enough
+  // that the last wave's tail stays small (C3: gy = 2, +0.7 % over one row; C4: 6)
+  unsigned gy = (unsigned)std::max(1, std::min(a.n_frames, (int)((9472 + gx - 1) / gx)));
   if (const char* e = getenv("GSB_K1_GY")) gy = (unsigned)std::max(1, std::min(a.n_frames, atoi(e)));   // A/B
   const dim3 grid(gx, gy);
   const bool dbg = a.dbg_rec != nullptr;
