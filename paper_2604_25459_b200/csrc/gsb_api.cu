@@ -192,15 +192,19 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
   s->tiles_y = (height + kTile - 1) / kTile;
   s->n_tiles = s->tiles_x * s->tiles_y;
   s->hist_stride = ((int64_t)s->n_tiles + 2 + 31) / 32 * 32;
-  // automatic chunk: >= 64 frames and ~64k tiles per chunk (small views get bigger chunks so
-  // every K4 launch has many waves of CTAs).  256k tiles would gain 0.3-0.7 % on device-resident
-  // renders (same-box sweep) but costs ~10 % end to end: gsb_render_host downloads each pass while
-  // the next one renders, and the last pass's download is not overlapped
-  const char* ct = getenv("GSB_CHUNK_TILES");   // experiments: tiles per automatic chunk
-  const int64_t chunk_tiles = ct ? std::max<int64_t>(1, atoll(ct)) : 65536;
-  const int auto_e = (int)std::min<int64_t>(kMaxChunk, std::max<int64_t>(64, (chunk_tiles + s->n_tiles - 1) / s->n_tiles));
-  const int E = (int)std::min<int64_t>(chunk_frames > 0 ? std::min(chunk_frames, kMaxChunk) : auto_e, F);
+  // automatic chunk: >= 64 frames and ~256k tiles per chunk for device-resident renders (each
+  // chunk's persistent K4b ends with a tail and its binning with a ramp: fewer, larger chunks
+  // are +1.5 % on C3 over 64k tiles, same-box), but ~64k tiles for gsb_render_host, which
+  // downloads each pass while the next renders (the last pass's download is not overlapped: 256k
+  // tiles cost ~10 % end to end).  Both use the same buffers (the host chunk is the smaller).
+  const char* ct = getenv("GSB_CHUNK_TILES");   // experiments: tiles per automatic device chunk
+  const int64_t chunk_tiles = ct ? std::max<int64_t>(1, atoll(ct)) : 262144;
+  auto auto_chunk = [&](int64_t tiles) {
+    return (int)std::min<int64_t>(kMaxChunk, std::max<int64_t>(64, (tiles + s->n_tiles - 1) / s->n_tiles));
+  };
+  const int E = (int)std::min<int64_t>(chunk_frames > 0 ? std::min(chunk_frames, kMaxChunk) : auto_chunk(chunk_tiles), F);
   s->chunk = E;
+  s->chunk_host = chunk_frames > 0 ? E : (int)std::min<int64_t>(E, auto_chunk(65536));
   int64_t cap = key_capacity;
   if (cap == 0) cap = std::max<int64_t>((int64_t)1 << 22, std::min<int64_t>(3 * (int64_t)E * std::max<int64_t>(s->n, 1), ((int64_t)1 << 32) - 1));
   s->cap = cap;

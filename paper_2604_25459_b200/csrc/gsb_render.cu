@@ -283,7 +283,7 @@ struct Pipeline {
   }
 
   gsb_status run_chunks() {
-    const int E = s->chunk;
+    const int E = (s->dl_rgb || s->dl_rgb8) ? s->chunk_host : s->chunk;   // host-io: smaller chunks
     const int nchunks = (F + E - 1) / E;
     for (int c = 0; c < nchunks; ++c) {
       const int f0 = c * E, nf = std::min(E, F - f0);

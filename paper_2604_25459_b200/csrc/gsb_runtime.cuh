@@ -122,6 +122,7 @@ struct gsb_scene_t {
   // reservation
   bool reserved = false;
   int max_frames = 0, res_w = 0, res_h = 0, chunk = 0;
+  int chunk_host = 0;   // frames per chunk of host-buffer renders (<= chunk)
   int tiles_x = 0, tiles_y = 0, n_tiles = 0;
   int64_t hist_stride = 0;
   int64_t cap = 0;
