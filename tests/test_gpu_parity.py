@@ -365,8 +365,17 @@ def test_edge_cases_empty_culled_tiny_and_lower_sh():
     assert r["rgb_fail"] == 0, r
 
 
-def test_host_path_matches_device_path():
-    cfg = synth.CONFIGS["T1"]
+@pytest.mark.parametrize("name", ["T1", "T2@640x480x70"])
+def test_host_path_matches_device_path(name):
+    """gsb_render_host equals gsb_render bit for bit.  The 640x480 case with 70 envs renders the
+    device path in one ~256k-tile chunk and the host path in 64-frame chunks (its downloads
+    overlap the next chunk): chunking never changes a frame."""
+    import dataclasses
+    base, _, size = name.partition("@")
+    cfg = synth.CONFIGS[base]
+    if size:
+        w, h, envs = (int(x) for x in size.split("x"))
+        cfg = dataclasses.replace(cfg, width=w, height=h, n_envs=envs)
     sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
     dev = gu.gpu_render(sc, b, cfg.width, cfg.height)
     g = gsb.Scene.from_synth(sc)
