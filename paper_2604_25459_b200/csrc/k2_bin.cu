@@ -78,28 +78,69 @@ __global__ void __launch_bounds__(kScanThreads) k2_scan_tiles(int* __restrict__ 
 // (mapped pinned memory) the values the host needs to size the binning — frame bases, longest
 // list, visible counts, long-list count — are also written straight to host memory, so the
 // readback never queues behind output copies on the copy engine.
-__global__ void k2_scan_frames(const uint32_t* __restrict__ off, int64_t stride, int n_tiles,
-                               int n_frames, uint64_t* __restrict__ frame_base, const int* __restrict__ vcount,
-                               const uint32_t* __restrict__ long_count, volatile uint64_t* __restrict__ host,
-                               int* __restrict__ overflow, int* __restrict__ sticky, uint64_t key_cap) {
-  if (threadIdx.x != 0) return;
-  uint64_t acc = 0, mx = 0;
-  for (int f = 0; f < n_frames; ++f) {
-    frame_base[f] = acc;
-    if (host) host[f] = acc;
-    acc += off[(size_t)f * stride + n_tiles];
-    mx = max(mx, (uint64_t)off[(size_t)f * stride + n_tiles + 1]);
+__global__ void __launch_bounds__(kScanThreads) k2_scan_frames(
+    const uint32_t* __restrict__ off, int64_t stride, int n_tiles, int n_frames, uint64_t* __restrict__ frame_base,
+    const int* __restrict__ vcount, const uint32_t* __restrict__ long_count, volatile uint64_t* __restrict__ host,
+    int* __restrict__ overflow, int* __restrict__ sticky, uint64_t key_cap) {
+  // block-wide exclusive scan of the frames' key counts, kScanThreads frames at a time (a single
+  // thread walking 1024 frames cost 0.4 ms per C4 chunk)
+  __shared__ unsigned long long wsum[kScanThreads / 32];
+  __shared__ unsigned long long carry_s, mx_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) carry_s = 0ull, mx_s = 0ull;
+  __syncthreads();
+  unsigned long long mx = 0ull;
+  for (int base = 0; base < n_frames; base += kScanThreads) {
+    const int f = base + tid;
+    const unsigned long long x = f < n_frames ? (unsigned long long)off[(size_t)f * stride + n_tiles] : 0ull;
+    if (f < n_frames) mx = max(mx, (unsigned long long)off[(size_t)f * stride + n_tiles + 1]);
+    unsigned long long inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const unsigned long long w = wsum[lane];
+      unsigned long long wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      wsum[lane] = wi - w;
+    }
+    __syncthreads();
+    const unsigned long long excl = carry_s + wsum[warp] + inc - x;
+    if (f < n_frames) {
+      frame_base[f] = excl;
+      if (host) {
+        host[f] = excl;
+        host[n_frames + 2 + f] = vcount ? (uint64_t)vcount[f] : 0ull;
+      }
+    }
+    __syncthreads();
+    if (tid == kScanThreads - 1) carry_s = excl + x;
+    __syncthreads();
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) atomicMax(&mx_s, mx);
+  if (host) __threadfence_system();   // this thread's mapped-memory writes
+  __syncthreads();
+  if (tid != 0) return;
+  const uint64_t acc = carry_s;
   frame_base[n_frames] = acc;
-  frame_base[n_frames + 1] = mx;
+  frame_base[n_frames + 1] = mx_s;
   if (overflow) {   // fixed plan: one pass per chunk; the chunk is skipped when it does not fit
     *overflow = acc > key_cap ? 1 : 0;            // this chunk (its slot's flag)
     if (acc > key_cap) *sticky = 1;               // read and reset by gsb_get_overflow
   }
   if (host) {
     host[n_frames] = acc;
-    host[n_frames + 1] = mx;
-    for (int f = 0; f < n_frames; ++f) host[n_frames + 2 + f] = vcount ? (uint64_t)vcount[f] : 0ull;
+    host[n_frames + 1] = mx_s;
     host[2 * n_frames + 2] = long_count ? (uint64_t)long_count[0] : 0ull;
     host[2 * n_frames + 3] = long_count ? (uint64_t)long_count[1] : 0ull;
     __threadfence_system();
@@ -112,7 +153,7 @@ void launch_k2_scan(int* hist, uint32_t* off, int64_t hist_stride, int n_frames,
                     uint64_t key_cap) {
   k2_scan_tiles<<<n_frames, kScanThreads, 0, s>>>(hist, off, hist_stride, n_tiles, long_list, long_count,
                                                   long_thresh);
-  k2_scan_frames<<<1, 32, 0, s>>>(off, hist_stride, n_tiles, n_frames, frame_base, vcount, long_count,
+  k2_scan_frames<<<1, kScanThreads, 0, s>>>(off, hist_stride, n_tiles, n_frames, frame_base, vcount, long_count,
                                   host_mapped, overflow, sticky, key_cap);
 }
 
