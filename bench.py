@@ -482,8 +482,12 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
         threads = os.cpu_count() or 1
+        # three samples (median, as the reference arm's steps): env 0 of the last timed step (also
+        # the live parity frame), then two more envs / pose steps
         smp = oracle_sample(cfg, scene, int(env_ids[0]), last_step, seed=0, threads=threads)
-        cpu = baseline_record([smp], threads, cfg, oracle_c1_full_frame(threads))
+        more = [oracle_sample(cfg, scene, int(env_ids[(k * B) // 3]), (last_step + k) % n_pose_sets, seed=k,
+                              threads=threads) for k in (1, 2)]
+        cpu = baseline_record([smp] + more, threads, cfg, oracle_c1_full_frame(threads))
         px, py = smp["px"], smp["py"]
         g_rgb = rgb[0, 0].permute(1, 2, 0).cpu().numpy()[py, px]
         g_dep = dep[0, 0].cpu().numpy()[py, px]

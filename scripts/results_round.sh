@@ -1,7 +1,7 @@
 #!/bin/bash
 # one bench line per config + the reference arm + a 2-rank run + graph timings (results table)
 # usage (on the GPU box): R=r2 bash scripts/results_round.sh
-R=${R:-r2}
+export R=${R:-r2}
 O=gpurun_out/${R}_results.jsonl
 : > $O
 timeout 900 python bench.py --steps 10 --warmup 3 >> $O 2> gpurun_out/${R}_bench_c3.err; echo c3=$?
@@ -14,7 +14,8 @@ GSB_DIST_BACKEND=gloo timeout 900 python bench.py --gpus 2 --steps 5 --warmup 3 
 timeout 600 python scripts/graph_bench.py C1 T1 C2 C3 > gpurun_out/${R}_graph_bench.jsonl 2>&1; echo graph=$?
 python - <<'PY'
 import json
-for l in open("gpurun_out/r2_results.jsonl"):
+import os
+for l in open("gpurun_out/%s_results.jsonl" % os.environ.get("R", "r2")):
     d = json.loads(l)
     print(d.get("impl", "gsb"), d["config"]["workload"][:40], round(d["value"], 1), d.get("n_gpus"),
           (d.get("path_roofline") or {}).get("frac"), (d.get("e2e") or {}).get("value"))
