@@ -34,8 +34,14 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 FP32_OPS_PER_PAIR = 18      # SURVEY §8(d) d.4 / DESIGN.md §6: compositing ops per evaluated pair
+# ... of which 14 are fp32 arithmetic (FMA pipe: dx, dy, quadratic form 5, +log2 o, tT, w, 4
+# accumulations), 4 compare/min (ALU pipe) and 1 ex2 (XU).  On sm_100a the FMA pipe runs 128
+# lanes/SM/clock for FFMA and packed FFMA2 alike while FFMA2 needs half the issue slots, so the
+# pair rate is bounded by the FMA pipe (14 / 128), not by issue (K4b roofline);
+# measured pipe rates: scripts/micro/ffma2_rate.cu (profiles/r3_pipe_rates.jsonl)
+FMA_OPS_PER_PAIR = 14
 SM_COUNT = 148
-LANES_PER_SM = 128
+LANES_PER_SM = 128          # FMA-pipe lanes per SM
 HASH_PROBE_ENVS = 4         # envs per rank whose frames are re-rendered by rank 0 alone
 # the paper's own number (context, not a target): "up to 2048 scenes at 640x480 with a total
 # throughput of up to 10,000 FPS", "~10k" 3DGS render FPS at 640x480 on an RTX 4090 +
@@ -428,7 +434,9 @@ def main():
     k4_avg_ms = sum(comp_ms) / max(sum(comp_launches), 1)
     pairs_per_launch = st["P"] / max(comp_launches[0], 1)
     achieved = FP32_OPS_PER_PAIR * pairs_per_launch / (k4_avg_ms / 1e3) / 1e12
-    peak = SM_COUNT * LANES_PER_SM * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    fma_rate = SM_COUNT * LANES_PER_SM * peaks.get("sm_max_mhz", 1965.0) * 1e6   # fp32 FMA-pipe ops/s
+    # the 18-op pair's peak rate: one pair per 14 FMA-pipe lane-cycles (the binding pipe)
+    peak = FP32_OPS_PER_PAIR * fma_rate / FMA_OPS_PER_PAIR / 1e12
     # whole-path roofline: T_roof = max(B_alg / BW, Ops_alg / R_fp32) per
     # step, from the oracle's work counts (V, K, P of the STATS render), not from our SASS
     F_step = B * C
@@ -436,15 +444,17 @@ def main():
     chunk_e = 64
     b_alg = F_step * ((240 if cfg.sh_degree == 3 else 60) * n_g / chunk_e + 8 * n_g) \
         + 108 * st["V"] + 32 * st["K"] + 16 * W * H * F_step
-    ops_alg = FP32_OPS_PER_PAIR * st["P"] + 15 * n_g * F_step + (190 if cfg.sh_degree == 3 else 105) * st["V"]
+    ops_alg = FMA_OPS_PER_PAIR * st["P"] + 15 * n_g * F_step + (190 if cfg.sh_degree == 3 else 105) * st["V"]
     bw = peaks.get("hbm_gbs", 6546.6) * 1e9
-    t_hbm, t_alu = b_alg / bw, ops_alg / (peak * 1e12)
+    t_hbm, t_alu = b_alg / bw, ops_alg / fma_rate
     t_roof = max(t_hbm, t_alu)
     path_roof = {"t_roof_ms_per_step": t_roof * 1e3, "bound": "alu" if t_alu >= t_hbm else "hbm",
                  "t_alu_ms": t_alu * 1e3, "t_hbm_ms": t_hbm * 1e3,
                  "frac": t_roof / (t_max / args.steps),
-                 "basis": "B_alg = (240|60)N/64 + 8N + 108V + 32K + 16Npx bytes and Ops_alg = 18P + 15N + "
-                          "(190|105)V fp32 ops per frame (SURVEY §8(d) d.4); BW = MEASURED_PEAKS hbm_gbs"}
+                 "basis": "B_alg = (240|60)N/64 + 8N + 108V + 32K + 16Npx bytes and Ops_alg = 14P + 15N + "
+                          "(190|105)V FMA-pipe fp32 ops per frame (SURVEY §8(d) d.4; 14 of the 18 ops per pair "
+                          "are FMA-pipe arithmetic, the 4 compares run on the ALU pipe); BW = MEASURED_PEAKS "
+                          "hbm_gbs; R = 148 SM x 128 FMA lanes x f"}
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "k4_ncu_summary.json")) as f:
@@ -527,8 +537,11 @@ def main():
                          "unit": "Top/s (fp32 thread-ops)", "frac": achieved / peak, "traffic": traffic,
                          "ops_per_launch": FP32_OPS_PER_PAIR * pairs_per_launch,
                          "avg_launch_ms": k4_avg_ms,
-                         "peak_basis": f"148 SM x 128 lanes x {peaks.get('sm_max_mhz', 1965.0)} MHz "
-                                       f"(B200_PROFILING.md unit counts; clock from MEASURED_PEAKS.json, {peaks_kind})"},
+                         "peak_basis": f"18 ops per pair x (148 SM x 128 FMA-pipe lanes x "
+                                       f"{peaks.get('sm_max_mhz', 1965.0)} MHz) / 14 FMA-pipe ops per pair: the FMA "
+                                       f"pipe binds (FFMA2 halves issue, not FMA-pipe time; ALU 4/64 and XU 1/16 "
+                                       f"lane-cycles per pair are below 14/128); unit counts B200_PROFILING.md and "
+                                       f"scripts/micro/ffma2_rate.cu, clock from MEASURED_PEAKS.json ({peaks_kind})"},
             "path_roofline": path_roof,
             "stage_ms_per_step": tsum,
             "counters": {"V_per_frame": st["V"] / (B * C), "K_per_frame": st["K"] / (B * C),

@@ -71,6 +71,65 @@ __device__ __forceinline__ float2 blend2(bool use0, float arg0, bool use1, float
   return make_float2(w0, w1);
 }
 
+// ---- packed binary32 pairs (sm_100a FFMA2 / FADD2 / FMUL2) ------------------------------------
+// A thread's two pixels share every per-record term; their per-pixel terms (vertical offset,
+// quadratic form, weight, transmittance, the four accumulators) are held as (pixel 0, pixel 1)
+// pairs in one 64-bit register pair and updated by one packed instruction instead of two.  Each
+// half is an IEEE binary32 RN operation, so the results equal the scalar code's bit for bit;
+// ptxas folds a scalar operand into a broadcast (`R.F32`) and a negation into the operand.
+typedef float2 f32x2;
+
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) { return make_float2(lo, hi); }
+__device__ __forceinline__ float2 up2(f32x2 v) { return v; }
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ f32x2 nfma2(f32x2 a, f32x2 b, f32x2 c) {   // fma(-a, b, c) per half
+  return __ffma2_rn(make_float2(-a.x, -a.y), b, c);
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) { return __fmul2_rn(a, b); }
+
+// acc += a * (x, x)
+__device__ __forceinline__ void acc2(f32x2& acc, f32x2 a, float x) { acc = __ffma2_rn(a, make_float2(x, x), acc); }
+
+// blend2() on packed pairs: T = (T0, T1), the accumulators R, G, B, D = (pixel 0, pixel 1) and
+// PYC = (pyc0, pyc1).  Same operations in the same order as blend2(), bit for bit.  The rare
+// termination entry takes its own copy of the accumulation, so the common path has no merge of
+// the weight and transmittance pairs (which would cost register-pair copies per entry).
+// `argn` is the next entry's quadratic form, evaluated ahead with the current pixel centres; a
+// pixel that terminates here has it set to -inf (alpha 0), as its moved centre would give.
+__device__ __forceinline__ f32x2 blend2p(f32x2 arg, const float4& r2, f32x2& T, f32x2& R, f32x2& G, f32x2& B,
+                                         f32x2& D, f32x2& PYC, int& ne0, int& ne1, int idx, f32x2& argn) {
+  const float2 ag = up2(arg);
+  const float a0 = ag.x >= kLog2AlphaMin ? fminf(kAlphaMax, ex2_approx(ag.x)) : 0.f;   // alpha >= 1/255
+  const float a1 = ag.y >= kLog2AlphaMin ? fminf(kAlphaMax, ex2_approx(ag.y)) : 0.f;
+  f32x2 w = mul2(pk2(a0, a1), T);
+  const f32x2 t = sub2(T, w);                            // T (1 - alpha)
+  const float2 tt = up2(t);
+  const bool s0 = tt.x < kTermT, s1 = tt.y < kTermT;     // stop before blending (R13)
+  if (__any_sync(0xffffffffu, s0 || s1)) {
+    float2 ww = up2(w), tn = tt, pc = up2(PYC);
+    const float2 T2 = up2(T);
+    float2 an = up2(argn);
+    if (s0) { ne0 = idx + 1; pc.x = kFar; ww.x = 0.f; tn.x = T2.x; an.x = -INFINITY; }
+    if (s1) { ne1 = idx + 1; pc.y = kFar; ww.y = 0.f; tn.y = T2.y; an.y = -INFINITY; }
+    w = pk2(ww.x, ww.y);
+    PYC = pk2(pc.x, pc.y);
+    argn = pk2(an.x, an.y);
+    acc2(R, w, r2.x);
+    acc2(G, w, r2.y);
+    acc2(B, w, r2.z);
+    acc2(D, w, r2.w);
+    T = pk2(tn.x, tn.y);
+  } else {
+    acc2(R, w, r2.x);
+    acc2(G, w, r2.y);
+    acc2(B, w, r2.z);
+    acc2(D, w, r2.w);
+    T = t;
+  }
+  return w;
+}
+
 // Reading R31 noise: counter-based Irwin-Hall(4) of 22-bit lowbias32-hashed uniforms (exact
 // integer arithmetic, so the oracle reproduces every draw); z * sqrt(3)/2^22 has unit variance.
 __device__ __forceinline__ uint32_t mix32(uint32_t x) {

@@ -402,13 +402,6 @@ __global__ void __launch_bounds__(kSortThreadsA) k4a_idx_sort(CompositeArgs a) {
 #endif
 constexpr int kWarpBits = GSB_WARP_BITS;
 constexpr int kWarpBins = 1 << kWarpBits;
-// K4b's selected-record loop keeps an outer i0 loop (one pass: nsel <= 32) whose end repeats the
-// round's "all pixels done" vote.  Both are redundant by logic, yet removing them measures -0.8 %
-// on C3 and -0.5 % on C4 (same-box A/B, r2; -1.0 % in r1): the code layout they produce schedules
-// the hot loop better.  GSB_K4B_I0=0 builds the plain form for A/B.
-#ifndef GSB_K4B_I0
-#define GSB_K4B_I0 1
-#endif
 #ifndef GSB_K4A_IDX
 #define GSB_K4A_IDX 1   // 0: the long lists by count_sort<1024> / packed_sort<4096> (A/B comparisons)
 #endif
@@ -534,6 +527,10 @@ __global__ void __launch_bounds__(kK4aWarps * 32) k4a_warp_sort(CompositeArgs a,
 // ------------------------------------------------------------------------------ K4b
 constexpr int kBlendWarps = 4;
 constexpr int kWarpBatch = 32;   // records staged per warp round (one per lane)
+#ifndef GSB_K4B_UNROLL
+#define GSB_K4B_UNROLL 2
+#endif
+constexpr int kBlendUnroll = GSB_K4B_UNROLL;   // unroll of the selected-record loop
 
 template <int N>
 __device__ __forceinline__ void cp_async_wait_group() {
@@ -547,11 +544,9 @@ template <bool SCORE>
 __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a, int* __restrict__ counter,
                                                                   int n_items) {
   __shared__ __align__(16) float4 stg[kBlendWarps][2][3][kWarpBatch];   // 12 KB
-  __shared__ uint8_t wlist[kBlendWarps][kWarpBatch];   // a round's records that reach the block
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float4 (*S)[3][kWarpBatch] = stg[warp];
-  uint8_t* wl = wlist[warp];
   for (;;) {   // (fixed plan: an overflowed chunk's counter starts at n_items, see launch_k4b_blend)
     int item = 0;
     if (lane == 0) item = atomicAdd(counter, 1);
@@ -574,12 +569,16 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
     const float pxc = (float)px + 0.5f;
     const float bcx = (float)bx0 + 4.0f, bcy = (float)by0 + 4.0f;  // block centre (pixel centres +-3.5)
 
-    float T0 = 1.f, r0c = 0.f, g0c = 0.f, b0c = 0.f, d0 = 0.f;
-    float T1 = 1.f, r1c = 0.f, g1c = 0.f, b1c = 0.f, d1 = 0.f;
-    float pyc0 = in0 ? (float)py0 + 0.5f : kFar;   // out-of-image pixels never pass the alpha test
-    float pyc1 = in1 ? (float)py0 + 1.5f : kFar;
+    // per-pixel state as (pixel 0, pixel 1) pairs (packed FFMA2/FADD2/FMUL2, k4_common.cuh)
+    f32x2 T = pk2(1.f, 1.f), R = pk2(0.f, 0.f), G = R, Bc = R, D = R;
+    // out-of-image pixels never pass the alpha test
+    f32x2 PYC = pk2(in0 ? (float)py0 + 0.5f : kFar, in1 ? (float)py0 + 1.5f : kFar);
+    auto all_done = [&]() {
+      const float2 pc = up2(PYC);
+      return __all_sync(FULL, pc.x == kFar && pc.y == kFar);
+    };
     int ne0 = len, ne1 = len;
-    const int rounds = __all_sync(FULL, pyc0 == kFar && pyc1 == kFar) ? 0 : (len + kWarpBatch - 1) / kWarpBatch;
+    const int rounds = all_done() ? 0 : (len + kWarpBatch - 1) / kWarpBatch;
 
     // stage round b (slot sl of this lane's record) into buffer b & 1; the slot of the round
     // after the next is read one round ahead, so no cp.async waits on a slot load
@@ -612,16 +611,19 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
         cp_async_wait_group<0>();
       }
       __syncwarp();
-      const float4* R0 = S[b & 1][0];
-      const float4* R1 = S[b & 1][1];
-      const float4* R2 = S[b & 1][2];
+      float4* R0 = S[b & 1][0];
+      float4* R1 = S[b & 1][1];
+      float4* R2 = S[b & 1][2];
       const int base = b * kWarpBatch;
       // this round's records that can reach the block (lower bound of the whitened quadratic
       // form over the block's pixel centres, 2 % margin: no per-pixel decision changes)
       bool ov = false;
+      float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q2 = q0;
+      float2 q1 = make_float2(0.f, 0.f);
       if (base + lane < len) {
-        const float4 q0 = R0[lane];
-        const float2 q1 = *reinterpret_cast<const float2*>(&R1[lane]);
+        q0 = R0[lane];
+        q1 = *reinterpret_cast<const float2*>(&R1[lane]);
+        q2 = R2[lane];
         const float xa = q0.x - (bcx + 3.5f), xb = q0.x - (bcx - 3.5f);
         const float ya = q0.y - (bcy + 3.5f), yb = q0.y - (bcy - 3.5f);
         const float dxm = fmaxf(fmaxf(xa, -xb), 0.f);
@@ -633,61 +635,64 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
         ov = lbq <= fmaf(q1.y - kLog2AlphaMin, 1.02f, 0.02f);
       }
       const unsigned hit = __ballot_sync(FULL, ov);
-      if (ov) wl[__popc(hit & lanemask_lt())] = (uint8_t)lane;
+      // the selected records moved, in order, to the front of the buffer (in place: every lane
+      // read its own record above), with the record's lane in R1.z for n_eval and scores; the
+      // loop then reads them at warp-uniform, consecutive addresses (broadcast loads, no index)
+      __syncwarp();
+      if (ov) {
+        const int k = __popc(hit & lanemask_lt());
+        R0[k] = q0;
+        R1[k] = make_float4(q1.x, q1.y, __int_as_float(lane), 0.f);
+        R2[k] = q2;
+      }
       __syncwarp();
       const int nsel = __popc(hit);
-#if GSB_K4B_I0
-      for (int i0 = 0; i0 < nsel; i0 += 32) {
-        const int i1 = min(nsel, i0 + 32);
-#pragma unroll 2
-        for (int i = i0; i < i1; ++i) {
-#else
-      {   // nsel <= 32: one pass over the selected records
-#pragma unroll 2
-        for (int i = 0; i < nsel; ++i) {
-#endif
-        const int j = wl[i];
-        const float4 q0 = R0[j];                                   // u, v, p, q
-        const float2 q1 = *reinterpret_cast<const float2*>(&R1[j]);  // r, log2 o
-        const float dx = q0.x - pxc;
-        const float t1 = q0.z * dx;
-        const float mm = fmaf(-t1, t1, q1.y);
-        const float qdx = q0.w * dx;
-        const float ta = fmaf(q1.x, q0.y - pyc0, qdx);
-        const float tb = fmaf(q1.x, q0.y - pyc1, qdx);
-        const float arg0 = fmaf(-ta, ta, mm);
-        const float arg1 = fmaf(-tb, tb, mm);
-        const bool use0 = arg0 >= kLog2AlphaMin;   // alpha >= 1/255
-        const bool use1 = arg1 >= kLog2AlphaMin;
+      // the quadratic form of selected record i (log2 of o e^power) for both pixels:
+      // ta = r (v - pyc) + q dx;  arg = log2 o - (p dx)^2 - ta^2
+      auto arg_of = [&](int i) -> f32x2 {
+        const float4 q0 = R0[i];                                   // u, v, p, q
+        const float2 q1 = *reinterpret_cast<const float2*>(&R1[i]);  // r, log2 o
+        const float dx = q0.x - pxc;                               // shared by both pixels
+        const f32x2 pq = mul2(pk2(q0.z, q0.w), pk2(dx, dx));      // (p dx, q dx)
+        const float mm = fmaf(-pq.x, pq.x, q1.y);
+        const f32x2 ta = fma2(pk2(q1.x, q1.x), sub2(pk2(q0.y, q0.y), PYC), pk2(pq.y, pq.y));
+        return nfma2(ta, ta, pk2(mm, mm));
+      };
+      // software pipeline: record i + 1's quadratic form is evaluated while record i blends (the
+      // two chains are independent; blend2p sets it to -inf for a pixel that terminates at i).
+      // Index nsel <= 32 reads the next sub-array of the staging buffer: in bounds, never used.
+      f32x2 argn = nsel > 0 ? arg_of(0) : pk2(0.f, 0.f);
+#pragma unroll kBlendUnroll
+      for (int i = 0; i < nsel; ++i) {
+        const f32x2 arg = argn;
+        argn = arg_of(i + 1);
         // no "does any lane blend" vote: after the block cull almost every staged record is used
-        // by some lane, and for the others blend2 is an exact no-op (w = 0: T, colour and depth
+        // by some lane, and for the others blend2p is an exact no-op (w = 0: T, colour and depth
         // unchanged), so the vote and its branch only cost issue slots (+4.8 % C3, same-box A/B)
-        const float4 q2 = R2[j];                                 // r, g, b, z
-        const float2 wb = blend2(use0, arg0, use1, arg1, q2, T0, r0c, g0c, b0c, d0, pyc0, ne0, T1, r1c, g1c, b1c,
-                                 d1, pyc1, ne1, base + j);
-        const float wb0 = wb.x, wb1 = wb.y;
+        const float4 q2 = R2[i];                                   // r, g, b, z
+        const int j = __float_as_int(R1[i].z);                     // the record's round position
+        const f32x2 wb = blend2p(arg, q2, T, R, G, Bc, D, PYC, ne0, ne1, base + j, argn);
         if constexpr (SCORE) {
-          const uint32_t tot = __reduce_add_sync(FULL, __float2uint_rn((wb0 + wb1) * kScoreFix));
-          const uint32_t mx = __reduce_max_sync(FULL, __float_as_uint(fmaxf(wb0, wb1)));
+          const float2 w2 = up2(wb);
+          const uint32_t tot = __reduce_add_sync(FULL, __float2uint_rn((w2.x + w2.y) * kScoreFix));
+          const uint32_t mx = __reduce_max_sync(FULL, __float_as_uint(fmaxf(w2.x, w2.y)));
           const uint32_t g = __shfl_sync(FULL, sl_cur, j) + (uint32_t)a.slot_base;
           if (lane == 0 && tot) {
             atomicAdd(a.score_sum + g, (float)tot * (1.f / kScoreFix));
             atomicMax(a.score_max + g, mx);
           }
         }
-        }
-#if GSB_K4B_I0
-        if (__all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) break;
-#endif
       }
       __syncwarp();   // buffer b & 1 is free for round b + 2
       sl_cur = sl_stg;
-      if (__all_sync(FULL, pyc0 == kFar && pyc1 == kFar)) break;
+      if (all_done()) break;
     }
     cp_async_wait_all();   // nothing may land in the buffers after this item
     __syncwarp();
-    store_pixels(a, (size_t)(a.f0 + fl), px, py0, in0, in1, T0, r0c, g0c, b0c, d0, ne0, T1, r1c, g1c, b1c, d1,
-                 ne1);
+    const float2 T2 = up2(T), R2p = up2(R), G2 = up2(G), B2 = up2(Bc), D2 = up2(D), pc = up2(PYC);
+    store_pixels(a, (size_t)(a.f0 + fl), px, py0, in0, in1, T2.x, R2p.x, G2.x, B2.x, D2.x, ne0, T2.y, R2p.y, G2.y,
+                 B2.y, D2.y, ne1);
+    const float pyc0 = pc.x, pyc1 = pc.y;
     if (a.stat_pairs) {
       unsigned long long v = (in0 ? (unsigned long long)ne0 : 0ull) + (in1 ? (unsigned long long)ne1 : 0ull);
 #pragma unroll
