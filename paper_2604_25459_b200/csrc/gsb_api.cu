@@ -61,7 +61,7 @@ gsb_status gsb_create_scene(const float* means, const float* scales, const float
     return fail(GSB_ERR_INVALID_ARGUMENT, "non-finite template value");
   gsb_status st = check_device(device);
   if (st != GSB_OK) return st;
-  const int np = (3 * nc + 3) / 4;
+  const int np = 3 * ((nc + 3) / 4);   // 3 float4 planes per group of 4 coefficients (gsb_common.cuh)
   for (int64_t i = 0; i < n; ++i) {
     const int b = body_id[i];
     if (b < -1 || b >= n_bodies) return fail(GSB_ERR_UNKNOWN_BODY, "body_id[%lld] = %d not in [-1, %d)", (long long)i, b, n_bodies);
@@ -133,13 +133,13 @@ gsb_status gsb_create_scene(const float* means, const float* scales, const float
     h0[j] = make_float4(L[0], L[1], L[2], L[3]);
     h1[j] = make_float4(L[4], L[5], L[6], L[7]);
     h2[j] = make_float4(L[8], opacities[i], (float)(2.0 * std::log(255.0 * o)), (float)std::log2(o));
-    for (int pl = 0; pl < np; ++pl) {
-      float v4[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int k = 0; k < 4; ++k) {
-        const int fidx = 4 * pl + k;
-        if (fidx < 3 * nc) v4[k] = sh[(size_t)i * 3 * nc + fidx];
-      }
-      hs[(size_t)pl * n + j] = make_float4(v4[0], v4[1], v4[2], v4[3]);
+    // group g of coefficients k = 4g .. 4g+3: (r, g) of k, k+1 | (r, g) of k+2, k+3 | b of all four
+    auto coef = [&](int k, int ch) { return k < nc ? sh[(size_t)i * 3 * nc + 3 * k + ch] : 0.f; };
+    for (int g4 = 0; g4 < np / 3; ++g4) {
+      const int k = 4 * g4;
+      hs[(size_t)(3 * g4) * n + j] = make_float4(coef(k, 0), coef(k, 1), coef(k + 1, 0), coef(k + 1, 1));
+      hs[(size_t)(3 * g4 + 1) * n + j] = make_float4(coef(k + 2, 0), coef(k + 2, 1), coef(k + 3, 0), coef(k + 3, 1));
+      hs[(size_t)(3 * g4 + 2) * n + j] = make_float4(coef(k, 2), coef(k + 1, 2), coef(k + 2, 2), coef(k + 3, 2));
     }
   }
   DeviceGuard g(device);

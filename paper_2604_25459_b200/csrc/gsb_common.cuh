@@ -9,8 +9,11 @@
 //     g_L0[N]    = (L00, L01, L02, L10)   L = R(q_i) diag(s_i): Sigma_local = L L^T
 //     g_L1[N]    = (L11, L12, L20, L21)
 //     g_L2[N]    = (L22, opacity, kappa = 2 ln(255 o), log2 o)
-//     g_sh[P][N] = SH coefficients, P = ceil(3 (D+1)^2 / 4) float4 planes, coefficient-major
-//   per frame-body table (K0 -> K1): 4 float4 = M row 0 | m0, row 1 | m1, row 2 | m2, c_body
+//     g_sh[P][N] = SH coefficients, P = 3 ceil((D+1)^2 / 4) float4 planes: per group of four
+//                  coefficients k..k+3 (degree order), (r_k, g_k, r_k+1, g_k+1), (r_k+2, g_k+2,
+//                  r_k+3, g_k+3), (b_k .. b_k+3): the (r, g) pairs feed packed FFMA2s in K1
+//   per frame-body table (K0 -> K1): 4 float4 = rows 0 and 1 of M | m interleaved as
+//     (M00, M10, M01, M11), (M02, M12, m0, m1) (packed (x, y) pairs in K1), row 2 | m2, c_body
 //   projected record (K1 -> K4), 48 B at [frame][internal index]:
 //     R0 = (u, v, p', q')          whitening factor of Sigma2D^-1 scaled by sqrt(log2(e)/2)
 //     R1 = (r', log2 o, ex, ey)    half-extents of the alpha >= 1/255 box (R8), inflated
@@ -31,7 +34,26 @@ constexpr float kTermT = 1e-4f;       // reading R13
 // log2(1/255): alpha >= 1/255  <=>  log2(o) - Q/2 * log2(e) >= log2(1/255)
 constexpr float kLog2AlphaMin = -7.99435343685885793f;
 
-struct FrameCam {
+// ---- packed binary32 pairs (sm_100a FFMA2 / FADD2 / FMUL2) ------------------------------------
+// Two independent binary32 values (K4: a thread's two pixels; K1: the x and y rows of the
+// projection, the r and g SH channels) held as a pair in one 64-bit register pair and updated by
+// one packed instruction instead of two.  Each half is an IEEE binary32 RN operation, so the
+// results equal the scalar code's bit for bit; ptxas folds a scalar operand into a broadcast
+// (`R.F32`) and a negation into the operand.
+typedef float2 f32x2;
+
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) { return make_float2(lo, hi); }
+__device__ __forceinline__ float2 up2(f32x2 v) { return v; }
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ f32x2 nfma2(f32x2 a, f32x2 b, f32x2 c) {   // fma(-a, b, c) per half
+  return __ffma2_rn(make_float2(-a.x, -a.y), b, c);
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ f32x2 bc2(float x) { return make_float2(x, x); }   // broadcast
+
+struct __align__(16) FrameCam {
   float fx, fy, cx, cy;
   float limx, limy;  // reading R6: 1.3 * W / (2 fx), 1.3 * H / (2 fy)
   float kx, ky;      // 1 + limx^2, 1 + limy^2 (K1's conservative screen-cull bound)

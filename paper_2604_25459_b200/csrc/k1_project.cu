@@ -87,8 +87,8 @@ __global__ void k0_setup(K0Rig rig, int n_frames, int n_cams, int n_bodies, int 
   for (int c = 0; c < 3; ++c)
     cb[c] = R[0][c] * (cw[0] - t[0]) + R[1][c] * (cw[1] - t[1]) + R[2][c] * (cw[2] - t[2]);
   float4* o = table + (size_t)idx * 4;
-  o[0] = make_float4(M[0][0], M[0][1], M[0][2], m[0]);
-  o[1] = make_float4(M[1][0], M[1][1], M[1][2], m[1]);
+  o[0] = make_float4(M[0][0], M[1][0], M[0][1], M[1][1]);   // rows 0 and 1 interleaved (gsb_common.cuh)
+  o[1] = make_float4(M[0][2], M[1][2], m[0], m[1]);
   o[2] = make_float4(M[2][0], M[2][1], M[2][2], m[2]);
   o[3] = make_float4(cb[0], cb[1], cb[2], 0.f);
   if (k < 0 && cams) {   // cams == nullptr: LiDAR frames (no intrinsics)
@@ -104,53 +104,55 @@ __global__ void k0_setup(K0Rig rig, int n_frames, int n_cams, int n_bodies, int 
 }
 
 // ------------------------------------------------------------------------------ SH (R18)
+// SH planes: per group of four coefficients (r,g | r,g), (r,g | r,g), (b b b b) (gsb_common.cuh);
+// the (r, g) pair accumulates by packed FFMA2 with the basis value broadcast, b by scalar FFMA,
+// both in coefficient (degree) order.
 template <int D>
 __device__ __forceinline__ float3 sh_colour(const float4* __restrict__ g_sh, int64_t n, int64_t i,
                                             float x, float y, float z) {
   constexpr int NC = (D + 1) * (D + 1);
-  constexpr int NP = (3 * NC + 3) / 4;
-  float c[NP * 4];
+  constexpr int NG = (NC + 3) / 4;
+  float4 q[3 * NG];
 #pragma unroll
-  for (int p = 0; p < NP; ++p) {
-    const float4 q = __ldg(g_sh + (size_t)p * n + i);
-    c[4 * p + 0] = q.x; c[4 * p + 1] = q.y; c[4 * p + 2] = q.z; c[4 * p + 3] = q.w;
-  }
+  for (int p = 0; p < 3 * NG; ++p) q[p] = __ldg(g_sh + (size_t)p * n + i);
   const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
-  float r = C0 * c[0], g = C0 * c[1], b = C0 * c[2];
+  float Y[4 * NG];
+#pragma unroll
+  for (int k = 0; k < 4 * NG; ++k) Y[k] = 0.f;
+  Y[0] = C0;
   if (D >= 1) {
-    const float y1 = -C1 * y, y2 = C1 * z, y3 = -C1 * x;
-    r += y1 * c[3] + y2 * c[6] + y3 * c[9];
-    g += y1 * c[4] + y2 * c[7] + y3 * c[10];
-    b += y1 * c[5] + y2 * c[8] + y3 * c[11];
+    Y[1] = -C1 * y; Y[2] = C1 * z; Y[3] = -C1 * x;
   }
   if (D >= 2) {
     const float xx = x * x, yy = y * y, zz = z * z;
-    const float Y[5] = {1.0925484305920792f * x * y, -1.0925484305920792f * y * z,
-                        0.31539156525252005f * (2.f * zz - xx - yy), -1.0925484305920792f * x * z,
-                        0.5462742152960396f * (xx - yy)};
-#pragma unroll
-    for (int j = 0; j < 5; ++j) {
-      r += Y[j] * c[3 * (4 + j) + 0];
-      g += Y[j] * c[3 * (4 + j) + 1];
-      b += Y[j] * c[3 * (4 + j) + 2];
-    }
+    Y[4] = 1.0925484305920792f * x * y;
+    Y[5] = -1.0925484305920792f * y * z;
+    Y[6] = 0.31539156525252005f * (2.f * zz - xx - yy);
+    Y[7] = -1.0925484305920792f * x * z;
+    Y[8] = 0.5462742152960396f * (xx - yy);
     if (D >= 3) {
-      const float Y3[7] = {-0.5900435899266435f * y * (3.f * xx - yy),
-                           2.890611442640554f * x * y * z,
-                           -0.4570457994644658f * y * (4.f * zz - xx - yy),
-                           0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy),
-                           -0.4570457994644658f * x * (4.f * zz - xx - yy),
-                           1.445305721320277f * z * (xx - yy),
-                           -0.5900435899266435f * x * (xx - 3.f * yy)};
-#pragma unroll
-      for (int j = 0; j < 7; ++j) {
-        r += Y3[j] * c[3 * (9 + j) + 0];
-        g += Y3[j] * c[3 * (9 + j) + 1];
-        b += Y3[j] * c[3 * (9 + j) + 2];
-      }
+      Y[9] = -0.5900435899266435f * y * (3.f * xx - yy);
+      Y[10] = 2.890611442640554f * x * y * z;
+      Y[11] = -0.4570457994644658f * y * (4.f * zz - xx - yy);
+      Y[12] = 0.3731763325901154f * z * (2.f * zz - 3.f * xx - 3.f * yy);
+      Y[13] = -0.4570457994644658f * x * (4.f * zz - xx - yy);
+      Y[14] = 1.445305721320277f * z * (xx - yy);
+      Y[15] = -0.5900435899266435f * x * (xx - 3.f * yy);
     }
   }
-  return make_float3(fmaxf(r + 0.5f, 0.f), fmaxf(g + 0.5f, 0.f), fmaxf(b + 0.5f, 0.f));
+  f32x2 rg = mul2(bc2(Y[0]), pk2(q[0].x, q[0].y));
+  float b = Y[0] * q[2].x;
+#pragma unroll
+  for (int k = 1; k < NC; ++k) {
+    const float4& p2 = q[3 * (k >> 2) + ((k >> 1) & 1)];   // the plane holding (r_k, g_k)
+    const f32x2 c = (k & 1) ? pk2(p2.z, p2.w) : pk2(p2.x, p2.y);
+    const float4& pb = q[3 * (k >> 2) + 2];
+    const float cb = (k & 3) == 0 ? pb.x : (k & 3) == 1 ? pb.y : (k & 3) == 2 ? pb.z : pb.w;
+    rg = fma2(bc2(Y[k]), c, rg);
+    b = fmaf(Y[k], cb, b);
+  }
+  rg = add2(rg, bc2(0.5f));
+  return make_float3(fmaxf(rg.x, 0.f), fmaxf(rg.y, 0.f), fmaxf(b + 0.5f, 0.f));
 }
 
 // accurate 2x2 determinant a*d - b*c (Kahan): error ~1.5 ulp of the result
@@ -206,38 +208,45 @@ __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
     float3 rgb = make_float3(0.f, 0.f, 0.f);
     int tx0 = 0, tx1 = -1, ty0 = 0, ty1 = -1;
     if (keep || (debug && in)) {
-      const float4 r0 = __ldg(tb + 0), r1 = __ldg(tb + 1);
-      const FrameCam cam = a.cams[f];
-      const float x = fmaf(r0.x, mean.x, fmaf(r0.y, mean.y, fmaf(r0.z, mean.z, r0.w)));
-      const float y = fmaf(r1.x, mean.x, fmaf(r1.y, mean.y, fmaf(r1.z, mean.z, r1.w)));
+      // rows 0 and 1 of M mu + m as one packed (x, y) chain (the table interleaves the rows)
+      const float4 t0 = __ldg(tb + 0), t1 = __ldg(tb + 1);   // (M00, M10, M01, M11), (M02, M12, m0, m1)
+      const float4* cp = reinterpret_cast<const float4*>(a.cams + f);
+      const float4 c0 = cp[0], c1 = cp[1];                 // (fx, fy, cx, cy), (limx, limy, kx, ky)
+      f32x2 xy = fma2(pk2(t1.x, t1.y), bc2(mean.z), pk2(t1.z, t1.w));
+      xy = fma2(pk2(t0.z, t0.w), bc2(mean.y), xy);
+      xy = fma2(pk2(t0.x, t0.y), bc2(mean.x), xy);
       const float iz = __fdividef(1.f, z);   // ~1 ulp: inside reading R28's position bound (K_POS eps S_z)
-      const float xz = x * iz, yz = y * iz;
-      u = fmaf(cam.fx, xz, cam.cx);
-      v = fmaf(cam.fy, yz, cam.cy);
-      const float jx = cam.fx * iz, jy = cam.fy * iz;
+      const f32x2 xyz = mul2(xy, bc2(iz));                       // (x / z, y / z)
+      const f32x2 uv = fma2(pk2(c0.x, c0.y), xyz, pk2(c0.z, c0.w));
+      u = uv.x;
+      v = uv.y;
+      const f32x2 jj = mul2(pk2(c0.x, c0.y), bc2(iz));          // (jx, jy) = (fx, fy) / z
       // Conservative screen cull: Sigma2D_xx <= jx^2 (1 + limx^2) smax^2 + 0.3 (rows of M are
       // orthonormal, |t/z| <= lim after the clamp), so the exact R9 extents are inside
       // bx, by; a Gaussian whose bound box misses the image has an empty R9 rect as well.
-      const float bx = 1.02f * sqrt_approx(kappa * fmaf(jx * jx * cam.kx, smax2, 0.3f)) + 1.f;
-      const float by = 1.02f * sqrt_approx(kappa * fmaf(jy * jy * cam.ky, smax2, 0.3f)) + 1.f;
+      const f32x2 ke = mul2(bc2(kappa), fma2(mul2(mul2(jj, jj), pk2(c1.z, c1.w)), bc2(smax2), bc2(0.3f)));
+      const f32x2 bxy = fma2(bc2(1.02f), mul2(ke, pk2(rsqrtf(ke.x), rsqrtf(ke.y))), bc2(1.f));   // sqrt_approx
+      const float bx = bxy.x, by = bxy.y;
       const bool offscreen = (u + bx < 0.f) || (u - bx > fw) || (v + by < 0.f) || (v - by > fh);
       if (!offscreen || debug) {
-        // EWA Jacobian with the 1.3 frustum clamp (reading R6), applied to M: rows of J M
-        const float txz = fminf(fmaxf(xz, -cam.limx), cam.limx);
-        const float tyz = fminf(fmaxf(yz, -cam.limy), cam.limy);
-        const float m0[3] = {jx * fmaf(-txz, r2.x, r0.x), jx * fmaf(-txz, r2.y, r0.y), jx * fmaf(-txz, r2.z, r0.z)};
-        const float m1[3] = {jy * fmaf(-tyz, r2.x, r1.x), jy * fmaf(-tyz, r2.y, r1.y), jy * fmaf(-tyz, r2.z, r1.z)};
-        // A = (J M) L (2x3); Sigma2D = A A^T + 0.3 I (reading R7)
-        float A0[3], A1[3];
+        // EWA Jacobian with the 1.3 frustum clamp (reading R6), applied to M: rows of J M, as
+        // (row 0, row 1) pairs m[c] = (jx (M0c - tx M2c), jy (M1c - ty M2c))
+        const float txz = fminf(fmaxf(xyz.x, -c1.x), c1.x);
+        const float tyz = fminf(fmaxf(xyz.y, -c1.y), c1.y);
+        const f32x2 nt = pk2(-txz, -tyz);
+        const f32x2 m[3] = {mul2(jj, fma2(nt, bc2(r2.x), pk2(t0.x, t0.y))),
+                            mul2(jj, fma2(nt, bc2(r2.y), pk2(t0.z, t0.w))),
+                            mul2(jj, fma2(nt, bc2(r2.z), pk2(t1.x, t1.y)))};
+        // A = (J M) L (2x3) as column pairs (A0c, A1c); Sigma2D = A A^T + 0.3 I (reading R7)
+        f32x2 A[3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          A0[c] = fmaf(m0[0], L[0][c], fmaf(m0[1], L[1][c], m0[2] * L[2][c]));
-          A1[c] = fmaf(m1[0], L[0][c], fmaf(m1[1], L[1][c], m1[2] * L[2][c]));
-        }
-        const float sxx0 = fmaf(A0[0], A0[0], fmaf(A0[1], A0[1], A0[2] * A0[2]));
-        const float syy0 = fmaf(A1[0], A1[0], fmaf(A1[1], A1[1], A1[2] * A1[2]));
-        const float sxy = fmaf(A0[0], A1[0], fmaf(A0[1], A1[1], A0[2] * A1[2]));
-        const float sxx = sxx0 + 0.3f, syy = syy0 + 0.3f;
+        for (int c = 0; c < 3; ++c) A[c] = fma2(m[0], bc2(L[0][c]), fma2(m[1], bc2(L[1][c]), mul2(m[2], bc2(L[2][c]))));
+        const f32x2 s0 = fma2(A[0], A[0], fma2(A[1], A[1], mul2(A[2], A[2])));   // (sxx0, syy0)
+        const float sxx0 = s0.x, syy0 = s0.y;
+        const float sxy = fmaf(A[0].x, A[0].y, fmaf(A[1].x, A[1].y, A[2].x * A[2].y));
+        const f32x2 s2 = add2(s0, bc2(0.3f));
+        const float sxx = s2.x, syy = s2.y;
+        const float A0[3] = {A[0].x, A[1].x, A[2].x}, A1[3] = {A[0].y, A[1].y, A[2].y};
         // det(A A^T) by Cauchy-Binet (sum of squared 2x2 minors) + 0.3 tr + 0.09: no cancellation
         const float n01 = det2(A0[0], A0[1], A1[0], A1[1]);
         const float n02 = det2(A0[0], A0[2], A1[0], A1[2]);

@@ -71,23 +71,6 @@ __device__ __forceinline__ float2 blend2(bool use0, float arg0, bool use1, float
   return make_float2(w0, w1);
 }
 
-// ---- packed binary32 pairs (sm_100a FFMA2 / FADD2 / FMUL2) ------------------------------------
-// A thread's two pixels share every per-record term; their per-pixel terms (vertical offset,
-// quadratic form, weight, transmittance, the four accumulators) are held as (pixel 0, pixel 1)
-// pairs in one 64-bit register pair and updated by one packed instruction instead of two.  Each
-// half is an IEEE binary32 RN operation, so the results equal the scalar code's bit for bit;
-// ptxas folds a scalar operand into a broadcast (`R.F32`) and a negation into the operand.
-typedef float2 f32x2;
-
-__device__ __forceinline__ f32x2 pk2(float lo, float hi) { return make_float2(lo, hi); }
-__device__ __forceinline__ float2 up2(f32x2 v) { return v; }
-__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) { return __ffma2_rn(a, b, c); }
-__device__ __forceinline__ f32x2 nfma2(f32x2 a, f32x2 b, f32x2 c) {   // fma(-a, b, c) per half
-  return __ffma2_rn(make_float2(-a.x, -a.y), b, c);
-}
-__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
-__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) { return __fmul2_rn(a, b); }
-
 // acc += a * (x, x)
 __device__ __forceinline__ void acc2(f32x2& acc, f32x2 a, float x) { acc = __ffma2_rn(a, make_float2(x, x), acc); }
 
@@ -97,8 +80,10 @@ __device__ __forceinline__ void acc2(f32x2& acc, f32x2 a, float x) { acc = __ffm
 // the weight and transmittance pairs (which would cost register-pair copies per entry).
 // `argn` is the next entry's quadratic form, evaluated ahead with the current pixel centres; a
 // pixel that terminates here has it set to -inf (alpha 0), as its moved centre would give.
+// `idx_of()` gives the entry's list position; it is evaluated only when some pixel terminates.
+template <class IdxFn>
 __device__ __forceinline__ f32x2 blend2p(f32x2 arg, const float4& r2, f32x2& T, f32x2& R, f32x2& G, f32x2& B,
-                                         f32x2& D, f32x2& PYC, int& ne0, int& ne1, int idx, f32x2& argn) {
+                                         f32x2& D, f32x2& PYC, int& ne0, int& ne1, IdxFn idx_of, f32x2& argn) {
   const float2 ag = up2(arg);
   const float a0 = ag.x >= kLog2AlphaMin ? fminf(kAlphaMax, ex2_approx(ag.x)) : 0.f;   // alpha >= 1/255
   const float a1 = ag.y >= kLog2AlphaMin ? fminf(kAlphaMax, ex2_approx(ag.y)) : 0.f;
@@ -110,6 +95,7 @@ __device__ __forceinline__ f32x2 blend2p(f32x2 arg, const float4& r2, f32x2& T, 
     float2 ww = up2(w), tn = tt, pc = up2(PYC);
     const float2 T2 = up2(T);
     float2 an = up2(argn);
+    const int idx = idx_of();
     if (s0) { ne0 = idx + 1; pc.x = kFar; ww.x = 0.f; tn.x = T2.x; an.x = -INFINITY; }
     if (s1) { ne1 = idx + 1; pc.y = kFar; ww.y = 0.f; tn.y = T2.y; an.y = -INFINITY; }
     w = pk2(ww.x, ww.y);

@@ -670,9 +670,11 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
         // by some lane, and for the others blend2p is an exact no-op (w = 0: T, colour and depth
         // unchanged), so the vote and its branch only cost issue slots (+4.8 % C3, same-box A/B)
         const float4 q2 = R2[i];                                   // r, g, b, z
-        const int j = __float_as_int(R1[i].z);                     // the record's round position
-        const f32x2 wb = blend2p(arg, q2, T, R, G, Bc, D, PYC, ne0, ne1, base + j, argn);
+        // the record's position in the round (n_eval; read only when a pixel terminates)
+        auto pos = [&]() { return base + __float_as_int(R1[i].z); };
+        const f32x2 wb = blend2p(arg, q2, T, R, G, Bc, D, PYC, ne0, ne1, pos, argn);
         if constexpr (SCORE) {
+          const int j = __float_as_int(R1[i].z);
           const float2 w2 = up2(wb);
           const uint32_t tot = __reduce_add_sync(FULL, __float2uint_rn((w2.x + w2.y) * kScoreFix));
           const uint32_t mx = __reduce_max_sync(FULL, __float_as_uint(fmaxf(w2.x, w2.y)));

@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(128) kl1_project(LidarL1Args a) {
   for (int fl = fl_lo; fl < fl_hi; ++fl) {
     const int f = a.f0 + fl;
     const float4* tb = a.table + ((size_t)f * a.nb1 + (body + 1)) * 4;
-    const float4 r0 = __ldg(tb + 0), r1 = __ldg(tb + 1), r2 = __ldg(tb + 2);
+    const float4 t0 = __ldg(tb + 0), t1 = __ldg(tb + 1), r2 = __ldg(tb + 2);   // rows 0, 1 interleaved
+    const float4 r0 = make_float4(t0.x, t0.z, t1.x, t1.z), r1 = make_float4(t0.y, t0.w, t1.y, t1.w);
     // R32 step 2: binary32 chain, every op rounded
     const float x0 = __fmaf_rn(r0.x, mean.x, __fmaf_rn(r0.y, mean.y, __fmaf_rn(r0.z, mean.z, r0.w)));
     const float x1 = __fmaf_rn(r1.x, mean.x, __fmaf_rn(r1.y, mean.y, __fmaf_rn(r1.z, mean.z, r1.w)));
