@@ -540,13 +540,17 @@ __device__ __forceinline__ void cp_async_wait_group() {
 // SCORE (GSB_FLAG_SCORES, reading R30): every blended weight is also summed (6.26 fixed point,
 // __reduce_add_sync) and maxed (exact, float bits) over the warp per record, then added to the
 // scene's per-Gaussian accumulators with one global atomic pair per (warp, record).
-template <bool SCORE>
+// MERGE: static-camera merge (tagged background record slots), else plain record slots.
+template <bool SCORE, bool MERGE>
 __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a, int* __restrict__ counter,
                                                                   int n_items) {
   __shared__ __align__(16) float4 stg[kBlendWarps][2][3][kWarpBatch];   // 12 KB
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float4 (*S)[3][kWarpBatch] = stg[warp];
+  // shared address of this lane's staging slot (buffer 0, row 0); rows kRowB, buffers kBufB apart
+  constexpr uint32_t kRowB = kWarpBatch * sizeof(float4), kBufB = 3 * kRowB;
+  const uint32_t s_lane = (uint32_t)__cvta_generic_to_shared(&S[0][0][lane]);
   for (;;) {   // (fixed plan: an overflowed chunk's counter starts at n_items, see launch_k4b_blend)
     int item = 0;
     if (lane == 0) item = atomicAdd(counter, 1);
@@ -584,10 +588,14 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
     // after the next is read one round ahead, so no cp.async waits on a slot load
     auto stage = [&](int b, uint32_t sl) {
       if (b * kWarpBatch + lane < len) {
-        const float4* r = (sl & kBgTag) ? a.bg_rec + (size_t)(sl & ~kBgTag) * 3 : rec + (size_t)sl * kRecQuads;
-        cp_async16(&S[b & 1][0][lane], r);
-        cp_async16(&S[b & 1][1][lane], r + 1);
-        cp_async16(&S[b & 1][2][lane], r + 2);
+        const float4* r = rec + (size_t)sl * kRecQuads;
+        if constexpr (MERGE) {
+          if (sl & kBgTag) r = a.bg_rec + (size_t)(sl & ~kBgTag) * 3;
+        }
+        const uint32_t d = s_lane + (uint32_t)(b & 1) * kBufB;
+        cp_async16s(d, r);
+        cp_async16s(d + kRowB, r + 1);
+        cp_async16s(d + 2 * kRowB, r + 2);
       }
       cp_async_commit();
     };
@@ -771,7 +779,7 @@ void launch_k4b_blend(const CompositeArgs& a, int* counter, cudaStream_t s) {
   if (!persistent) {
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4b_blend<false>, kBlendWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4b_blend<false, false>, kBlendWarps * 32, 0);
     // GSB_K4B_PER_SM=8 (one below the register limit) lets the other streams' latency-bound
     // kernels co-reside: C3 +0.6 %, C4 +1.8 %, C6 +0.8 % of step throughput, but K4b's own live
     // event time grows with the sharing (bench roofline 0.90 -> 0.76); the default keeps 9
@@ -782,8 +790,14 @@ void launch_k4b_blend(const CompositeArgs& a, int* counter, cudaStream_t s) {
   if (a.overflow) k4b_counter_init<<<1, 1, 0, s>>>(counter, a.overflow, (int)items);
   else cudaMemsetAsync(counter, 0, sizeof(int), s);
   const unsigned g = (unsigned)std::min<long long>(persistent, (items + kBlendWarps - 1) / kBlendWarps);
-  if (a.score_sum) k4b_blend<true><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
-  else k4b_blend<false><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
+  const bool merge = a.bg_off != nullptr;
+  if (a.score_sum) {
+    if (merge) k4b_blend<true, true><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
+    else k4b_blend<true, false><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
+  } else {
+    if (merge) k4b_blend<false, true><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
+    else k4b_blend<false, false><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
+  }
 }
 
 }  // namespace gsb
