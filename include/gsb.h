@@ -381,7 +381,9 @@ gsb_status gsb_debug_bin_sort(const float* u, const float* v, const float* sxx, 
  *                radix beyond), 3 = fused K4
  *                small, 4 = fused K4 packed, 5 = K4a one CTA per list (counting sort <= 1024 keys
  *                in smem, HBM radix beyond; the LiDAR path's sort)
- *   key_mode     0 = keys carry the record slot (gsb_render's default), 1 = keys carry the id
+ *   key_mode     0 = keys carry the record slot (gsb_render's default), 1 = keys carry the id,
+ *                2 = slot keys with K4b block masks in their low 4 bits (variants 1 and 2 only;
+ *                the mask is set to slot & 15 and checked to travel with its entry)
  *   out_tile_offsets [F, T_t + 1] DEVICE int64 (absolute positions in out_ids),
  *   out_ids      [cap] DEVICE uint32: creation ids of every (frame, tile) list in sorted order
  *   out_K, out_variant (HOST): total keys and the variant that ran (1..5).

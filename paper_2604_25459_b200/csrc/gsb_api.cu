@@ -215,6 +215,7 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
   for (int sl = 0; sl < 2; ++sl) {
     CUDA_TRY(dalloc(&s->rec[sl], (size_t)E * std::max<int64_t>(s->n, 1) * kRecQuads));
     CUDA_TRY(dalloc(&s->emit[sl], (size_t)E * std::max<int64_t>(s->n, 1)));
+    CUDA_TRY(dalloc(&s->trim[sl], (size_t)E * std::max<int64_t>(s->n, 1)));
     CUDA_TRY(dalloc(&s->vcount[sl], (size_t)E));
     CUDA_TRY(dalloc(&s->vis_bits[sl], (size_t)E * std::max<int64_t>(s->vis_words, 1)));
     CUDA_TRY(dalloc(&s->long_list[sl], (size_t)E * s->n_tiles));

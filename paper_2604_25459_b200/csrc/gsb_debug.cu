@@ -115,7 +115,8 @@ gsb_status gsb_debug_tile_lists(const float* u, const float* v, const float* sxx
                                 int32_t variant, int32_t key_mode, int64_t* out_offsets, uint32_t* out_ids,
                                 int64_t cap, int64_t* out_K, int32_t* out_variant, gsb_stream stream) {
   if (F < 1 || n < 0 || width < 1 || height < 1 || width > kMaxDim || height > kMaxDim || cap < 0 || !out_K ||
-      !out_offsets || variant < 0 || variant > 5 || key_mode < 0 || key_mode > 1 ||
+      !out_offsets || variant < 0 || variant > 5 || key_mode < 0 || key_mode > 2 ||
+      (key_mode == 2 && variant != 1 && variant != 2) ||
       (n > 0 && (!u || !v || !sxx || !syy || !kappa || !zbits || !valid || !slot_ids)))
     return fail(GSB_ERR_INVALID_ARGUMENT, "bad debug_tile_lists arguments");
   if (n >= (int64_t)1 << 31) return fail(GSB_ERR_CAPACITY, "n >= 2^31");
@@ -205,17 +206,20 @@ gsb_status gsb_debug_tile_lists(const float* u, const float* v, const float* sxx
   DBG_TRY(dalloc(&keys_alt, std::max<uint64_t>(K, 1)));
   DBG_TRY(dalloc(&sorted, std::max<uint64_t>(K, 1)));
   DBG_TRY(dalloc(&lists, std::max<uint64_t>(K, 1)));
-  const bool slot_keys = key_mode == 0;
+  const bool synth = key_mode == 2;   // slot keys + block masks (mask = slot & 15, K4a carries it)
+  const bool slot_keys = key_mode == 0 || synth;
   ChunkArgs a{};
   a.rec = nullptr; a.emit = emit; a.ids = slot_keys ? nullptr : d_ids; a.n = n; a.vis_bits = vbits;
   a.vis_words = vwords; a.hist = hist; a.hist_stride = stride; a.off = off; a.frame_base = fbase;
   a.n_tiles = n_tiles; a.tiles_x = tiles_x; a.fs = 0; a.fe = F; a.key_base = 0; a.long_list = nullptr;
   a.keys = keys; a.keys_alt = keys_alt; a.sorted = sorted;
+  if (synth) { a.mask_bits = kMaskBits; a.synth_mask = 1; }
   launch_k2_emit(a, st);
   CompositeArgs c{};
   c.rec = nullptr; c.n = n; c.off = off; c.frame_base = fbase; c.hist_stride = stride; c.sorted = sorted;
   c.keys = keys; c.keys_alt = keys_alt; c.key_base = 0; c.inv = d_inv; c.slot_base = 0;
   c.keys_internal_ids = slot_keys ? d_ids : nullptr;
+  if (synth) c.key_shift = kMaskBits;
   c.fs = 0; c.fe = F; c.f0 = 0; c.width = width; c.height = height; c.tiles_x = tiles_x; c.n_tiles = n_tiles;
   if (var == 1 && n_long > 0) {       // the render's K4a: warp per short list + CTA per long list
     DBG_TRY(dalloc(&d_long, (size_t)n_long));
@@ -235,6 +239,8 @@ gsb_status gsb_debug_tile_lists(const float* u, const float* v, const float* sxx
   std::vector<uint32_t> hs((size_t)K);
   if (K > 0) DBG_TRY(cudaMemcpyAsync(hs.data(), sorted, sizeof(uint32_t) * K, cudaMemcpyDeviceToHost, st));
   DBG_TRY(cudaStreamSynchronize(st));
+  if (synth)   // every entry must carry its own slot's mask; a mismatch reads as an invalid id
+    for (uint64_t k = 0; k < K; ++k) hs[k] = ((hs[k] >> kMaskBits) & 15u) == (hs[k] & 15u) ? hs[k] >> kMaskBits : 0xfffffffeu;
   for (uint64_t k = 0; k < K; ++k) hs[k] = hs[k] < (uint64_t)n ? (uint32_t)hids[hs[k]].x : 0xffffffffu;
   if (K > 0) DBG_TRY(cudaMemcpyAsync(out_ids, hs.data(), sizeof(uint32_t) * K, cudaMemcpyHostToDevice, st));
   std::vector<int64_t> ho((size_t)F * (n_tiles + 1));

@@ -58,6 +58,9 @@ struct K1Args {
   // outputs
   float4* rec;     // [E][N][3] records at the internal index, nullptr for debug-only launches
   uint2* emit;     // [E][N] (bits(z), rect) for the key emission
+  uint8_t* trim;   // [E][N] or nullptr: K4b block-mask trims (bit 0: left 8 columns of the rect's
+                   // first tile column unreachable, 1: right 8 of the last, 2: top 8 rows of the
+                   // first tile row, 3: bottom 8 of the last), from the conservative R8 box
   uint32_t* vis_bits;  // [E][vis_words] visibility ballot of each warp (32 internal indices)
   int64_t vis_words;   // ceil(N / 32)
   int* vcount;     // [E] visible pairs (statistics)
@@ -89,7 +92,14 @@ struct ChunkArgs {
   uint64_t* keys_alt;     // [cap]   scratch for oversize segments
   uint32_t* sorted;       // [cap]   sorted ids of the lists K3 sorted
   const int* overflow;    // GSB_FLAG_FIXED_PLAN: the chunk's flag (keys beyond capacity: skip), or nullptr
+  // K4b block masks (slot keys only): key low word = slot << kMaskBits | mask of the 8x8 blocks of
+  // the tile the record can reach (from K1's trims); 0 = off.  synth_mask (debug hook):
+  // mask = slot & 15
+  int mask_bits;
+  int synth_mask;
+  const uint8_t* trim;    // [E][N] K1's block-mask trims (mask_bits without synth_mask)
 };
+constexpr int kMaskBits = 4;
 
 struct CompositeArgs {
   const float4* rec;
@@ -132,6 +142,9 @@ struct CompositeArgs {
   // (K2b with ids = nullptr); equal-depth runs are then re-ordered by the creation id ids[slot].x
   // so the order is still (bits(z), id) of reading R10, and no id -> slot gather is needed
   const int2* keys_internal_ids;   // template (id, body) of the launch's range, or nullptr
+  // K4b block masks: with key_shift = kMaskBits the key's low word (and each sorted entry) is
+  // (slot << 4 | mask), mask bit b = "the record can reach 8x8 block b of the tile" (K2b); 0 = off
+  int key_shift;
   // lists longer than kWarpSortCap of this chunk ((frame << 16 | tile), from K2a): the split path's
   // K4a sorts short lists one warp per tile and these with a CTA each; nullptr = CTA per tile
   const uint32_t* long_list;
@@ -248,6 +261,8 @@ void launch_k3_prebin_gather(const uint32_t* sorted, const uint64_t* frame_base,
 void launch_k4_composite(const CompositeArgs& a, bool long_lists, cudaStream_t s);
 // split path (plain / observation renders): K4a tile sort into a.sorted, then K4b persistent
 // per-warp compositing; counter = one int of device scratch
+// the K4a variants the split path picks by default sort keys with block masks (key_shift)
+bool k4a_masks_supported();
 void launch_k4a_sort(const CompositeArgs& a, bool long_lists, cudaStream_t s);
 void launch_k4b_blend(const CompositeArgs& a, int* counter, cudaStream_t s);
 void launch_k4_scores_export(const float* wsum, const uint32_t* wmax, const int2* ids, int64_t n, float* out_sum,

@@ -69,6 +69,7 @@ struct Pipeline {
     a.f0 = f0; a.n_frames = nf; a.width = W; a.height = H; a.tiles_x = tiles_x;
     a.near_plane = p->near_plane; a.far_plane = p->far_plane;
     a.rec = s->rec[sl]; a.emit = s->emit[sl];
+    a.trim = (!merge && block_masks_on()) ? s->trim[sl] : nullptr;
     a.vcount = s->vcount[sl]; a.hist = s->hist[sl]; a.hist_stride = s->hist_stride;
     a.vis_bits = s->vis_bits[sl]; a.vis_words = s->vis_words;
     tm.begin(KC_PROJECT, sp);
@@ -112,6 +113,12 @@ struct Pipeline {
     if (fixed) a.overflow = s->d_overflow + 1 + sl;
     const bool slot_keys = !merge && slot_keys_on();
     if (slot_keys) a.ids = nullptr;   // key low word = index in the launch range = record slot
+    // K4b block masks: plain split passes with slot keys (not scores: they reduce each record
+    // over the whole warp) and the default K4a variants
+    const bool masks = split && slot_keys && !(p->flags & GSB_FLAG_SCORES) && block_masks_on() &&
+                       k4a_masks_supported() && count < ((int64_t)1 << (32 - kMaskBits)) &&
+                       n_keys >= mask_min_avg() * (uint64_t)(fe - fs) * n_tiles;
+    if (masks) { a.mask_bits = kMaskBits; a.trim = s->trim[sl]; }
     tm.begin(KC_EMIT, sb);
     launch_k2_emit(a, sb);
     if (count > 0) s->launches++;
@@ -130,6 +137,7 @@ struct Pipeline {
       c.bg_cum = s->d_bgcum;
     }
     if (slot_keys) c.keys_internal_ids = s->d_ids + first;
+    if (masks) c.key_shift = kMaskBits;
     c.long_list = s->long_list[sl];   // K4a: lists > kWarpSortCap get a CTA each
     c.n_long = n_long;
     if (fixed) {   // the long-list count and the chunk's overflow flag stay on the device

@@ -84,6 +84,19 @@ inline uint64_t split_min_avg() {
   return e ? (uint64_t)strtoull(e, nullptr, 10) : 0u;
 }
 
+inline bool block_masks_on() {   // GSB_BLOCK_MASKS=0: K4b culls every staged record itself (A/B)
+  const char* e = getenv("GSB_BLOCK_MASKS");
+  return !(e && e[0] == '0');
+}
+
+// block masks pay where lists are long (C4 +5.4 %, C5 +3.1 %) and lose where they are short and the
+// Gaussians large (C2 -7 %: the masks are bounding-box trims, looser than K4b's elliptic cull; C3
+// +0.3 %): used for passes averaging at least this many keys per tile (GSB_MASK_MIN_AVG)
+inline uint64_t mask_min_avg() {
+  const char* e = getenv("GSB_MASK_MIN_AVG");
+  return e ? (uint64_t)strtoull(e, nullptr, 10) : 512u;
+}
+
 inline bool slot_keys_on() {   // GSB_SLOT_KEYS=0: keys carry the creation id on every path
   const char* e = getenv("GSB_SLOT_KEYS");
   return !(e && e[0] == '0');
@@ -130,6 +143,7 @@ struct gsb_scene_t {
   gsb::FrameCam* cams = nullptr;
   float4* rec[2] = {nullptr, nullptr};
   uint2* emit[2] = {nullptr, nullptr};
+  uint8_t* trim[2] = {nullptr, nullptr};   // [E][N] K4b block-mask trims of the visible pairs (K1 -> K2b)
   int* vcount[2] = {nullptr, nullptr};
   uint32_t* vis_bits[2] = {nullptr, nullptr};
   uint32_t* long_list[2] = {nullptr, nullptr};   // lists too long for K4's fused sort
@@ -205,7 +219,7 @@ struct gsb_scene_t {
   void free_workspace() {
     cudaFree(table); cudaFree(cams);
     for (int s = 0; s < 2; ++s) {
-      cudaFree(rec[s]); cudaFree(emit[s]); emit[s] = nullptr; cudaFree(vcount[s]); cudaFree(hist[s]); cudaFree(off[s]); cudaFree(vis_bits[s]);
+      cudaFree(rec[s]); cudaFree(emit[s]); emit[s] = nullptr; cudaFree(trim[s]); trim[s] = nullptr; cudaFree(vcount[s]); cudaFree(hist[s]); cudaFree(off[s]); cudaFree(vis_bits[s]);
       cudaFree(long_list[s]); cudaFree(long_cnt[s]);
       vis_bits[s] = nullptr; long_list[s] = nullptr; long_cnt[s] = nullptr;
       cudaFree(frame_base[s]);

@@ -371,8 +371,9 @@ __device__ __forceinline__ bool packed_sort(const uint64_t* __restrict__ gkeys, 
 constexpr int kRunSlots = 4;
 constexpr int kShortRun = 32;
 
+// sh: low bits of the key's low word that are not part of the slot (K4b block masks; 0 or 4)
 template <int NT, typename P>
-__device__ __forceinline__ bool fix_equal_depth_runs(P r, int n, const int2* __restrict__ ids) {
+__device__ __forceinline__ bool fix_equal_depth_runs(P r, int n, const int2* __restrict__ ids, int sh = 0) {
   const int tid = threadIdx.x;
   int starts[kRunSlots], ends[kRunSlots];   // runs [start, end) found in the read-only pass
   int ns = 0;
@@ -396,9 +397,9 @@ __device__ __forceinline__ bool fix_equal_depth_runs(P r, int n, const int2* __r
     const int s0 = starts[k], s1 = ends[k];
     for (int i = s0 + 1; i < s1; ++i) {   // insertion sort by creation id (runs are short)
       const uint64_t key = r[i];
-      const int id = __ldg(&ids[(uint32_t)key].x);
+      const int id = __ldg(&ids[(uint32_t)key >> sh].x);
       int j = i - 1;
-      while (j >= s0 && __ldg(&ids[(uint32_t)r[j]].x) > id) {
+      while (j >= s0 && __ldg(&ids[(uint32_t)r[j] >> sh].x) > id) {
         r[j + 1] = r[j];
         --j;
       }
@@ -411,10 +412,11 @@ __device__ __forceinline__ bool fix_equal_depth_runs(P r, int n, const int2* __r
 
 // the fallback: key low words slot -> creation id (the high word, bits(z), is kept)
 template <int NT, typename P>
-__device__ __forceinline__ void slot_keys_to_id_keys(P r, int n, const int2* __restrict__ ids) {
+__device__ __forceinline__ void slot_keys_to_id_keys(P r, int n, const int2* __restrict__ ids, int sh = 0) {
   for (int e = threadIdx.x; e < n; e += NT) {
     const uint64_t k = r[e];
-    r[e] = (k & 0xffffffff00000000ull) | (uint32_t)__ldg(&ids[(uint32_t)k].x);
+    const uint32_t lo = (uint32_t)k;   // (slot << sh | mask) -> (id << sh | mask)
+    r[e] = (k & 0xffffffff00000000ull) | ((uint32_t)__ldg(&ids[lo >> sh].x) << sh) | (lo & ((1u << sh) - 1u));
   }
   __syncthreads();
 }

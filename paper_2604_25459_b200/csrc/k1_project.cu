@@ -305,6 +305,14 @@ __global__ void __launch_bounds__(128, 8) k1_project(K1Args a) {
       r[1] = make_float4(rw, log2o, ex, ey);
       r[2] = make_float4(rgb.x, rgb.y, rgb.z, z);
       a.emit[(size_t)fl * a.n + i] = make_uint2(__float_as_uint(z), rect);
+      if (a.trim) {
+        // K4b block masks: which half-tile borders of the rect the conservative R8 box (u +- ex,
+        // v +- ey) does not reach — the 8x8 blocks there hold no pixel centre of alpha >= 1/255
+        const float x_lo = (float)(tx0 * kTile) + 7.5f, x_hi = (float)(tx1 * kTile) + 8.5f;
+        const float y_lo = (float)(ty0 * kTile) + 7.5f, y_hi = (float)(ty1 * kTile) + 8.5f;
+        a.trim[(size_t)fl * a.n + i] = (uint8_t)((u - ex > x_lo ? 1u : 0u) | (u + ex < x_hi ? 2u : 0u) |
+                                                 (v - ey > y_lo ? 4u : 0u) | (v + ey < y_hi ? 8u : 0u));
+      }
     }
     if (bal) warp_tile_count(vis, rect, a.tiles_x, a.hist + (size_t)fl * a.hist_stride, tile_scratch[threadIdx.x >> 5]);
   }

@@ -177,17 +177,33 @@ __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
   const int lane = threadIdx.x & 31;
   const bool has = (word >> lane) & 1u;
   uint32_t rect = 0, zb = 0, id = 0;
+  uint32_t trim = 0;   // block masks: K1's trims of this pair
   if (has) {
     const uint2 er = __ldg(a.emit + (size_t)fl * a.n + i);
     zb = er.x;
     rect = er.y;
     id = a.ids ? (uint32_t)__ldg(&a.ids[i].x) : (uint32_t)i;
+    if (a.mask_bits && !a.synth_mask) trim = __ldg(a.trim + (size_t)fl * a.n + i);
   }
-  const uint64_t key = ((uint64_t)zb << 32) | (uint64_t)id;   // unique (reading R10)
+  // unique (reading R10); with block masks the low word is (id << 4 | mask of the tile)
+  const uint64_t key = ((uint64_t)zb << 32) | (uint64_t)(a.mask_bits ? id << kMaskBits : id);
+  // the key for tile (tx, ty): + the 4-bit mask of the tile's 8x8 blocks (bit 2 by + bx) the
+  // record can reach: all four, less the half-tile borders K1 trimmed at the rect's edges
+  // (debug hook: mask = slot & 15)
   int* cur = a.hist + (size_t)fl * a.hist_stride;
   const uint32_t* off = a.off + (size_t)fl * a.hist_stride;
   uint64_t* keys = a.keys + (a.frame_base[fl] - a.key_base);
   const int tx0 = rect & 0xff, tx1 = (rect >> 8) & 0xff, ty0 = (rect >> 16) & 0xff, ty1 = rect >> 24;
+  auto key_at = [&](int tx, int ty) -> uint64_t {
+    if (!a.mask_bits) return key;
+    if (a.synth_mask) return key | (id & 15u);
+    uint32_t m = 15u;
+    if (tx == tx0 && (trim & 1u)) m &= ~5u;    // left column of blocks (0, 2)
+    if (tx == tx1 && (trim & 2u)) m &= ~10u;   // right column (1, 3)
+    if (ty == ty0 && (trim & 4u)) m &= ~3u;    // top row (0, 1)
+    if (ty == ty1 && (trim & 8u)) m &= ~12u;   // bottom row (2, 3)
+    return key | m;
+  };
   const int nt = has ? (tx1 - tx0 + 1) * (ty1 - ty0 + 1) : 0;
   const bool big = nt > kBigRect;
   const bool part = nt > 0 && !big;
@@ -232,7 +248,7 @@ __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
       const bool act = part && r < nt;
       const uint32_t b = __shfl_sync(FULL, base, act ? (ty - ub.y0) * ub.w + (tx - ub.x0) : 0);
       if (act) {
-        keys[off[ty * a.tiles_x + tx] + b + rk[r]] = key;
+        keys[off[ty * a.tiles_x + tx] + b + rk[r]] = key_at(tx, ty);
         if (++tx > tx1) { tx = tx0; ++ty; }
       }
     }
@@ -242,7 +258,7 @@ __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
       if (r < rounds) {
         const int j = (ty - ub.y0) * ub.w + (tx - ub.x0);
         const uint32_t b = __shfl_sync(FULL, base, part && r < nt ? j : 0);
-        if (part && r < nt) keys[off[ty * a.tiles_x + tx] + b + rk[r]] = key;
+        if (part && r < nt) keys[off[ty * a.tiles_x + tx] + b + rk[r]] = key_at(tx, ty);
         if (++tx > tx1) { tx = tx0; ++ty; }
       }
     }
@@ -257,7 +273,7 @@ __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
     int base = 0;
     if (act && lane == leader) base = atomicAdd(cur + t, __popc(peers));
     base = __shfl_sync(FULL, base, leader);
-    if (act) keys[off[t] + base + __popc(peers & lanemask_lt())] = key;
+    if (act) keys[off[t] + base + __popc(peers & lanemask_lt())] = key_at(tx, ty);
     if (++tx > tx1) { tx = tx0; ++ty; }
   }
   unsigned bm = __ballot_sync(FULL, big);
@@ -265,7 +281,9 @@ __global__ void __launch_bounds__(256) k2_emit(ChunkArgs a) {
     const int j = __ffs(bm) - 1;
     bm &= bm - 1;
     const uint32_t rj = __shfl_sync(FULL, rect, j);
-    const uint64_t kj = __shfl_sync(FULL, key, j);
+    // a big rect (> kBigRect tiles): every block of each tile (conservative)
+    const uint64_t kj = __shfl_sync(FULL, key, j) |
+                        (a.mask_bits ? (a.synth_mask ? (uint64_t)(__shfl_sync(FULL, id, j) & 15u) : 15ull) : 0ull);
     const int jx0 = rj & 0xff, jx1 = (rj >> 8) & 0xff, jy0 = (rj >> 16) & 0xff, jy1 = rj >> 24;
     for (int y = jy0; y <= jy1; ++y)
       for (int x = jx0 + lane; x <= jx1; x += 32) {

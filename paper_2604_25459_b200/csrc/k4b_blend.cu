@@ -247,6 +247,13 @@ struct K4aIdxShared {
   uint16_t buf[kIdxCap];
 };
 
+// K4b block masks (CompositeArgs::key_shift = kMaskBits): a key's low word is (slot << 4 | mask)
+// and so is the sorted entry; an id-keyed low word (id << sh | mask) maps to (slot << sh | mask)
+__device__ __forceinline__ uint32_t id_word_to_slot_word(const CompositeArgs& a, uint32_t w) {
+  const int sh = a.key_shift;
+  return ((uint32_t)(__ldg(a.inv + (w >> sh)) - a.slot_base) << sh) | (w & ((1u << sh) - 1u));
+}
+
 // the HBM path of one list: LSD radix of 64-bit keys in keys / keys_alt (gsb_sort.cuh)
 __device__ __forceinline__ void k4a_hbm_list(const CompositeArgs& a, uint64_t start, int len, uint32_t* dst,
                                              SortShared<kSortThreadsA>& ss) {
@@ -260,15 +267,15 @@ __device__ __forceinline__ void k4a_hbm_list(const CompositeArgs& a, uint64_t st
   uint64_t* r = in_b ? gb : ga;
   if (!kid) {
     for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)r[e]) - base);
-  } else if (fix_equal_depth_runs<kSortThreadsA>(r, len, kid)) {
+  } else if (fix_equal_depth_runs<kSortThreadsA>(r, len, kid, a.key_shift)) {
     for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)r[e];
   } else {
     uint64_t* o = in_b ? ga : gb;
-    slot_keys_to_id_keys<kSortThreadsA>(r, len, kid);
+    slot_keys_to_id_keys<kSortThreadsA>(r, len, kid, a.key_shift);
     const bool in_o = segment_sort(r, o, len, ss);
     __syncthreads();
     const uint64_t* rr = in_o ? o : r;
-    for (int e = tid; e < len; e += kSortThreadsA) dst[e] = (uint32_t)(__ldg(a.inv + (uint32_t)rr[e]) - base);
+    for (int e = tid; e < len; e += kSortThreadsA) dst[e] = id_word_to_slot_word(a, (uint32_t)rr[e]);
   }
 }
 
@@ -336,12 +343,12 @@ __device__ __forceinline__ bool k4a_idx_list(const CompositeArgs& a, const uint6
       if (eq > kShortRun + 1) {
         long_run = true;
       } else {
-        const int idp = __ldg(&kid[(uint32_t)key].x);
+        const int idp = __ldg(&kid[(uint32_t)key >> a.key_shift].x);
         rank = 0;
         for (int q = s0; q < s1; ++q) {
           const uint64_t kq = __ldg(gk + sm.buf[q]);
           const uint32_t zq = hi32(kq);
-          rank += zq < z || (zq == z && kq != key && __ldg(&kid[(uint32_t)kq].x) < idp);
+          rank += zq < z || (zq == z && kq != key && __ldg(&kid[(uint32_t)kq >> a.key_shift].x) < idp);
         }
       }
     }
@@ -495,12 +502,12 @@ __global__ void __launch_bounds__(kK4aWarps * 32) k4a_warp_sort(CompositeArgs a,
       if (eq > kShortRun + 1) {
         long_run = true;
       } else {
-        const int idp = __ldg(&kid[(uint32_t)key].x);
+        const int idp = __ldg(&kid[(uint32_t)key >> a.key_shift].x);
         rank = 0;
         for (int q = s0; q < s1; ++q) {
           const uint64_t kq = sm.buf[q];
           const uint32_t zq = hi32(kq);
-          rank += zq < z || (zq == z && q != p && __ldg(&kid[(uint32_t)kq].x) < idp);
+          rank += zq < z || (zq == z && q != p && __ldg(&kid[(uint32_t)kq >> a.key_shift].x) < idp);
         }
       }
     }
@@ -508,9 +515,11 @@ __global__ void __launch_bounds__(kK4aWarps * 32) k4a_warp_sort(CompositeArgs a,
   }
   if (__any_sync(FULL, long_run)) {   // long equal-depth runs: re-key by id, re-rank by (z, id)
     __syncwarp();
-    for (int p = lane; p < n; p += 32) {
+    const int sh = a.key_shift;
+    for (int p = lane; p < n; p += 32) {   // (slot << sh | mask) -> (id << sh | mask)
       const uint64_t k = sm.buf[p];
-      sm.buf[p] = (k & 0xffffffff00000000ull) | (uint32_t)__ldg(&kid[(uint32_t)k].x);
+      const uint32_t lo = (uint32_t)k;
+      sm.buf[p] = (k & 0xffffffff00000000ull) | ((uint32_t)__ldg(&kid[lo >> sh].x) << sh) | (lo & ((1u << sh) - 1u));
     }
     __syncwarp();
     for (int p = lane; p < n; p += 32) {
@@ -519,7 +528,7 @@ __global__ void __launch_bounds__(kK4aWarps * 32) k4a_warp_sort(CompositeArgs a,
       const int s0 = b ? (int)sm.bins[b - 1] : 0, s1 = (int)sm.bins[b];
       int rank = 0;
       for (int q = s0; q < s1; ++q) rank += sm.buf[q] < key;
-      dst[s0 + rank] = (uint32_t)(__ldg(a.inv + (uint32_t)key) - base);
+      dst[s0 + rank] = id_word_to_slot_word(a, (uint32_t)key);
     }
   }
 }
@@ -541,10 +550,18 @@ __device__ __forceinline__ void cp_async_wait_group() {
 // __reduce_add_sync) and maxed (exact, float bits) over the warp per record, then added to the
 // scene's per-Gaussian accumulators with one global atomic pair per (warp, record).
 // MERGE: static-camera merge (tagged background record slots), else plain record slots.
-template <bool SCORE, bool MERGE>
+// MASKED (CompositeArgs::key_shift = kMaskBits): every sorted entry carries the 4-bit mask of the
+// tile's 8x8 blocks its record can reach (K2b, the same lower bound and margin as the cull below),
+// so a warp never stages or tests a record outside its block: it scans its list 32 entries at a
+// time, queues the hits (slot, list position) in shared memory and stages full rounds of 32 hit
+// records — no per-round cull, and a third of the rounds (C3: 13 of 32 staged records were hits).
+template <bool SCORE, bool MERGE, bool MASKED>
 __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a, int* __restrict__ counter,
                                                                   int n_items) {
   __shared__ __align__(16) float4 stg[kBlendWarps][2][3][kWarpBatch];   // 12 KB
+  constexpr int kQ = 2 * kWarpBatch;   // hit queue (ring) per warp
+  __shared__ uint2 hitq[MASKED ? kBlendWarps : 1][MASKED ? kQ : 1];           // (slot, list position)
+  __shared__ uint32_t hitpos[MASKED ? kBlendWarps : 1][2][MASKED ? kWarpBatch : 1];   // staged positions
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float4 (*S)[3][kWarpBatch] = stg[warp];
@@ -584,118 +601,202 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
     int ne0 = len, ne1 = len;
     const int rounds = all_done() ? 0 : (len + kWarpBatch - 1) / kWarpBatch;
 
-    // stage round b (slot sl of this lane's record) into buffer b & 1; the slot of the round
-    // after the next is read one round ahead, so no cp.async waits on a slot load
-    auto stage = [&](int b, uint32_t sl) {
-      if (b * kWarpBatch + lane < len) {
-        const float4* r = rec + (size_t)sl * kRecQuads;
-        if constexpr (MERGE) {
-          if (sl & kBgTag) r = a.bg_rec + (size_t)(sl & ~kBgTag) * 3;
-        }
-        const uint32_t d = s_lane + (uint32_t)(b & 1) * kBufB;
-        cp_async16s(d, r);
-        cp_async16s(d + kRowB, r + 1);
-        cp_async16s(d + 2 * kRowB, r + 2);
-      }
-      cp_async_commit();
-    };
-    auto slot_of = [&](int b) -> uint32_t {
-      const int k = b * kWarpBatch + lane;
-      return k < len ? __ldg(slots + k) : 0u;
-    };
-    uint32_t sl_next = 0, sl_cur = 0, sl_stg = 0;   // slots of rounds b + 2, b, b + 1 (this lane)
-    if (rounds > 0) {
-      sl_cur = slot_of(0);
-      stage(0, sl_cur);
-      sl_next = slot_of(1);
-    }
-    for (int b = 0; b < rounds; ++b) {
-      if (b + 1 < rounds) {
-        sl_stg = sl_next;
-        stage(b + 1, sl_next);
-        sl_next = slot_of(b + 2);
-        cp_async_wait_group<1>();
-      } else {
-        cp_async_wait_group<0>();
-      }
-      __syncwarp();
-      float4* R0 = S[b & 1][0];
-      float4* R1 = S[b & 1][1];
-      float4* R2 = S[b & 1][2];
-      const int base = b * kWarpBatch;
-      // this round's records that can reach the block (lower bound of the whitened quadratic
-      // form over the block's pixel centres, 2 % margin: no per-pixel decision changes)
-      bool ov = false;
-      float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q2 = q0;
-      float2 q1 = make_float2(0.f, 0.f);
-      if (base + lane < len) {
-        q0 = R0[lane];
-        q1 = *reinterpret_cast<const float2*>(&R1[lane]);
-        q2 = R2[lane];
-        const float xa = q0.x - (bcx + 3.5f), xb = q0.x - (bcx - 3.5f);
-        const float ya = q0.y - (bcy + 3.5f), yb = q0.y - (bcy - 3.5f);
-        const float dxm = fmaxf(fmaxf(xa, -xb), 0.f);
-        const float lmin = fmaf(q0.w, q0.w >= 0.f ? xa : xb, q1.x * ya);
-        const float lmax = fmaf(q0.w, q0.w >= 0.f ? xb : xa, q1.x * yb);
-        const float lm = fmaxf(fmaxf(lmin, -lmax), 0.f);
-        const float px_ = q0.z * dxm;
-        const float lbq = fmaf(px_, px_, lm * lm);
-        ov = lbq <= fmaf(q1.y - kLog2AlphaMin, 1.02f, 0.02f);
-      }
-      const unsigned hit = __ballot_sync(FULL, ov);
-      // the selected records moved, in order, to the front of the buffer (in place: every lane
-      // read its own record above), with the record's lane in R1.z for n_eval and scores; the
-      // loop then reads them at warp-uniform, consecutive addresses (broadcast loads, no index)
-      __syncwarp();
-      if (ov) {
-        const int k = __popc(hit & lanemask_lt());
-        R0[k] = q0;
-        R1[k] = make_float4(q1.x, q1.y, __int_as_float(lane), 0.f);
-        R2[k] = q2;
-      }
-      __syncwarp();
-      const int nsel = __popc(hit);
-      // the quadratic form of selected record i (log2 of o e^power) for both pixels:
+    if constexpr (MASKED) {
+      // the quadratic form (log2 of o e^power) of staged record i for both pixels:
       // ta = r (v - pyc) + q dx;  arg = log2 o - (p dx)^2 - ta^2
-      auto arg_of = [&](int i) -> f32x2 {
-        const float4 q0 = R0[i];                                   // u, v, p, q
-        const float2 q1 = *reinterpret_cast<const float2*>(&R1[i]);  // r, log2 o
-        const float dx = q0.x - pxc;                               // shared by both pixels
-        const f32x2 pq = mul2(pk2(q0.z, q0.w), pk2(dx, dx));      // (p dx, q dx)
-        const float mm = fmaf(-pq.x, pq.x, q1.y);
-        const f32x2 ta = fma2(pk2(q1.x, q1.x), sub2(pk2(q0.y, q0.y), PYC), pk2(pq.y, pq.y));
+      auto arg_at = [&](const float4* R0, const float4* R1, int i) -> f32x2 {
+        const float4 r0 = R0[i];                                   // u, v, p, q
+        const float2 r1 = *reinterpret_cast<const float2*>(&R1[i]);  // r, log2 o
+        const float dx = r0.x - pxc;                               // shared by both pixels
+        const f32x2 pq = mul2(pk2(r0.z, r0.w), pk2(dx, dx));      // (p dx, q dx)
+        const float mm = fmaf(-pq.x, pq.x, r1.y);
+        const f32x2 ta = fma2(pk2(r1.x, r1.x), sub2(pk2(r0.y, r0.y), PYC), pk2(pq.y, pq.y));
         return nfma2(ta, ta, pk2(mm, mm));
       };
-      // software pipeline: record i + 1's quadratic form is evaluated while record i blends (the
-      // two chains are independent; blend2p sets it to -inf for a pixel that terminates at i).
-      // Index nsel <= 32 reads the next sub-array of the staging buffer: in bounds, never used.
-      f32x2 argn = nsel > 0 ? arg_of(0) : pk2(0.f, 0.f);
+      uint2* Q = hitq[warp];
+      const uint32_t bit = 1u << blk;
+      const int nwin = all_done() ? 0 : (len + kWarpBatch - 1) / kWarpBatch;
+      int win = 0, qh = 0, qn = 0;   // next window to scan; queue head and length (warp-uniform)
+      // this lane's entries of the next two windows (read ahead: no scan waits on a fresh load)
+      uint32_t w1 = lane < len ? __ldg(slots + lane) : 0u;
+      uint32_t w2 = kWarpBatch + lane < len ? __ldg(slots + kWarpBatch + lane) : 0u;
+      // scan windows until the queue holds a full round or the list ends
+      auto fill = [&]() {
+        while (qn < kWarpBatch && win < nwin) {
+          const uint32_t w = w1;
+          w1 = w2;
+          const int k2 = (win + 2) * kWarpBatch + lane;
+          w2 = k2 < len ? __ldg(slots + k2) : 0u;
+          const int pos = win * kWarpBatch + lane;
+          const bool hit = pos < len && (w & bit);
+          const unsigned hm = __ballot_sync(FULL, hit);
+          if (hit) Q[(qh + qn + __popc(hm & lanemask_lt())) & (kQ - 1)] = make_uint2(w >> kMaskBits, (uint32_t)pos);
+          qn += __popc(hm);
+          ++win;
+        }
+        __syncwarp();
+      };
+      // stage the queue's first min(qn, 32) hits into buffer buf (one record per lane)
+      auto stage_q = [&](int buf) -> int {
+        const int n = min(qn, kWarpBatch);
+        if (lane < n) {
+          const uint2 e = Q[(qh + lane) & (kQ - 1)];
+          const float4* r = rec + (size_t)e.x * kRecQuads;
+          const uint32_t d = s_lane + (uint32_t)buf * kBufB;
+          cp_async16s(d, r);
+          cp_async16s(d + kRowB, r + 1);
+          cp_async16s(d + 2 * kRowB, r + 2);
+          hitpos[warp][buf][lane] = e.y;
+        }
+        cp_async_commit();
+        qh = (qh + n) & (kQ - 1);
+        qn -= n;
+        return n;
+      };
+      fill();
+      int n_cur = stage_q(0);
+      for (int b = 0; n_cur > 0; ++b) {
+        fill();
+        const int n_next = stage_q((b + 1) & 1);
+        cp_async_wait_group<1>();
+        __syncwarp();
+        const float4* R0 = S[b & 1][0];
+        const float4* R1 = S[b & 1][1];
+        const float4* R2 = S[b & 1][2];
+        const uint32_t* P = hitpos[warp][b & 1];
+        // software pipeline: the next entry's quadratic form is evaluated while this one blends
+        // (independent chains; blend2p sets it to -inf for a pixel that terminates here).
+        // Index n_cur <= 32 reads the next sub-array of the staging buffer: in bounds, never used.
+        f32x2 argn = arg_at(R0, R1, 0);
 #pragma unroll kBlendUnroll
-      for (int i = 0; i < nsel; ++i) {
-        const f32x2 arg = argn;
-        argn = arg_of(i + 1);
-        // no "does any lane blend" vote: after the block cull almost every staged record is used
-        // by some lane, and for the others blend2p is an exact no-op (w = 0: T, colour and depth
-        // unchanged), so the vote and its branch only cost issue slots (+4.8 % C3, same-box A/B)
-        const float4 q2 = R2[i];                                   // r, g, b, z
-        // the record's position in the round (n_eval; read only when a pixel terminates)
-        auto pos = [&]() { return base + __float_as_int(R1[i].z); };
-        const f32x2 wb = blend2p(arg, q2, T, R, G, Bc, D, PYC, ne0, ne1, pos, argn);
-        if constexpr (SCORE) {
-          const int j = __float_as_int(R1[i].z);
-          const float2 w2 = up2(wb);
-          const uint32_t tot = __reduce_add_sync(FULL, __float2uint_rn((w2.x + w2.y) * kScoreFix));
-          const uint32_t mx = __reduce_max_sync(FULL, __float_as_uint(fmaxf(w2.x, w2.y)));
-          const uint32_t g = __shfl_sync(FULL, sl_cur, j) + (uint32_t)a.slot_base;
-          if (lane == 0 && tot) {
-            atomicAdd(a.score_sum + g, (float)tot * (1.f / kScoreFix));
-            atomicMax(a.score_max + g, mx);
+        for (int i = 0; i < n_cur; ++i) {
+          const f32x2 arg = argn;
+          argn = arg_at(R0, R1, i + 1);
+          const float4 q2 = R2[i];                                 // r, g, b, z
+          auto pos = [&]() { return (int)P[i]; };                  // list position (n_eval)
+          blend2p(arg, q2, T, R, G, Bc, D, PYC, ne0, ne1, pos, argn);
+        }
+        // the "all pixels done" vote once per round of 32 hits (voting after every terminating
+        // entry, or every 16 entries, costs more than the entries it saves: same-box A/B)
+        const bool done = all_done();
+        __syncwarp();   // buffer b & 1 is free for round b + 2
+        if (done) break;
+        n_cur = n_next;
+      }
+    } else {
+      // stage round b (slot sl of this lane's record) into buffer b & 1; the slot of the round
+      // after the next is read one round ahead, so no cp.async waits on a slot load
+      auto stage = [&](int b, uint32_t sl) {
+        if (b * kWarpBatch + lane < len) {
+          const float4* r = rec + (size_t)sl * kRecQuads;
+          if constexpr (MERGE) {
+            if (sl & kBgTag) r = a.bg_rec + (size_t)(sl & ~kBgTag) * 3;
+          }
+          const uint32_t d = s_lane + (uint32_t)(b & 1) * kBufB;
+          cp_async16s(d, r);
+          cp_async16s(d + kRowB, r + 1);
+          cp_async16s(d + 2 * kRowB, r + 2);
+        }
+        cp_async_commit();
+      };
+      auto slot_of = [&](int b) -> uint32_t {
+        const int k = b * kWarpBatch + lane;
+        return k < len ? __ldg(slots + k) : 0u;
+      };
+      uint32_t sl_next = 0, sl_cur = 0, sl_stg = 0;   // slots of rounds b + 2, b, b + 1 (this lane)
+      if (rounds > 0) {
+        sl_cur = slot_of(0);
+        stage(0, sl_cur);
+        sl_next = slot_of(1);
+      }
+      for (int b = 0; b < rounds; ++b) {
+        if (b + 1 < rounds) {
+          sl_stg = sl_next;
+          stage(b + 1, sl_next);
+          sl_next = slot_of(b + 2);
+          cp_async_wait_group<1>();
+        } else {
+          cp_async_wait_group<0>();
+        }
+        __syncwarp();
+        float4* R0 = S[b & 1][0];
+        float4* R1 = S[b & 1][1];
+        float4* R2 = S[b & 1][2];
+        const int base = b * kWarpBatch;
+        // this round's records that can reach the block (lower bound of the whitened quadratic
+        // form over the block's pixel centres, 2 % margin: no per-pixel decision changes)
+        bool ov = false;
+        float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q2 = q0;
+        float2 q1 = make_float2(0.f, 0.f);
+        if (base + lane < len) {
+          q0 = R0[lane];
+          q1 = *reinterpret_cast<const float2*>(&R1[lane]);
+          q2 = R2[lane];
+          const float xa = q0.x - (bcx + 3.5f), xb = q0.x - (bcx - 3.5f);
+          const float ya = q0.y - (bcy + 3.5f), yb = q0.y - (bcy - 3.5f);
+          const float dxm = fmaxf(fmaxf(xa, -xb), 0.f);
+          const float lmin = fmaf(q0.w, q0.w >= 0.f ? xa : xb, q1.x * ya);
+          const float lmax = fmaf(q0.w, q0.w >= 0.f ? xb : xa, q1.x * yb);
+          const float lm = fmaxf(fmaxf(lmin, -lmax), 0.f);
+          const float px_ = q0.z * dxm;
+          const float lbq = fmaf(px_, px_, lm * lm);
+          ov = lbq <= fmaf(q1.y - kLog2AlphaMin, 1.02f, 0.02f);
+        }
+        const unsigned hit = __ballot_sync(FULL, ov);
+        // the selected records moved, in order, to the front of the buffer (in place: every lane
+        // read its own record above), with the record's lane in R1.z for n_eval and scores; the
+        // loop then reads them at warp-uniform, consecutive addresses (broadcast loads, no index)
+        __syncwarp();
+        if (ov) {
+          const int k = __popc(hit & lanemask_lt());
+          R0[k] = q0;
+          R1[k] = make_float4(q1.x, q1.y, __int_as_float(lane), 0.f);
+          R2[k] = q2;
+        }
+        __syncwarp();
+        const int nsel = __popc(hit);
+        // the quadratic form of selected record i (log2 of o e^power) for both pixels:
+        // ta = r (v - pyc) + q dx;  arg = log2 o - (p dx)^2 - ta^2
+        auto arg_of = [&](int i) -> f32x2 {
+          const float4 q0 = R0[i];                                   // u, v, p, q
+          const float2 q1 = *reinterpret_cast<const float2*>(&R1[i]);  // r, log2 o
+          const float dx = q0.x - pxc;                               // shared by both pixels
+          const f32x2 pq = mul2(pk2(q0.z, q0.w), pk2(dx, dx));      // (p dx, q dx)
+          const float mm = fmaf(-pq.x, pq.x, q1.y);
+          const f32x2 ta = fma2(pk2(q1.x, q1.x), sub2(pk2(q0.y, q0.y), PYC), pk2(pq.y, pq.y));
+          return nfma2(ta, ta, pk2(mm, mm));
+        };
+        // software pipeline: record i + 1's quadratic form is evaluated while record i blends (the
+        // two chains are independent; blend2p sets it to -inf for a pixel that terminates at i).
+        // Index nsel <= 32 reads the next sub-array of the staging buffer: in bounds, never used.
+        f32x2 argn = nsel > 0 ? arg_of(0) : pk2(0.f, 0.f);
+  #pragma unroll kBlendUnroll
+        for (int i = 0; i < nsel; ++i) {
+          const f32x2 arg = argn;
+          argn = arg_of(i + 1);
+          // no "does any lane blend" vote: after the block cull almost every staged record is used
+          // by some lane, and for the others blend2p is an exact no-op (w = 0: T, colour and depth
+          // unchanged), so the vote and its branch only cost issue slots (+4.8 % C3, same-box A/B)
+          const float4 q2 = R2[i];                                   // r, g, b, z
+          // the record's position in the round (n_eval; read only when a pixel terminates)
+          auto pos = [&]() { return base + __float_as_int(R1[i].z); };
+          const f32x2 wb = blend2p(arg, q2, T, R, G, Bc, D, PYC, ne0, ne1, pos, argn);
+          if constexpr (SCORE) {
+            const int j = __float_as_int(R1[i].z);
+            const float2 w2 = up2(wb);
+            const uint32_t tot = __reduce_add_sync(FULL, __float2uint_rn((w2.x + w2.y) * kScoreFix));
+            const uint32_t mx = __reduce_max_sync(FULL, __float_as_uint(fmaxf(w2.x, w2.y)));
+            const uint32_t g = __shfl_sync(FULL, sl_cur, j) + (uint32_t)a.slot_base;
+            if (lane == 0 && tot) {
+              atomicAdd(a.score_sum + g, (float)tot * (1.f / kScoreFix));
+              atomicMax(a.score_max + g, mx);
+            }
           }
         }
+        __syncwarp();   // buffer b & 1 is free for round b + 2
+        sl_cur = sl_stg;
+        if (all_done()) break;
       }
-      __syncwarp();   // buffer b & 1 is free for round b + 2
-      sl_cur = sl_stg;
-      if (all_done()) break;
     }
     cp_async_wait_all();   // nothing may land in the buffers after this item
     __syncwarp();
@@ -725,6 +826,10 @@ static void launch_k4a_variant(const CompositeArgs& a, unsigned grid, cudaStream
 static bool warp_k4a_on() {   // GSB_K4A=cta: one CTA per list for every list (A/B comparisons)
   const char* e = getenv("GSB_K4A");
   return !(e && e[0] == 'c');
+}
+
+bool k4a_masks_supported() {   // warp / index sorts (and their HBM fallback) are mask-aware
+  return GSB_K4A_IDX && warp_k4a_on();
 }
 
 void launch_k4a_sort(const CompositeArgs& a, bool long_lists, cudaStream_t s) {
@@ -779,7 +884,7 @@ void launch_k4b_blend(const CompositeArgs& a, int* counter, cudaStream_t s) {
   if (!persistent) {
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4b_blend<false, false>, kBlendWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4b_blend<false, false, false>, kBlendWarps * 32, 0);
     // GSB_K4B_PER_SM=8 (one below the register limit) lets the other streams' latency-bound
     // kernels co-reside: C3 +0.6 %, C4 +1.8 %, C6 +0.8 % of step throughput, but K4b's own live
     // event time grows with the sharing (bench roofline 0.90 -> 0.76); the default keeps 9
@@ -791,12 +896,14 @@ void launch_k4b_blend(const CompositeArgs& a, int* counter, cudaStream_t s) {
   else cudaMemsetAsync(counter, 0, sizeof(int), s);
   const unsigned g = (unsigned)std::min<long long>(persistent, (items + kBlendWarps - 1) / kBlendWarps);
   const bool merge = a.bg_off != nullptr;
-  if (a.score_sum) {
-    if (merge) k4b_blend<true, true><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
-    else k4b_blend<true, false><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
+  if (a.key_shift) {   // block masks: plain slot-key passes only (Pipeline::pass)
+    k4b_blend<false, false, true><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
+  } else if (a.score_sum) {
+    if (merge) k4b_blend<true, true, false><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
+    else k4b_blend<true, false, false><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
   } else {
-    if (merge) k4b_blend<false, true><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
-    else k4b_blend<false, false><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
+    if (merge) k4b_blend<false, true, false><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
+    else k4b_blend<false, false, false><<<g, kBlendWarps * 32, 0, s>>>(a, counter, (int)items);
   }
 }
 

@@ -76,6 +76,8 @@ def test_production_tile_lists_small_configs(name):
     frames = [(e, c) for e in range(cfg.n_envs) for c in range(cfg.n_cams)]
     arr, zb, va = _oracle_fp32(sc, b, cfg, frames)
     _check(arr, zb, va, cfg.width, cfg.height, variants=(0, 1, 2, 3, 4, 5), seed=len(name))
+    # K4b block masks ride in the keys' low bits through K4a's warp / index / HBM sorts
+    _check(arr, zb, va, cfg.width, cfg.height, variants=(1, 2), key_modes=(2,), seed=len(name))
 
 
 @pytest.mark.parametrize("size", [32, 64, 160])
@@ -98,6 +100,7 @@ def test_production_tile_lists_ties_and_oversize_lists(size):
     zb = z.view(np.uint32)
     va = (rng.random((F, N)) < 0.95).astype(np.uint8)
     offs = _check(arr, zb, va, W, H, variants=(1, 2, 3, 4, 5), seed=5)
+    _check(arr, zb, va, W, H, variants=(1, 2), key_modes=(2,), seed=5)   # with block masks
     L = np.diff(offs, axis=1)
     if size == 32:
         assert L.max() > 4096
