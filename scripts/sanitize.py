@@ -1,4 +1,5 @@
 """Small renders for compute-sanitizer (memcheck / racecheck / synccheck / initcheck)."""
+import os
 import sys
 
 import numpy as np
@@ -8,8 +9,10 @@ sys.path.insert(0, ".")
 import paper_2604_25459_b200 as gsb  # noqa: E402
 import synth  # noqa: E402
 
-for name in ("T1", "T6", "T3"):
-    cfg = synth.CONFIGS[name]
+for name in ("T1", "T6", "T3", "T1-masked"):
+    # T1-masked: K4b block masks forced on (they serve long-list passes only by default)
+    os.environ["GSB_MASK_MIN_AVG"] = "0" if name.endswith("masked") else "512"
+    cfg = synth.CONFIGS[name.split("-")[0]]
     sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
     g = gsb.Scene.from_synth(sc)
     g.reserve(cfg.n_envs, cfg.n_cams, cfg.width, cfg.height)

@@ -489,6 +489,23 @@ def test_split_and_fused_compositing_bit_identical(name, monkeypatch):
     assert outs["split"]["stats"] == outs["fused"]["stats"]
 
 
+@pytest.mark.parametrize("name", ["C1", "T1", "T2", "T3", "T4", "T5", "T6"])
+def test_block_masks_bit_identical(name, monkeypatch):
+    """K4b block masks (K1's bounding-box trims -> 4-bit block masks in K2b's keys -> the masked
+    K4b's hit queue) only skip records that reach no pixel of a block, so forcing them on every
+    pass (GSB_MASK_MIN_AVG=0) or off (GSB_BLOCK_MASKS=0) gives bit-identical outputs."""
+    cfg = synth.CONFIGS[name]
+    sc, b = synth.make_scene(cfg), synth.make_batch(cfg)
+    outs = {}
+    for mode in ("on", "off"):
+        monkeypatch.setenv("GSB_MASK_MIN_AVG", "0")
+        monkeypatch.setenv("GSB_BLOCK_MASKS", "1" if mode == "on" else "0")
+        outs[mode] = gu.gpu_render(sc, b, cfg.width, cfg.height, stats=True)
+    for k in ("rgb", "depth", "alpha", "n_eval"):
+        assert np.array_equal(outs["on"][k], outs["off"][k]), k
+    assert outs["on"]["stats"] == outs["off"]["stats"]
+
+
 @pytest.mark.parametrize("n,spread,layers,size", [(600, 0.25, 1, 128), (400, 0.3, 40, 128), (2500, 0.05, 1, 128),
                                                   (3000, 0.3, 1, 32), (3000, 0.3, 25, 32)])
 @pytest.mark.parametrize("path", ["split", "fused"])
