@@ -455,10 +455,14 @@ def main():
                           "(190|105)V FMA-pipe fp32 ops per frame (SURVEY §8(d) d.4; 14 of the 18 ops per pair "
                           "are FMA-pipe arithmetic, the 4 compares run on the ALU pipe); BW = MEASURED_PEAKS "
                           "hbm_gbs; R = 148 SM x 128 FMA lanes x f"}
+    # measured DRAM bytes of the dominant kernel per launch: the ncu --set full capture's bytes per
+    # frame (profiles/k4_ncu_summary.json, captured on its own config) x this run's frames per launch
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "k4_ncu_summary.json")) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            ks = json.load(f)
+        if ks.get("config") == args.config and ks.get("dram_bytes_per_frame"):
+            traffic = ks["dram_bytes_per_frame"] * (B * C) / max(comp_launches[0], 1)
     except Exception:
         pass
 

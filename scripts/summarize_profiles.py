@@ -55,8 +55,9 @@ for k in ("k4b", "k4a", "k4", "k1", "k2", "k3"):
         d = summary(rep)[0]
         rd = float(d["dram__bytes_read.sum"].split()[0]) * (1e6 if "Mbyte" in d["dram__bytes_read.sum"] else 1e9 if "Gbyte" in d["dram__bytes_read.sum"] else 1.0)
         wr = float(d["dram__bytes_write.sum"].split()[0]) * (1e6 if "Mbyte" in d["dram__bytes_write.sum"] else 1e9 if "Gbyte" in d["dram__bytes_write.sum"] else 1.0)
-        json.dump({"tag": tag, "kernel": "k4b_blend" if k == "k4b" else "k4_composite", "dram_bytes_read": rd, "dram_bytes_write": wr,
-                   "dram_bytes_per_launch": rd + wr, "frames_per_launch": 64,
-                   "source": f"profiles/{tag}_{k}_ncu_full.txt"},
+        fpl = int(os.environ.get("FRAMES_PER_LAUNCH", "219"))   # C3: ceil(262144 / 1200) frames per chunk
+        json.dump({"tag": tag, "kernel": "k4b_blend" if k == "k4b" else "k4_composite", "config": "C3",
+                   "dram_bytes_read": rd, "dram_bytes_write": wr, "frames_per_launch": fpl,
+                   "dram_bytes_per_frame": (rd + wr) / fpl, "source": f"profiles/{tag}_{k}_ncu_full.txt"},
                   open(os.path.join(dst, "k4_ncu_summary.json"), "w"), indent=1)
     print("wrote", k)
