@@ -202,7 +202,9 @@ gsb_status gsb_reserve(gsb_scene s, int32_t max_envs, int32_t n_cams, int32_t wi
   auto auto_chunk = [&](int64_t tiles) {
     return (int)std::min<int64_t>(kMaxChunk, std::max<int64_t>(64, (tiles + s->n_tiles - 1) / s->n_tiles));
   };
-  const int E = (int)std::min<int64_t>(chunk_frames > 0 ? std::min(chunk_frames, kMaxChunk) : auto_chunk(chunk_tiles), F);
+  int E = (int)std::min<int64_t>(chunk_frames > 0 ? std::min(chunk_frames, kMaxChunk) : auto_chunk(chunk_tiles), F);
+  // K4b addresses a chunk's records with 32-bit (frame * N + slot) indices
+  E = (int)std::max<int64_t>(1, std::min<int64_t>(E, (int64_t)0xffffffffu / std::max<int64_t>(s->n, 1)));
   s->chunk = E;
   s->chunk_host = chunk_frames > 0 ? E : (int)std::min<int64_t>(E, auto_chunk(65536));
   int64_t cap = key_capacity;

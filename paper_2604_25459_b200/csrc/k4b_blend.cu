@@ -586,6 +586,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
     const TileList L = tile_list(a, fl, t);
     const int len = L.len + L.lb;   // merged length (lb = 0 unless static-camera merge)
     const float4* rec = a.rec + (size_t)fl * a.n * kRecQuads;
+    const uint32_t rbase = (uint32_t)((int64_t)fl * a.n);   // record index base (< 2^32: gsb_reserve)
     const uint32_t* slots = a.sorted + L.start;
     const float pxc = (float)px + 0.5f;
     const float bcx = (float)bx0 + 4.0f, bcy = (float)by0 + 4.0f;  // block centre (pixel centres +-3.5)
@@ -688,7 +689,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
       // after the next is read one round ahead, so no cp.async waits on a slot load
       auto stage = [&](int b, uint32_t sl) {
         if (b * kWarpBatch + lane < len) {
-          const float4* r = rec + (size_t)sl * kRecQuads;
+          const float4* r = a.rec + (size_t)(rbase + sl) * kRecQuads;
           if constexpr (MERGE) {
             if (sl & kBgTag) r = a.bg_rec + (size_t)(sl & ~kBgTag) * 3;
           }
