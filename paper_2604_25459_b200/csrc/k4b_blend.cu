@@ -535,7 +535,12 @@ __global__ void __launch_bounds__(kK4aWarps * 32) k4a_warp_sort(CompositeArgs a,
 
 // ------------------------------------------------------------------------------ K4b
 constexpr int kBlendWarps = 4;
-constexpr int kWarpBatch = 32;   // records staged per warp round (one per lane)
+constexpr int kWarpBatch = 32;   // records per warp window / masked round (one per lane)
+#ifndef GSB_K4B_PER
+#define GSB_K4B_PER 1   // 2: 64-record rounds (C3 -1.7 %, C4 -1.3 %: the fixed per-round work is not the cost)
+#endif
+constexpr int kPer = GSB_K4B_PER;               // unmasked path: records staged per lane per round
+constexpr int kRound = kPer * kWarpBatch;       // unmasked path: records per round
 #ifndef GSB_K4B_UNROLL
 #define GSB_K4B_UNROLL 2
 #endif
@@ -558,15 +563,15 @@ __device__ __forceinline__ void cp_async_wait_group() {
 template <bool SCORE, bool MERGE, bool MASKED>
 __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a, int* __restrict__ counter,
                                                                   int n_items) {
-  __shared__ __align__(16) float4 stg[kBlendWarps][2][3][kWarpBatch];   // 12 KB
+  __shared__ __align__(16) float4 stg[kBlendWarps][2][3][kRound];   // 12 KB per record per lane
   constexpr int kQ = 2 * kWarpBatch;   // hit queue (ring) per warp
   __shared__ uint2 hitq[MASKED ? kBlendWarps : 1][MASKED ? kQ : 1];           // (slot, list position)
   __shared__ uint32_t hitpos[MASKED ? kBlendWarps : 1][2][MASKED ? kWarpBatch : 1];   // staged positions
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float4 (*S)[3][kWarpBatch] = stg[warp];
+  float4 (*S)[3][kRound] = stg[warp];
   // shared address of this lane's staging slot (buffer 0, row 0); rows kRowB, buffers kBufB apart
-  constexpr uint32_t kRowB = kWarpBatch * sizeof(float4), kBufB = 3 * kRowB;
+  constexpr uint32_t kRowB = kRound * sizeof(float4), kBufB = 3 * kRowB;
   const uint32_t s_lane = (uint32_t)__cvta_generic_to_shared(&S[0][0][lane]);
   for (;;) {   // (fixed plan: an overflowed chunk's counter starts at n_items, see launch_k4b_blend)
     int item = 0;
@@ -600,7 +605,7 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
       return __all_sync(FULL, pc.x == kFar && pc.y == kFar);
     };
     int ne0 = len, ne1 = len;
-    const int rounds = all_done() ? 0 : (len + kWarpBatch - 1) / kWarpBatch;
+    const int rounds = all_done() ? 0 : (len + kRound - 1) / kRound;
 
     if constexpr (MASKED) {
       // the quadratic form (log2 of o e^power) of staged record i for both pixels:
@@ -685,26 +690,35 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
         n_cur = n_next;
       }
     } else {
-      // stage round b (slot sl of this lane's record) into buffer b & 1; the slot of the round
-      // after the next is read one round ahead, so no cp.async waits on a slot load
-      auto stage = [&](int b, uint32_t sl) {
-        if (b * kWarpBatch + lane < len) {
-          const float4* r = a.rec + (size_t)(rbase + sl) * kRecQuads;
-          if constexpr (MERGE) {
-            if (sl & kBgTag) r = a.bg_rec + (size_t)(sl & ~kBgTag) * 3;
+      // stage round b (slots sl[p] of this lane's records p * 32 + lane) into buffer b & 1; the
+      // slots of the round after the next are read one round ahead, so no cp.async waits on them
+      struct Slots { uint32_t v[kPer]; };
+      auto stage = [&](int b, const Slots& sl) {
+#pragma unroll
+        for (int p = 0; p < kPer; ++p) {
+          if (b * kRound + p * kWarpBatch + lane < len) {
+            const float4* r = a.rec + (size_t)(rbase + sl.v[p]) * kRecQuads;
+            if constexpr (MERGE) {
+              if (sl.v[p] & kBgTag) r = a.bg_rec + (size_t)(sl.v[p] & ~kBgTag) * 3;
+            }
+            const uint32_t d = s_lane + (uint32_t)(b & 1) * kBufB + (uint32_t)p * (kWarpBatch * sizeof(float4));
+            cp_async16s(d, r);
+            cp_async16s(d + kRowB, r + 1);
+            cp_async16s(d + 2 * kRowB, r + 2);
           }
-          const uint32_t d = s_lane + (uint32_t)(b & 1) * kBufB;
-          cp_async16s(d, r);
-          cp_async16s(d + kRowB, r + 1);
-          cp_async16s(d + 2 * kRowB, r + 2);
         }
         cp_async_commit();
       };
-      auto slot_of = [&](int b) -> uint32_t {
-        const int k = b * kWarpBatch + lane;
-        return k < len ? __ldg(slots + k) : 0u;
+      auto slot_of = [&](int b) -> Slots {
+        Slots r;
+#pragma unroll
+        for (int p = 0; p < kPer; ++p) {
+          const int k = b * kRound + p * kWarpBatch + lane;
+          r.v[p] = k < len ? __ldg(slots + k) : 0u;
+        }
+        return r;
       };
-      uint32_t sl_next = 0, sl_cur = 0, sl_stg = 0;   // slots of rounds b + 2, b, b + 1 (this lane)
+      Slots sl_next{}, sl_cur{}, sl_stg{};   // slots of rounds b + 2, b, b + 1 (this lane)
       if (rounds > 0) {
         sl_cur = slot_of(0);
         stage(0, sl_cur);
@@ -723,39 +737,52 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
         float4* R0 = S[b & 1][0];
         float4* R1 = S[b & 1][1];
         float4* R2 = S[b & 1][2];
-        const int base = b * kWarpBatch;
+        const int base = b * kRound;
         // this round's records that can reach the block (lower bound of the whitened quadratic
         // form over the block's pixel centres, 2 % margin: no per-pixel decision changes)
-        bool ov = false;
-        float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q2 = q0;
-        float2 q1 = make_float2(0.f, 0.f);
-        if (base + lane < len) {
-          q0 = R0[lane];
-          q1 = *reinterpret_cast<const float2*>(&R1[lane]);
-          q2 = R2[lane];
-          const float xa = q0.x - (bcx + 3.5f), xb = q0.x - (bcx - 3.5f);
-          const float ya = q0.y - (bcy + 3.5f), yb = q0.y - (bcy - 3.5f);
-          const float dxm = fmaxf(fmaxf(xa, -xb), 0.f);
-          const float lmin = fmaf(q0.w, q0.w >= 0.f ? xa : xb, q1.x * ya);
-          const float lmax = fmaf(q0.w, q0.w >= 0.f ? xb : xa, q1.x * yb);
-          const float lm = fmaxf(fmaxf(lmin, -lmax), 0.f);
-          const float px_ = q0.z * dxm;
-          const float lbq = fmaf(px_, px_, lm * lm);
-          ov = lbq <= fmaf(q1.y - kLog2AlphaMin, 1.02f, 0.02f);
+        bool ov[kPer];
+        float4 q0[kPer], q2[kPer];
+        float2 q1[kPer];
+        unsigned hit[kPer];
+#pragma unroll
+        for (int p = 0; p < kPer; ++p) {
+          const int e = p * kWarpBatch + lane;
+          ov[p] = false;
+          q0[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+          q2[p] = q0[p];
+          q1[p] = make_float2(0.f, 0.f);
+          if (base + e < len) {
+            q0[p] = R0[e];
+            q1[p] = *reinterpret_cast<const float2*>(&R1[e]);
+            q2[p] = R2[e];
+            const float xa = q0[p].x - (bcx + 3.5f), xb = q0[p].x - (bcx - 3.5f);
+            const float ya = q0[p].y - (bcy + 3.5f), yb = q0[p].y - (bcy - 3.5f);
+            const float dxm = fmaxf(fmaxf(xa, -xb), 0.f);
+            const float lmin = fmaf(q0[p].w, q0[p].w >= 0.f ? xa : xb, q1[p].x * ya);
+            const float lmax = fmaf(q0[p].w, q0[p].w >= 0.f ? xb : xa, q1[p].x * yb);
+            const float lm = fmaxf(fmaxf(lmin, -lmax), 0.f);
+            const float px_ = q0[p].z * dxm;
+            const float lbq = fmaf(px_, px_, lm * lm);
+            ov[p] = lbq <= fmaf(q1[p].y - kLog2AlphaMin, 1.02f, 0.02f);
+          }
+          hit[p] = __ballot_sync(FULL, ov[p]);
         }
-        const unsigned hit = __ballot_sync(FULL, ov);
         // the selected records moved, in order, to the front of the buffer (in place: every lane
-        // read its own record above), with the record's lane in R1.z for n_eval and scores; the
-        // loop then reads them at warp-uniform, consecutive addresses (broadcast loads, no index)
+        // read its own records above), with the record's round position in R1.z for n_eval and
+        // scores; the loop then reads them at warp-uniform, consecutive addresses (broadcast loads)
         __syncwarp();
-        if (ov) {
-          const int k = __popc(hit & lanemask_lt());
-          R0[k] = q0;
-          R1[k] = make_float4(q1.x, q1.y, __int_as_float(lane), 0.f);
-          R2[k] = q2;
+        int nsel = 0;
+#pragma unroll
+        for (int p = 0; p < kPer; ++p) {
+          if (ov[p]) {
+            const int k = nsel + __popc(hit[p] & lanemask_lt());
+            R0[k] = q0[p];
+            R1[k] = make_float4(q1[p].x, q1[p].y, __int_as_float(p * kWarpBatch + lane), 0.f);
+            R2[k] = q2[p];
+          }
+          nsel += __popc(hit[p]);
         }
         __syncwarp();
-        const int nsel = __popc(hit);
         // the quadratic form of selected record i (log2 of o e^power) for both pixels:
         // ta = r (v - pyc) + q dx;  arg = log2 o - (p dx)^2 - ta^2
         auto arg_of = [&](int i) -> f32x2 {
@@ -787,7 +814,13 @@ __global__ void __launch_bounds__(kBlendWarps * 32, 8) k4b_blend(CompositeArgs a
             const float2 w2 = up2(wb);
             const uint32_t tot = __reduce_add_sync(FULL, __float2uint_rn((w2.x + w2.y) * kScoreFix));
             const uint32_t mx = __reduce_max_sync(FULL, __float_as_uint(fmaxf(w2.x, w2.y)));
-            const uint32_t g = __shfl_sync(FULL, sl_cur, j) + (uint32_t)a.slot_base;
+            uint32_t sj = 0;
+#pragma unroll
+            for (int p = 0; p < kPer; ++p) {
+              const uint32_t v = __shfl_sync(FULL, sl_cur.v[p], j & 31);
+              if ((j >> 5) == p) sj = v;
+            }
+            const uint32_t g = sj + (uint32_t)a.slot_base;
             if (lane == 0 && tot) {
               atomicAdd(a.score_sum + g, (float)tot * (1.f / kScoreFix));
               atomicMax(a.score_max + g, mx);
