@@ -52,6 +52,7 @@ struct Pipeline {
   int32_t* out_neval;
   int64_t first = 0, count = 0;   // Gaussian range [first, first + count) of the internal order
   bool merge = false;             // static cameras: merge with the pre-binned background lists
+  bool masks_wanted = false;      // some pass of this render wanted K4b block masks
   bool fixed = false;             // GSB_FLAG_FIXED_PLAN: no host sync, no data-dependent launch choice
   uint32_t n_vlong = 0;           // the chunk's lists longer than kFusedSortCap
 
@@ -69,7 +70,10 @@ struct Pipeline {
     a.f0 = f0; a.n_frames = nf; a.width = W; a.height = H; a.tiles_x = tiles_x;
     a.near_plane = p->near_plane; a.far_plane = p->far_plane;
     a.rec = s->rec[sl]; a.emit = s->emit[sl];
-    a.trim = (!merge && block_masks_on()) ? s->trim[sl] : nullptr;
+    // trims only while block masks are in use (a render's first pass decides for the next render)
+    const bool trims = !merge && block_masks_on() && s->mask_hint;
+    a.trim = trims ? s->trim[sl] : nullptr;
+    s->trim_valid[sl] = trims;
     a.vcount = s->vcount[sl]; a.hist = s->hist[sl]; a.hist_stride = s->hist_stride;
     a.vis_bits = s->vis_bits[sl]; a.vis_words = s->vis_words;
     tm.begin(KC_PROJECT, sp);
@@ -115,9 +119,11 @@ struct Pipeline {
     if (slot_keys) a.ids = nullptr;   // key low word = index in the launch range = record slot
     // K4b block masks: plain split passes with slot keys (not scores: they reduce each record
     // over the whole warp) and the default K4a variants
-    const bool masks = split && slot_keys && !(p->flags & GSB_FLAG_SCORES) && block_masks_on() &&
-                       k4a_masks_supported() && count < ((int64_t)1 << (32 - kMaskBits)) &&
-                       n_keys >= mask_min_avg() * (uint64_t)(fe - fs) * n_tiles;
+    const bool want_masks = split && slot_keys && !(p->flags & GSB_FLAG_SCORES) && block_masks_on() &&
+                            k4a_masks_supported() && count < ((int64_t)1 << (32 - kMaskBits)) &&
+                            n_keys >= mask_min_avg() * (uint64_t)(fe - fs) * n_tiles;
+    const bool masks = want_masks && s->trim_valid[sl];   // K2b needs K1's trims of this chunk
+    masks_wanted |= want_masks;
     if (masks) { a.mask_bits = kMaskBits; a.trim = s->trim[sl]; }
     tm.begin(KC_EMIT, sb);
     launch_k2_emit(a, sb);
@@ -359,6 +365,7 @@ gsb_status render_impl(gsb_scene s, const K0Rig& rig, int n_envs, int n_cams, co
   pl.first = merge ? s->n_bg : 0;      // static cameras: only the robot Gaussians per frame
   pl.count = s->n - pl.first;
   gsb_status r = pl.run(rig, n_cams);
+  if (r == GSB_OK && !merge && F > 0) s->mask_hint = pl.masks_wanted;   // K1 trims for the next render
   s->stats_valid = (r == GSB_OK) && (p->flags & GSB_FLAG_STATS);
   s->timing_valid = (r == GSB_OK) && timing;
   return r;

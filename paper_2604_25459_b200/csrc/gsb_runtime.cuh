@@ -144,6 +144,8 @@ struct gsb_scene_t {
   float4* rec[2] = {nullptr, nullptr};
   uint2* emit[2] = {nullptr, nullptr};
   uint8_t* trim[2] = {nullptr, nullptr};   // [E][N] K4b block-mask trims of the visible pairs (K1 -> K2b)
+  bool trim_valid[2] = {false, false};     // K1 wrote the trims of the chunk in this slot
+  bool mask_hint = true;                   // a pass of the last render wanted block masks: K1 writes trims
   int* vcount[2] = {nullptr, nullptr};
   uint32_t* vis_bits[2] = {nullptr, nullptr};
   uint32_t* long_list[2] = {nullptr, nullptr};   // lists too long for K4's fused sort
