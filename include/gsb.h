@@ -108,7 +108,8 @@ gsb_status gsb_create_scene(const float* means, const float* scales, const float
 
 /* Size the device workspace for renders of up to max_envs envs x n_cams cameras at
  * width x height (allocations happen here, never in gsb_render).  chunk_frames = number of
- * env-camera frames processed per pipeline chunk (0 = automatic).  key_capacity = tile keys
+ * env-camera frames processed per pipeline chunk (0 = automatic; capped so that chunk frames x
+ * N < 2^32, K4b's 32-bit record index).  key_capacity = tile keys
  * held per chunk (0 = automatic); a chunk whose keys exceed it is split by frames, a single
  * frame exceeding it fails with GSB_ERR_CAPACITY.  flags: GSB_RESERVE_HOST_IO. */
 gsb_status gsb_reserve(gsb_scene scene, int32_t max_envs, int32_t n_cams, int32_t width,
